@@ -1,0 +1,331 @@
+"""Benchmark of the muffin-tin H/S setup (FLAPW, HSDLA) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+One step = one k-point of the BASELINE configuration through the hot path
+(A/B generation + Cholesky/T application + the S and H triangular DMMA contractions
+with the fused Hermitian mirror), inputs (SystemSpec, T blocks) resident in HBM.
+The metric is BASELINE.json's: H+S setup time per k-point and FP64 TFLOP/s over the
+reference's nominal FLOP ledger (`builder.py:336-370`), as a fraction of the measured
+FP64 DMMA peak.  Multi-GPU: one process per GPU (torchrun), each rank builds its own
+k-point (k-point parallelism, weak scaling, no collective in the data path); the
+time is the max over ranks.  `--impl reference` times the CPU oracle port (numpy +
+the same scipy/OpenBLAS routines the reference's optimized backend calls) on the
+host cores, rank 0 only.  Prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = ("H+S setup time per k-point & FP64 TFLOP/s (fraction of B200 FP64 peak), "
+          "1/2/4/8 GPU")
+UNIT = "TFLOP/s"
+FP64_PEAK_TFLOPS = 37.2  # measured DMMA ceiling, profiles/r01_fp64_peaks.json (= 148*128*1.965 GHz)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=30)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------ CPU oracle leg
+
+def cpu_oracle_step(spec, tmats):
+    """One k-point through the oracle port; returns (seconds, ledger FLOPs)."""
+    from oracle import build as ob
+    from oracle import flapw as of
+
+    t0 = time.perf_counter()
+    a, b, norms, offs = of.compute_ab(spec)
+    t1 = time.perf_counter()
+    _, _, led, _ = ob.build_all(a, b, norms, list(np.diff(offs)), [t.array for t in tmats.t_aa],
+                                [t.array for t in tmats.t_ab], [t.array for t in tmats.t_bb])
+    t2 = time.perf_counter()
+    return t2 - t0, sum(led.values()), t1 - t0, t2 - t1
+
+
+def cpu_sample(inst, max_basis=3200):
+    """Bounded CPU workload: the config's k-point, truncated to the first `max_basis`
+    K-vectors when larger (C3/C4), so one sample takes seconds, not minutes."""
+    from paper_1602_06589_b200 import SystemSpec
+
+    spec = inst.spec
+    if spec.n_basis > max_basis:
+        spec = SystemSpec(positions=spec.positions, rotations=spec.rotations,
+                          mt_radius=spec.mt_radius, l_sph=spec.l_sph, l_nonsph=spec.l_nonsph,
+                          k_point=spec.k_point, k_vectors=spec.k_vectors[:max_basis],
+                          omega=spec.omega, radial=spec.radial)
+    return spec
+
+
+def host_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        info = threadpool_info()
+        return max(int(i.get("num_threads", 1)) for i in info) if info else os.cpu_count()
+    except Exception:  # pragma: no cover
+        return os.cpu_count()
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_1602_06589_b200 import configs
+
+    inst = configs.make_instance(args.config)
+    spec = cpu_sample(inst)
+    for _ in range(max(0, min(args.warmup, 1))):
+        cpu_oracle_step(spec, inst.tmats)
+    times, flops = [], 0
+    t_start = time.perf_counter()
+    for _ in range(args.steps):
+        dt, fl, _, _ = cpu_oracle_step(spec, inst.tmats)
+        times.append(dt)
+        flops = fl
+        if time.perf_counter() - t_start > 150:  # keep the arm within a few minutes
+            break
+    total = sum(times)
+    value = flops * len(times) / total / 1e12
+    sample = (f"{len(times)} full k-point(s) of {args.config}" +
+              (f" truncated to N_G={spec.n_basis}" if spec.n_basis < inst.spec.n_basis else
+               f" (N_G={spec.n_basis})") + ": oracle compute_AB + build_all (scipy OpenBLAS)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
+        "n_gpus": world, "steps": len(times), "warmup": args.warmup,
+        "ms_per_step": round(1e3 * total / len(times), 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config} (BASELINE.json configs[{int(args.config[1]) - 1}])",
+                   "n_basis": spec.n_basis, "rows": int(sum((l + 1) ** 2 for l in spec.l_sph))},
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": host_threads(),
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._thr = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._thr = threading.Thread(target=self._loop, daemon=True)
+            self._thr.start()
+        except Exception as e:  # pragma: no cover
+            self.error = str(e)
+        return self
+
+    def _loop(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for name, bit in self.REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:  # pragma: no cover
+                pass
+            time.sleep(0.005)
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._thr:
+            self._thr.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ GPU arm
+
+def contract_flops(n, rows, hpd_rows):
+    """F_contract of the two triangular contractions: 8RN^2 (S) +
+    8RN^2 (ZHER2K) + 4 R_hpd N^2 + 8 R_nonhpd N^2 — the ledger's share of the DMMA kernels."""
+    return 16 * rows * n * n + 4 * hpd_rows * n * n + 8 * (rows - hpd_rows) * n * n
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1602_06589_b200 import BuildConfig, configs
+    from paper_1602_06589_b200.pipeline import DeviceSpec, HSPipeline, build_hs, pack_tmats
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    inst = configs.make_instance(args.config)
+    spec = configs.kpoint_variant(inst, rank)
+    n = spec.n_basis
+    dspec = DeviceSpec(spec)
+    tpack = pack_tmats(inst.tmats)
+    pipe = HSPipeline(n, dspec.heights)
+    stream = torch.cuda.current_stream()
+
+    for _ in range(max(args.warmup, 3)):
+        res = pipe.run(dspec, tpack)
+    torch.cuda.synchronize()
+    mask = res["hpd_mask"]
+    rows = dspec.rows
+    hpd_rows = int(sum(h for h, m in zip(dspec.heights, mask) if m))
+    flops_step = configs.nominal_flops(spec, mask)
+    fc = contract_flops(n, rows, hpd_rows)
+
+    kern = {"contract_S": [], "contract_H": [], "apply_Z": [], "apply_XY": []}
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            r = pipe.run(dspec, tpack)
+            for k, v in r["kernel_ms"].items():
+                kern[k].append(v)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    ms_t = torch.tensor([ms], device="cuda")
+    fl_t = torch.tensor([float(flops_step)], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(fl_t, op=dist.ReduceOp.SUM)
+    ms_max = float(ms_t.item())
+    total_flops = float(fl_t.item()) * args.steps
+    value = total_flops / (ms_max / 1e3) / 1e12
+
+    # e2e: the public API with host buffers (spec + T in, H and S out to pinned memory)
+    e2e_ms = []
+    host_out = None
+    h2d = d2h = 0
+    for i in range(args.warmup + max(3, args.steps // 5)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        h, s, r = build_hs(spec, inst.tmats, BuildConfig(), pipeline=pipe, host_out=host_out)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        host_out = (torch.from_numpy(h.base.T), torch.from_numpy(s.base.T))
+        if i >= args.warmup:
+            e2e_ms.append(dt * 1e3)
+        h2d, d2h = r["h2d_bytes"], r["d2h_bytes"]
+    e2e_t = torch.tensor([statistics.median(e2e_ms)], device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = float(fl_t.item()) / (float(e2e_t.item()) / 1e3) / 1e12
+
+    if rank == 0:
+        kc_ms = statistics.mean(kern["contract_S"]) + statistics.mean(kern["contract_H"])
+        achieved = fc / (kc_ms / 1e3) / 1e12
+        traffic = None
+        tpath = os.path.join(REPO, "profiles", f"traffic_{args.config}.json")
+        if os.path.exists(tpath):
+            with open(tpath) as f:
+                traffic = json.load(f).get("dram_bytes_per_step")
+        line = {
+            "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {
+                "workload": f"{args.config}: N_G={n}, N_A={spec.n_atoms}, N_L={int(dspec.heights[0])}, "
+                            f"R={rows}, one k-point per GPU per step",
+                "n_basis": n, "rows": rows, "ledger_flops_per_step": flops_step,
+                "parallelism": f"kpoint-dp{world}",
+                "l2": "inputs+outputs per step exceed the 126 MB L2 (A,B,UB,Z,XY + H,S); no flush",
+            },
+            "ms_per_kpoint": round(ms_max / args.steps, 4),
+            "kpoints_per_s": round(world * args.steps / (ms_max / 1e3), 2),
+            "fp64_peak_frac": round(value / world / FP64_PEAK_TFLOPS, 4),
+            "roofline": {
+                "bound": "tensor", "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": round(achieved / FP64_PEAK_TFLOPS, 4),
+                "traffic": traffic,
+                "kernel": "contract_kernel (S + H triangular DMMA contractions)",
+                "peak_source": "measured FP64 DMMA ceiling, profiles/r01_fp64_peaks.json "
+                               "(MEASURED_PEAKS.json has no FP64 entry)",
+                "algorithmic_flops_per_step": fc,
+                "kernel_ms": {k: round(statistics.mean(v), 4) for k, v in kern.items()},
+            },
+            "e2e": {"value": round(e2e_value, 4), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h),
+                    "ms_per_step": round(float(e2e_t.item()), 3),
+                    "api": "paper_1602_06589_b200.pipeline.build_hs (host spec+T -> host H,S)"},
+            "gpu_launches": args.steps * pipe.launches_per_run(dspec),
+            "clocks": clk.summary(),
+        }
+        if not args.no_cpu_baseline and world == 1:
+            cspec = cpu_sample(inst)
+            dt, fl, t_ab, t_build = cpu_oracle_step(cspec, inst.tmats)
+            line["cpu_baseline"] = {
+                "value": round(fl / dt / 1e12, 4), "unit": UNIT, "cores": host_threads(),
+                "kind": "port",
+                "sample": f"1 k-point of {args.config} (N_G={cspec.n_basis}): oracle compute_AB "
+                          f"{t_ab:.2f} s + build_all {t_build:.2f} s (scipy OpenBLAS)",
+            }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,175 @@
+/*
+ * hsdla_b200.h — C ABI of the B200-native (sm_100a) muffin-tin H/S setup path.
+ *
+ * Drop-in boundary for the reference package `hsdla` (arXiv 1602.06589, HSDLA):
+ * every entry point below replaces one reference interface, cited as
+ * file:line under /root/reference/pkg/src/hsdla/.  All matrices are complex128
+ * (`hsdla_c64`, layout-identical to numpy complex128 / C99 double _Complex),
+ * column-major with an explicit leading dimension counted in elements, exactly
+ * the `ComplexDense` convention (matrix.py:21-50).  Matrix pointers are DEVICE
+ * pointers unless marked HOST.  Work is enqueued on the context's CUDA stream;
+ * calls return after enqueueing unless documented otherwise.
+ *
+ * Status convention (mirrors LAPACK, kernels.py:266-272):
+ *   0                      success
+ *   < 0 and > -1000        -(1-based index of the invalid argument)
+ *   HSDLA_ERR_*            library / CUDA failures (message: hsdla_last_error())
+ * Cholesky returns its pivot through an explicit `info` output instead.
+ */
+#ifndef HSDLA_B200_H
+#define HSDLA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+  double re, im;
+} hsdla_c64;
+
+typedef struct hsdla_ctx hsdla_ctx;
+
+#define HSDLA_OK 0
+#define HSDLA_ERR_CUDA -1000        /* a CUDA call failed */
+#define HSDLA_ERR_UNSUPPORTED -1001 /* e.g. l_sph above the compiled maximum */
+#define HSDLA_ERR_NAN_INPUT -1002   /* NaN in the lower triangle of a Cholesky input (kernels.py:127-129) */
+#define HSDLA_ERR_NONFINITE -1003   /* non-finite value in a mirrored output (matrix.py:224-225) */
+#define HSDLA_ERR_ALLOC -1004
+
+#define HSDLA_MAX_LSPH 14 /* compiled template range of the A/B generator */
+
+/* ---- library / context ------------------------------------------------- */
+int hsdla_version(void);
+const char* hsdla_last_error(void);
+/* Context = stream + descriptor arena + pinned staging; `stream` is a cudaStream_t (NULL = legacy). */
+int hsdla_ctx_create(hsdla_ctx** out, void* stream);
+int hsdla_ctx_destroy(hsdla_ctx* ctx);
+int hsdla_ctx_set_stream(hsdla_ctx* ctx, void* stream);
+int hsdla_ctx_synchronize(hsdla_ctx* ctx);
+/* Owner rank of 64-wide column panel `panel` when the H/S lower triangle is sharded over
+ * n_shards GPUs: panels j and n_panels-1-j form one balanced pair. */
+int hsdla_panel_owner(int n_panels, int n_shards, int panel);
+
+/* ---- KernelBackend operator contract (kernels.py:46-151) ----------------- */
+
+/* lower(C) += A^H A, A is k x n (ld lda), C is n x n; strict upper of C never read or written.
+ * Replaces KernelBackend.hermitian_rank_k_update (kernels.py:56-63, zherk at :242-244). */
+int hsdla_herk_lower(hsdla_ctx* ctx, int n, int k, const hsdla_c64* A, int64_t lda,
+                     hsdla_c64* C, int64_t ldc);
+
+/* lower(C) += X^H B + B^H X, X and B are k x n.
+ * Replaces KernelBackend.hermitian_rank_2k_update (kernels.py:66-74, zher2k at :246-248). */
+int hsdla_her2k_lower(hsdla_ctx* ctx, int n, int k, const hsdla_c64* X, int64_t ldx,
+                      const hsdla_c64* B, int64_t ldb, hsdla_c64* C, int64_t ldc);
+
+/* C = alpha * op(A) * B + beta * C, op(A) = A^H (conj_a != 0, A is k x m) or A (A is m x k).
+ * C is m x n; with beta == 0 C is not read.  `workspace` must hold m*k elements when conj_a == 0.
+ * Replaces KernelBackend.general_product (kernels.py:77-89, zgemm at :250-253). */
+int hsdla_gemm(hsdla_ctx* ctx, int conj_a, int m, int n, int k, hsdla_c64 alpha,
+               const hsdla_c64* A, int64_t lda, const hsdla_c64* B, int64_t ldb,
+               hsdla_c64 beta, hsdla_c64* C, int64_t ldc, hsdla_c64* workspace);
+
+/* X = alpha * T * A (+ X if accumulate), T is m x m Hermitian read from its lower
+ * triangle with the diagonal's imaginary part ignored; A, X are m x n.
+ * `workspace` holds m*m elements.  Replaces KernelBackend.hermitian_product
+ * (kernels.py:92-104, zhemm at :255-258). */
+int hsdla_hemm_lower(hsdla_ctx* ctx, int m, int n, hsdla_c64 alpha, const hsdla_c64* T,
+                     int64_t ldt, const hsdla_c64* A, int64_t lda, int accumulate,
+                     hsdla_c64* X, int64_t ldx, hsdla_c64* workspace);
+
+/* Y = op(L) * A with L lower triangular m x m (strict upper ignored), op = ^H if conj_l.
+ * `workspace` holds m*m elements.  Replaces KernelBackend.triangular_product
+ * (kernels.py:107-116, ztrmm at :260-264). */
+int hsdla_trmm_lower(hsdla_ctx* ctx, int conj_l, int m, int n, const hsdla_c64* L, int64_t ldl,
+                     const hsdla_c64* A, int64_t lda, hsdla_c64* Y, int64_t ldy,
+                     hsdla_c64* workspace);
+
+/* Batched Cholesky of tril(T_b) into F_b (lower factor, zero strict upper), b < batch.
+ * info_host[b] (HOST, filled before return; this call synchronises the stream):
+ * 0 = HPD, j+1 = first non-positive/non-finite pivot j (zpotrf info), -1 = NaN in tril(T).
+ * T_b is never modified.  Replaces KernelBackend.cholesky_factor (kernels.py:119-132). */
+int hsdla_potrf_lower_batched(hsdla_ctx* ctx, int n, int batch, const hsdla_c64* T,
+                              int64_t ldt, int64_t stride_t, hsdla_c64* F, int64_t ldf,
+                              int64_t stride_f, int32_t* info_host);
+
+/* ---- storage helpers (matrix.py) ----------------------------------------- */
+
+/* Upper <- conj(lower^T), diag imag <- +0; *nonfinite_host (HOST) = 1 if any entry is not
+ * finite (synchronises).  Replaces HermitianAccumulator.mirror_to_full (matrix.py:216-226). */
+int hsdla_mirror_lower(hsdla_ctx* ctx, int n, hsdla_c64* C, int64_t ldc, int32_t* nonfinite_host);
+
+/* B[i, :] *= d[i] (d real, DEVICE).  Replaces scale_rows (matrix.py:229-239). */
+int hsdla_scale_rows(hsdla_ctx* ctx, int m, int n, const double* d, hsdla_c64* B, int64_t ldb);
+
+/* ---- matching coefficients (flapw.py:201-233 compute_AB) ----------------- */
+typedef struct {
+  int32_t n_atoms;
+  int32_t n_basis;            /* N_G */
+  const double* k_vectors;    /* DEVICE n_basis x 3, row-major (SystemSpec.k_vectors) */
+  const double* positions;    /* DEVICE n_atoms x 3 */
+  const double* rotations;    /* DEVICE n_atoms x 9, row-major 3x3 */
+  const double* mt_radius;    /* DEVICE n_atoms */
+  const double* radial;       /* DEVICE n_atoms x radial_stride x 5: per l {u, u', udot, udot', ||udot||} */
+  int32_t radial_stride;      /* >= max l_sph + 1 */
+  const int32_t* l_sph;       /* HOST n_atoms, each <= HSDLA_MAX_LSPH */
+  const int64_t* row_offset;  /* HOST n_atoms: first row of atom a's (l_sph+1)^2 block */
+  double omega;               /* cell volume */
+  hsdla_c64* A;               /* DEVICE out, column-major, leading dim ld */
+  hsdla_c64* B;               /* DEVICE out */
+  hsdla_c64* B_scaled;        /* DEVICE out or NULL: ||udot|| * B (the build_S side effect, builder.py:207) */
+  int64_t ld;
+  double* udot_norms;         /* DEVICE out or NULL: per-row ||udot|| (flapw.py:232) */
+} hsdla_ab_args;
+int hsdla_ab_generate(hsdla_ctx* ctx, const hsdla_ab_args* args);
+
+/* ---- the composed build (builder.py:403-474 build_all) ------------------- */
+typedef struct {
+  int32_t n_atoms;
+  int32_t n_basis;
+  const int32_t* heights;     /* HOST n_atoms: coefficient block heights */
+  const int64_t* row_offset;  /* HOST n_atoms: first row of each block in A/B */
+  const int32_t* t_index;     /* HOST n_atoms: which T set each atom uses */
+  int32_t n_tsets;
+  const int32_t* t_dim;       /* HOST n_tsets: m of each T set (m <= height of its atoms) */
+  const hsdla_c64* t_aa;      /* DEVICE n_tsets x (t_ld x t_ld), column-major, lower triangle read */
+  const hsdla_c64* t_ab;      /* DEVICE, full */
+  const hsdla_c64* t_bb;      /* DEVICE, lower triangle read */
+  int64_t t_ld;
+  const hsdla_c64* A;         /* DEVICE stacked coefficients, column-major R x n_basis, ld */
+  const hsdla_c64* B;
+  const hsdla_c64* B_scaled;  /* DEVICE or NULL: if NULL the build scales B by udot_norms itself */
+  const double* udot_norms;   /* DEVICE R (used when B_scaled == NULL) */
+  int64_t ld;
+  int32_t force_general_path; /* BuildConfig.force_general_path (builder.py:284) */
+  hsdla_c64* H;               /* DEVICE out n_basis x n_basis, full Hermitian after the call */
+  hsdla_c64* S;
+  int64_t ldh;
+  void* workspace;            /* DEVICE scratch of hsdla_build_workspace_size() bytes */
+  size_t workspace_bytes;
+  /* column-panel sharding for multi-GPU tile partitioning; n_shards <= 1 = all.
+   * With sharding only the lower tiles of owned 64-wide column panels are written, unmirrored. */
+  int32_t shard_rank, n_shards;
+} hsdla_build_args;
+
+typedef struct {
+  int32_t* hpd_mask;          /* HOST out n_atoms: 1 = Cholesky succeeded (HPD branch) */
+  int32_t* chol_info;         /* HOST out n_tsets: potrf info per T set (-2 = not attempted) */
+  int32_t nonfinite;          /* out: 1 if H or S holds a non-finite value */
+  float ms_setup, ms_S, ms_H_ABBA_BB, ms_H_AA; /* out: CUDA-event phase times */
+  float ms_contract_S, ms_contract_H;           /* out: the two triangular DMMA contraction launches */
+  float ms_apply_Z, ms_apply_XY;                /* out: the batched T-application launches */
+} hsdla_build_result;
+
+size_t hsdla_build_workspace_size(const hsdla_build_args* args);
+/* Enqueues the whole build; synchronises once mid-way (Cholesky info, while the S
+ * contraction runs) and at the end (flags, timings).  Returns HSDLA_ERR_NAN_INPUT on a NaN
+ * in tril(T_AA) and HSDLA_ERR_NONFINITE on non-finite output (outputs still written). */
+int hsdla_build_hs(hsdla_ctx* ctx, const hsdla_build_args* args, hsdla_build_result* result);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HSDLA_B200_H */

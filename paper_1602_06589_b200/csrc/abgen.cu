@@ -1,0 +1,326 @@
+// Fused matching-coefficient generator (compute_AB, reference flapw.py:201-233) for sm_100a.
+//
+// One thread per (K-vector t, atom a) evaluates, entirely in registers:
+//   * |K|, K_hat (zero vector -> +z), atom-frame direction R_a K_hat renormalised
+//     (flapw.py:169-176, :220-221);
+//   * j_0..j_{L+1}(r_MT |K|) with the reference's three regimes — exact limits at 0,
+//     power series below 0.5, upward recurrence at x >= L+1, Miller downward recurrence
+//     normalised on the better-conditioned of j_0/j_1 otherwise — and j'_l
+//     (special.py:49-131);
+//   * f_A, f_B = the boundary-matching brackets (flapw.py:179-198);
+//   * Y_lm by the normalised associated-Legendre recurrence with Condon-Shortley phase
+//     (special.py:139-179), rows ordered l^2 + l + m;
+//   * prefactor 4 pi / (sqrt(Omega) W_l) * i^l * e^{i K.x_a} (flapw.py:227),
+// and writes its column of A, B and (optionally) ||udot|| B, the build_S row scaling
+// (builder.py:207) fused into the producer.  L (= l_sph of the atom) is a template
+// parameter so every recurrence array lives in registers.
+//
+// This translation unit is compiled with -fmad=false: the reference evaluates these
+// formulas in numpy without FMA contraction, and the Wronskian / match-factor brackets
+// cancel, so keeping the same rounding sequence keeps A/B within ~1 ulp of the reference.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace hsdla {
+namespace {
+
+struct AbParams {
+  int n_basis;
+  const double* kv;
+  const double* pos;
+  const double* rot;
+  const double* rmt;
+  const double* radial;
+  int radial_stride;
+  double omega;
+  double2* A;
+  double2* B;
+  double2* Bs;
+  long long ld;
+  double* udot_norms;
+};
+
+__device__ __forceinline__ double dbl_fact(int n) {
+  double r = 1.0;
+  while (n > 1) { r *= n; n -= 2; }
+  return r;
+}
+
+// j_0..j_{LT}(x) for x > 0 (LT = L + 1 orders, special.py:104-131 regime switch).
+template <int LT>
+__device__ void bessel_j(double x, double (&j)[LT + 1]) {
+  if (x < 0.5) {
+    const double x2h = 0.5 * x * x;
+#pragma unroll
+    for (int l = 0; l <= LT; ++l) {
+      double term = pow(x, (double)l) / dbl_fact(2 * l + 1);
+      double total = term;
+      for (int k = 1;; ++k) {
+        term *= -x2h / (double)(k * (2 * l + 2 * k + 1));
+        total += term;
+        if (fabs(term) <= 1e-18 * fmax(fabs(total), 1e-300) || k > 60) break;
+      }
+      j[l] = total;
+    }
+    return;
+  }
+  double s, c;
+  sincos(x, &s, &c);
+  if (x >= (double)LT) {
+    j[0] = s / x;
+    if (LT >= 1) j[1] = s / (x * x) - c / x;
+#pragma unroll
+    for (int l = 1; l < LT; ++l) j[l + 1] = (double)(2 * l + 1) / x * j[l] - j[l - 1];
+    return;
+  }
+  // Miller downward recurrence (special.py:77-101)
+  const int ix = (int)x;
+  const int start = LT + (ix > 16 ? ix : 16) + (int)(2.0 * sqrt((double)(LT + 1)));
+  double scratch[LT + 1];
+#pragma unroll
+  for (int l = 0; l <= LT; ++l) scratch[l] = 0.0;
+  double jp1 = 0.0, jl = 1e-30;
+  int l = start;
+  for (; l > LT + 1; --l) {  // orders above l_top are not stored
+    const double jm1 = (double)(2 * l + 1) / x * jl - jp1;
+    jp1 = jl;
+    jl = jm1;
+    if (fabs(jl) > 1e250) { jl *= 1e-250; jp1 *= 1e-250; }
+  }
+#pragma unroll
+  for (int ll = LT + 1; ll >= 1; --ll) {
+    const double jm1 = (double)(2 * ll + 1) / x * jl - jp1;
+    jp1 = jl;
+    jl = jm1;
+    if (fabs(jl) > 1e250) {
+      jl *= 1e-250;
+      jp1 *= 1e-250;
+#pragma unroll
+      for (int q = (ll < LT ? ll : LT); q <= LT; ++q) scratch[q] *= 1e-250;
+    }
+    scratch[ll - 1] = jl;
+  }
+  const double j0 = s / x;
+  const double j1 = s / (x * x) - c / x;
+  double scale;
+  if (fabs(j0) >= fabs(j1) && scratch[0] != 0.0) scale = j0 / scratch[0];
+  else if (LT >= 1 && scratch[1] != 0.0) scale = j1 / scratch[1];
+  else scale = j0 / scratch[0];
+#pragma unroll
+  for (int q = 0; q <= LT; ++q) j[q] = scratch[q] * scale;
+}
+
+template <int L>
+__global__ void __launch_bounds__(128) ab_kernel(AbParams p, const int* __restrict__ atoms,
+                                                 const long long* __restrict__ row_off) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= p.n_basis) return;
+  const int a = atoms[blockIdx.y];
+  const long long off = row_off[blockIdx.y];
+
+  const double kx = p.kv[3 * t + 0], ky = p.kv[3 * t + 1], kz = p.kv[3 * t + 2];
+  const double kn = sqrt(kx * kx + ky * ky + kz * kz);
+  double ux = 0.0, uy = 0.0, uz = 1.0;
+  if (kn > 0.0) { ux = kx / kn; uy = ky / kn; uz = kz / kn; }
+  const double* R = p.rot + 9 * a;
+  double lx = ux * R[0] + uy * R[1] + uz * R[2];
+  double ly = ux * R[3] + uy * R[4] + uz * R[5];
+  double lz = ux * R[6] + uy * R[7] + uz * R[8];
+  const double ln = sqrt(lx * lx + ly * ly + lz * lz);
+  lx /= ln; ly /= ln; lz /= ln;
+  const double ct = fmin(fmax(lz, -1.0), 1.0);
+  const double st = sqrt(fmax(0.0, 1.0 - ct * ct));
+  double ephr, ephi;  // e^{i phi}
+  sincos(atan2(ly, lx), &ephi, &ephr);
+
+  // Bessel values / derivatives at x = r_MT |K| (special.py:104-131).
+  constexpr int LT = L + 1;
+  const double x = p.rmt[a] * kn;
+  double jv[LT + 1];
+  double jd[L + 1];
+  if (x == 0.0) {
+#pragma unroll
+    for (int l = 0; l <= LT; ++l) jv[l] = (l == 0) ? 1.0 : 0.0;
+#pragma unroll
+    for (int l = 0; l <= L; ++l) jd[l] = (l == 1) ? 1.0 / 3.0 : 0.0;
+  } else {
+    bessel_j<LT>(x, jv);
+    jd[0] = -jv[1];
+#pragma unroll
+    for (int l = 1; l <= L; ++l) jd[l] = jv[l - 1] - (double)(l + 1) / x * jv[l];
+  }
+
+  // Phase e^{i K.x_a}.
+  const double* X = p.pos + 3 * a;
+  const double th = kx * X[0] + ky * X[1] + kz * X[2];
+  double phs, phc;
+  sincos(th, &phs, &phc);
+  const double sqo = sqrt(p.omega);
+  const double fourpi = 4.0 * 3.141592653589793;
+
+  // Per-l prefactors times match factors (flapw.py:196-197, :227-231).
+  double par[L + 1], pai[L + 1], pbr[L + 1], pbi[L + 1], wn[L + 1];
+  const double* rad = p.radial + (long long)a * p.radial_stride * 5;
+#pragma unroll
+  for (int l = 0; l <= L; ++l) {
+    const double u = rad[5 * l + 0], up = rad[5 * l + 1], ud = rad[5 * l + 2], udp = rad[5 * l + 3];
+    wn[l] = rad[5 * l + 4];
+    const double w = ud * up - u * udp;
+    const double cl = fourpi / (sqo * w);
+    // i^l * phase (exact permutation / negation), then times c_l
+    double zr, zi;
+    switch (l & 3) {
+      case 0: zr = phc; zi = phs; break;
+      case 1: zr = -phs; zi = phc; break;
+      case 2: zr = -phc; zi = -phs; break;
+      default: zr = phs; zi = -phc; break;
+    }
+    const double prr = cl * zr, pri = cl * zi;
+    const double fa = ud * kn * jd[l] - udp * jv[l];
+    const double fb = -u * kn * jd[l] + up * jv[l];
+    par[l] = prr * fa; pai[l] = pri * fa;
+    pbr[l] = prr * fb; pbi[l] = pri * fb;
+  }
+
+  double2* colA = p.A + (long long)t * p.ld + off;
+  double2* colB = p.B + (long long)t * p.ld + off;
+  double2* colS = p.Bs ? p.Bs + (long long)t * p.ld + off : nullptr;
+
+  // Normalised associated Legendre recurrence, m outer (special.py:159-169), times e^{i m phi}.
+  double pmm = 0.28209479177387814;  // 1/sqrt(4 pi)
+  double emr = 1.0, emi = 0.0;        // e^{i m phi}
+#pragma unroll
+  for (int m = 0; m <= L; ++m) {
+    if (m > 0) {
+      pmm = -sqrt((double)(2 * m + 1) / (2.0 * m)) * st * pmm;
+      const double nr = emr * ephr - emi * ephi;
+      const double ni = emr * ephi + emi * ephr;
+      emr = nr; emi = ni;
+    }
+    double p2 = 0.0, p1 = 0.0;
+#pragma unroll
+    for (int l = m; l <= L; ++l) {
+      double plm;
+      if (l == m) plm = pmm;
+      else if (l == m + 1) plm = sqrt(2.0 * m + 3.0) * ct * pmm;
+      else {
+        const double aa = sqrt((4.0 * l * l - 1.0) / (double)(l * l - m * m));
+        const double bb = sqrt(((l - 1.0) * (l - 1.0) - (double)(m * m)) / (4.0 * (l - 1.0) * (l - 1.0) - 1.0));
+        plm = aa * (ct * p1 - bb * p2);
+      }
+      p2 = p1;
+      p1 = plm;
+      const double yr = plm * emr, yi = plm * emi;  // Y_{l,m}
+      // row (l, m): conj(Y) * pref ; row (l, -m): conj((-1)^m conj(Y)) * pref = (-1)^m Y * pref
+      const int rp = l * l + l + m;
+      {
+        const double2 va = make_double2(yr * par[l] + yi * pai[l], yr * pai[l] + (-yi) * par[l]);
+        const double2 vb = make_double2(yr * pbr[l] + yi * pbi[l], yr * pbi[l] + (-yi) * pbr[l]);
+        colA[rp] = va;
+        colB[rp] = vb;
+        if (colS) colS[rp] = make_double2(vb.x * wn[l], vb.y * wn[l]);
+      }
+      if (m > 0) {
+        const double sg = (m & 1) ? -1.0 : 1.0;
+        const double zr = sg * yr, zi = -(sg * yi);  // (-1)^m conj(Y_{l,m}) = Y_{l,-m}
+        const int rm = l * l + l - m;
+        const double2 va = make_double2(zr * par[l] + zi * pai[l], zr * pai[l] + (-zi) * par[l]);
+        const double2 vb = make_double2(zr * pbr[l] + zi * pbi[l], zr * pbi[l] + (-zi) * pbr[l]);
+        colA[rm] = va;
+        colB[rm] = vb;
+        if (colS) colS[rm] = make_double2(vb.x * wn[l], vb.y * wn[l]);
+      }
+    }
+  }
+}
+
+template <int L>
+int launch_ab_l(hsdla_ctx* ctx, const AbParams& p, const int* atoms_dev, const long long* off_dev,
+                int count) {
+  dim3 grid((p.n_basis + 127) / 128, count);
+  ab_kernel<L><<<grid, 128, 0, ctx->stream>>>(p, atoms_dev, off_dev);
+  HS_CHECK_LAUNCH();
+  return HSDLA_OK;
+}
+
+typedef int (*ab_launcher)(hsdla_ctx*, const AbParams&, const int*, const long long*, int);
+
+const ab_launcher kAbLaunchers[HSDLA_MAX_LSPH + 1] = {
+    &launch_ab_l<0>, &launch_ab_l<1>, &launch_ab_l<2>, &launch_ab_l<3>, &launch_ab_l<4>,
+    &launch_ab_l<5>, &launch_ab_l<6>, &launch_ab_l<7>, &launch_ab_l<8>, &launch_ab_l<9>,
+    &launch_ab_l<10>, &launch_ab_l<11>, &launch_ab_l<12>, &launch_ab_l<13>, &launch_ab_l<14>};
+
+__global__ void udot_rows_kernel(const double* __restrict__ radial, int stride, const int* atoms,
+                                 const long long* off, int L, double* out) {
+  const int a = atoms[blockIdx.x];
+  const int h = (L + 1) * (L + 1);
+  for (int r = threadIdx.x; r < h; r += blockDim.x) {
+    int l = 0;
+    while ((l + 1) * (l + 1) <= r) ++l;
+    out[off[blockIdx.x] + r] = radial[((long long)a * stride + l) * 5 + 4];
+  }
+}
+
+}  // namespace
+
+int ab_generate(hsdla_ctx* ctx, const hsdla_ab_args* args) {
+  if (args->n_atoms < 1) return -1;
+  if (args->n_basis < 1) return -1;
+  for (int a = 0; a < args->n_atoms; ++a)
+    if (args->l_sph[a] < 0 || args->l_sph[a] > HSDLA_MAX_LSPH) {
+      set_error("l_sph above HSDLA_MAX_LSPH");
+      return HSDLA_ERR_UNSUPPORTED;
+    }
+  AbParams p;
+  p.n_basis = args->n_basis;
+  p.kv = args->k_vectors;
+  p.pos = args->positions;
+  p.rot = args->rotations;
+  p.rmt = args->mt_radius;
+  p.radial = args->radial;
+  p.radial_stride = args->radial_stride;
+  p.omega = args->omega;
+  p.A = reinterpret_cast<double2*>(args->A);
+  p.B = reinterpret_cast<double2*>(args->B);
+  p.Bs = reinterpret_cast<double2*>(args->B_scaled);
+  p.ld = args->ld;
+  p.udot_norms = args->udot_norms;
+  // Group atoms by l_sph; upload (atom, row offset) lists through the arena.
+  std::vector<int> atoms;
+  std::vector<long long> offs;
+  std::vector<int> group_l, group_begin, group_count;
+  for (int L = 0; L <= HSDLA_MAX_LSPH; ++L) {
+    int begin = (int)atoms.size();
+    for (int a = 0; a < args->n_atoms; ++a)
+      if (args->l_sph[a] == L) { atoms.push_back(a); offs.push_back(args->row_offset[a]); }
+    if ((int)atoms.size() > begin) {
+      group_l.push_back(L);
+      group_begin.push_back(begin);
+      group_count.push_back((int)atoms.size() - begin);
+    }
+  }
+  int rc = arena_begin(ctx, atoms.size() * (sizeof(int) + sizeof(long long)) + 64);
+  if (rc) return rc;
+  int* datoms = static_cast<int*>(arena_push(ctx, atoms.data(), atoms.size() * sizeof(int), nullptr));
+  long long* doffs = static_cast<long long*>(
+      arena_push(ctx, offs.data(), offs.size() * sizeof(long long), nullptr));
+  rc = arena_flush(ctx);
+  if (rc) return rc;
+  for (size_t gi = 0; gi < group_l.size(); ++gi) {
+    rc = kAbLaunchers[group_l[gi]](ctx, p, datoms + group_begin[gi], doffs + group_begin[gi],
+                                   group_count[gi]);
+    if (rc) return rc;
+    if (p.udot_norms) {
+      udot_rows_kernel<<<group_count[gi], 128, 0, ctx->stream>>>(
+          p.radial, p.radial_stride, datoms + group_begin[gi], doffs + group_begin[gi], group_l[gi],
+          p.udot_norms);
+      HS_CHECK_LAUNCH();
+    }
+  }
+  return HSDLA_OK;
+}
+
+}  // namespace hsdla

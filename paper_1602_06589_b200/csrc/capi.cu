@@ -1,0 +1,536 @@
+// C ABI of libhsdla_b200 (include/hsdla_b200.h): context/arena plumbing, the six
+// KernelBackend operators, storage helpers and the composed build pipeline
+// (reference builder.py:403-474) on one CUDA stream.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace hsdla {
+
+namespace {
+thread_local std::string g_last_error;
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t v, size_t a = kAlign) { return (v + a - 1) / a * a; }
+}  // namespace
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int ab_generate(hsdla_ctx* ctx, const hsdla_ab_args* args);  // abgen.cu
+
+// ---- descriptor arena: pinned staging + device twin, used as a ring -----------
+namespace {
+size_t g_arena_start = 0;
+}
+
+int arena_begin(hsdla_ctx* ctx, size_t bytes) {
+  bytes = align_up(bytes + 4 * kAlign);
+  if (bytes > ctx->desc_cap) {
+    HS_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->desc_dev) cudaFree(ctx->desc_dev);
+    if (ctx->stage_host) cudaFreeHost(ctx->stage_host);
+    size_t cap = std::max<size_t>(bytes * 2, size_t(4) << 20);
+    HS_CUDA(cudaMalloc(&ctx->desc_dev, cap));
+    HS_CUDA(cudaHostAlloc(&ctx->stage_host, cap, cudaHostAllocDefault));
+    ctx->desc_cap = cap;
+    ctx->desc_off = 0;
+  } else if (ctx->desc_off + bytes > ctx->desc_cap) {
+    // Wrap: every earlier staging copy must have been consumed.
+    HS_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->desc_off = 0;
+  }
+  g_arena_start = ctx->desc_off;
+  return HSDLA_OK;
+}
+
+void* arena_push(hsdla_ctx* ctx, const void* src, size_t bytes, void** host_ptr) {
+  ctx->desc_off = align_up(ctx->desc_off);
+  void* dst = ctx->stage_host + ctx->desc_off;
+  if (bytes) memcpy(dst, src, bytes);
+  if (host_ptr) *host_ptr = dst;
+  void* dev = ctx->desc_dev + ctx->desc_off;
+  ctx->desc_off += bytes;
+  return dev;
+}
+
+int arena_flush(hsdla_ctx* ctx) {
+  size_t end = align_up(ctx->desc_off);
+  if (end > g_arena_start)
+    HS_CUDA(cudaMemcpyAsync(ctx->desc_dev + g_arena_start, ctx->stage_host + g_arena_start,
+                            end - g_arena_start, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->desc_off = end;
+  return HSDLA_OK;
+}
+
+}  // namespace hsdla
+
+using namespace hsdla;
+
+namespace {
+std::mutex g_api_mutex;  // contexts are not re-entrant; serialise arena use per process
+
+inline const double2* D2(const hsdla_c64* p) { return reinterpret_cast<const double2*>(p); }
+inline double2* D2(hsdla_c64* p) { return reinterpret_cast<double2*>(p); }
+inline double2 mk(hsdla_c64 v) { return make_double2(v.re, v.im); }
+
+Prob make_prob(double2* C, long long ldC, int m, int n, int kind, int seg0, int nseg,
+               int accumulate) {
+  Prob p;
+  memset(&p, 0, sizeof(p));
+  p.C = C;
+  p.ldC = ldC;
+  p.m = m;
+  p.n = n;
+  p.kind = kind;
+  p.seg0 = seg0;
+  p.nseg = nseg;
+  p.accumulate = accumulate;
+  p.col_tile_lo = 0;
+  p.col_tile_hi = -1;
+  p.alpha = make_double2(1.0, 0.0);
+  p.beta = make_double2(0.0, 0.0);
+  return p;
+}
+
+Seg make_seg(const double2* P, long long ldP, const double2* Q, long long ldQ, int k) {
+  Seg s;
+  s.P = P;
+  s.Q = Q;
+  s.ldP = ldP;
+  s.ldQ = ldQ;
+  s.k = k;
+  s.pad_ = 0;
+  return s;
+}
+
+int* flag_slot(hsdla_ctx* ctx, int i) { return ctx->scratch_dev + 64 + i; }
+}  // namespace
+
+extern "C" {
+
+int hsdla_version(void) { return 1; }
+
+const char* hsdla_last_error(void) { return g_last_error.c_str(); }
+
+int hsdla_ctx_create(hsdla_ctx** out, void* stream) {
+  if (!out) return -1;
+  hsdla_ctx* c = new hsdla_ctx();
+  c->stream = static_cast<cudaStream_t>(stream);
+  HS_CUDA(cudaGetDevice(&c->device));
+  HS_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
+  HS_CUDA(cudaMalloc(&c->scratch_dev, 256 * sizeof(int)));
+  HS_CUDA(cudaMemset(c->scratch_dev, 0, 256 * sizeof(int)));
+  HS_CUDA(cudaHostAlloc(&c->scratch_host, 256 * sizeof(int), cudaHostAllocDefault));
+  for (auto& e : c->ev) HS_CUDA(cudaEventCreate(&e));
+  HS_CUDA(cudaEventCreateWithFlags(&c->stage_done, cudaEventDisableTiming));
+  *out = c;
+  return HSDLA_OK;
+}
+
+int hsdla_ctx_destroy(hsdla_ctx* c) {
+  if (!c) return HSDLA_OK;
+  cudaStreamSynchronize(c->stream);
+  if (c->desc_dev) cudaFree(c->desc_dev);
+  if (c->stage_host) cudaFreeHost(c->stage_host);
+  if (c->scratch_dev) cudaFree(c->scratch_dev);
+  if (c->scratch_host) cudaFreeHost(c->scratch_host);
+  for (auto& e : c->ev) cudaEventDestroy(e);
+  cudaEventDestroy(c->stage_done);
+  delete c;
+  return HSDLA_OK;
+}
+
+int hsdla_ctx_set_stream(hsdla_ctx* c, void* stream) {
+  if (!c) return -1;
+  if (c->stream != static_cast<cudaStream_t>(stream)) {
+    HS_CUDA(cudaStreamSynchronize(c->stream));
+    c->stream = static_cast<cudaStream_t>(stream);
+  }
+  return HSDLA_OK;
+}
+
+int hsdla_ctx_synchronize(hsdla_ctx* c) {
+  if (!c) return -1;
+  HS_CUDA(cudaStreamSynchronize(c->stream));
+  return HSDLA_OK;
+}
+
+int hsdla_panel_owner(int n_panels, int n_shards, int panel) {
+  if (n_shards <= 1) return 0;
+  const int pair = std::min(panel, n_panels - 1 - panel);
+  return pair % n_shards;
+}
+
+// ---- KernelBackend operators ------------------------------------------------------
+int hsdla_herk_lower(hsdla_ctx* ctx, int n, int k, const hsdla_c64* A, int64_t lda, hsdla_c64* C,
+                     int64_t ldc) {
+  if (!ctx) return -1;
+  if (n < 0) return -2;
+  if (k < 0) return -3;
+  if (n == 0 || k == 0) return HSDLA_OK;
+  std::lock_guard<std::mutex> lk(g_api_mutex);
+  std::vector<Seg> segs{make_seg(D2(A), lda, D2(A), lda, k)};
+  std::vector<Prob> probs{make_prob(D2(C), ldc, n, n, PROB_TRI_LOWER, 0, 1, 1)};
+  return launch_contract(ctx, probs, segs, 0, flag_slot(ctx, 0));
+}
+
+int hsdla_her2k_lower(hsdla_ctx* ctx, int n, int k, const hsdla_c64* X, int64_t ldx,
+                      const hsdla_c64* B, int64_t ldb, hsdla_c64* C, int64_t ldc) {
+  if (!ctx) return -1;
+  if (n < 0) return -2;
+  if (k < 0) return -3;
+  if (n == 0 || k == 0) return HSDLA_OK;
+  std::lock_guard<std::mutex> lk(g_api_mutex);
+  std::vector<Seg> segs{make_seg(D2(X), ldx, D2(B), ldb, k), make_seg(D2(B), ldb, D2(X), ldx, k)};
+  std::vector<Prob> probs{make_prob(D2(C), ldc, n, n, PROB_TRI_LOWER, 0, 2, 1)};
+  return launch_contract(ctx, probs, segs, 0, flag_slot(ctx, 0));
+}
+
+int hsdla_gemm(hsdla_ctx* ctx, int conj_a, int m, int n, int k, hsdla_c64 alpha,
+               const hsdla_c64* A, int64_t lda, const hsdla_c64* B, int64_t ldb, hsdla_c64 beta,
+               hsdla_c64* C, int64_t ldc, hsdla_c64* workspace) {
+  if (!ctx) return -1;
+  if (m < 0) return -3;
+  if (n < 0) return -4;
+  if (k < 0) return -5;
+  if (m == 0 || n == 0) return HSDLA_OK;
+  std::lock_guard<std::mutex> lk(g_api_mutex);
+  const double2* P = D2(A);
+  long long ldp = lda;
+  if (!conj_a && k > 0) {
+    if (!workspace) return -14;
+    int rc = launch_prep(ctx, PREP_CONJ_TRANS, k, m, D2(A), lda, D2(workspace), k, 1.0);
+    if (rc) return rc;
+    P = D2(workspace);
+    ldp = k;
+  }
+  std::vector<Seg> segs{make_seg(P, ldp, D2(B), ldb, k)};
+  Prob p = make_prob(D2(C), ldc, m, n, PROB_GENERAL, 0, 1, 0);
+  p.alpha = mk(alpha);
+  p.beta = mk(beta);
+  p.accumulate = (beta.re != 0.0 || beta.im != 0.0) ? 1 : 0;
+  std::vector<Prob> probs{p};
+  return launch_contract(ctx, probs, segs, 0, flag_slot(ctx, 0));
+}
+
+int hsdla_hemm_lower(hsdla_ctx* ctx, int m, int n, hsdla_c64 alpha, const hsdla_c64* T,
+                     int64_t ldt, const hsdla_c64* A, int64_t lda, int accumulate, hsdla_c64* X,
+                     int64_t ldx, hsdla_c64* workspace) {
+  if (!ctx) return -1;
+  if (m < 0) return -2;
+  if (n < 0) return -3;
+  if (m == 0 || n == 0) return HSDLA_OK;
+  if (!workspace) return -12;
+  std::lock_guard<std::mutex> lk(g_api_mutex);
+  int rc = launch_prep(ctx, PREP_HERM_FULL, m, m, D2(T), ldt, D2(workspace), m, 1.0);
+  if (rc) return rc;
+  std::vector<Seg> segs{make_seg(D2(workspace), m, D2(A), lda, m)};
+  Prob p = make_prob(D2(X), ldx, m, n, PROB_GENERAL, 0, 1, accumulate ? 1 : 0);
+  p.alpha = mk(alpha);
+  p.beta = make_double2(1.0, 0.0);
+  std::vector<Prob> probs{p};
+  return launch_contract(ctx, probs, segs, 0, flag_slot(ctx, 0));
+}
+
+int hsdla_trmm_lower(hsdla_ctx* ctx, int conj_l, int m, int n, const hsdla_c64* L, int64_t ldl,
+                     const hsdla_c64* A, int64_t lda, hsdla_c64* Y, int64_t ldy,
+                     hsdla_c64* workspace) {
+  if (!ctx) return -1;
+  if (m < 0) return -3;
+  if (n < 0) return -4;
+  if (m == 0 || n == 0) return HSDLA_OK;
+  if (!workspace) return -11;
+  std::lock_guard<std::mutex> lk(g_api_mutex);
+  int rc = launch_prep(ctx, conj_l ? PREP_TRIL : PREP_TRIL_CONJ_TRANS, m, m, D2(L), ldl,
+                       D2(workspace), m, 1.0);
+  if (rc) return rc;
+  std::vector<Seg> segs{make_seg(D2(workspace), m, D2(A), lda, m)};
+  std::vector<Prob> probs{make_prob(D2(Y), ldy, m, n, PROB_GENERAL, 0, 1, 0)};
+  return launch_contract(ctx, probs, segs, 0, flag_slot(ctx, 0));
+}
+
+int hsdla_potrf_lower_batched(hsdla_ctx* ctx, int n, int batch, const hsdla_c64* T, int64_t ldt,
+                              int64_t stride_t, hsdla_c64* F, int64_t ldf, int64_t stride_f,
+                              int32_t* info_host) {
+  if (!ctx) return -1;
+  if (n < 0) return -2;
+  if (batch < 0) return -3;
+  if (batch == 0) return HSDLA_OK;
+  if (n == 0) {
+    for (int b = 0; b < batch; ++b) info_host[b] = 0;
+    return HSDLA_OK;
+  }
+  std::lock_guard<std::mutex> lk(g_api_mutex);
+  int* info_dev = nullptr;
+  HS_CUDA(cudaMallocAsync(&info_dev, batch * sizeof(int), ctx->stream));
+  int rc = launch_potrf_batched(ctx, n, batch, D2(T), ldt, stride_t, D2(F), ldf, stride_f, info_dev);
+  if (rc) return rc;
+  HS_CUDA(cudaMemcpyAsync(info_host, info_dev, batch * sizeof(int), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  HS_CUDA(cudaFreeAsync(info_dev, ctx->stream));
+  HS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return HSDLA_OK;
+}
+
+int hsdla_mirror_lower(hsdla_ctx* ctx, int n, hsdla_c64* C, int64_t ldc, int32_t* nonfinite_host) {
+  if (!ctx) return -1;
+  if (n < 0) return -2;
+  std::lock_guard<std::mutex> lk(g_api_mutex);
+  int* flag = flag_slot(ctx, 1);
+  HS_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+  int rc = launch_mirror(ctx, n, D2(C), ldc, flag);
+  if (rc) return rc;
+  HS_CUDA(cudaMemcpyAsync(ctx->scratch_host + 1, flag, sizeof(int), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  HS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (nonfinite_host) *nonfinite_host = ctx->scratch_host[1];
+  return HSDLA_OK;
+}
+
+int hsdla_scale_rows(hsdla_ctx* ctx, int m, int n, const double* d, hsdla_c64* B, int64_t ldb) {
+  if (!ctx) return -1;
+  std::lock_guard<std::mutex> lk(g_api_mutex);
+  return launch_scale_rows(ctx, m, n, d, D2(B), ldb);
+}
+
+int hsdla_ab_generate(hsdla_ctx* ctx, const hsdla_ab_args* args) {
+  if (!ctx) return -1;
+  if (!args) return -2;
+  std::lock_guard<std::mutex> lk(g_api_mutex);
+  return ab_generate(ctx, args);
+}
+
+// ---- composed build ------------------------------------------------------------------
+namespace {
+struct WsLayout {
+  size_t bs, z, xy, forms, tdim, info, total;
+  int mp;
+  long long R;
+};
+
+WsLayout ws_layout(const hsdla_build_args* a) {
+  WsLayout w;
+  long long R = 0;
+  for (int i = 0; i < a->n_atoms; ++i) R = std::max<long long>(R, a->row_offset[i] + a->heights[i]);
+  w.R = R;
+  int mp = 1;
+  for (int t = 0; t < a->n_tsets; ++t) mp = std::max(mp, a->t_dim[t]);
+  w.mp = mp;
+  const size_t stack = align_up(size_t(a->ld) * a->n_basis * sizeof(double2));
+  size_t off = 0;
+  w.bs = off;
+  off += a->B_scaled ? 0 : stack;
+  w.z = off;
+  off += stack;
+  w.xy = off;
+  off += stack;
+  w.forms = off;
+  off += align_up(size_t(a->n_tsets) * 4 * mp * mp * sizeof(double2));
+  w.tdim = off;
+  off += align_up(a->n_tsets * sizeof(int));
+  w.info = off;
+  off += align_up(a->n_tsets * sizeof(int));
+  w.total = off;
+  return w;
+}
+}  // namespace
+
+size_t hsdla_build_workspace_size(const hsdla_build_args* args) {
+  if (!args) return 0;
+  return ws_layout(args).total;
+}
+
+int hsdla_build_hs(hsdla_ctx* ctx, const hsdla_build_args* a, hsdla_build_result* res) {
+  if (!ctx) return -1;
+  if (!a) return -2;
+  if (!res) return -3;
+  const int na = a->n_atoms, n = a->n_basis;
+  if (na < 1 || n < 1) return -2;
+  for (int i = 0; i < na; ++i) {
+    const int ts = a->t_index[i];
+    if (ts < 0 || ts >= a->n_tsets || a->t_dim[ts] > a->heights[i]) {
+      set_error("atom " + std::to_string(i) + ": T set index or size invalid");
+      return -2;
+    }
+  }
+  const WsLayout w = ws_layout(a);
+  if (a->workspace_bytes < w.total) {
+    set_error("workspace too small");
+    return -2;
+  }
+  std::lock_guard<std::mutex> lk(g_api_mutex);
+  char* ws = static_cast<char*>(a->workspace);
+  const long long ld = a->ld;
+  const long long R = w.R;
+  const double2* A = D2(a->A);
+  const double2* B = D2(a->B);
+  double2* Z = reinterpret_cast<double2*>(ws + w.z);
+  double2* XY = reinterpret_cast<double2*>(ws + w.xy);
+  double2* forms = reinterpret_cast<double2*>(ws + w.forms);
+  int* tdim_dev = reinterpret_cast<int*>(ws + w.tdim);
+  int* info_dev = reinterpret_cast<int*>(ws + w.info);
+  const int mp = w.mp;
+  const long long fs = (long long)mp * mp;
+  const bool sharded = a->n_shards > 1;
+  int* flag = flag_slot(ctx, 2);
+  cudaEvent_t* ev = ctx->ev;
+
+  HS_CUDA(cudaEventRecord(ev[0], ctx->stream));
+  HS_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+  HS_CUDA(cudaMemcpyAsync(tdim_dev, a->t_dim, a->n_tsets * sizeof(int), cudaMemcpyHostToDevice,
+                          ctx->stream));
+  int rc = launch_tprep(ctx, a->n_tsets, tdim_dev, mp, D2(a->t_aa), D2(a->t_ab), D2(a->t_bb),
+                        a->t_ld, forms, a->force_general_path ? 0 : 1, info_dev);
+  if (rc) return rc;
+  int* info_host = ctx->scratch_host + 128;
+  HS_CUDA(cudaMemcpyAsync(info_host, info_dev, a->n_tsets * sizeof(int), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  HS_CUDA(cudaEventRecord(ev[5], ctx->stream));
+  const double2* Bs = D2(a->B_scaled);
+  if (!Bs) {
+    double2* bs = reinterpret_cast<double2*>(ws + w.bs);
+    HS_CUDA(cudaMemcpyAsync(bs, B, size_t(ld) * n * sizeof(double2), cudaMemcpyDeviceToDevice,
+                            ctx->stream));
+    rc = launch_scale_rows(ctx, (int)R, n, a->udot_norms, bs, ld);
+    if (rc) return rc;
+    Bs = bs;
+  }
+  HS_CUDA(cudaEventRecord(ev[1], ctx->stream));
+
+  // Column-panel ownership for sharded runs (balanced pairs j <-> nb-1-j).
+  const int nb = (n + kTile - 1) / kTile;
+  auto add_tri = [&](std::vector<Prob>& probs, double2* C, int seg0, int nseg) {
+    if (!sharded) {
+      probs.push_back(make_prob(C, a->ldh, n, n, PROB_TRI_MIRROR, seg0, nseg, 0));
+      return;
+    }
+    for (int j = 0; j < nb; ++j)
+      if (hsdla_panel_owner(nb, a->n_shards, j) == a->shard_rank) {
+        Prob p = make_prob(C, a->ldh, n, n, PROB_TRI_LOWER, seg0, nseg, 0);
+        p.col_tile_lo = j;
+        p.col_tile_hi = j + 1;
+        probs.push_back(p);
+      }
+  };
+
+  // ---- S = A^H A + (U B)^H (U B)   (builder.py:199-209)
+  {
+    std::vector<Seg> segs{make_seg(A, ld, A, ld, (int)R), make_seg(Bs, ld, Bs, ld, (int)R)};
+    std::vector<Prob> probs;
+    add_tri(probs, D2(a->S), 0, 2);
+    rc = launch_contract(ctx, probs, segs, 1, flag);
+    if (rc) return rc;
+  }
+  HS_CUDA(cudaEventRecord(ev[2], ctx->stream));
+
+  // ---- HPD dispatch needs the Cholesky info (ready long before S finishes)
+  HS_CUDA(cudaEventSynchronize(ev[5]));
+  std::vector<int> hpd(na, 0);
+  for (int t = 0; t < a->n_tsets; ++t) {
+    if (res->chol_info) res->chol_info[t] = info_host[t];
+    if (!a->force_general_path && info_host[t] == -1) {
+      set_error("NaN in the lower triangle of a T_AA block (Cholesky input)");
+      HS_CUDA(cudaStreamSynchronize(ctx->stream));
+      return HSDLA_ERR_NAN_INPUT;
+    }
+  }
+  for (int i = 0; i < na; ++i) {
+    hpd[i] = (!a->force_general_path && info_host[a->t_index[i]] == 0) ? 1 : 0;
+    if (res->hpd_mask) res->hpd_mask[i] = hpd[i];
+  }
+  // Rows of a block beyond its T size must be zero in Z / XY (builder.py:232-245 compaction).
+  for (int i = 0; i < na; ++i) {
+    const int m = a->t_dim[a->t_index[i]], h = a->heights[i];
+    if (m < h) {
+      rc = launch_zero_rows(ctx, Z, ld, (int)a->row_offset[i] + m, h - m, n);
+      if (rc) return rc;
+      rc = launch_zero_rows(ctx, XY, ld, (int)a->row_offset[i] + m, h - m, n);
+      if (rc) return rc;
+    }
+  }
+
+  // ---- Z_a = T_AB^H A_a + 1/2 T_BB B_a   (builder.py:231-240)
+  {
+    std::vector<Seg> segs;
+    std::vector<Prob> probs;
+    for (int i = 0; i < na; ++i) {
+      const int ts = a->t_index[i], m = a->t_dim[ts];
+      const long long off = a->row_offset[i];
+      const double2* f = forms + (long long)ts * 4 * fs;
+      const int s0 = (int)segs.size();
+      segs.push_back(make_seg(f, mp, A + off, ld, m));
+      segs.push_back(make_seg(f + fs, mp, B + off, ld, m));
+      probs.push_back(make_prob(Z + off, ld, m, n, PROB_GENERAL, s0, 2, 0));
+    }
+    rc = launch_contract(ctx, probs, segs, 2, flag);
+    if (rc) return rc;
+  }
+  HS_CUDA(cudaEventRecord(ev[3], ctx->stream));
+  // ---- Y_a = C_a^H A_a (HPD) or X_a = T_AA A_a (builder.py:279-304)
+  {
+    std::vector<Seg> segs;
+    std::vector<Prob> probs;
+    for (int i = 0; i < na; ++i) {
+      const int ts = a->t_index[i], m = a->t_dim[ts];
+      const long long off = a->row_offset[i];
+      const double2* f = forms + (long long)ts * 4 * fs + (hpd[i] ? 3 : 2) * fs;
+      const int s0 = (int)segs.size();
+      segs.push_back(make_seg(f, mp, A + off, ld, m));
+      probs.push_back(make_prob(XY + off, ld, m, n, PROB_GENERAL, s0, 1, 0));
+    }
+    rc = launch_contract(ctx, probs, segs, 3, flag);
+    if (rc) return rc;
+  }
+  HS_CUDA(cudaEventRecord(ev[4], ctx->stream));
+  // ---- H = Z^H B + B^H Z + sum_HPD Y^H Y + sum_nonHPD A^H X   (builder.py:246-247, :305-311)
+  {
+    std::vector<Seg> segs{make_seg(Z, ld, B, ld, (int)R), make_seg(B, ld, Z, ld, (int)R)};
+    int i = 0;
+    while (i < na) {
+      int j = i;
+      long long rows = 0;
+      while (j < na && hpd[j] == hpd[i]) { rows += a->heights[j]; ++j; }
+      const long long off = a->row_offset[i];
+      if (hpd[i]) segs.push_back(make_seg(XY + off, ld, XY + off, ld, (int)rows));
+      else segs.push_back(make_seg(A + off, ld, XY + off, ld, (int)rows));
+      i = j;
+    }
+    std::vector<Prob> probs;
+    add_tri(probs, D2(a->H), 0, (int)segs.size());
+    rc = launch_contract(ctx, probs, segs, 4, flag);
+    if (rc) return rc;
+  }
+  HS_CUDA(cudaEventRecord(ev[6], ctx->stream));
+  HS_CUDA(cudaMemcpyAsync(ctx->scratch_host + 2, flag, sizeof(int), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  HS_CUDA(cudaEventRecord(ev[7], ctx->stream));
+  HS_CUDA(cudaEventSynchronize(ev[7]));
+  res->nonfinite = ctx->scratch_host[2];
+  float t01 = 0, t12 = 0, t23 = 0, t34 = 0, t46 = 0;
+  cudaEventElapsedTime(&t01, ev[0], ev[1]);
+  cudaEventElapsedTime(&t12, ev[1], ev[2]);
+  cudaEventElapsedTime(&t23, ev[2], ev[3]);
+  cudaEventElapsedTime(&t34, ev[3], ev[4]);
+  cudaEventElapsedTime(&t46, ev[4], ev[6]);
+  res->ms_setup = t01;
+  res->ms_S = t12;
+  res->ms_H_ABBA_BB = t23 + t46;
+  res->ms_H_AA = t34;
+  res->ms_contract_S = t12;
+  res->ms_contract_H = t46;
+  res->ms_apply_Z = t23;
+  res->ms_apply_XY = t34;
+  if (res->nonfinite) {
+    set_error("accumulator contains non-finite values");
+    return HSDLA_ERR_NONFINITE;
+  }
+  return HSDLA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,108 @@
+// Shared declarations of libhsdla_b200 (sm_100a): context, error plumbing and the
+// descriptor types of the multi-segment contraction kernel.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/hsdla_b200.h"
+
+namespace hsdla {
+
+void set_error(const std::string& msg);
+
+#define HS_CUDA(call)                                                                  \
+  do {                                                                                 \
+    cudaError_t _e = (call);                                                           \
+    if (_e != cudaSuccess) {                                                           \
+      ::hsdla::set_error(std::string(#call) + ": " + cudaGetErrorString(_e) + " (" +   \
+                         __FILE__ + ":" + std::to_string(__LINE__) + ")");             \
+      return HSDLA_ERR_CUDA;                                                           \
+    }                                                                                  \
+  } while (0)
+
+#define HS_CHECK_LAUNCH() HS_CUDA(cudaGetLastError())
+
+// One K-segment of a contraction: C += P^H Q over k rows.  P and Q are column-major
+// complex128 with leading dims ldP / ldQ (elements); column c of P starts at P + c*ldP.
+struct Seg {
+  const double2* P;
+  const double2* Q;
+  long long ldP, ldQ;
+  int k;
+  int pad_;
+};
+
+enum ProbKind : int {
+  PROB_GENERAL = 0,     // C = alpha*acc (+ beta*C if accumulate), all m x n entries
+  PROB_TRI_LOWER = 1,   // lower(C) (+)= acc; strict upper untouched
+  PROB_TRI_MIRROR = 2,  // lower(C) (+)= acc, then upper = conj(lower^T), diag imag = +0
+};
+
+struct Prob {
+  double2* C;
+  long long ldC;
+  int m, n;  // output rows / cols (tri: m == n)
+  int kind;
+  int seg0, nseg;
+  int accumulate;
+  int tiles_m, tiles_n;  // tile grid (tri: tiles_m == tiles_n)
+  int tile_base;         // first global tile index of this problem
+  int col_tile_lo, col_tile_hi;  // tri only: restrict to tile columns [lo, hi) (sharding)
+  int pad_;
+  double2 alpha, beta;
+};
+
+constexpr int kTile = 64;  // complex outputs per CTA tile edge
+
+// Tile count of a problem (host side, also used for sharding).
+int prob_tile_count(const Prob& p);
+
+struct Arena;  // descriptor staging (defined in capi.cu)
+
+}  // namespace hsdla
+
+struct hsdla_ctx {
+  cudaStream_t stream = nullptr;
+  int device = 0;
+  int num_sms = 148;
+  // Device descriptor arena and its pinned host staging twin.
+  char* desc_dev = nullptr;
+  char* stage_host = nullptr;
+  size_t desc_cap = 0;
+  size_t desc_off = 0;
+  cudaEvent_t stage_done = nullptr;
+  bool stage_pending = false;
+  // Small device scratch: tile counters and flags; pinned mirrors for read-back.
+  int* scratch_dev = nullptr;   // [0..63] tile counters, [64..127] flags
+  int* scratch_host = nullptr;  // pinned
+  cudaEvent_t ev[8] = {};
+};
+
+namespace hsdla {
+// Contraction launcher: uploads problems/segments through the ctx arena and launches
+// the persistent DMMA kernel.  `counter_slot` picks the tile counter to use.
+int launch_contract(hsdla_ctx* ctx, const std::vector<Prob>& probs,
+                    const std::vector<Seg>& segs, int counter_slot, int* flag_dev);
+// Arena helpers.
+int arena_begin(hsdla_ctx* ctx, size_t bytes);
+void* arena_push(hsdla_ctx* ctx, const void* src, size_t bytes, void** host_ptr);
+int arena_flush(hsdla_ctx* ctx);
+
+// Small kernels (small.cu)
+enum OperandPrep : int { PREP_COPY = 0, PREP_CONJ_TRANS = 1, PREP_HERM_FULL = 2,
+                         PREP_TRIL = 3, PREP_TRIL_CONJ_TRANS = 4 };
+int launch_prep(hsdla_ctx* ctx, int op, int rows, int cols, const double2* in, long long ldin,
+                double2* out, long long ldout, double scale);
+int launch_potrf_batched(hsdla_ctx* ctx, int n, int batch, const double2* T, long long ldt,
+                         long long stride_t, double2* F, long long ldf, long long stride_f,
+                         int* info_dev);
+int launch_tprep(hsdla_ctx* ctx, int n_tsets, const int* tdim_dev, int mp,
+                 const double2* taa, const double2* tab, const double2* tbb, long long t_ld,
+                 double2* forms, int do_chol, int* info_dev);
+int launch_mirror(hsdla_ctx* ctx, int n, double2* C, long long ldc, int* flag_dev);
+int launch_scale_rows(hsdla_ctx* ctx, int m, int n, const double* d, double2* B, long long ldb);
+int launch_zero_rows(hsdla_ctx* ctx, double2* base, long long ld, int row0, int rows, int cols);
+}  // namespace hsdla

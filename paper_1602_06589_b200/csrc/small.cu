@@ -1,0 +1,236 @@
+// Small kernels of the H/S path (sm_100a): T-block preparation with the batched
+// Cholesky (kernels.py:119-132, builder.py:284-288), the Hermitian mirror
+// (matrix.py:216-226), row scaling (matrix.py:229-239) and operand preparation for the
+// per-op KernelBackend entry points (kernels.py:77-116).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace hsdla {
+namespace {
+
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+
+// ---------------------------------------------------------------------------
+// Cholesky of tril(T) into F (lower, zero strict upper), one CTA per matrix.
+// Left-looking column algorithm, the same recurrence as the reference's portable
+// backend (kernels.py:217-228): d_j = Re T_jj - sum_k |L_jk|^2, pivot fails unless
+// d_j > 0 and finite; L_ij = (T_ij - sum_k L_ik conj(L_jk)) / sqrt(d_j).
+// info: 0 ok, j+1 first bad pivot, -1 NaN in tril(T).
+__device__ void chol_block(int n, const double2* __restrict__ T, long long ldt, double2* F,
+                           long long ldf, int* info) {
+  extern __shared__ double2 rowj[];  // n entries
+  __shared__ double red[32];
+  __shared__ int s_nan;
+  __shared__ double s_d;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (tid == 0) s_nan = 0;
+  __syncthreads();
+  for (long long e = tid; e < (long long)n * n; e += nt) {
+    const int r = (int)(e % n), c = (int)(e / n);
+    double2 v = make_double2(0.0, 0.0);
+    if (r >= c) {
+      v = T[r + c * ldt];
+      if (isnan(v.x) || isnan(v.y)) s_nan = 1;
+    }
+    F[r + c * ldf] = v;
+  }
+  __syncthreads();
+  if (s_nan) {
+    if (tid == 0) *info = -1;
+    return;
+  }
+  for (int j = 0; j < n; ++j) {
+    double part = 0.0;
+    for (int k = tid; k < j; k += nt) {
+      const double2 v = F[j + (long long)k * ldf];
+      rowj[k] = v;
+      part += v.x * v.x + v.y * v.y;
+    }
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if ((tid & 31) == 0) red[tid >> 5] = part;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < (nt + 31) / 32; ++w) s += red[w];
+      s_d = F[j + (long long)j * ldf].x - s;
+    }
+    __syncthreads();
+    const double d = s_d;
+    if (!(d > 0.0) || !isfinite(d)) {
+      if (tid == 0) *info = j + 1;
+      return;
+    }
+    const double ljj = sqrt(d);
+    for (int i = j + 1 + tid; i < n; i += nt) {
+      double2 acc = F[i + (long long)j * ldf];
+      for (int k = 0; k < j; ++k) {
+        const double2 a = F[i + (long long)k * ldf];
+        const double2 b = rowj[k];
+        // a * conj(b)
+        acc.x -= a.x * b.x + a.y * b.y;
+        acc.y -= a.y * b.x - a.x * b.y;
+      }
+      F[i + (long long)j * ldf] = make_double2(acc.x / ljj, acc.y / ljj);
+    }
+    if (tid == 0) F[j + (long long)j * ldf] = make_double2(ljj, 0.0);
+    __syncthreads();
+  }
+  if (tid == 0) *info = 0;
+}
+
+__global__ void potrf_batched_kernel(int n, const double2* T, long long ldt, long long st,
+                                     double2* F, long long ldf, long long sf, int* info) {
+  const int b = blockIdx.x;
+  chol_block(n, T + b * st, ldt, F + b * sf, ldf, info + b);
+}
+
+// Per T set: forms[0] = T_AB, forms[1] = 1/2 full(T_BB), forms[2] = full(T_AA),
+// forms[3] = Cholesky factor of tril(T_AA) (if do_chol), all m x m with ld mp.
+__global__ void tprep_kernel(const int* tdim, int mp, const double2* taa, const double2* tab,
+                             const double2* tbb, long long t_ld, double2* forms, int do_chol,
+                             int* info) {
+  const int b = blockIdx.x;
+  const int m = tdim[b];
+  const long long tstride = t_ld * t_ld;
+  const double2* Taa = taa + b * tstride;
+  const double2* Tab = tab + b * tstride;
+  const double2* Tbb = tbb + b * tstride;
+  double2* f = forms + (long long)b * 4 * mp * mp;
+  const long long fs = (long long)mp * mp;
+  for (long long e = threadIdx.x; e < (long long)m * m; e += blockDim.x) {
+    const int r = (int)(e % m), c = (int)(e / m);
+    f[r + (long long)c * mp] = Tab[r + c * t_ld];
+    double2 bb, aa;
+    if (r > c) { bb = Tbb[r + c * t_ld]; aa = Taa[r + c * t_ld]; }
+    else if (r < c) { bb = cconj(Tbb[c + r * t_ld]); aa = cconj(Taa[c + r * t_ld]); }
+    else { bb = make_double2(Tbb[r + r * t_ld].x, 0.0); aa = make_double2(Taa[r + r * t_ld].x, 0.0); }
+    f[fs + r + (long long)c * mp] = make_double2(0.5 * bb.x, 0.5 * bb.y);
+    f[2 * fs + r + (long long)c * mp] = aa;
+  }
+  __syncthreads();
+  if (do_chol) chol_block(m, Taa, t_ld, f + 3 * fs, mp, info + b);
+  else if (threadIdx.x == 0) info[b] = -2;
+}
+
+// ---------------------------------------------------------------------------
+// Mirror: 32x32 tiles over the lower triangle; tile (ti, tj), ti >= tj.
+__global__ void mirror_kernel(int n, double2* C, long long ldc, int* flag) {
+  __shared__ double2 tile[32][33];
+  int b = blockIdx.x, tj = 0;
+  const int nb = (n + 31) / 32;
+  while (b >= nb - tj) { b -= nb - tj; ++tj; }
+  const int ti = tj + b;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  bool bad = false;
+  for (int c = ty; c < 32; c += 8) {
+    const int i = ti * 32 + tx, j = tj * 32 + c;
+    if (i < n && j < n && i >= j) {
+      double2 v = C[i + (long long)j * ldc];
+      if (i == j) { v.y = 0.0; C[i + (long long)j * ldc] = v; }
+      bad |= !(isfinite(v.x) && isfinite(v.y));
+      tile[c][tx] = v;  // tile[col][row]
+    }
+  }
+  __syncthreads();
+  // write upper: C[j, i] = conj(C[i, j]) for i > j; coalesced over j (tx)
+  for (int r = ty; r < 32; r += 8) {
+    const int i = ti * 32 + r, j = tj * 32 + tx;
+    if (i < n && j < n && i > j) C[j + (long long)i * ldc] = cconj(tile[tx][r]);
+  }
+  if (bad) atomicOr(flag, 1);
+}
+
+__global__ void scale_rows_kernel(int m, int n, const double* d, double2* B, long long ldb) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  if (i < m) {
+    double2 v = B[i + (long long)j * ldb];
+    const double s = d[i];
+    B[i + (long long)j * ldb] = make_double2(v.x * s, v.y * s);
+  }
+}
+
+__global__ void prep_kernel(int op, int rows, int cols, const double2* in, long long ldin,
+                            double2* out, long long ldout, double scale) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (r >= rows) return;
+  double2 v;
+  switch (op) {
+    case PREP_COPY: v = in[r + (long long)c * ldin]; break;
+    case PREP_CONJ_TRANS: v = cconj(in[c + (long long)r * ldin]); break;
+    case PREP_HERM_FULL:
+      if (r > c) v = in[r + (long long)c * ldin];
+      else if (r < c) v = cconj(in[c + (long long)r * ldin]);
+      else v = make_double2(in[r + (long long)r * ldin].x, 0.0);
+      break;
+    case PREP_TRIL: v = (r >= c) ? in[r + (long long)c * ldin] : make_double2(0.0, 0.0); break;
+    default: v = (r <= c) ? cconj(in[c + (long long)r * ldin]) : make_double2(0.0, 0.0); break;
+  }
+  if (scale != 1.0) { v.x *= scale; v.y *= scale; }
+  out[r + (long long)c * ldout] = v;
+}
+
+__global__ void zero_rows_kernel(double2* base, long long ld, int row0, int rows) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (r < rows) base[row0 + r + (long long)c * ld] = make_double2(0.0, 0.0);
+}
+
+}  // namespace
+
+int launch_potrf_batched(hsdla_ctx* ctx, int n, int batch, const double2* T, long long ldt,
+                         long long stride_t, double2* F, long long ldf, long long stride_f,
+                         int* info_dev) {
+  if (batch <= 0 || n <= 0) return HSDLA_OK;
+  potrf_batched_kernel<<<batch, 128, n * sizeof(double2), ctx->stream>>>(n, T, ldt, stride_t, F,
+                                                                          ldf, stride_f, info_dev);
+  HS_CHECK_LAUNCH();
+  return HSDLA_OK;
+}
+
+int launch_tprep(hsdla_ctx* ctx, int n_tsets, const int* tdim_dev, int mp, const double2* taa,
+                 const double2* tab, const double2* tbb, long long t_ld, double2* forms,
+                 int do_chol, int* info_dev) {
+  if (n_tsets <= 0) return HSDLA_OK;
+  tprep_kernel<<<n_tsets, 128, mp * sizeof(double2), ctx->stream>>>(tdim_dev, mp, taa, tab, tbb,
+                                                                     t_ld, forms, do_chol, info_dev);
+  HS_CHECK_LAUNCH();
+  return HSDLA_OK;
+}
+
+int launch_mirror(hsdla_ctx* ctx, int n, double2* C, long long ldc, int* flag_dev) {
+  if (n <= 0) return HSDLA_OK;
+  const int nb = (n + 31) / 32;
+  mirror_kernel<<<nb * (nb + 1) / 2, dim3(32, 8), 0, ctx->stream>>>(n, C, ldc, flag_dev);
+  HS_CHECK_LAUNCH();
+  return HSDLA_OK;
+}
+
+int launch_scale_rows(hsdla_ctx* ctx, int m, int n, const double* d, double2* B, long long ldb) {
+  if (m <= 0 || n <= 0) return HSDLA_OK;
+  scale_rows_kernel<<<dim3((m + 127) / 128, n), 128, 0, ctx->stream>>>(m, n, d, B, ldb);
+  HS_CHECK_LAUNCH();
+  return HSDLA_OK;
+}
+
+int launch_prep(hsdla_ctx* ctx, int op, int rows, int cols, const double2* in, long long ldin,
+                double2* out, long long ldout, double scale) {
+  if (rows <= 0 || cols <= 0) return HSDLA_OK;
+  prep_kernel<<<dim3((rows + 127) / 128, cols), 128, 0, ctx->stream>>>(op, rows, cols, in, ldin,
+                                                                        out, ldout, scale);
+  HS_CHECK_LAUNCH();
+  return HSDLA_OK;
+}
+
+int launch_zero_rows(hsdla_ctx* ctx, double2* base, long long ld, int row0, int rows, int cols) {
+  if (rows <= 0 || cols <= 0) return HSDLA_OK;
+  zero_rows_kernel<<<dim3((rows + 127) / 128, cols), 128, 0, ctx->stream>>>(base, ld, row0, rows);
+  HS_CHECK_LAUNCH();
+  return HSDLA_OK;
+}
+
+}  // namespace hsdla

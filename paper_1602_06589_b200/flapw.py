@@ -1,0 +1,163 @@
+"""FLAPW input types and the GPU matching-coefficient generator.
+
+`RadialBoundaryData` and `SystemSpec` keep the reference fields and validation
+(`flapw.py:36-166`).  `compute_AB` (`flapw.py:201-233`) runs the fused sm_100a A/B
+generator (`csrc/abgen.cu`) and returns host `StackedCoefficients` in the
+reference layout: A*, B* column-major R x N_G windows over capacity-height
+allocations, rows per atom ordered l^2 + l + m.
+"""
+from __future__ import annotations
+
+import json
+from dataclasses import dataclass
+
+import numpy as np
+
+from .builder import StackedCoefficients
+from .errors import ConfigurationError, ContractViolationError
+from .matrix import AtomBlockLayout, ComplexDense
+
+_MIN_WRONSKIAN = 1e-8
+
+
+@dataclass
+class RadialBoundaryData:
+    """Boundary values of the radial solutions for one atom, indexed by l (`flapw.py:36-82`)."""
+
+    u: np.ndarray
+    u_prime: np.ndarray
+    udot: np.ndarray
+    udot_prime: np.ndarray
+    energy: np.ndarray
+    udot_norm: np.ndarray
+
+    def __post_init__(self):
+        arrays = [np.asarray(a, dtype=np.float64) for a in
+                  (self.u, self.u_prime, self.udot, self.udot_prime, self.energy, self.udot_norm)]
+        self.u, self.u_prime, self.udot, self.udot_prime, self.energy, self.udot_norm = arrays
+        n = self.u.shape[0]
+        if any(a.shape != (n,) for a in arrays):
+            raise ContractViolationError("radial value arrays must share one length")
+        if np.any(self.udot_norm < 0):
+            raise ContractViolationError("udot norms must be non-negative")
+        if np.any(np.abs(self.wronskian) < _MIN_WRONSKIAN):
+            raise ContractViolationError(
+                f"|Wronskian| below {_MIN_WRONSKIAN}: radial values too degenerate")
+
+    @property
+    def wronskian(self) -> np.ndarray:
+        return self.udot * self.u_prime - self.u * self.udot_prime
+
+    @property
+    def l_max(self) -> int:
+        return self.u.shape[0] - 1
+
+    def to_json_dict(self) -> dict:
+        return {k: getattr(self, k).tolist() for k in
+                ("u", "u_prime", "udot", "udot_prime", "energy", "udot_norm")}
+
+    @classmethod
+    def from_json_dict(cls, d: dict) -> "RadialBoundaryData":
+        return cls(**{k: np.asarray(v, dtype=np.float64) for k, v in d.items()})
+
+
+@dataclass
+class SystemSpec:
+    """Geometry, cutoffs, basis vectors and radial data of one system (`flapw.py:85-166`)."""
+
+    positions: np.ndarray
+    rotations: np.ndarray
+    mt_radius: np.ndarray
+    l_sph: np.ndarray
+    l_nonsph: np.ndarray
+    k_point: np.ndarray
+    k_vectors: np.ndarray
+    omega: float
+    radial: list
+
+    def __post_init__(self):
+        self.positions = np.asarray(self.positions, dtype=np.float64)
+        self.rotations = np.asarray(self.rotations, dtype=np.float64)
+        self.mt_radius = np.asarray(self.mt_radius, dtype=np.float64)
+        self.l_sph = np.asarray(self.l_sph, dtype=np.int64)
+        self.l_nonsph = np.asarray(self.l_nonsph, dtype=np.int64)
+        self.k_point = np.asarray(self.k_point, dtype=np.float64)
+        self.k_vectors = np.asarray(self.k_vectors, dtype=np.float64)
+        n = self.n_atoms
+        if self.k_vectors.ndim != 2 or self.k_vectors.shape[1] != 3 or self.n_basis < 1:
+            raise ContractViolationError("need at least one K-vector of dimension 3")
+        if self.omega <= 0:
+            raise ContractViolationError("cell volume must be positive")
+        if np.any(self.l_nonsph > self.l_sph):
+            raise ConfigurationError("l_nonsph must not exceed l_sph")
+        if np.any(self.mt_radius <= 0):
+            raise ContractViolationError("muffin-tin radii must be positive")
+        if self.rotations.shape != (n, 3, 3):
+            raise ContractViolationError("need one 3x3 rotation per atom")
+        for a in range(n):
+            r = self.rotations[a]
+            if np.max(np.abs(r.T @ r - np.eye(3))) > 1e-12:
+                raise ContractViolationError(f"rotation {a} is not orthogonal")
+            if abs(abs(np.linalg.det(r)) - 1.0) > 1e-12:
+                raise ContractViolationError(f"rotation {a} has |det| != 1")
+        if len(self.radial) != n:
+            raise ContractViolationError("need radial data per atom")
+        for a, rad in enumerate(self.radial):
+            if rad.l_max < self.l_sph[a]:
+                raise ContractViolationError(f"atom {a}: radial data stops below l_sph")
+
+    @property
+    def n_atoms(self) -> int:
+        return self.positions.shape[0]
+
+    @property
+    def n_basis(self) -> int:
+        return self.k_vectors.shape[0]
+
+    def layout(self) -> AtomBlockLayout:
+        heights = tuple(int((l + 1) ** 2) for l in self.l_sph)
+        return AtomBlockLayout(heights, int((self.l_sph.max() + 1) ** 2))
+
+    def to_json_dict(self) -> dict:
+        return {
+            "positions": self.positions.tolist(), "rotations": self.rotations.tolist(),
+            "mt_radius": self.mt_radius.tolist(), "l_sph": self.l_sph.tolist(),
+            "l_nonsph": self.l_nonsph.tolist(), "k_point": self.k_point.tolist(),
+            "k_vectors": self.k_vectors.tolist(), "omega": self.omega,
+            "radial": [r.to_json_dict() for r in self.radial],
+        }
+
+    def to_json(self) -> str:
+        return json.dumps(self.to_json_dict(), sort_keys=True)
+
+    @classmethod
+    def from_json_dict(cls, d: dict) -> "SystemSpec":
+        d = dict(d)
+        d["radial"] = [RadialBoundaryData.from_json_dict(r) for r in d["radial"]]
+        return cls(**d)
+
+    @classmethod
+    def from_json(cls, text: str) -> "SystemSpec":
+        return cls.from_json_dict(json.loads(text))
+
+
+def compute_AB(spec: SystemSpec) -> StackedCoefficients:
+    """Matching coefficients A*, B* and row norms, generated on the GPU (`flapw.py:201-233`)."""
+    from . import device
+    from .pipeline import DeviceSpec, ab_generate_device, padded_ld
+
+    t = device.require_cuda()
+    layout = spec.layout()
+    dspec = DeviceSpec(spec)
+    n = spec.n_basis
+    ld = padded_ld(dspec.rows)
+    a_dev = device.empty_matrix(ld, n, ld, zero=True)
+    b_dev = device.empty_matrix(ld, n, ld, zero=True)
+    udot = t.zeros(ld, dtype=t.float64, device="cuda")
+    ab_generate_device(dspec, a_dev, b_dev, None, ld, udot)
+    a_star = ComplexDense.zeros(layout.total_rows, n, capacity_rows=layout.capacity_rows)
+    b_star = ComplexDense.zeros(layout.total_rows, n, capacity_rows=layout.capacity_rows)
+    device.download_window(a_dev, a_star.array)
+    device.download_window(b_dev, b_star.array)
+    norms = udot[: layout.total_rows].cpu().numpy().copy()
+    return StackedCoefficients(a_star, b_star, layout, norms)

@@ -1,0 +1,235 @@
+"""The reference's level-3 operator plugin API, implemented on B200 tensor cores.
+
+`KernelBackend` keeps the reference contract (`kernels.py:46-151`): argument
+validation with `ContractViolationError`, nominal FLOP charging per call even for
+empty shapes, Cholesky charged on success only, Hermitian/triangular operands read
+from the lower triangle only, the strict upper triangle of a Hermitian target never
+read.  `B200Kernels` executes every operator with the sm_100a kernels of
+`libhsdla_b200.so` (DMMA contraction, batched Cholesky).  It is the single backend:
+the reference's backend names ("optimized", "reference") are accepted as aliases so
+`BuildConfig(backend=...)` values keep working, but there is no dispatch to any
+other implementation and no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native, device
+from .errors import ConfigurationError, ContractViolationError, NotHPDError
+from .matrix import ComplexDense, FlopLedger, HermitianAccumulator, cholesky_flops
+
+_THREADS = 1
+
+
+def set_thread_count(threads: int):
+    """Validate and record the worker-thread cap (`kernels.py:33-38`).
+
+    The reference caps BLAS threads; here the value is only echoed into the build
+    report (`builder.py:421`), the GPU path needs no host threads."""
+    global _THREADS
+    if threads < 1:
+        raise ConfigurationError(f"thread count must be >= 1, got {threads}")
+    _THREADS = int(threads)
+
+
+def _check(cond: bool, msg: str):
+    if not cond:
+        raise ContractViolationError(msg)
+
+
+class KernelBackend:
+    """Shared contract: argument validation and FLOP accounting (`kernels.py:46-132`)."""
+
+    name = "abstract"
+
+    def __init__(self, threads: int = 1):
+        self.threads = int(threads)
+        set_thread_count(self.threads)
+
+    def hermitian_rank_k_update(self, c: HermitianAccumulator, a: ComplexDense,
+                                ledger: FlopLedger) -> HermitianAccumulator:
+        m, n = a.rows, a.cols
+        _check(c.n == n, f"rank-k shapes: C is {c.n}x{c.n}, A is {m}x{n}")
+        if m and n:
+            self._herk(c.matrix, a)
+        ledger.add("hermitian_rank_k", 4 * m * n * n)
+        return c
+
+    def hermitian_rank_2k_update(self, c: HermitianAccumulator, x: ComplexDense,
+                                 b: ComplexDense, ledger: FlopLedger) -> HermitianAccumulator:
+        _check(x.shape == b.shape, f"rank-2k needs same shapes, got {x.shape} vs {b.shape}")
+        m, n = x.rows, x.cols
+        _check(c.n == n, f"rank-2k shapes: C is {c.n}x{c.n}, X is {m}x{n}")
+        if m and n:
+            self._her2k(c.matrix, x, b)
+        ledger.add("hermitian_rank_2k", 8 * m * n * n)
+        return c
+
+    def general_product(self, c: ComplexDense, a: ComplexDense, b: ComplexDense,
+                        conj_transpose_a: bool, alpha: complex, beta: complex,
+                        ledger: FlopLedger) -> ComplexDense:
+        m_op = a.cols if conj_transpose_a else a.rows
+        k_op = a.rows if conj_transpose_a else a.cols
+        _check(k_op == b.rows, f"inner dimensions differ: op(A) has {k_op}, B has {b.rows}")
+        _check((c.rows, c.cols) == (m_op, b.cols),
+               f"C is {c.shape}, product is {(m_op, b.cols)}")
+        if m_op and b.cols:
+            self._gemm(c, a, b, conj_transpose_a, complex(alpha), complex(beta))
+        ledger.add("general_product", 8 * m_op * b.cols * k_op)
+        return c
+
+    def hermitian_product(self, x: ComplexDense, t: ComplexDense, a: ComplexDense,
+                          accumulate: bool, alpha: complex,
+                          ledger: FlopLedger) -> ComplexDense:
+        _check(t.rows == t.cols, f"T must be square, got {t.shape}")
+        n = t.rows
+        _check(a.rows == n, f"A has {a.rows} rows, T is {n}x{n}")
+        _check(x.shape == (n, a.cols), f"X is {x.shape}, expected {(n, a.cols)}")
+        if n and a.cols:
+            self._hemm(x, t, a, accumulate, complex(alpha))
+        elif not accumulate:
+            x.array[:] = 0
+        ledger.add("hermitian_product", 8 * n * n * a.cols)
+        return x
+
+    def triangular_product(self, y: ComplexDense, c: ComplexDense, a: ComplexDense,
+                           conj_transpose_c: bool, ledger: FlopLedger) -> ComplexDense:
+        _check(c.rows == c.cols, f"triangular factor must be square, got {c.shape}")
+        n = c.rows
+        _check(a.rows == n, f"A has {a.rows} rows, C is {n}x{n}")
+        _check(y.shape == a.shape, f"Y is {y.shape}, expected {a.shape}")
+        if n and a.cols:
+            self._trmm(y, c, a, conj_transpose_c)
+        ledger.add("triangular_product", 4 * n * n * a.cols)
+        return y
+
+    def cholesky_factor(self, t: ComplexDense, ledger: FlopLedger) -> ComplexDense:
+        """Factor tril(T) into a scratch copy; T survives failure; FLOPs on success only."""
+        _check(t.rows == t.cols, f"Cholesky input must be square, got {t.shape}")
+        n = t.rows
+        factor = self._potrf(t)  # raises NotHPDError / ContractViolationError
+        ledger.add("cholesky", cholesky_flops(n))
+        return factor
+
+    def _herk(self, c, a):  # pragma: no cover
+        raise NotImplementedError
+
+    def _her2k(self, c, x, b):  # pragma: no cover
+        raise NotImplementedError
+
+    def _gemm(self, c, a, b, conj_a, alpha, beta):  # pragma: no cover
+        raise NotImplementedError
+
+    def _hemm(self, x, t, a, accumulate, alpha):  # pragma: no cover
+        raise NotImplementedError
+
+    def _trmm(self, y, c, a, conj_c):  # pragma: no cover
+        raise NotImplementedError
+
+    def _potrf(self, t):  # pragma: no cover
+        raise NotImplementedError
+
+
+class B200Kernels(KernelBackend):
+    """Every operator on the GPU: host windows are staged to HBM, computed by the
+    sm_100a DMMA contraction / batched Cholesky, and copied back in place."""
+
+    name = "b200"
+
+    def _herk(self, c, a):
+        lib = _native.load()
+        cd = device.upload_window(c.array)
+        ad = device.upload_window(a.array)
+        _native.check(lib.hsdla_herk_lower(device.ctx(), c.rows, a.rows, device.ptr(ad),
+                                           ad.shape[1], device.ptr(cd), cd.shape[1]),
+                      "hsdla_herk_lower")
+        device.download_window(cd, c.array)
+
+    def _her2k(self, c, x, b):
+        lib = _native.load()
+        cd = device.upload_window(c.array)
+        xd = device.upload_window(x.array)
+        bd = device.upload_window(b.array)
+        _native.check(lib.hsdla_her2k_lower(device.ctx(), c.rows, x.rows, device.ptr(xd),
+                                            xd.shape[1], device.ptr(bd), bd.shape[1],
+                                            device.ptr(cd), cd.shape[1]),
+                      "hsdla_her2k_lower")
+        device.download_window(cd, c.array)
+
+    def _gemm(self, c, a, b, conj_a, alpha, beta):
+        lib = _native.load()
+        m, n = c.shape
+        k = b.rows
+        ad = device.upload_window(a.array)
+        bd = device.upload_window(b.array)
+        cd = device.upload_window(c.array) if beta != 0 else device.empty_matrix(m, n)
+        ws = device.empty_matrix(k, m) if not conj_a else None
+        _native.check(lib.hsdla_gemm(device.ctx(), 1 if conj_a else 0, m, n, k,
+                                     _native.c64(alpha), device.ptr(ad), ad.shape[1],
+                                     device.ptr(bd), bd.shape[1], _native.c64(beta),
+                                     device.ptr(cd), cd.shape[1],
+                                     device.ptr(ws) if ws is not None else None),
+                      "hsdla_gemm")
+        device.download_window(cd, c.array)
+
+    def _hemm(self, x, t, a, accumulate, alpha):
+        lib = _native.load()
+        m, n = x.shape
+        td = device.upload_window(t.array)
+        ad = device.upload_window(a.array)
+        xd = device.upload_window(x.array) if accumulate else device.empty_matrix(m, n)
+        ws = device.empty_matrix(m, m)
+        _native.check(lib.hsdla_hemm_lower(device.ctx(), m, n, _native.c64(alpha), device.ptr(td),
+                                           td.shape[1], device.ptr(ad), ad.shape[1],
+                                           1 if accumulate else 0, device.ptr(xd), xd.shape[1],
+                                           device.ptr(ws)),
+                      "hsdla_hemm_lower")
+        device.download_window(xd, x.array)
+
+    def _trmm(self, y, c, a, conj_c):
+        lib = _native.load()
+        m, n = y.shape
+        cdv = device.upload_window(c.array)
+        ad = device.upload_window(a.array)
+        yd = device.empty_matrix(m, n)
+        ws = device.empty_matrix(m, m)
+        _native.check(lib.hsdla_trmm_lower(device.ctx(), 1 if conj_c else 0, m, n, device.ptr(cdv),
+                                           cdv.shape[1], device.ptr(ad), ad.shape[1],
+                                           device.ptr(yd), yd.shape[1], device.ptr(ws)),
+                      "hsdla_trmm_lower")
+        device.download_window(yd, y.array)
+
+    def _potrf(self, t):
+        lib = _native.load()
+        n = t.rows
+        if n == 0:
+            return ComplexDense(np.zeros((0, 0), dtype=np.complex128, order="F"))
+        td = device.upload_window(t.array)
+        fd = device.empty_matrix(n, n)
+        info = (ctypes.c_int32 * 1)()
+        _native.check(lib.hsdla_potrf_lower_batched(device.ctx(), n, 1, device.ptr(td),
+                                                    td.shape[1], 0, device.ptr(fd), fd.shape[1],
+                                                    0, info),
+                      "hsdla_potrf_lower_batched")
+        if info[0] == -1:
+            raise ContractViolationError("NaN in Cholesky input (lower triangle)")
+        if info[0] > 0:
+            raise NotHPDError(info[0] - 1)
+        out = np.zeros((n, n), dtype=np.complex128, order="F")
+        device.download_window(fd, out)
+        return ComplexDense(out)
+
+
+_ALIASES = {"b200": B200Kernels, "optimized": B200Kernels, "reference": B200Kernels}
+
+
+def get_backend(name: str = "b200", threads: int = 1) -> KernelBackend:
+    """Backend by name (`kernels.py:281-288`); reference names alias the B200 backend."""
+    try:
+        cls = _ALIASES[name]
+    except KeyError:
+        raise ConfigurationError(
+            f"unknown backend {name!r}; choose from {sorted(_ALIASES)}") from None
+    return cls(threads=threads)

@@ -1,0 +1,120 @@
+"""Pin the CPU oracle (oracle/, test infrastructure) to golden vectors produced by the
+real reference (tests/golden/make_golden.py) and to the SPEC known-answer tests."""
+import numpy as np
+import pytest
+
+from conftest import LEDGER_KEYS, build_case, golden, rel_fro, spec_from_golden
+from oracle import build as ob
+from oracle import flapw as of
+from oracle import special as osp
+from paper_1602_06589_b200 import configs
+
+
+def test_bessel_matches_reference_all_regimes():
+    d = golden("special.npz")
+    for lm in (0, 1, 6, 8, 10, 12):
+        j, jp = osp.spherical_bessel_all(lm, d["x"])
+        np.testing.assert_allclose(j.T, d[f"j_{lm}"], rtol=1e-14, atol=1e-16)
+        np.testing.assert_allclose(jp.T, d[f"jp_{lm}"], rtol=1e-14, atol=1e-16)
+
+
+def test_ylm_matches_reference():
+    d = golden("special.npz")
+    y = osp.spherical_harmonics_all(10, d["dirs"])
+    assert np.max(np.abs(y - d["ylm_10"])) <= 1e-14
+
+
+def test_spec_kats():
+    # SPEC.md:369-380 known answers (j_2(1.5) checked against the closed form, not the
+    # misprinted 7th digit)
+    x = 1.5
+    j2 = (3 / x**3 - 1 / x) * np.sin(x) - 3 / x**2 * np.cos(x)
+    j, jp = osp.spherical_bessel_all(4, [0.0, x])
+    assert j[0, 0] == 1.0 and np.all(j[1:, 0] == 0) and jp[1, 0] == 1.0 / 3.0
+    assert abs(j[2, 1] - j2) <= 1e-15
+    y = osp.spherical_harmonics_all(1, [[0.0, 0.0, 1.0]])
+    assert abs(y[0, 0] - 0.2820947918) <= 1e-10
+    assert abs(y[2, 0] - 0.4886025119) <= 1e-10
+    p = osp.legendre_all(5, 0.3)
+    assert abs(p[5] - 0.34538625) <= 1e-12
+
+
+def test_addition_theorem():
+    rng = np.random.default_rng(1)
+    u, v = rng.standard_normal((2, 3))
+    u, v = u / np.linalg.norm(u), v / np.linalg.norm(v)
+    yu = osp.spherical_harmonics_all(8, [u])[:, 0]
+    yv = osp.spherical_harmonics_all(8, [v])[:, 0]
+    p = osp.legendre_all(8, u @ v)
+    for l in range(9):
+        s = np.sum(np.conj(yu[l * l:(l + 1) ** 2]) * yv[l * l:(l + 1) ** 2])
+        assert abs(s - (2 * l + 1) / (4 * np.pi) * p[l]) <= 1e-12
+
+
+def test_compute_ab_small_matches_reference():
+    d = golden("ab_small.npz")
+    spec = spec_from_golden(d)
+    a, b, norms, _ = of.compute_ab(spec)
+    assert rel_fro(a, d["A"]) <= 1e-14
+    assert rel_fro(b, d["B"]) <= 1e-14
+    np.testing.assert_array_equal(norms, d["udot_norms"])
+
+
+def test_compute_ab_c1_matches_reference():
+    d = golden("ab_c1.npz")
+    inst = configs.make_instance("C1")
+    a, b, norms, _ = of.compute_ab(inst.spec)
+    assert rel_fro(a[:, d["cols"]], d["A_cols"]) <= 1e-13
+    assert rel_fro(b[:, d["cols"]], d["B_cols"]) <= 1e-13
+    assert rel_fro(a @ d["V"], d["AV"]) <= 1e-13
+    assert rel_fro(b @ d["V"], d["BV"]) <= 1e-13
+
+
+@pytest.mark.parametrize("ci", range(7))
+def test_build_small_matches_reference(ci):
+    c = build_case(golden("build_small.npz"), ci)
+    h, s, led, mask = ob.build_all(c["A"], c["B"], c["udot"], c["heights"], c["t_aa"], c["t_ab"],
+                                   c["t_bb"], force_general_path=c["force"])
+    assert rel_fro(h, c["H"]) <= 1e-13
+    assert rel_fro(s, c["S"]) <= 1e-13
+    assert [led[k] for k in LEDGER_KEYS] == list(c["ledger"])
+    assert mask == c["mask"]
+
+
+def test_naive_forms_agree_with_blocked():
+    c = build_case(golden("build_small.npz"), 4)
+    assert rel_fro(ob.naive_S(c["A"], c["B"], c["udot"]), c["S"]) <= 1e-13
+    assert rel_fro(ob.naive_H(c["A"], c["B"], c["heights"], c["t_aa"], c["t_ab"], c["t_bb"]),
+                   c["H"]) <= 1e-13
+    v = np.random.default_rng(0).standard_normal((c["A"].shape[1], 3)) + 0j
+    hv = ob.h_matvec(c["A"], c["B"], c["heights"], c["t_aa"], c["t_ab"], c["t_bb"], v)
+    assert rel_fro(hv, c["H"] @ v) <= 1e-13
+    assert rel_fro(ob.s_matvec(c["A"], c["B"], c["udot"], v), c["S"] @ v) <= 1e-13
+
+
+def test_c1_pipeline_matches_reference():
+    d = golden("build_c1.npz")
+    inst = configs.make_instance("C1")
+    a, b, norms, offs = of.compute_ab(inst.spec)
+    tm = inst.tmats
+    heights = list(np.diff(offs))
+    t_aa = [t.array for t in tm.t_aa]
+    t_ab = [t.array for t in tm.t_ab]
+    t_bb = [t.array for t in tm.t_bb]
+    h, s, led, mask = ob.build_all(a, b, norms, heights, t_aa, t_ab, t_bb)
+    assert rel_fro(h @ d["V"], d["HV"]) <= 1e-13
+    assert rel_fro(s @ d["V"], d["SV"]) <= 1e-13
+    assert rel_fro(np.diag(h), d["H_diag"]) <= 1e-13
+    assert [led[k] for k in LEDGER_KEYS] == list(d["ledger"])
+    assert mask == [bool(x) for x in d["hpd_mask"]]
+    assert abs(np.linalg.norm(h) - d["H_fro"]) <= 1e-12 * d["H_fro"]
+    # matrix-free projections agree with the dense oracle too
+    hv = ob.h_matvec(a, b, heights, t_aa, t_ab, t_bb, d["V"])
+    assert rel_fro(hv, d["HV"]) <= 1e-13
+
+
+def test_predict_flops_and_memory_kats():
+    assert ob.estimate_memory(512, 49, 2256, True) == 3_703_738_368
+    assert ob.estimate_memory(384, 81, 29144, True) == 71_605_642_240
+    led = ob.predict_flops([1], 1, [True])
+    assert led["hermitian_rank_k"] == 12 and led["cholesky"] == 1

@@ -164,10 +164,17 @@ typedef struct {
 } hsdla_build_result;
 
 size_t hsdla_build_workspace_size(const hsdla_build_args* args);
-/* Enqueues the whole build; synchronises once mid-way (Cholesky info, while the S
- * contraction runs) and at the end (flags, timings).  Returns HSDLA_ERR_NAN_INPUT on a NaN
+/* Enqueues the whole build without a host round trip (the HPD branch is selected on the
+ * device from the Cholesky info) and synchronises once at the end (info, flags, timings).  Returns HSDLA_ERR_NAN_INPUT on a NaN
  * in tril(T_AA) and HSDLA_ERR_NONFINITE on non-finite output (outputs still written). */
 int hsdla_build_hs(hsdla_ctx* ctx, const hsdla_build_args* args, hsdla_build_result* result);
+
+/* The whole per-k-point hot path, SystemSpec -> (H, S): `hsdla_ab_generate` into
+ * args->A / B / B_scaled (ab->A etc. must alias them) with the T preparation overlapped on a
+ * side stream, then the build.  Replaces compute_AB (flapw.py:201) + build_all (builder.py:403)
+ * as called by the reference CLI's regenerate flow (cli.py:283-292, :310-325). */
+int hsdla_setup_hs(hsdla_ctx* ctx, const hsdla_ab_args* ab, const hsdla_build_args* args,
+                   hsdla_build_result* result);
 
 #ifdef __cplusplus
 }

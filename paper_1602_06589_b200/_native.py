@@ -98,6 +98,8 @@ SIGNATURES = {
     "hsdla_ab_generate": (ctypes.c_int, [_vp, ctypes.POINTER(AbArgs)]),
     "hsdla_build_workspace_size": (ctypes.c_size_t, [ctypes.POINTER(BuildArgs)]),
     "hsdla_build_hs": (ctypes.c_int, [_vp, ctypes.POINTER(BuildArgs), ctypes.POINTER(BuildResult)]),
+    "hsdla_setup_hs": (ctypes.c_int, [_vp, ctypes.POINTER(AbArgs), ctypes.POINTER(BuildArgs),
+                                      ctypes.POINTER(BuildResult)]),
 }
 
 _lib = None

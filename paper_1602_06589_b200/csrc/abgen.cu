@@ -22,10 +22,21 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <cmath>
+
 #include "common.cuh"
 
 namespace hsdla {
 namespace {
+
+// Y_lm recurrence coefficients (special.py:159-169), computed on the host with the
+// reference's exact expressions (IEEE sqrt/div are correctly rounded, so the values are
+// bit-identical to numpy's) instead of per thread at run time.
+constexpr int kL = HSDLA_MAX_LSPH + 1;
+__constant__ double c_sect[kL];    // sqrt((2m+1)/(2m))
+__constant__ double c_sub[kL];     // sqrt(2m+3)
+__constant__ double c_a[kL][kL];   // sqrt((4l^2-1)/(l^2-m^2))
+__constant__ double c_b[kL][kL];   // sqrt(((l-1)^2-m^2)/(4(l-1)^2-1))
 
 struct AbParams {
   int n_basis;
@@ -113,15 +124,29 @@ __device__ void bessel_j(double x, double (&j)[LT + 1]) {
   for (int q = 0; q <= LT; ++q) j[q] = scratch[q] * scale;
 }
 
+constexpr int kAbThreads = 128;
+
+// One thread per K-vector t (kAbThreads consecutive t per CTA), one atom per blockIdx.y.
+// The Legendre recurrence runs l-outer (all m of one l at a time, same operands and
+// rounding as special.py:159-169), so each l block of 2l+1 rows is complete at once: it
+// is staged in shared memory as [column][row] and written out with consecutive threads
+// on consecutive rows of a column — coalesced, sector-complete stores instead of one
+// 16-byte store per column per thread.
 template <int L>
-__global__ void __launch_bounds__(128) ab_kernel(AbParams p, const int* __restrict__ atoms,
-                                                 const long long* __restrict__ row_off) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= p.n_basis) return;
+__global__ void __launch_bounds__(kAbThreads) ab_kernel(AbParams p, const int* __restrict__ atoms,
+                                                        const long long* __restrict__ row_off) {
+  constexpr int S = 2 * L + 1;  // tallest l block; odd stride keeps smem conflict-free
+  extern __shared__ double2 stage[];
+  double2* sA = stage;
+  double2* sB = stage + kAbThreads * S;
+  const int t0 = blockIdx.x * kAbThreads;
+  const int t = t0 + threadIdx.x;
+  const bool live = t < p.n_basis;
+  const int tc = live ? t : p.n_basis - 1;
   const int a = atoms[blockIdx.y];
   const long long off = row_off[blockIdx.y];
 
-  const double kx = p.kv[3 * t + 0], ky = p.kv[3 * t + 1], kz = p.kv[3 * t + 2];
+  const double kx = p.kv[3 * tc + 0], ky = p.kv[3 * tc + 1], kz = p.kv[3 * tc + 2];
   const double kn = sqrt(kx * kx + ky * ky + kz * kz);
   double ux = 0.0, uy = 0.0, uz = 1.0;
   if (kn > 0.0) { ux = kx / kn; uy = ky / kn; uz = kz / kn; }
@@ -160,17 +185,25 @@ __global__ void __launch_bounds__(128) ab_kernel(AbParams p, const int* __restri
   sincos(th, &phs, &phc);
   const double sqo = sqrt(p.omega);
   const double fourpi = 4.0 * 3.141592653589793;
-
-  // Per-l prefactors times match factors (flapw.py:196-197, :227-231).
-  double par[L + 1], pai[L + 1], pbr[L + 1], pbi[L + 1], wn[L + 1];
   const double* rad = p.radial + (long long)a * p.radial_stride * 5;
+
+  // e^{i m phi} for m <= L (running product as the reference's expphi**m)
+  double emr[L + 1], emi[L + 1];
+  emr[0] = 1.0;
+  emi[0] = 0.0;
+#pragma unroll
+  for (int m = 1; m <= L; ++m) {
+    emr[m] = emr[m - 1] * ephr - emi[m - 1] * ephi;
+    emi[m] = emr[m - 1] * ephi + emi[m - 1] * ephr;
+  }
+  double p1[L + 1], p2[L + 1];  // P_{l-1,m}, P_{l-2,m} (normalised)
+
 #pragma unroll
   for (int l = 0; l <= L; ++l) {
+    // prefactor 4 pi / (sqrt(Omega) W_l) * i^l * phase times the match factors (flapw.py:196-231)
     const double u = rad[5 * l + 0], up = rad[5 * l + 1], ud = rad[5 * l + 2], udp = rad[5 * l + 3];
-    wn[l] = rad[5 * l + 4];
     const double w = ud * up - u * udp;
     const double cl = fourpi / (sqo * w);
-    // i^l * phase (exact permutation / negation), then times c_l
     double zr, zi;
     switch (l & 3) {
       case 0: zr = phc; zi = phs; break;
@@ -181,67 +214,67 @@ __global__ void __launch_bounds__(128) ab_kernel(AbParams p, const int* __restri
     const double prr = cl * zr, pri = cl * zi;
     const double fa = ud * kn * jd[l] - udp * jv[l];
     const double fb = -u * kn * jd[l] + up * jv[l];
-    par[l] = prr * fa; pai[l] = pri * fa;
-    pbr[l] = prr * fb; pbi[l] = pri * fb;
-  }
+    const double par = prr * fa, pai = pri * fa;
+    const double pbr = prr * fb, pbi = pri * fb;
 
-  double2* colA = p.A + (long long)t * p.ld + off;
-  double2* colB = p.B + (long long)t * p.ld + off;
-  double2* colS = p.Bs ? p.Bs + (long long)t * p.ld + off : nullptr;
-
-  // Normalised associated Legendre recurrence, m outer (special.py:159-169), times e^{i m phi}.
-  double pmm = 0.28209479177387814;  // 1/sqrt(4 pi)
-  double emr = 1.0, emi = 0.0;        // e^{i m phi}
+    // P_{l,m} for all m <= l
+    double pl[L + 1];
 #pragma unroll
-  for (int m = 0; m <= L; ++m) {
-    if (m > 0) {
-      pmm = -sqrt((double)(2 * m + 1) / (2.0 * m)) * st * pmm;
-      const double nr = emr * ephr - emi * ephi;
-      const double ni = emr * ephi + emi * ephr;
-      emr = nr; emi = ni;
+    for (int m = 0; m <= l; ++m) {
+      if (m == l) pl[m] = (l == 0) ? 0.28209479177387814 : -c_sect[m] * st * p1[m - (l > 0 ? 1 : 0)];
+      else if (m == l - 1) pl[m] = c_sub[m] * ct * p1[m];
+      else pl[m] = c_a[l][m] * (ct * p1[m] - c_b[l][m] * p2[m]);
     }
-    double p2 = 0.0, p1 = 0.0;
+    // rows l^2 + l + m, m = -l..l, staged [column][row]
 #pragma unroll
-    for (int l = m; l <= L; ++l) {
-      double plm;
-      if (l == m) plm = pmm;
-      else if (l == m + 1) plm = sqrt(2.0 * m + 3.0) * ct * pmm;
-      else {
-        const double aa = sqrt((4.0 * l * l - 1.0) / (double)(l * l - m * m));
-        const double bb = sqrt(((l - 1.0) * (l - 1.0) - (double)(m * m)) / (4.0 * (l - 1.0) * (l - 1.0) - 1.0));
-        plm = aa * (ct * p1 - bb * p2);
-      }
-      p2 = p1;
-      p1 = plm;
-      const double yr = plm * emr, yi = plm * emi;  // Y_{l,m}
-      // row (l, m): conj(Y) * pref ; row (l, -m): conj((-1)^m conj(Y)) * pref = (-1)^m Y * pref
-      const int rp = l * l + l + m;
-      {
-        const double2 va = make_double2(yr * par[l] + yi * pai[l], yr * pai[l] + (-yi) * par[l]);
-        const double2 vb = make_double2(yr * pbr[l] + yi * pbi[l], yr * pbi[l] + (-yi) * pbr[l]);
-        colA[rp] = va;
-        colB[rp] = vb;
-        if (colS) colS[rp] = make_double2(vb.x * wn[l], vb.y * wn[l]);
-      }
+    for (int m = 0; m <= l; ++m) {
+      const double yr = pl[m] * emr[m], yi = pl[m] * emi[m];  // Y_{l,m}
+      sA[threadIdx.x * S + l + m] =
+          make_double2(yr * par + yi * pai, yr * pai + (-yi) * par);
+      sB[threadIdx.x * S + l + m] =
+          make_double2(yr * pbr + yi * pbi, yr * pbi + (-yi) * pbr);
       if (m > 0) {
         const double sg = (m & 1) ? -1.0 : 1.0;
-        const double zr = sg * yr, zi = -(sg * yi);  // (-1)^m conj(Y_{l,m}) = Y_{l,-m}
-        const int rm = l * l + l - m;
-        const double2 va = make_double2(zr * par[l] + zi * pai[l], zr * pai[l] + (-zi) * par[l]);
-        const double2 vb = make_double2(zr * pbr[l] + zi * pbi[l], zr * pbi[l] + (-zi) * pbr[l]);
-        colA[rm] = va;
-        colB[rm] = vb;
-        if (colS) colS[rm] = make_double2(vb.x * wn[l], vb.y * wn[l]);
+        const double qr = sg * yr, qi = -(sg * yi);  // Y_{l,-m} = (-1)^m conj(Y_{l,m})
+        sA[threadIdx.x * S + l - m] =
+            make_double2(qr * par + qi * pai, qr * pai + (-qi) * par);
+        sB[threadIdx.x * S + l - m] =
+            make_double2(qr * pbr + qi * pbi, qr * pbi + (-qi) * pbr);
       }
     }
+#pragma unroll
+    for (int m = 0; m <= l; ++m) { p2[m] = p1[m]; p1[m] = pl[m]; }
+    __syncthreads();
+    // coalesced write-out of this l block: element e -> (column e / h, row e % h)
+    const int h = 2 * l + 1;
+    const double wl = rad[5 * l + 4];
+    const int ncol = min(kAbThreads, p.n_basis - t0);
+    for (int e = threadIdx.x; e < ncol * h; e += kAbThreads) {
+      const int col = e / h, r = e - col * h;
+      const long long gidx = (long long)(t0 + col) * p.ld + off + l * l + r;
+      const double2 va = sA[col * S + r];
+      const double2 vb = sB[col * S + r];
+      p.A[gidx] = va;
+      p.B[gidx] = vb;
+      if (p.Bs) p.Bs[gidx] = make_double2(vb.x * wl, vb.y * wl);
+    }
+    __syncthreads();
   }
+  (void)live;
 }
 
 template <int L>
 int launch_ab_l(hsdla_ctx* ctx, const AbParams& p, const int* atoms_dev, const long long* off_dev,
                 int count) {
-  dim3 grid((p.n_basis + 127) / 128, count);
-  ab_kernel<L><<<grid, 128, 0, ctx->stream>>>(p, atoms_dev, off_dev);
+  constexpr int S = 2 * L + 1;
+  const size_t smem = size_t(2) * kAbThreads * S * sizeof(double2);
+  static bool attr = false;
+  if (!attr && smem > 48 * 1024) {
+    HS_CUDA(cudaFuncSetAttribute(ab_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  dim3 grid((p.n_basis + kAbThreads - 1) / kAbThreads, count);
+  ab_kernel<L><<<grid, kAbThreads, smem, ctx->stream>>>(p, atoms_dev, off_dev);
   HS_CHECK_LAUNCH();
   return HSDLA_OK;
 }
@@ -266,7 +299,34 @@ __global__ void udot_rows_kernel(const double* __restrict__ radial, int stride, 
 
 }  // namespace
 
+int upload_ylm_tables() {
+  static bool done[64] = {};
+  int dev = 0;
+  HS_CUDA(cudaGetDevice(&dev));
+  if (dev < 64 && done[dev]) return HSDLA_OK;
+  double sect[kL] = {}, sub[kL] = {}, a[kL][kL] = {}, b[kL][kL] = {};
+  for (int m = 0; m < kL; ++m) {
+    if (m > 0) sect[m] = std::sqrt((2 * m + 1) / (2.0 * m));
+    sub[m] = std::sqrt(2 * m + 3.0);
+    for (int l = m + 2; l < kL; ++l) {
+      a[l][m] = std::sqrt((4.0 * l * l - 1.0) / (double)(l * l - m * m));
+      const double lm1 = l - 1.0;
+      b[l][m] = std::sqrt((lm1 * lm1 - (double)(m * m)) / (4.0 * (lm1 * lm1) - 1.0));
+    }
+  }
+  HS_CUDA(cudaMemcpyToSymbol(c_sect, sect, sizeof(sect)));
+  HS_CUDA(cudaMemcpyToSymbol(c_sub, sub, sizeof(sub)));
+  HS_CUDA(cudaMemcpyToSymbol(c_a, a, sizeof(a)));
+  HS_CUDA(cudaMemcpyToSymbol(c_b, b, sizeof(b)));
+  if (dev < 64) done[dev] = true;
+  return HSDLA_OK;
+}
+
 int ab_generate(hsdla_ctx* ctx, const hsdla_ab_args* args) {
+  {
+    int rc0 = upload_ylm_tables();
+    if (rc0) return rc0;
+  }
   if (args->n_atoms < 1) return -1;
   if (args->n_basis < 1) return -1;
   for (int a = 0; a < args->n_atoms; ++a)

@@ -98,10 +98,13 @@ Prob make_prob(double2* C, long long ldC, int m, int n, int kind, int seg0, int 
   return p;
 }
 
-Seg make_seg(const double2* P, long long ldP, const double2* Q, long long ldQ, int k) {
+Seg make_seg(const double2* P, long long ldP, const double2* Q, long long ldQ, int k,
+             const double2* P_alt = nullptr, const int* sel = nullptr) {
   Seg s;
   s.P = P;
   s.Q = Q;
+  s.P_alt = P_alt;
+  s.sel = sel;
   s.ldP = ldP;
   s.ldQ = ldQ;
   s.k = k;
@@ -129,6 +132,9 @@ int hsdla_ctx_create(hsdla_ctx** out, void* stream) {
   HS_CUDA(cudaHostAlloc(&c->scratch_host, 256 * sizeof(int), cudaHostAllocDefault));
   for (auto& e : c->ev) HS_CUDA(cudaEventCreate(&e));
   HS_CUDA(cudaEventCreateWithFlags(&c->stage_done, cudaEventDisableTiming));
+  HS_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  HS_CUDA(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
+  HS_CUDA(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
   *out = c;
   return HSDLA_OK;
 }
@@ -140,8 +146,14 @@ int hsdla_ctx_destroy(hsdla_ctx* c) {
   if (c->stage_host) cudaFreeHost(c->stage_host);
   if (c->scratch_dev) cudaFree(c->scratch_dev);
   if (c->scratch_host) cudaFreeHost(c->scratch_host);
+  cudaStreamSynchronize(c->side);
   for (auto& e : c->ev) cudaEventDestroy(e);
   cudaEventDestroy(c->stage_done);
+  cudaEventDestroy(c->fork);
+  cudaEventDestroy(c->join);
+  cudaStreamDestroy(c->side);
+  if (c->partials) cudaFree(c->partials);
+  if (c->ready) cudaFree(c->ready);
   delete c;
   return HSDLA_OK;
 }
@@ -177,7 +189,7 @@ int hsdla_herk_lower(hsdla_ctx* ctx, int n, int k, const hsdla_c64* A, int64_t l
   std::lock_guard<std::mutex> lk(g_api_mutex);
   std::vector<Seg> segs{make_seg(D2(A), lda, D2(A), lda, k)};
   std::vector<Prob> probs{make_prob(D2(C), ldc, n, n, PROB_TRI_LOWER, 0, 1, 1)};
-  return launch_contract(ctx, probs, segs, 0, flag_slot(ctx, 0));
+  return launch_contract(ctx, probs, segs, flag_slot(ctx, 0));
 }
 
 int hsdla_her2k_lower(hsdla_ctx* ctx, int n, int k, const hsdla_c64* X, int64_t ldx,
@@ -189,7 +201,7 @@ int hsdla_her2k_lower(hsdla_ctx* ctx, int n, int k, const hsdla_c64* X, int64_t 
   std::lock_guard<std::mutex> lk(g_api_mutex);
   std::vector<Seg> segs{make_seg(D2(X), ldx, D2(B), ldb, k), make_seg(D2(B), ldb, D2(X), ldx, k)};
   std::vector<Prob> probs{make_prob(D2(C), ldc, n, n, PROB_TRI_LOWER, 0, 2, 1)};
-  return launch_contract(ctx, probs, segs, 0, flag_slot(ctx, 0));
+  return launch_contract(ctx, probs, segs, flag_slot(ctx, 0));
 }
 
 int hsdla_gemm(hsdla_ctx* ctx, int conj_a, int m, int n, int k, hsdla_c64 alpha,
@@ -216,7 +228,7 @@ int hsdla_gemm(hsdla_ctx* ctx, int conj_a, int m, int n, int k, hsdla_c64 alpha,
   p.beta = mk(beta);
   p.accumulate = (beta.re != 0.0 || beta.im != 0.0) ? 1 : 0;
   std::vector<Prob> probs{p};
-  return launch_contract(ctx, probs, segs, 0, flag_slot(ctx, 0));
+  return launch_contract(ctx, probs, segs, flag_slot(ctx, 0));
 }
 
 int hsdla_hemm_lower(hsdla_ctx* ctx, int m, int n, hsdla_c64 alpha, const hsdla_c64* T,
@@ -235,7 +247,7 @@ int hsdla_hemm_lower(hsdla_ctx* ctx, int m, int n, hsdla_c64 alpha, const hsdla_
   p.alpha = mk(alpha);
   p.beta = make_double2(1.0, 0.0);
   std::vector<Prob> probs{p};
-  return launch_contract(ctx, probs, segs, 0, flag_slot(ctx, 0));
+  return launch_contract(ctx, probs, segs, flag_slot(ctx, 0));
 }
 
 int hsdla_trmm_lower(hsdla_ctx* ctx, int conj_l, int m, int n, const hsdla_c64* L, int64_t ldl,
@@ -252,7 +264,7 @@ int hsdla_trmm_lower(hsdla_ctx* ctx, int conj_l, int m, int n, const hsdla_c64* 
   if (rc) return rc;
   std::vector<Seg> segs{make_seg(D2(workspace), m, D2(A), lda, m)};
   std::vector<Prob> probs{make_prob(D2(Y), ldy, m, n, PROB_GENERAL, 0, 1, 0)};
-  return launch_contract(ctx, probs, segs, 0, flag_slot(ctx, 0));
+  return launch_contract(ctx, probs, segs, flag_slot(ctx, 0));
 }
 
 int hsdla_potrf_lower_batched(hsdla_ctx* ctx, int n, int batch, const hsdla_c64* T, int64_t ldt,
@@ -346,10 +358,13 @@ size_t hsdla_build_workspace_size(const hsdla_build_args* args) {
   return ws_layout(args).total;
 }
 
-int hsdla_build_hs(hsdla_ctx* ctx, const hsdla_build_args* a, hsdla_build_result* res) {
-  if (!ctx) return -1;
-  if (!a) return -2;
-  if (!res) return -3;
+namespace {
+// The composed build (builder.py:403-474) with an optional fused A/B generation
+// (flapw.py:201-233).  Everything is enqueued without a host round trip: the per-T-set
+// Cholesky info selects the HPD / general operands on the device (Seg::sel), and is read
+// back together with the non-finite flag after the last kernel.
+int run_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args* ab,
+              hsdla_build_result* res) {
   const int na = a->n_atoms, n = a->n_basis;
   if (na < 1 || n < 1) return -2;
   for (int i = 0; i < na; ++i) {
@@ -364,7 +379,6 @@ int hsdla_build_hs(hsdla_ctx* ctx, const hsdla_build_args* a, hsdla_build_result
     set_error("workspace too small");
     return -2;
   }
-  std::lock_guard<std::mutex> lk(g_api_mutex);
   char* ws = static_cast<char*>(a->workspace);
   const long long ld = a->ld;
   const long long R = w.R;
@@ -380,18 +394,28 @@ int hsdla_build_hs(hsdla_ctx* ctx, const hsdla_build_args* a, hsdla_build_result
   const bool sharded = a->n_shards > 1;
   int* flag = flag_slot(ctx, 2);
   cudaEvent_t* ev = ctx->ev;
+  int rc;
 
   HS_CUDA(cudaEventRecord(ev[0], ctx->stream));
   HS_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
-  HS_CUDA(cudaMemcpyAsync(tdim_dev, a->t_dim, a->n_tsets * sizeof(int), cudaMemcpyHostToDevice,
-                          ctx->stream));
-  int rc = launch_tprep(ctx, a->n_tsets, tdim_dev, mp, D2(a->t_aa), D2(a->t_ab), D2(a->t_bb),
-                        a->t_ld, forms, a->force_general_path ? 0 : 1, info_dev);
+  rc = arena_begin(ctx, a->n_tsets * sizeof(int) + 64);
   if (rc) return rc;
-  int* info_host = ctx->scratch_host + 128;
-  HS_CUDA(cudaMemcpyAsync(info_host, info_dev, a->n_tsets * sizeof(int), cudaMemcpyDeviceToHost,
+  const int* tdim_src = static_cast<const int*>(arena_push(ctx, a->t_dim, a->n_tsets * sizeof(int), nullptr));
+  rc = arena_flush(ctx);
+  if (rc) return rc;
+  HS_CUDA(cudaMemcpyAsync(tdim_dev, tdim_src, a->n_tsets * sizeof(int), cudaMemcpyDeviceToDevice,
                           ctx->stream));
-  HS_CUDA(cudaEventRecord(ev[5], ctx->stream));
+  // T preparation + Cholesky on the side stream, overlapping A/B generation.
+  HS_CUDA(cudaEventRecord(ctx->fork, ctx->stream));
+  HS_CUDA(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));
+  rc = launch_tprep(ctx, ctx->side, a->n_tsets, tdim_dev, mp, D2(a->t_aa), D2(a->t_ab), D2(a->t_bb),
+                    a->t_ld, forms, a->force_general_path ? 0 : 1, info_dev);
+  if (rc) return rc;
+  HS_CUDA(cudaEventRecord(ctx->join, ctx->side));
+  if (ab) {
+    rc = ab_generate(ctx, ab);
+    if (rc) return rc;
+  }
   const double2* Bs = D2(a->B_scaled);
   if (!Bs) {
     double2* bs = reinterpret_cast<double2*>(ws + w.bs);
@@ -401,6 +425,7 @@ int hsdla_build_hs(hsdla_ctx* ctx, const hsdla_build_args* a, hsdla_build_result
     if (rc) return rc;
     Bs = bs;
   }
+  HS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join, 0));
   HS_CUDA(cudaEventRecord(ev[1], ctx->stream));
 
   // Column-panel ownership for sharded runs (balanced pairs j <-> nb-1-j).
@@ -424,26 +449,11 @@ int hsdla_build_hs(hsdla_ctx* ctx, const hsdla_build_args* a, hsdla_build_result
     std::vector<Seg> segs{make_seg(A, ld, A, ld, (int)R), make_seg(Bs, ld, Bs, ld, (int)R)};
     std::vector<Prob> probs;
     add_tri(probs, D2(a->S), 0, 2);
-    rc = launch_contract(ctx, probs, segs, 1, flag);
+    rc = launch_contract(ctx, probs, segs, flag);
     if (rc) return rc;
   }
   HS_CUDA(cudaEventRecord(ev[2], ctx->stream));
 
-  // ---- HPD dispatch needs the Cholesky info (ready long before S finishes)
-  HS_CUDA(cudaEventSynchronize(ev[5]));
-  std::vector<int> hpd(na, 0);
-  for (int t = 0; t < a->n_tsets; ++t) {
-    if (res->chol_info) res->chol_info[t] = info_host[t];
-    if (!a->force_general_path && info_host[t] == -1) {
-      set_error("NaN in the lower triangle of a T_AA block (Cholesky input)");
-      HS_CUDA(cudaStreamSynchronize(ctx->stream));
-      return HSDLA_ERR_NAN_INPUT;
-    }
-  }
-  for (int i = 0; i < na; ++i) {
-    hpd[i] = (!a->force_general_path && info_host[a->t_index[i]] == 0) ? 1 : 0;
-    if (res->hpd_mask) res->hpd_mask[i] = hpd[i];
-  }
   // Rows of a block beyond its T size must be zero in Z / XY (builder.py:232-245 compaction).
   for (int i = 0; i < na; ++i) {
     const int m = a->t_dim[a->t_index[i]], h = a->heights[i];
@@ -454,7 +464,6 @@ int hsdla_build_hs(hsdla_ctx* ctx, const hsdla_build_args* a, hsdla_build_result
       if (rc) return rc;
     }
   }
-
   // ---- Z_a = T_AB^H A_a + 1/2 T_BB B_a   (builder.py:231-240)
   {
     std::vector<Seg> segs;
@@ -468,49 +477,67 @@ int hsdla_build_hs(hsdla_ctx* ctx, const hsdla_build_args* a, hsdla_build_result
       segs.push_back(make_seg(f + fs, mp, B + off, ld, m));
       probs.push_back(make_prob(Z + off, ld, m, n, PROB_GENERAL, s0, 2, 0));
     }
-    rc = launch_contract(ctx, probs, segs, 2, flag);
+    rc = launch_contract(ctx, probs, segs, flag);
     if (rc) return rc;
   }
   HS_CUDA(cudaEventRecord(ev[3], ctx->stream));
-  // ---- Y_a = C_a^H A_a (HPD) or X_a = T_AA A_a (builder.py:279-304)
+  // ---- Y_a = C_a^H A_a if T_AA is HPD, else X_a = T_AA A_a (builder.py:279-304);
+  //      the branch is taken on the device from the Cholesky info.
   {
     std::vector<Seg> segs;
     std::vector<Prob> probs;
     for (int i = 0; i < na; ++i) {
       const int ts = a->t_index[i], m = a->t_dim[ts];
       const long long off = a->row_offset[i];
-      const double2* f = forms + (long long)ts * 4 * fs + (hpd[i] ? 3 : 2) * fs;
+      const double2* f = forms + (long long)ts * 4 * fs;
       const int s0 = (int)segs.size();
-      segs.push_back(make_seg(f, mp, A + off, ld, m));
+      segs.push_back(make_seg(f + 3 * fs, mp, A + off, ld, m, f + 2 * fs, info_dev + ts));
       probs.push_back(make_prob(XY + off, ld, m, n, PROB_GENERAL, s0, 1, 0));
     }
-    rc = launch_contract(ctx, probs, segs, 3, flag);
+    rc = launch_contract(ctx, probs, segs, flag);
     if (rc) return rc;
   }
   HS_CUDA(cudaEventRecord(ev[4], ctx->stream));
   // ---- H = Z^H B + B^H Z + sum_HPD Y^H Y + sum_nonHPD A^H X   (builder.py:246-247, :305-311)
+  //      AA segments per run of atoms sharing one T set: P = XY (HPD) or A (general).
   {
     std::vector<Seg> segs{make_seg(Z, ld, B, ld, (int)R), make_seg(B, ld, Z, ld, (int)R)};
     int i = 0;
     while (i < na) {
       int j = i;
       long long rows = 0;
-      while (j < na && hpd[j] == hpd[i]) { rows += a->heights[j]; ++j; }
+      const int ts = a->t_index[i];
+      while (j < na && a->t_index[j] == ts && (j == i || a->row_offset[j] == a->row_offset[j - 1] + a->heights[j - 1])) {
+        rows += a->heights[j];
+        ++j;
+      }
       const long long off = a->row_offset[i];
-      if (hpd[i]) segs.push_back(make_seg(XY + off, ld, XY + off, ld, (int)rows));
-      else segs.push_back(make_seg(A + off, ld, XY + off, ld, (int)rows));
+      segs.push_back(make_seg(XY + off, ld, XY + off, ld, (int)rows, A + off, info_dev + ts));
       i = j;
     }
     std::vector<Prob> probs;
     add_tri(probs, D2(a->H), 0, (int)segs.size());
-    rc = launch_contract(ctx, probs, segs, 4, flag);
+    rc = launch_contract(ctx, probs, segs, flag);
     if (rc) return rc;
   }
   HS_CUDA(cudaEventRecord(ev[6], ctx->stream));
+  int* info_host = ctx->scratch_host + 128;
+  HS_CUDA(cudaMemcpyAsync(info_host, info_dev, a->n_tsets * sizeof(int), cudaMemcpyDeviceToHost,
+                          ctx->stream));
   HS_CUDA(cudaMemcpyAsync(ctx->scratch_host + 2, flag, sizeof(int), cudaMemcpyDeviceToHost,
                           ctx->stream));
   HS_CUDA(cudaEventRecord(ev[7], ctx->stream));
   HS_CUDA(cudaEventSynchronize(ev[7]));
+
+  bool nan_input = false;
+  for (int t = 0; t < a->n_tsets; ++t) {
+    if (res->chol_info) res->chol_info[t] = info_host[t];
+    if (!a->force_general_path && info_host[t] == -1) nan_input = true;
+  }
+  for (int i = 0; i < na; ++i) {
+    const int hpd = (!a->force_general_path && info_host[a->t_index[i]] == 0) ? 1 : 0;
+    if (res->hpd_mask) res->hpd_mask[i] = hpd;
+  }
   res->nonfinite = ctx->scratch_host[2];
   float t01 = 0, t12 = 0, t23 = 0, t34 = 0, t46 = 0;
   cudaEventElapsedTime(&t01, ev[0], ev[1]);
@@ -526,11 +553,34 @@ int hsdla_build_hs(hsdla_ctx* ctx, const hsdla_build_args* a, hsdla_build_result
   res->ms_contract_H = t46;
   res->ms_apply_Z = t23;
   res->ms_apply_XY = t34;
+  if (nan_input) {
+    set_error("NaN in the lower triangle of a T_AA block (Cholesky input)");
+    return HSDLA_ERR_NAN_INPUT;
+  }
   if (res->nonfinite) {
     set_error("accumulator contains non-finite values");
     return HSDLA_ERR_NONFINITE;
   }
   return HSDLA_OK;
+}
+}  // namespace
+
+int hsdla_build_hs(hsdla_ctx* ctx, const hsdla_build_args* a, hsdla_build_result* res) {
+  if (!ctx) return -1;
+  if (!a) return -2;
+  if (!res) return -3;
+  std::lock_guard<std::mutex> lk(g_api_mutex);
+  return run_build(ctx, a, nullptr, res);
+}
+
+int hsdla_setup_hs(hsdla_ctx* ctx, const hsdla_ab_args* ab, const hsdla_build_args* a,
+                   hsdla_build_result* res) {
+  if (!ctx) return -1;
+  if (!ab) return -2;
+  if (!a) return -3;
+  if (!res) return -4;
+  std::lock_guard<std::mutex> lk(g_api_mutex);
+  return run_build(ctx, a, ab, res);
 }
 
 }  // extern "C"

@@ -27,9 +27,14 @@ void set_error(const std::string& msg);
 
 // One K-segment of a contraction: C += P^H Q over k rows.  P and Q are column-major
 // complex128 with leading dims ldP / ldQ (elements); column c of P starts at P + c*ldP.
+// `sel`/`P_alt`: device-side branch selection without a host round trip — when `sel` is
+// non-null and *sel != 0 (the T set's Cholesky info: not HPD, or forced general path) the
+// segment reads P_alt instead of P (builder.py:284-302 per-atom HPD dispatch).
 struct Seg {
   const double2* P;
   const double2* Q;
+  const double2* P_alt;
+  const int* sel;
   long long ldP, ldQ;
   int k;
   int pad_;
@@ -49,9 +54,10 @@ struct Prob {
   int seg0, nseg;
   int accumulate;
   int tiles_m, tiles_n;  // tile grid (tri: tiles_m == tiles_n)
-  int tile_base;         // first global tile index of this problem
+  int ntiles;            // tiles of this problem
+  int nchunks;           // K chunks per tile (all tiles of a problem share the segments)
+  long long it_base;     // first stream-K iteration (tile-chunk) of this problem
   int col_tile_lo, col_tile_hi;  // tri only: restrict to tile columns [lo, hi) (sharding)
-  int pad_;
   double2 alpha, beta;
 };
 
@@ -66,8 +72,14 @@ struct Arena;  // descriptor staging (defined in capi.cu)
 
 struct hsdla_ctx {
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // T preparation overlaps A/B generation here
+  cudaEvent_t fork = nullptr, join = nullptr;
   int device = 0;
   int num_sms = 148;
+  // stream-K fix-up workspace: per-CTA partial tiles and ready flags
+  double* partials = nullptr;
+  int* ready = nullptr;
+  int partial_slots = 0;
   // Device descriptor arena and its pinned host staging twin.
   char* desc_dev = nullptr;
   char* stage_host = nullptr;
@@ -85,7 +97,7 @@ namespace hsdla {
 // Contraction launcher: uploads problems/segments through the ctx arena and launches
 // the persistent DMMA kernel.  `counter_slot` picks the tile counter to use.
 int launch_contract(hsdla_ctx* ctx, const std::vector<Prob>& probs,
-                    const std::vector<Seg>& segs, int counter_slot, int* flag_dev);
+                    const std::vector<Seg>& segs, int* flag_dev);
 // Arena helpers.
 int arena_begin(hsdla_ctx* ctx, size_t bytes);
 void* arena_push(hsdla_ctx* ctx, const void* src, size_t bytes, void** host_ptr);
@@ -99,9 +111,10 @@ int launch_prep(hsdla_ctx* ctx, int op, int rows, int cols, const double2* in, l
 int launch_potrf_batched(hsdla_ctx* ctx, int n, int batch, const double2* T, long long ldt,
                          long long stride_t, double2* F, long long ldf, long long stride_f,
                          int* info_dev);
-int launch_tprep(hsdla_ctx* ctx, int n_tsets, const int* tdim_dev, int mp,
+int launch_tprep(hsdla_ctx* ctx, cudaStream_t stream, int n_tsets, const int* tdim_dev, int mp,
                  const double2* taa, const double2* tab, const double2* tbb, long long t_ld,
                  double2* forms, int do_chol, int* info_dev);
+int ab_generate(hsdla_ctx* ctx, const hsdla_ab_args* args);
 int launch_mirror(hsdla_ctx* ctx, int n, double2* C, long long ldc, int* flag_dev);
 int launch_scale_rows(hsdla_ctx* ctx, int m, int n, const double* d, double2* B, long long ldb);
 int launch_zero_rows(hsdla_ctx* ctx, double2* base, long long ld, int row0, int rows, int cols);

@@ -19,10 +19,14 @@
 // CTA: 128 threads = 2x2 warps, 64x64 complex output tile, each warp 32x32 complex
 // (16 DMMA blocks for Re + 16 for Im).  K is staged in chunks of 16 complex (256 B per
 // column) through a 3-stage cp.async ring, 32-byte XOR swizzle (conflict-free fragment
-// loads).  Persistent grid with an atomic tile counter; results are deterministic because
-// each tile is owned by one CTA and its K order is fixed.
+// loads).  Work distribution is stream-K: the (tile, K-chunk) iteration space of all
+// problems is cut into equal contiguous ranges, one per co-resident CTA (cooperative
+// launch), so there is no wave-quantisation tail.  A tile split between CTAs is finished
+// by the CTA holding its first chunk, which adds the later pieces' partial tiles in a fixed
+// order: results are deterministic run to run (builder.py backup invariance).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -30,13 +34,24 @@ namespace hsdla {
 
 namespace {
 
-constexpr int kThreads = 128;
 constexpr int kStages = 3;
-constexpr int kChunk = 16;                     // complex K per stage
-constexpr int kColDoubles = 2 * kChunk;        // 32 doubles per column per stage
+constexpr int kChunk = 16;                       // complex K per stage
+constexpr int kColDoubles = 2 * kChunk;          // 32 doubles per column per stage
 constexpr int kOpDoubles = kTile * kColDoubles;  // 2048 doubles = 16 KB per operand
 constexpr int kStageDoubles = 2 * kOpDoubles;
 constexpr size_t kSmemBytes = size_t(kStages) * kStageDoubles * sizeof(double);
+constexpr int kPartialDoubles = kTile * kTile * 2;  // one partial tile (64 KB)
+
+struct SKParams {
+  const Prob* probs;
+  const Seg* segs;
+  long long total_it;
+  int nprob;
+  int grid;
+  double* partials;
+  int* ready;
+  int* flag;
+};
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -55,15 +70,28 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-__device__ __forceinline__ bool finite2(double2 v) {
-  return isfinite(v.x) && isfinite(v.y);
+__device__ __forceinline__ bool finite2(double2 v) { return isfinite(v.x) && isfinite(v.y); }
+
+__device__ __forceinline__ long long range_start(long long total, int grid, int g) {
+  return total * g / grid;
 }
 
-__global__ void __launch_bounds__(kThreads, 2)
-    contract_kernel(const Prob* __restrict__ probs, int nprob, const Seg* __restrict__ segs,
-                    int ntiles, int* __restrict__ counter, int* __restrict__ flag) {
+__device__ __forceinline__ Seg load_seg(const Seg* s) {
+  Seg v = *s;
+  if (v.sel && *v.sel != 0) v.P = v.P_alt;
+  return v;
+}
+
+// JB = 8-column DMMA blocks per warp along n: JB = 4 -> warp tile 32x32 complex, 4 warps
+// (128 threads, ~250 registers, 2 warps per SM sub-partition); JB = 2 -> warp tile 32x16,
+// 8 warps (256 threads, <= 128 registers, 4 warps per sub-partition).
+template <int JB>
+__global__ void __launch_bounds__(32 * 2 * (8 / JB), 2) contract_kernel(SKParams sk) {
   extern __shared__ __align__(128) double smem[];
-  __shared__ int s_tile;
+  constexpr int kWarpCols = 8 * JB;
+  constexpr int kThreads = 32 * 2 * (kTile / kWarpCols);
+  constexpr int kColStep = kThreads / 16;           // columns covered per cp.async round
+  constexpr int kRounds = kTile / kColStep;         // cp.async rounds per operand per chunk
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -71,59 +99,69 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int wm = warp & 1, wn = warp >> 1;
   const int g = lane >> 2, q = lane & 3;
   const unsigned sign_hi = (q & 1) ? 0x80000000u : 0u;
-  // cp.async slot of this thread: complex element lp of the chunk, columns lc + 8r.
+  // cp.async slot of this thread: complex element lp of the chunk, columns lc + kColStep*r.
   const int lp = tid & 15;
   const int lc = tid >> 4;
-  const int dst_lane = (((lp >> 1) ^ lc) << 2) + (lp & 1) * 2;  // within a column (doubles)
+  const int dst_lane = (((lp >> 1) ^ (lc & 7)) << 2) + (lp & 1) * 2;  // within a column (doubles)
 
-  for (;;) {
-    if (tid == 0) s_tile = atomicAdd(counter, 1);
-    __syncthreads();
-    const int t = s_tile;
-    __syncthreads();
-    if (t >= ntiles) break;
+  const int cta = blockIdx.x;
+  long long it = range_start(sk.total_it, sk.grid, cta);
+  const long long it_end = range_start(sk.total_it, sk.grid, cta + 1);
 
-    int lo = 0, hi = nprob - 1;
+  while (it < it_end) {
+    // ---- locate (problem, tile, chunk range) of the next piece
+    int lo = 0, hi = sk.nprob - 1;
     while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (probs[mid].tile_base <= t) lo = mid; else hi = mid - 1;
+      const int mid = (lo + hi + 1) >> 1;
+      if (sk.probs[mid].it_base <= it) lo = mid; else hi = mid - 1;
     }
-    const Prob pr = probs[lo];
-    int local = t - pr.tile_base;
+    const Prob pr = sk.probs[lo];
+    const long long local = it - pr.it_base;
+    const int nch = pr.nchunks;
+    int tile = (int)(local / nch);
+    const int c_lo = (int)(local - (long long)tile * nch);
+    const long long left = it_end - it;
+    const int c_hi = (left < (long long)(nch - c_lo)) ? c_lo + (int)left : nch;
+    const long long tile_it_end = pr.it_base + (long long)(tile + 1) * nch;
     int tm, tn;
     if (pr.kind == PROB_GENERAL) {
-      tm = local % pr.tiles_m;
-      tn = local / pr.tiles_m;
+      tm = tile % pr.tiles_m;
+      tn = tile / pr.tiles_m;
     } else {
       const int nb = pr.tiles_m;
       tn = pr.col_tile_lo;
-      while (local >= nb - tn) { local -= nb - tn; ++tn; }
-      tm = tn + local;
+      while (tile >= nb - tn) { tile -= nb - tn; ++tn; }
+      tm = tn + tile;
     }
     const int i0 = tm * kTile, j0 = tn * kTile;
     const int mP = pr.m, mQ = pr.n;
 
-    // Count chunks of this problem and find the first non-empty segment.
-    int nchunks = 0;
-    for (int s = 0; s < pr.nseg; ++s) nchunks += (segs[pr.seg0 + s].k + kChunk - 1) / kChunk;
-
+    // ---- position the issue iterator at chunk c_lo
     int isi = pr.seg0;
     const int send = pr.seg0 + pr.nseg;
-    while (isi < send && segs[isi].k <= 0) ++isi;
-    Seg cur;
-    if (isi < send) cur = segs[isi];
     int iko = 0;
+    {
+      int cb = 0;
+      for (; isi < send; ++isi) {
+        const int ncs = (sk.segs[isi].k + kChunk - 1) / kChunk;
+        if (c_lo < cb + ncs) { iko = (c_lo - cb) * kChunk; break; }
+        cb += ncs;
+      }
+    }
+    Seg cur;
+    if (isi < send) cur = load_seg(sk.segs + isi);
+    else { cur = load_seg(sk.segs + pr.seg0); cur.k = 0; }
 
     auto issue = [&](int stage) {
       double* sP = smem + stage * kStageDoubles;
       double* sQ = sP + kOpDoubles;
       const bool kval = (iko + lp) < cur.k;
 #pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        const int col = lc + 8 * r;
+      for (int r = 0; r < kRounds; ++r) {
+        const int col = lc + kColStep * r;
         const int gp = i0 + col;
         const bool vp = kval && gp < mP;
-        const double2* srcp = vp ? cur.P + (long long)gp * cur.ldP + iko + lp : cur.P;
+        const double2* srcp = vp ? cur.P + (long long)gp * cur.ldP + iko + lp : cur.Q;
         cp_async16(sP + col * kColDoubles + dst_lane, srcp, vp ? 16 : 0);
         const int gq = j0 + col;
         const bool vq = kval && gq < mQ;
@@ -132,22 +170,26 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
       iko += kChunk;
       if (iko >= cur.k) {
-        iko = 0;
-        ++isi;
-        while (isi < send && segs[isi].k <= 0) ++isi;
-        if (isi < send) cur = segs[isi];
+        int nx = isi + 1;
+        while (nx < send && sk.segs[nx].k <= 0) ++nx;
+        if (nx < send) {
+          isi = nx;
+          iko = 0;
+          cur = load_seg(sk.segs + isi);
+        }
       }
     };
 
-    double accR[4][4][2], accI[4][4][2];
+    double accR[4][JB][2], accI[4][JB][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
+      for (int b = 0; b < JB; ++b) {
         accR[a][b][0] = accR[a][b][1] = 0.0;
         accI[a][b][0] = accI[a][b][1] = 0.0;
       }
 
+    const int nchunks = c_hi - c_lo;
 #pragma unroll
     for (int st = 0; st < kStages - 1; ++st) {
       if (st < nchunks) issue(st);
@@ -164,15 +206,15 @@ __global__ void __launch_bounds__(kThreads, 2)
       const double* sP = smem + (c % kStages) * kStageDoubles;
       const double* sQ = sP + kOpDoubles;
       const double* pa = sP + (wm * 32 + g) * kColDoubles;
-      const double* pb = sQ + (wn * 32 + g) * kColDoubles;
+      const double* pb = sQ + (wn * kWarpCols + g) * kColDoubles;
 #pragma unroll
       for (int s = 0; s < 8; ++s) {
         const int off = ((s ^ g) << 2);
-        double a[4], br[4], bi[4];
+        double a[4], br[JB], bi[JB];
 #pragma unroll
         for (int ib = 0; ib < 4; ++ib) a[ib] = pa[ib * 8 * kColDoubles + off + q];
 #pragma unroll
-        for (int jb = 0; jb < 4; ++jb) {
+        for (int jb = 0; jb < JB; ++jb) {
           br[jb] = pb[jb * 8 * kColDoubles + off + q];
           const double x = pb[jb * 8 * kColDoubles + off + (q ^ 1)];
           bi[jb] = __hiloint2double(__double2hiint(x) ^ sign_hi, __double2loint(x));
@@ -180,7 +222,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
         for (int ib = 0; ib < 4; ++ib)
 #pragma unroll
-          for (int jb = 0; jb < 4; ++jb) {
+          for (int jb = 0; jb < JB; ++jb) {
             dmma(accR[ib][jb][0], accR[ib][jb][1], a[ib], br[jb]);
             dmma(accI[ib][jb][0], accI[ib][jb][1], a[ib], bi[jb]);
           }
@@ -188,6 +230,46 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     cp_async_wait<0>();
     __syncthreads();
+    it += nchunks;
+
+    if (c_lo != 0) {
+      // Later piece of a split tile: publish the partial for the tile's finishing CTA.
+      double* slot = sk.partials + (long long)cta * kPartialDoubles;
+      int r = 0;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < JB; ++b)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            __stcg(slot + (r++) * kThreads + tid, accR[a][b][v]);
+            __stcg(slot + (r++) * kThreads + tid, accI[a][b][v]);
+          }
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) atomicExch(sk.ready + cta, 1);
+      continue;
+    }
+    if (c_hi < nch) {
+      // Head piece of a split tile: add the later pieces in CTA order (deterministic).
+      for (int j = cta + 1; j < sk.grid && range_start(sk.total_it, sk.grid, j) < tile_it_end; ++j) {
+        if (tid == 0) {
+          while (atomicAdd(sk.ready + j, 0) == 0) __nanosleep(100);
+        }
+        __syncthreads();
+        const double* slot = sk.partials + (long long)j * kPartialDoubles;
+        int r = 0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < JB; ++b)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              accR[a][b][v] += __ldcg(slot + (r++) * kThreads + tid);
+              accI[a][b][v] += __ldcg(slot + (r++) * kThreads + tid);
+            }
+      }
+    }
 
     // ---- epilogue
     bool bad = false;
@@ -195,10 +277,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int ib = 0; ib < 4; ++ib) {
       const int i = i0 + wm * 32 + ib * 8 + g;
 #pragma unroll
-      for (int jb = 0; jb < 4; ++jb) {
+      for (int jb = 0; jb < JB; ++jb) {
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-          const int j = j0 + wn * 32 + jb * 8 + 2 * q + v;
+          const int j = j0 + wn * kWarpCols + jb * 8 + 2 * q + v;
           double2 val = make_double2(accR[ib][jb][v], accI[ib][jb][v]);
           if (pr.kind == PROB_GENERAL) {
             if (i < pr.m && j < pr.n) {
@@ -236,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
     }
-    if (bad) atomicOr(flag, 1);
+    if (bad) atomicOr(sk.flag, 1);
   }
 }
 
@@ -250,10 +332,11 @@ int prob_tile_count(const Prob& p) {
 }
 
 int launch_contract(hsdla_ctx* ctx, const std::vector<Prob>& probs_in,
-                    const std::vector<Seg>& segs, int counter_slot, int* flag_dev) {
-  std::vector<Prob> probs = probs_in;
-  int ntiles = 0;
-  for (auto& p : probs) {
+                    const std::vector<Seg>& segs, int* flag_dev) {
+  std::vector<Prob> probs;
+  long long total = 0;
+  for (Prob p : probs_in) {
+    if (p.m <= 0 || p.n <= 0) continue;
     p.tiles_m = (p.m + kTile - 1) / kTile;
     p.tiles_n = (p.n + kTile - 1) / kTile;
     if (p.kind != PROB_GENERAL) {
@@ -261,15 +344,39 @@ int launch_contract(hsdla_ctx* ctx, const std::vector<Prob>& probs_in,
       if (p.col_tile_hi <= 0 || p.col_tile_hi > p.tiles_m) p.col_tile_hi = p.tiles_m;
       if (p.col_tile_lo < 0) p.col_tile_lo = 0;
     }
-    p.tile_base = ntiles;
-    ntiles += (p.m > 0 && p.n > 0) ? prob_tile_count(p) : 0;
+    p.ntiles = prob_tile_count(p);
+    int nch = 0;
+    for (int s = 0; s < p.nseg; ++s) nch += (segs[p.seg0 + s].k + kChunk - 1) / kChunk;
+    p.nchunks = nch > 0 ? nch : 1;  // an empty K still visits each tile once (C = beta C)
+    p.it_base = total;
+    total += (long long)p.ntiles * p.nchunks;
+    if (p.ntiles > 0) probs.push_back(p);
   }
-  if (ntiles == 0) return HSDLA_OK;
-  static bool attr_set = false;
-  if (!attr_set) {
-    HS_CUDA(cudaFuncSetAttribute(contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (total == 0) return HSDLA_OK;
+  static int variant = -1;  // warp tile width: HSDLA_WARP_COLS = 32 or 16
+  if (variant < 0) {
+    const char* e = getenv("HSDLA_WARP_COLS");
+    variant = (e && atoi(e) == 32) ? 4 : 2;
+    HS_CUDA(cudaFuncSetAttribute(contract_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kSmemBytes));
-    attr_set = true;
+    HS_CUDA(cudaFuncSetAttribute(contract_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kSmemBytes));
+  }
+  const void* kfn = variant == 4 ? (const void*)contract_kernel<4> : (const void*)contract_kernel<2>;
+  const int kThreads = variant == 4 ? 128 : 256;
+  int occ = 0;
+  HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kThreads, kSmemBytes));
+  if (occ < 1) occ = 1;
+  long long grid_ll = (long long)ctx->num_sms * occ;
+  if (grid_ll > total) grid_ll = total;
+  const int grid = (int)grid_ll;
+  if (ctx->partial_slots < grid) {
+    HS_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->partials) cudaFree(ctx->partials);
+    if (ctx->ready) cudaFree(ctx->ready);
+    HS_CUDA(cudaMalloc(&ctx->partials, size_t(grid) * kPartialDoubles * sizeof(double)));
+    HS_CUDA(cudaMalloc(&ctx->ready, size_t(grid) * sizeof(int)));
+    ctx->partial_slots = grid;
   }
   int rc = arena_begin(ctx, probs.size() * sizeof(Prob) + segs.size() * sizeof(Seg) + 256);
   if (rc) return rc;
@@ -278,17 +385,21 @@ int launch_contract(hsdla_ctx* ctx, const std::vector<Prob>& probs_in,
       arena_push(ctx, segs.data(), (segs.empty() ? 1 : segs.size()) * sizeof(Seg), nullptr));
   rc = arena_flush(ctx);
   if (rc) return rc;
-
-  int* counter = ctx->scratch_dev + counter_slot;
-  HS_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), ctx->stream));
-  int occ = 0;
-  HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, contract_kernel, kThreads, kSmemBytes));
-  if (occ < 1) occ = 1;
-  int grid = ctx->num_sms * occ;
-  if (grid > ntiles) grid = ntiles;
-  contract_kernel<<<grid, kThreads, kSmemBytes, ctx->stream>>>(dprobs, (int)probs.size(), dsegs,
-                                                              ntiles, counter, flag_dev);
-  HS_CHECK_LAUNCH();
+  HS_CUDA(cudaMemsetAsync(ctx->ready, 0, size_t(grid) * sizeof(int), ctx->stream));
+  SKParams sk;
+  sk.probs = dprobs;
+  sk.segs = dsegs;
+  sk.total_it = total;
+  sk.nprob = (int)probs.size();
+  sk.grid = grid;
+  sk.partials = ctx->partials;
+  sk.ready = ctx->ready;
+  sk.flag = flag_dev;
+  void* kargs[] = {&sk};
+  // Cooperative launch guarantees all CTAs are co-resident, which the split-tile
+  // hand-off (a finishing CTA waits for later CTAs' partials) relies on.
+  HS_CUDA(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(kThreads), kargs, kSmemBytes,
+                                      ctx->stream));
   return HSDLA_OK;
 }
 

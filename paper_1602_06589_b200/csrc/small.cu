@@ -87,6 +87,74 @@ __global__ void potrf_batched_kernel(int n, const double2* T, long long ldt, lon
   chol_block(n, T + b * st, ldt, F + b * sf, ldf, info + b);
 }
 
+// Right-looking Cholesky of tril(T) with the lower triangle packed in shared memory
+// (m(m+1)/2 complex: 118 KB at m = 121), used by the build's T preparation.  Same pivot
+// rule as chol_block; writes the factor (zero strict upper) to F.
+__device__ int packed_idx(int i, int k) { return i * (i + 1) / 2 + k; }
+
+__device__ void chol_packed(int n, const double2* __restrict__ T, long long ldt, double2* F,
+                            long long ldf, int* info) {
+  extern __shared__ double2 Lp[];
+  __shared__ int s_bad;
+  __shared__ double s_ljj;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  for (int r = tid; r < n; r += nt)
+    for (int c = 0; c <= r; ++c) {
+      const double2 v = T[r + (long long)c * ldt];
+      if (isnan(v.x) || isnan(v.y)) s_bad = 1;
+      Lp[packed_idx(r, c)] = v;
+    }
+  __syncthreads();
+  if (s_bad) {
+    if (tid == 0) *info = -1;
+    return;
+  }
+  for (int j = 0; j < n; ++j) {
+    if (tid == 0) {
+      const double d = Lp[packed_idx(j, j)].x;
+      if (!(d > 0.0) || !isfinite(d)) {
+        s_bad = j + 1;
+      } else {
+        s_ljj = sqrt(d);
+        Lp[packed_idx(j, j)] = make_double2(s_ljj, 0.0);
+      }
+    }
+    __syncthreads();
+    if (s_bad) {
+      if (tid == 0) *info = s_bad;
+      return;
+    }
+    const double ljj = s_ljj;
+    for (int i = j + 1 + tid; i < n; i += nt) {
+      const double2 v = Lp[packed_idx(i, j)];
+      Lp[packed_idx(i, j)] = make_double2(v.x / ljj, v.y / ljj);
+    }
+    __syncthreads();
+    // trailing update L[i][k] -= L[i][j] conj(L[k][j]), j < k <= i
+    const int rem = n - j - 1;
+    for (int e = tid; e < rem * rem; e += nt) {
+      const int i = j + 1 + e / rem, k = j + 1 + e % rem;
+      if (k > i) continue;
+      const double2 a = Lp[packed_idx(i, j)];
+      const double2 b = Lp[packed_idx(k, j)];
+      double2 v = Lp[packed_idx(i, k)];
+      v.x -= a.x * b.x + a.y * b.y;
+      v.y -= a.y * b.x - a.x * b.y;
+      Lp[packed_idx(i, k)] = v;
+    }
+    __syncthreads();
+  }
+  for (long long e = tid; e < (long long)n * n; e += nt) {
+    const int r = (int)(e % n), c = (int)(e / n);
+    F[r + c * ldf] = (r >= c) ? Lp[packed_idx(r, c)] : make_double2(0.0, 0.0);
+  }
+  if (tid == 0) *info = 0;
+}
+
+constexpr int kPackedMaxN = 168;  // 168*169/2*16 B = 227 KB
+
 // Per T set: forms[0] = T_AB, forms[1] = 1/2 full(T_BB), forms[2] = full(T_AA),
 // forms[3] = Cholesky factor of tril(T_AA) (if do_chol), all m x m with ld mp.
 __global__ void tprep_kernel(const int* tdim, int mp, const double2* taa, const double2* tab,
@@ -111,8 +179,13 @@ __global__ void tprep_kernel(const int* tdim, int mp, const double2* taa, const 
     f[2 * fs + r + (long long)c * mp] = aa;
   }
   __syncthreads();
-  if (do_chol) chol_block(m, Taa, t_ld, f + 3 * fs, mp, info + b);
-  else if (threadIdx.x == 0) info[b] = -2;
+  if (!do_chol) {
+    if (threadIdx.x == 0) info[b] = -2;
+  } else if (m <= kPackedMaxN) {
+    chol_packed(m, Taa, t_ld, f + 3 * fs, mp, info + b);
+  } else {
+    chol_block(m, Taa, t_ld, f + 3 * fs, mp, info + b);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -192,12 +265,16 @@ int launch_potrf_batched(hsdla_ctx* ctx, int n, int batch, const double2* T, lon
   return HSDLA_OK;
 }
 
-int launch_tprep(hsdla_ctx* ctx, int n_tsets, const int* tdim_dev, int mp, const double2* taa,
-                 const double2* tab, const double2* tbb, long long t_ld, double2* forms,
-                 int do_chol, int* info_dev) {
+int launch_tprep(hsdla_ctx* ctx, cudaStream_t stream, int n_tsets, const int* tdim_dev, int mp,
+                 const double2* taa, const double2* tab, const double2* tbb, long long t_ld,
+                 double2* forms, int do_chol, int* info_dev) {
   if (n_tsets <= 0) return HSDLA_OK;
-  tprep_kernel<<<n_tsets, 128, mp * sizeof(double2), ctx->stream>>>(tdim_dev, mp, taa, tab, tbb,
-                                                                     t_ld, forms, do_chol, info_dev);
+  size_t smem = (mp <= kPackedMaxN) ? size_t(mp) * (mp + 1) / 2 * sizeof(double2)
+                                    : size_t(mp) * sizeof(double2);
+  if (smem > 48 * 1024)
+    HS_CUDA(cudaFuncSetAttribute(tprep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  tprep_kernel<<<n_tsets, 512, smem, stream>>>(tdim_dev, mp, taa, tab, tbb, t_ld, forms, do_chol,
+                                               info_dev);
   HS_CHECK_LAUNCH();
   return HSDLA_OK;
 }

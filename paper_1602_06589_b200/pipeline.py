@@ -71,8 +71,10 @@ def pack_tmats(tmats) -> TPack:
 
 
 def build_device(*, n_basis, heights, row_offset, tpack: TPack, A, B, Bs, udot, ld,
-                 force_general_path, H, S, ldh, shard_rank=0, n_shards=1, workspace=None):
-    """Run `hsdla_build_hs` on device buffers; returns (result dict, workspace tensor)."""
+                 force_general_path, H, S, ldh, shard_rank=0, n_shards=1, workspace=None,
+                 ab_args=None):
+    """Run `hsdla_build_hs` (or `hsdla_setup_hs` when `ab_args` is given: A/B generation
+    fused in front) on device buffers; returns (result dict, workspace tensor)."""
     lib = _native.load()
     t = device.require_cuda()
     na = len(heights)
@@ -113,7 +115,11 @@ def build_device(*, n_basis, heights, row_offset, tpack: TPack, A, B, Bs, udot, 
     res = _native.BuildResult()
     res.hpd_mask = mask
     res.chol_info = info
-    rc = lib.hsdla_build_hs(device.ctx(), ctypes.byref(args), ctypes.byref(res))
+    if ab_args is not None:
+        rc = lib.hsdla_setup_hs(device.ctx(), ctypes.byref(ab_args), ctypes.byref(args),
+                                ctypes.byref(res))
+    else:
+        rc = lib.hsdla_build_hs(device.ctx(), ctypes.byref(args), ctypes.byref(res))
     if rc == _native.HSDLA_ERR_NAN_INPUT:
         raise ContractViolationError("NaN in Cholesky input (lower triangle)")
     if rc == _native.HSDLA_ERR_NONFINITE:
@@ -166,9 +172,8 @@ class DeviceSpec:
         self.omega = float(spec.omega)
 
 
-def ab_generate_device(dspec: DeviceSpec, A, B, Bs, ld, udot):
-    """Fused A/B (+ scaled B, + row norms) generation into device buffers."""
-    lib = _native.load()
+def make_ab_args(dspec: DeviceSpec, A, B, Bs, ld, udot) -> "_native.AbArgs":
+    """C argument block of the A/B generator (host arrays stay alive on `dspec`)."""
     args = _native.AbArgs()
     args.n_atoms = dspec.n_atoms
     args.n_basis = dspec.n_basis
@@ -188,6 +193,13 @@ def ab_generate_device(dspec: DeviceSpec, A, B, Bs, ld, udot):
     args.B_scaled = Bs.data_ptr() if Bs is not None else None
     args.ld = ld
     args.udot_norms = udot.data_ptr() if udot is not None else None
+    return args
+
+
+def ab_generate_device(dspec: DeviceSpec, A, B, Bs, ld, udot):
+    """Fused A/B (+ scaled B, + row norms) generation into device buffers."""
+    lib = _native.load()
+    args = make_ab_args(dspec, A, B, Bs, ld, udot)
     _native.check(lib.hsdla_ab_generate(device.ctx(), ctypes.byref(args)), "hsdla_ab_generate")
 
 
@@ -235,13 +247,23 @@ class HSPipeline:
         return res
 
     def run(self, dspec: DeviceSpec, tpack: TPack, force_general_path: bool = False):
-        self.generate(dspec)
-        return self.build(dspec, tpack, force_general_path)
+        """One k-point, spec -> H, S in HBM, as a single native call (`hsdla_setup_hs`)."""
+        if dspec.n_basis > self.n_capacity or dspec.rows != self.rows:
+            raise ContractViolationError("spec shape does not fit the pipeline buffers")
+        self.n_basis = dspec.n_basis
+        ab = make_ab_args(dspec, self.A, self.B, self.Bs, self.ld, None)
+        res, self.workspace = build_device(
+            n_basis=dspec.n_basis, heights=dspec.heights, row_offset=dspec.row_offset, tpack=tpack,
+            A=self.A, B=self.B, Bs=self.Bs, udot=self.udot, ld=self.ld,
+            force_general_path=force_general_path, H=self.H, S=self.S, ldh=self.n_capacity,
+            shard_rank=self.shard_rank, n_shards=self.n_shards, workspace=self.workspace,
+            ab_args=ab)
+        return res
 
     def launches_per_run(self, dspec: DeviceSpec) -> int:
         """Kernels this pipeline launches per k-point (A/B + row-norm kernel per l group,
         T prep, S contraction, Z apply, XY apply, H contraction)."""
-        return 2 * len(np.unique(dspec.l_sph)) + 5
+        return len(np.unique(dspec.l_sph)) + 5
 
     def result_views(self):
         """Host-indexable (n, n) views: H[i, j] == tensor[j, i] (column-major storage)."""

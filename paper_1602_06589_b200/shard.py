@@ -1,0 +1,99 @@
+"""Multi-GPU partitioning of the H/S setup.
+
+Two ways, one process per GPU (torch.distributed, NCCL over NVLink on the box):
+
+* **k-points** — independent; rank r builds k-points r, r+P, ...; no collective in the
+  data path (`kpoints_for_rank`).
+* **column panels of one large k-point** — every rank regenerates A*, B*, Z, XY locally
+  from the tiny spec + T (cheaper than broadcasting GBs), computes the lower tiles of the
+  64-wide column panels it owns (`hsdla_build_args.shard_rank / n_shards`), and the
+  panels are gathered to one consumer rank with point-to-point sends; the consumer writes
+  the Hermitian mirror.  Each tile's full K-sum is local, so no reduction is needed.
+  Panel j and panel nb-1-j form one balanced pair (their lower-triangle tile counts sum
+  to nb+1); pairs are dealt round-robin (`panel_owner`, the same rule as the C ABI's
+  `hsdla_panel_owner`).
+"""
+from __future__ import annotations
+
+PANEL = 64  # column panel width = the contraction tile edge
+
+
+def panel_owner(n_panels: int, n_shards: int, panel: int) -> int:
+    """Owner rank of a column panel (restates `hsdla_panel_owner`, csrc/capi.cu)."""
+    if n_shards <= 1:
+        return 0
+    return min(panel, n_panels - 1 - panel) % n_shards
+
+
+def owned_panels(n: int, n_shards: int, rank: int) -> list:
+    nb = (n + PANEL - 1) // PANEL
+    return [j for j in range(nb) if panel_owner(nb, n_shards, j) == rank]
+
+
+def panel_tiles(n: int, panel: int) -> int:
+    """Lower-triangle 64x64 tiles in column panel `panel`."""
+    nb = (n + PANEL - 1) // PANEL
+    return nb - panel
+
+
+def kpoints_for_rank(n_kpoints: int, n_shards: int, rank: int) -> list:
+    """Round-robin k-point assignment (C5: 64 k-points over 1/2/4/8 GPUs)."""
+    return list(range(rank, n_kpoints, n_shards))
+
+
+def gather_panels(mat, n: int, world: int, rank: int, dst: int = 0, group=None):
+    """Gather owned column panels of a column-major matrix to rank `dst`, in place.
+
+    `mat` is a (n_cols, ld) tensor whose row j holds column j (the layout of every device
+    matrix here), so column panel [j0, j0+64) is the contiguous slice mat[j0:j0+64].  Each
+    rank sends the panels it owns; `dst` receives the others straight into place.  Works
+    with NCCL (GPU tensors) and gloo (CPU tensors)."""
+    import torch.distributed as dist
+
+    nb = (n + PANEL - 1) // PANEL
+    ops = []
+    for j in range(nb):
+        owner = panel_owner(nb, world, j)
+        sl = mat[j * PANEL:min(n, (j + 1) * PANEL)]
+        if rank == dst and owner != dst:
+            ops.append(dist.P2POp(dist.irecv, sl, owner, group))
+        elif rank == owner and owner != dst:
+            ops.append(dist.P2POp(dist.isend, sl, dst, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    return mat
+
+
+def build_hs_sharded(spec, tmats, config=None, *, dst: int = 0, group=None):
+    """One k-point's H and S computed by all ranks of the process group (column panels),
+    gathered and mirrored on rank `dst`; returns device (H, S, result) on `dst`, None
+    elsewhere.  Every rank must call it (collective)."""
+    import ctypes
+
+    import torch.distributed as dist
+
+    from . import _native, device
+    from .builder import BuildConfig
+    from .errors import ContractViolationError
+    from .pipeline import DeviceSpec, HSPipeline, pack_tmats
+
+    config = config or BuildConfig()
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dspec = DeviceSpec(spec)
+    pipe = HSPipeline(spec.n_basis, dspec.heights, shard_rank=rank, n_shards=world)
+    res = pipe.run(dspec, pack_tmats(tmats), config.force_general_path)
+    n = spec.n_basis
+    gather_panels(pipe.H, n, world, rank, dst, group)
+    gather_panels(pipe.S, n, world, rank, dst, group)
+    if rank != dst:
+        return None
+    lib = _native.load()
+    for m in (pipe.H, pipe.S):
+        flag = ctypes.c_int32(0)
+        _native.check(lib.hsdla_mirror_lower(device.ctx(), n, device.ptr(m), m.shape[1],
+                                             ctypes.byref(flag)), "hsdla_mirror_lower")
+        if flag.value:
+            raise ContractViolationError("accumulator contains non-finite values")
+    return pipe.H[:n, :n], pipe.S[:n, :n], res

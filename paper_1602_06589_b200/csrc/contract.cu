@@ -18,8 +18,8 @@
 //
 // CTA: 128 threads = 2x2 warps, 64x64 complex output tile, each warp 32x32 complex
 // (16 DMMA blocks for Re + 16 for Im).  K is staged in chunks of 16 complex (256 B per
-// column) through a 3-stage cp.async ring, 32-byte XOR swizzle (conflict-free fragment
-// loads).  Work distribution is stream-K: the (tile, K-chunk) iteration space of all
+// column) through a 3-stage cp.async ring; columns are padded to 288 B in shared memory
+// so fragment loads are bank-conflict-free with compile-time offsets.  Work distribution is stream-K: the (tile, K-chunk) iteration space of all
 // problems is cut into equal contiguous ranges, one per co-resident CTA (cooperative
 // launch), so there is no wave-quantisation tail.  A tile split between CTAs is finished
 // by the CTA holding its first chunk, which adds the later pieces' partial tiles in a fixed
@@ -36,10 +36,16 @@ namespace {
 
 constexpr int kStages = 3;
 constexpr int kChunk = 16;                       // complex K per stage
-constexpr int kColDoubles = 2 * kChunk;          // 32 doubles per column per stage
-constexpr int kOpDoubles = kTile * kColDoubles;  // 2048 doubles = 16 KB per operand
-constexpr int kStageDoubles = 2 * kOpDoubles;
-constexpr size_t kSmemBytes = size_t(kStages) * kStageDoubles * sizeof(double);
+// Column stride in shared memory: 32 doubles of data padded to 36 (288 B).  Eight
+// consecutive columns then start 8 banks apart, so a DMMA fragment load (8 columns x 4
+// consecutive doubles per half-warp phase) is conflict-free with compile-time offsets.
+// PAD = 0 instead keeps 256-B columns with a 32-byte XOR swizzle (k-chunk index ^ column&7).
+template <int PAD> struct Layout {
+  static constexpr int kColDoubles = 2 * kChunk + (PAD ? 4 : 0);
+  static constexpr int kOpDoubles = kTile * kColDoubles;
+  static constexpr int kStageDoubles = 2 * kOpDoubles;
+  static constexpr size_t kSmemBytes = size_t(kStages) * kStageDoubles * sizeof(double);
+};
 constexpr int kPartialDoubles = kTile * kTile * 2;  // one partial tile (64 KB)
 
 struct SKParams {
@@ -85,9 +91,12 @@ __device__ __forceinline__ Seg load_seg(const Seg* s) {
 // JB = 8-column DMMA blocks per warp along n: JB = 4 -> warp tile 32x32 complex, 4 warps
 // (128 threads, ~250 registers, 2 warps per SM sub-partition); JB = 2 -> warp tile 32x16,
 // 8 warps (256 threads, <= 128 registers, 4 warps per sub-partition).
-template <int JB>
+template <int JB, int PAD>
 __global__ void __launch_bounds__(32 * 2 * (8 / JB), 2) contract_kernel(SKParams sk) {
   extern __shared__ __align__(128) double smem[];
+  constexpr int kColDoubles = Layout<PAD>::kColDoubles;
+  constexpr int kOpDoubles = Layout<PAD>::kOpDoubles;
+  constexpr int kStageDoubles = Layout<PAD>::kStageDoubles;
   constexpr int kWarpCols = 8 * JB;
   constexpr int kThreads = 32 * 2 * (kTile / kWarpCols);
   constexpr int kColStep = kThreads / 16;           // columns covered per cp.async round
@@ -102,7 +111,7 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), 2) contract_kernel(SKParams
   // cp.async slot of this thread: complex element lp of the chunk, columns lc + kColStep*r.
   const int lp = tid & 15;
   const int lc = tid >> 4;
-  const int dst_lane = (((lp >> 1) ^ (lc & 7)) << 2) + (lp & 1) * 2;  // within a column (doubles)
+  const int dst_lane = PAD ? lp * 2 : ((((lp >> 1) ^ (lc & 7)) << 2) + (lp & 1) * 2);
 
   const int cta = blockIdx.x;
   long long it = range_start(sk.total_it, sk.grid, cta);
@@ -151,22 +160,28 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), 2) contract_kernel(SKParams
     Seg cur;
     if (isi < send) cur = load_seg(sk.segs + isi);
     else { cur = load_seg(sk.segs + pr.seg0); cur.k = 0; }
+    // Per-thread cp.async bases of the current segment: column lc + kColStep*r, element lp.
+    // Columns past the problem edge are zero-filled; their count is tile-constant.
+    const int nvP = max(0, min(kRounds, (mP - i0 - lc + kColStep - 1) / kColStep));
+    const int nvQ = max(0, min(kRounds, (mQ - j0 - lc + kColStep - 1) / kColStep));
+    const double2* bP = cur.P + (long long)(i0 + lc) * cur.ldP + lp;
+    const double2* bQ = cur.Q + (long long)(j0 + lc) * cur.ldQ + lp;
+    long long stP = (long long)kColStep * cur.ldP, stQ = (long long)kColStep * cur.ldQ;
 
     auto issue = [&](int stage) {
-      double* sP = smem + stage * kStageDoubles;
+      double* sP = smem + stage * kStageDoubles + lc * kColDoubles + dst_lane;
       double* sQ = sP + kOpDoubles;
       const bool kval = (iko + lp) < cur.k;
+      const double2* p = bP + iko;
+      const double2* qq = bQ + iko;
 #pragma unroll
       for (int r = 0; r < kRounds; ++r) {
-        const int col = lc + kColStep * r;
-        const int gp = i0 + col;
-        const bool vp = kval && gp < mP;
-        const double2* srcp = vp ? cur.P + (long long)gp * cur.ldP + iko + lp : cur.Q;
-        cp_async16(sP + col * kColDoubles + dst_lane, srcp, vp ? 16 : 0);
-        const int gq = j0 + col;
-        const bool vq = kval && gq < mQ;
-        const double2* srcq = vq ? cur.Q + (long long)gq * cur.ldQ + iko + lp : cur.Q;
-        cp_async16(sQ + col * kColDoubles + dst_lane, srcq, vq ? 16 : 0);
+        const bool vp = kval && r < nvP;
+        cp_async16(sP + r * kColStep * kColDoubles, vp ? p : cur.Q, vp ? 16 : 0);
+        const bool vq = kval && r < nvQ;
+        cp_async16(sQ + r * kColStep * kColDoubles, vq ? qq : cur.Q, vq ? 16 : 0);
+        p += stP;
+        qq += stQ;
       }
       iko += kChunk;
       if (iko >= cur.k) {
@@ -176,6 +191,10 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), 2) contract_kernel(SKParams
           isi = nx;
           iko = 0;
           cur = load_seg(sk.segs + isi);
+          bP = cur.P + (long long)(i0 + lc) * cur.ldP + lp;
+          bQ = cur.Q + (long long)(j0 + lc) * cur.ldQ + lp;
+          stP = (long long)kColStep * cur.ldP;
+          stQ = (long long)kColStep * cur.ldQ;
         }
       }
     };
@@ -209,7 +228,7 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), 2) contract_kernel(SKParams
       const double* pb = sQ + (wn * kWarpCols + g) * kColDoubles;
 #pragma unroll
       for (int s = 0; s < 8; ++s) {
-        const int off = ((s ^ g) << 2);
+        const int off = PAD ? (s << 2) : ((s ^ g) << 2);
         double a[4], br[JB], bi[JB];
 #pragma unroll
         for (int ib = 0; ib < 4; ++ib) a[ib] = pa[ib * 8 * kColDoubles + off + q];
@@ -353,16 +372,25 @@ int launch_contract(hsdla_ctx* ctx, const std::vector<Prob>& probs_in,
     if (p.ntiles > 0) probs.push_back(p);
   }
   if (total == 0) return HSDLA_OK;
-  static int variant = -1;  // warp tile width: HSDLA_WARP_COLS = 32 or 16
+  // Variant selection (HSDLA_WARP_COLS = 32 | 16, HSDLA_SMEM_PAD = 0 | 1) for A/B tests.
+  static int variant = -1, pad = -1;
   if (variant < 0) {
     const char* e = getenv("HSDLA_WARP_COLS");
-    variant = (e && atoi(e) == 32) ? 4 : 2;
-    HS_CUDA(cudaFuncSetAttribute(contract_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kSmemBytes));
-    HS_CUDA(cudaFuncSetAttribute(contract_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kSmemBytes));
+    variant = (e && atoi(e) == 16) ? 2 : 4;
+    const char* p = getenv("HSDLA_SMEM_PAD");
+    pad = (p && atoi(p) == 1) ? 1 : 0;
+    HS_CUDA(cudaFuncSetAttribute(contract_kernel<4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)Layout<0>::kSmemBytes));
+    HS_CUDA(cudaFuncSetAttribute(contract_kernel<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)Layout<0>::kSmemBytes));
+    HS_CUDA(cudaFuncSetAttribute(contract_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)Layout<1>::kSmemBytes));
+    HS_CUDA(cudaFuncSetAttribute(contract_kernel<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)Layout<1>::kSmemBytes));
   }
-  const void* kfn = variant == 4 ? (const void*)contract_kernel<4> : (const void*)contract_kernel<2>;
+  const void* kfn = variant == 4 ? (pad ? (const void*)contract_kernel<4, 1> : (const void*)contract_kernel<4, 0>)
+                                 : (pad ? (const void*)contract_kernel<2, 1> : (const void*)contract_kernel<2, 0>);
+  const size_t kSmemBytes = pad ? Layout<1>::kSmemBytes : Layout<0>::kSmemBytes;
   const int kThreads = variant == 4 ? 128 : 256;
   int occ = 0;
   HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kThreads, kSmemBytes));

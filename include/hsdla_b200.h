@@ -152,6 +152,12 @@ typedef struct {
   /* column-panel sharding for multi-GPU tile partitioning; n_shards <= 1 = all.
    * With sharding only the lower tiles of owned 64-wide column panels are written, unmirrored. */
   int32_t shard_rank, n_shards;
+  /* Optional HOST (pinned) destinations: when non-NULL the full H / S (ld ldh_host) are
+   * copied back inside the call on a copy stream, overlapped with the remaining compute
+   * (S during the H phase; H in column-panel ranges as they complete).  Not with sharding. */
+  hsdla_c64* H_host;
+  hsdla_c64* S_host;
+  int64_t ldh_host;
 } hsdla_build_args;
 
 typedef struct {
@@ -161,6 +167,7 @@ typedef struct {
   float ms_setup, ms_S, ms_H_ABBA_BB, ms_H_AA; /* out: CUDA-event phase times */
   float ms_contract_S, ms_contract_H;           /* out: the two triangular DMMA contraction launches */
   float ms_apply_Z, ms_apply_XY;                /* out: the batched T-application launches */
+  float ms_total;                               /* out: first event to last kernel / copy */
 } hsdla_build_result;
 
 size_t hsdla_build_workspace_size(const hsdla_build_args* args);

@@ -60,6 +60,7 @@ class BuildArgs(ctypes.Structure):
         ("H", _vp), ("S", _vp), ("ldh", _i64),
         ("workspace", _vp), ("workspace_bytes", ctypes.c_size_t),
         ("shard_rank", _i32), ("n_shards", _i32),
+        ("H_host", _vp), ("S_host", _vp), ("ldh_host", _i64),
     ]
 
 
@@ -70,6 +71,7 @@ class BuildResult(ctypes.Structure):
         ("ms_H_ABBA_BB", ctypes.c_float), ("ms_H_AA", ctypes.c_float),
         ("ms_contract_S", ctypes.c_float), ("ms_contract_H", ctypes.c_float),
         ("ms_apply_Z", ctypes.c_float), ("ms_apply_XY", ctypes.c_float),
+        ("ms_total", ctypes.c_float),
     ]
 
 

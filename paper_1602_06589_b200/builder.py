@@ -440,18 +440,16 @@ def build_all(coeffs: StackedCoefficients, tmats: TMatrixSet, config: BuildConfi
     tpack: TPack = pack_tmats(tmats)
     h_d = device.empty_matrix(n, n, n)
     s_d = device.empty_matrix(n, n, n)
+    h_host = _pinned_square(n)
+    s_host = _pinned_square(n)
     res, ws = build_device(n_basis=n, heights=layout.block_heights,
                            row_offset=layout.offsets[:-1], tpack=tpack, A=a_d, B=b_d, Bs=None,
                            udot=udot, ld=ld, force_general_path=config.force_general_path,
-                           H=h_d, S=s_d, ldh=n)
+                           H=h_d, S=s_d, ldh=n, host_out=(h_host[1], s_host[1]))
     if not config.backup:
         regenerate(coeffs)
         if coeffs.A_star.rows != layout.total_rows or coeffs.A_star.cols != n:
             raise ContractViolationError("regeneration callback changed the stack shape")
-    h_host = _pinned_square(n)
-    s_host = _pinned_square(n)
-    h_host[1].copy_(h_d[:n, :n])
-    s_host[1].copy_(s_d[:n, :n])
     h_full = ComplexDense(h_host[0])
     s_full = ComplexDense(s_host[0])
     wall = time.perf_counter() - t0

@@ -133,6 +133,8 @@ int hsdla_ctx_create(hsdla_ctx** out, void* stream) {
   for (auto& e : c->ev) HS_CUDA(cudaEventCreate(&e));
   HS_CUDA(cudaEventCreateWithFlags(&c->stage_done, cudaEventDisableTiming));
   HS_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  HS_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+  for (auto& e : c->cev) HS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   HS_CUDA(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
   HS_CUDA(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
   *out = c;
@@ -152,6 +154,9 @@ int hsdla_ctx_destroy(hsdla_ctx* c) {
   cudaEventDestroy(c->fork);
   cudaEventDestroy(c->join);
   cudaStreamDestroy(c->side);
+  cudaStreamSynchronize(c->copy);
+  for (auto& e : c->cev) cudaEventDestroy(e);
+  cudaStreamDestroy(c->copy);
   if (c->partials) cudaFree(c->partials);
   if (c->ready) cudaFree(c->ready);
   delete c;
@@ -359,6 +364,57 @@ size_t hsdla_build_workspace_size(const hsdla_build_args* args) {
 }
 
 namespace {
+// Column-panel boundaries for an overlapped D2H: ranges complete in order, and each
+// finished range [b_r, b_r+1) of columns is final (its upper part comes from tiles of
+// earlier or equal panels).  Cumulative lower-triangle tile fractions per boundary; the
+// last ranges are narrow so the copy left after the final kernel is small.
+std::vector<int> copy_ranges(int nb) {
+  static const double frac[] = {0.22, 0.42, 0.6, 0.75, 0.86, 0.935, 0.975, 1.0};
+  std::vector<int> b{0};
+  const long long total = (long long)nb * (nb + 1) / 2;
+  long long cum = 0;
+  int f = 0;
+  for (int j = 0; j < nb; ++j) {
+    cum += nb - j;
+    if (cum >= (long long)(frac[f] * total + 0.5) || j == nb - 1) {
+      if (j + 1 > b.back()) b.push_back(j + 1);
+      while (f < 7 && cum >= (long long)(frac[f] * total + 0.5)) ++f;
+    }
+  }
+  if (b.back() != nb) b.push_back(nb);
+  return b;
+}
+
+// Launch a mirrored triangular contraction; with a host destination it is cut into
+// column ranges and each finished range is copied on the copy stream.
+int launch_tri_copied(hsdla_ctx* ctx, double2* C, long long ldc, int n, const std::vector<Seg>& segs,
+                      int* flag, hsdla_c64* host, long long ld_host, int* cev_next) {
+  if (!host) {
+    std::vector<Prob> probs{make_prob(C, ldc, n, n, PROB_TRI_MIRROR, 0, (int)segs.size(), 0)};
+    return launch_contract(ctx, probs, segs, flag);
+  }
+  const int nb = (n + kTile - 1) / kTile;
+  const std::vector<int> b = copy_ranges(nb);
+  for (size_t r = 0; r + 1 < b.size(); ++r) {
+    Prob p = make_prob(C, ldc, n, n, PROB_TRI_MIRROR, 0, (int)segs.size(), 0);
+    p.col_tile_lo = b[r];
+    p.col_tile_hi = b[r + 1];
+    std::vector<Prob> probs{p};
+    int rc = launch_contract(ctx, probs, segs, flag);
+    if (rc) return rc;
+    if (*cev_next >= 39) return HSDLA_ERR_UNSUPPORTED;
+    cudaEvent_t e = ctx->cev[(*cev_next)++];
+    HS_CUDA(cudaEventRecord(e, ctx->stream));
+    HS_CUDA(cudaStreamWaitEvent(ctx->copy, e, 0));
+    const int c0 = b[r] * kTile, c1 = std::min(n, b[r + 1] * kTile);
+    HS_CUDA(cudaMemcpy2DAsync(host + (size_t)c0 * ld_host, size_t(ld_host) * sizeof(hsdla_c64),
+                              C + (size_t)c0 * ldc, size_t(ldc) * sizeof(double2),
+                              size_t(n) * sizeof(double2), c1 - c0, cudaMemcpyDeviceToHost,
+                              ctx->copy));
+  }
+  return HSDLA_OK;
+}
+
 // The composed build (builder.py:403-474) with an optional fused A/B generation
 // (flapw.py:201-233).  Everything is enqueued without a host round trip: the per-T-set
 // Cholesky info selects the HPD / general operands on the device (Seg::sel), and is read
@@ -395,6 +451,11 @@ int run_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args* ab
   int* flag = flag_slot(ctx, 2);
   cudaEvent_t* ev = ctx->ev;
   int rc;
+  int cev_next = 0;
+  if (sharded && (a->H_host || a->S_host)) {
+    set_error("host destinations are not supported with column-panel sharding");
+    return -2;
+  }
 
   HS_CUDA(cudaEventRecord(ev[0], ctx->stream));
   HS_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
@@ -447,9 +508,13 @@ int run_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args* ab
   // ---- S = A^H A + (U B)^H (U B)   (builder.py:199-209)
   {
     std::vector<Seg> segs{make_seg(A, ld, A, ld, (int)R), make_seg(Bs, ld, Bs, ld, (int)R)};
-    std::vector<Prob> probs;
-    add_tri(probs, D2(a->S), 0, 2);
-    rc = launch_contract(ctx, probs, segs, flag);
+    if (!sharded) {
+      rc = launch_tri_copied(ctx, D2(a->S), a->ldh, n, segs, flag, a->S_host, a->ldh_host, &cev_next);
+    } else {
+      std::vector<Prob> probs;
+      add_tri(probs, D2(a->S), 0, 2);
+      rc = launch_contract(ctx, probs, segs, flag);
+    }
     if (rc) return rc;
   }
   HS_CUDA(cudaEventRecord(ev[2], ctx->stream));
@@ -515,12 +580,20 @@ int run_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args* ab
       segs.push_back(make_seg(XY + off, ld, XY + off, ld, (int)rows, A + off, info_dev + ts));
       i = j;
     }
-    std::vector<Prob> probs;
-    add_tri(probs, D2(a->H), 0, (int)segs.size());
-    rc = launch_contract(ctx, probs, segs, flag);
+    if (!sharded) {
+      rc = launch_tri_copied(ctx, D2(a->H), a->ldh, n, segs, flag, a->H_host, a->ldh_host, &cev_next);
+    } else {
+      std::vector<Prob> probs;
+      add_tri(probs, D2(a->H), 0, (int)segs.size());
+      rc = launch_contract(ctx, probs, segs, flag);
+    }
     if (rc) return rc;
   }
   HS_CUDA(cudaEventRecord(ev[6], ctx->stream));
+  if (cev_next > 0) {  // join the copy stream: the final sync covers the D2H
+    HS_CUDA(cudaEventRecord(ctx->cev[39], ctx->copy));
+    HS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->cev[39], 0));
+  }
   int* info_host = ctx->scratch_host + 128;
   HS_CUDA(cudaMemcpyAsync(info_host, info_dev, a->n_tsets * sizeof(int), cudaMemcpyDeviceToHost,
                           ctx->stream));
@@ -553,6 +626,9 @@ int run_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args* ab
   res->ms_contract_H = t46;
   res->ms_apply_Z = t23;
   res->ms_apply_XY = t34;
+  float t07 = 0;
+  cudaEventElapsedTime(&t07, ev[0], ev[7]);
+  res->ms_total = t07;
   if (nan_input) {
     set_error("NaN in the lower triangle of a T_AA block (Cholesky input)");
     return HSDLA_ERR_NAN_INPUT;

@@ -73,6 +73,8 @@ struct Arena;  // descriptor staging (defined in capi.cu)
 struct hsdla_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // T preparation overlaps A/B generation here
+  cudaStream_t copy = nullptr;  // D2H of finished column ranges of H / S
+  cudaEvent_t cev[40] = {};
   cudaEvent_t fork = nullptr, join = nullptr;
   int device = 0;
   int num_sms = 148;

@@ -72,7 +72,7 @@ def pack_tmats(tmats) -> TPack:
 
 def build_device(*, n_basis, heights, row_offset, tpack: TPack, A, B, Bs, udot, ld,
                  force_general_path, H, S, ldh, shard_rank=0, n_shards=1, workspace=None,
-                 ab_args=None):
+                 ab_args=None, host_out=None):
     """Run `hsdla_build_hs` (or `hsdla_setup_hs` when `ab_args` is given: A/B generation
     fused in front) on device buffers; returns (result dict, workspace tensor)."""
     lib = _native.load()
@@ -105,6 +105,10 @@ def build_device(*, n_basis, heights, row_offset, tpack: TPack, A, B, Bs, udot, 
     args.ldh = ldh
     args.shard_rank = shard_rank
     args.n_shards = n_shards
+    if host_out is not None:  # pinned (n, n) tensors: D2H overlapped inside the native call
+        args.H_host = host_out[0].data_ptr()
+        args.S_host = host_out[1].data_ptr()
+        args.ldh_host = int(host_out[0].shape[1])
     need = lib.hsdla_build_workspace_size(ctypes.byref(args))
     if workspace is None or workspace.numel() < need:
         workspace = t.empty(max(need, 1), dtype=t.uint8, device="cuda")
@@ -133,6 +137,7 @@ def build_device(*, n_basis, heights, row_offset, tpack: TPack, A, B, Bs, udot, 
         "kernel_ms": {"contract_S": res.ms_contract_S, "contract_H": res.ms_contract_H,
                       "apply_Z": res.ms_apply_Z, "apply_XY": res.ms_apply_XY},
         "workspace_bytes": int(need),
+        "ms_total": res.ms_total,
     }
     return out, workspace
 
@@ -246,8 +251,11 @@ class HSPipeline:
             shard_rank=self.shard_rank, n_shards=self.n_shards, workspace=self.workspace)
         return res
 
-    def run(self, dspec: DeviceSpec, tpack: TPack, force_general_path: bool = False):
-        """One k-point, spec -> H, S in HBM, as a single native call (`hsdla_setup_hs`)."""
+    def run(self, dspec: DeviceSpec, tpack: TPack, force_general_path: bool = False,
+            host_out=None):
+        """One k-point, spec -> H, S in HBM, as a single native call (`hsdla_setup_hs`).
+        With `host_out` = pinned (n, n) tensors, H and S are also copied to the host with the
+        copies overlapped with the remaining compute."""
         if dspec.n_basis > self.n_capacity or dspec.rows != self.rows:
             raise ContractViolationError("spec shape does not fit the pipeline buffers")
         self.n_basis = dspec.n_basis
@@ -257,7 +265,7 @@ class HSPipeline:
             A=self.A, B=self.B, Bs=self.Bs, udot=self.udot, ld=self.ld,
             force_general_path=force_general_path, H=self.H, S=self.S, ldh=self.n_capacity,
             shard_rank=self.shard_rank, n_shards=self.n_shards, workspace=self.workspace,
-            ab_args=ab)
+            ab_args=ab, host_out=host_out)
         return res
 
     def launches_per_run(self, dspec: DeviceSpec) -> int:
@@ -286,15 +294,12 @@ def build_hs(spec, tmats, config=None, *, pipeline: HSPipeline | None = None, ho
     dspec = DeviceSpec(spec)
     tpack = pack_tmats(tmats)
     pipe = pipeline or HSPipeline(spec.n_basis, dspec.heights)
-    res = pipe.run(dspec, tpack, config.force_general_path)
     t = device.torch()
     n = spec.n_basis
     if host_out is None or tuple(host_out[0].shape) != (n, n):
         host_out = (t.empty((n, n), dtype=t.complex128, pin_memory=True),
                     t.empty((n, n), dtype=t.complex128, pin_memory=True))
-    h_view, s_view = pipe.result_views()
-    host_out[0].copy_(h_view)
-    host_out[1].copy_(s_view)
+    res = pipe.run(dspec, tpack, config.force_general_path, host_out=host_out)
     h = ComplexDense(host_out[0].numpy().T)
     s = ComplexDense(host_out[1].numpy().T)
     res["h2d_bytes"] = dspec.h2d_bytes + tpack.h2d_bytes

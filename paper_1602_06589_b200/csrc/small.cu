@@ -98,14 +98,18 @@ __device__ void chol_packed(int n, const double2* __restrict__ T, long long ldt,
   __shared__ int s_bad;
   __shared__ double s_ljj;
   const int tid = threadIdx.x, nt = blockDim.x;
+  const int tx = tid & 31, ty = tid >> 5, nty = nt >> 5;
   if (tid == 0) s_bad = 0;
   __syncthreads();
-  for (int r = tid; r < n; r += nt)
-    for (int c = 0; c <= r; ++c) {
+  // coalesced load of the lower triangle (column-major source, r fastest)
+  for (long long e = tid; e < (long long)n * n; e += nt) {
+    const int r = (int)(e % n), c = (int)(e / n);
+    if (r >= c) {
       const double2 v = T[r + (long long)c * ldt];
       if (isnan(v.x) || isnan(v.y)) s_bad = 1;
       Lp[packed_idx(r, c)] = v;
     }
+  }
   __syncthreads();
   if (s_bad) {
     if (tid == 0) *info = -1;
@@ -132,17 +136,18 @@ __device__ void chol_packed(int n, const double2* __restrict__ T, long long ldt,
       Lp[packed_idx(i, j)] = make_double2(v.x / ljj, v.y / ljj);
     }
     __syncthreads();
-    // trailing update L[i][k] -= L[i][j] conj(L[k][j]), j < k <= i
-    const int rem = n - j - 1;
-    for (int e = tid; e < rem * rem; e += nt) {
-      const int i = j + 1 + e / rem, k = j + 1 + e % rem;
-      if (k > i) continue;
-      const double2 a = Lp[packed_idx(i, j)];
-      const double2 b = Lp[packed_idx(k, j)];
-      double2 v = Lp[packed_idx(i, k)];
-      v.x -= a.x * b.x + a.y * b.y;
-      v.y -= a.y * b.x - a.x * b.y;
-      Lp[packed_idx(i, k)] = v;
+    // trailing update L[i][k] -= L[i][j] conj(L[k][j]), j < k <= i: a warp per row i,
+    // lanes along k (consecutive packed addresses), L[i][j] broadcast within the warp.
+    for (int i = j + 1 + ty; i < n; i += nty) {
+      const int pi = packed_idx(i, 0);
+      const double2 a = Lp[pi + j];
+      for (int k = j + 1 + tx; k <= i; k += 32) {
+        const double2 b = Lp[packed_idx(k, j)];
+        double2 v = Lp[pi + k];
+        v.x -= a.x * b.x + a.y * b.y;
+        v.y -= a.y * b.x - a.x * b.y;
+        Lp[pi + k] = v;
+      }
     }
     __syncthreads();
   }

@@ -226,8 +226,10 @@ def test_c2_end_to_end_vs_oracle(pkg):
     assert rep.ledger == pkg.predict_flops(len(heights), heights, inst.spec.n_basis, mask)
 
 
-def test_device_pipeline_matches_drop_in_bitwise(pkg):
-    """HSPipeline (A/B generated in HBM, B scaled in the producer) == compute_AB + build_all."""
+def test_device_pipeline_matches_drop_in(pkg):
+    """HSPipeline (A/B generated in HBM, B scaled in the producer) == compute_AB + build_all.
+    The two paths cut the stream-K work differently (the drop-in copies column ranges to the
+    host as they finish), so agreement is to rounding, not bitwise."""
     from paper_1602_06589_b200 import configs
     from paper_1602_06589_b200.pipeline import DeviceSpec, HSPipeline, pack_tmats
 
@@ -239,8 +241,9 @@ def test_device_pipeline_matches_drop_in_bitwise(pkg):
     n = inst.spec.n_basis
     h = pipe.H[:n, :n].cpu().numpy().T
     s = pipe.S[:n, :n].cpu().numpy().T
-    np.testing.assert_array_equal(h, h_ref.array)
-    np.testing.assert_array_equal(s, s_ref.array)
+    assert rel_fro(h, h_ref.array) <= 1e-14
+    assert rel_fro(s, s_ref.array) <= 1e-14
+    np.testing.assert_array_equal(h, h.conj().T)
     assert all(res["hpd_mask"])
 
 
@@ -276,7 +279,8 @@ def test_backup_invariance_bitwise(pkg):
 
 def test_build_hs_overlapped_host_copy_matches_device(pkg):
     """build_hs copies H, S to pinned host memory in column ranges overlapped with the
-    compute; the host result equals the device result bitwise and the reference golden."""
+    compute; the host result matches the device-only run and the reference golden, and
+    repeated calls are bitwise identical."""
     from paper_1602_06589_b200 import configs
     from paper_1602_06589_b200.pipeline import DeviceSpec, HSPipeline, build_hs, pack_tmats
 
@@ -286,8 +290,10 @@ def test_build_hs_overlapped_host_copy_matches_device(pkg):
     pipe = HSPipeline(inst.spec.n_basis, dspec.heights)
     pipe.run(dspec, pack_tmats(inst.tmats))
     hd, sd = (m.cpu().numpy().T for m in pipe.result_views())
-    np.testing.assert_array_equal(h.array, hd)
-    np.testing.assert_array_equal(s.array, sd)
+    assert rel_fro(h.array, hd) <= 1e-14 and rel_fro(s.array, sd) <= 1e-14
+    h2, s2, _ = build_hs(inst.spec, inst.tmats)
+    np.testing.assert_array_equal(h.array, h2.array)
+    np.testing.assert_array_equal(s.array, s2.array)
     d = golden("build_c1.npz")
     assert rel_fro(h.array @ d["V"], d["HV"]) <= TOL
     assert res["d2h_bytes"] == 2 * 16 * inst.spec.n_basis ** 2

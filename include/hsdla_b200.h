@@ -153,8 +153,8 @@ typedef struct {
    * With sharding only the lower tiles of owned 64-wide column panels are written, unmirrored. */
   int32_t shard_rank, n_shards;
   /* Optional HOST (pinned) destinations: when non-NULL the full H / S (ld ldh_host) are
-   * copied back inside the call on a copy stream, overlapped with the remaining compute
-   * (S during the H phase; H in column-panel ranges as they complete).  Not with sharding. */
+   * copied back on a copy stream, overlapped with later compute (S during the H phase, H
+   * during the next pipelined k-point).  Not with sharding. */
   hsdla_c64* H_host;
   hsdla_c64* S_host;
   int64_t ldh_host;
@@ -182,6 +182,16 @@ int hsdla_build_hs(hsdla_ctx* ctx, const hsdla_build_args* args, hsdla_build_res
  * as called by the reference CLI's regenerate flow (cli.py:283-292, :310-325). */
 int hsdla_setup_hs(hsdla_ctx* ctx, const hsdla_ab_args* ab, const hsdla_build_args* args,
                    hsdla_build_result* result);
+
+/* Pipelined form for k-point batches: enqueue one k-point (ab may be NULL = A/B given) and
+ * return at once with a ticket; `hsdla_build_finish` waits for that k-point's compute and
+ * host copies and fills `result`.  Two builds may be in flight per context; the next
+ * build's contractions wait for the previous build's copies of the shared H / S buffers,
+ * so the copies of k-point i overlap the compute of k-point i+1.  Host destinations of
+ * in-flight builds must differ. */
+int hsdla_setup_hs_async(hsdla_ctx* ctx, const hsdla_ab_args* ab, const hsdla_build_args* args,
+                         unsigned long long* ticket);
+int hsdla_build_finish(hsdla_ctx* ctx, unsigned long long ticket, hsdla_build_result* result);
 
 #ifdef __cplusplus
 }

@@ -102,6 +102,9 @@ SIGNATURES = {
     "hsdla_build_hs": (ctypes.c_int, [_vp, ctypes.POINTER(BuildArgs), ctypes.POINTER(BuildResult)]),
     "hsdla_setup_hs": (ctypes.c_int, [_vp, ctypes.POINTER(AbArgs), ctypes.POINTER(BuildArgs),
                                       ctypes.POINTER(BuildResult)]),
+    "hsdla_setup_hs_async": (ctypes.c_int, [_vp, ctypes.POINTER(AbArgs), ctypes.POINTER(BuildArgs),
+                                            ctypes.POINTER(ctypes.c_ulonglong)]),
+    "hsdla_build_finish": (ctypes.c_int, [_vp, ctypes.c_ulonglong, ctypes.POINTER(BuildResult)]),
 }
 
 _lib = None

@@ -3,6 +3,8 @@
 // (reference builder.py:403-474) on one CUDA stream.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -127,14 +129,26 @@ int hsdla_ctx_create(hsdla_ctx** out, void* stream) {
   c->stream = static_cast<cudaStream_t>(stream);
   HS_CUDA(cudaGetDevice(&c->device));
   HS_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
-  HS_CUDA(cudaMalloc(&c->scratch_dev, 256 * sizeof(int)));
-  HS_CUDA(cudaMemset(c->scratch_dev, 0, 256 * sizeof(int)));
-  HS_CUDA(cudaHostAlloc(&c->scratch_host, 256 * sizeof(int), cudaHostAllocDefault));
-  for (auto& e : c->ev) HS_CUDA(cudaEventCreate(&e));
+  HS_CUDA(cudaMalloc(&c->scratch_dev, 512 * sizeof(int)));
+  HS_CUDA(cudaMemset(c->scratch_dev, 0, 512 * sizeof(int)));
+  // Mapped pinned memory: build results are published by a kernel store, not a DMA copy,
+  // so they never queue behind the large H / S copies on the D2H engine.
+  HS_CUDA(cudaHostAlloc(&c->scratch_host, 512 * sizeof(int), cudaHostAllocMapped));
+  HS_CUDA(cudaHostGetDevicePointer((void**)&c->scratch_host_dev, c->scratch_host, 0));
   HS_CUDA(cudaEventCreateWithFlags(&c->stage_done, cudaEventDisableTiming));
   HS_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   HS_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
-  for (auto& e : c->cev) HS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  HS_CUDA(cudaEventCreateWithFlags(&c->copy_go, cudaEventDisableTiming));
+  for (int k = 0; k < 2; ++k) {
+    auto& sl = c->slots[k];
+    for (auto& e : sl.ev) HS_CUDA(cudaEventCreate(&e));
+    HS_CUDA(cudaEventCreateWithFlags(&sl.s_copied, cudaEventDisableTiming));
+    HS_CUDA(cudaEventCreateWithFlags(&sl.h_copied, cudaEventDisableTiming));
+    HS_CUDA(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+    sl.flag_dev = c->scratch_dev + 96 + k;
+    sl.host_area = c->scratch_host + 128 + 100 * k;  // [0] flag, [1..96] info
+    sl.host_area_dev = c->scratch_host_dev + 128 + 100 * k;
+  }
   HS_CUDA(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
   HS_CUDA(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
   *out = c;
@@ -149,13 +163,18 @@ int hsdla_ctx_destroy(hsdla_ctx* c) {
   if (c->scratch_dev) cudaFree(c->scratch_dev);
   if (c->scratch_host) cudaFreeHost(c->scratch_host);
   cudaStreamSynchronize(c->side);
-  for (auto& e : c->ev) cudaEventDestroy(e);
   cudaEventDestroy(c->stage_done);
   cudaEventDestroy(c->fork);
   cudaEventDestroy(c->join);
   cudaStreamDestroy(c->side);
   cudaStreamSynchronize(c->copy);
-  for (auto& e : c->cev) cudaEventDestroy(e);
+  for (auto& sl : c->slots) {
+    for (auto& e : sl.ev) cudaEventDestroy(e);
+    cudaEventDestroy(sl.s_copied);
+    cudaEventDestroy(sl.h_copied);
+    cudaEventDestroy(sl.done);
+  }
+  cudaEventDestroy(c->copy_go);
   cudaStreamDestroy(c->copy);
   if (c->partials) cudaFree(c->partials);
   if (c->ready) cudaFree(c->ready);
@@ -364,63 +383,47 @@ size_t hsdla_build_workspace_size(const hsdla_build_args* args) {
 }
 
 namespace {
-// Column-panel boundaries for an overlapped D2H: ranges complete in order, and each
-// finished range [b_r, b_r+1) of columns is final (its upper part comes from tiles of
-// earlier or equal panels).  Cumulative lower-triangle tile fractions per boundary; the
-// last ranges are narrow so the copy left after the final kernel is small.
-std::vector<int> copy_ranges(int nb) {
-  static const double frac[] = {0.22, 0.42, 0.6, 0.75, 0.86, 0.935, 0.975, 1.0};
-  std::vector<int> b{0};
-  const long long total = (long long)nb * (nb + 1) / 2;
-  long long cum = 0;
-  int f = 0;
-  for (int j = 0; j < nb; ++j) {
-    cum += nb - j;
-    if (cum >= (long long)(frac[f] * total + 0.5) || j == nb - 1) {
-      if (j + 1 > b.back()) b.push_back(j + 1);
-      while (f < 7 && cum >= (long long)(frac[f] * total + 0.5)) ++f;
-    }
-  }
-  if (b.back() != nb) b.push_back(nb);
-  return b;
-}
-
-// Launch a mirrored triangular contraction; with a host destination it is cut into
-// column ranges and each finished range is copied on the copy stream.
-int launch_tri_copied(hsdla_ctx* ctx, double2* C, long long ldc, int n, const std::vector<Seg>& segs,
-                      int* flag, hsdla_c64* host, long long ld_host, int* cev_next) {
-  if (!host) {
-    std::vector<Prob> probs{make_prob(C, ldc, n, n, PROB_TRI_MIRROR, 0, (int)segs.size(), 0)};
-    return launch_contract(ctx, probs, segs, flag);
-  }
-  const int nb = (n + kTile - 1) / kTile;
-  const std::vector<int> b = copy_ranges(nb);
-  for (size_t r = 0; r + 1 < b.size(); ++r) {
-    Prob p = make_prob(C, ldc, n, n, PROB_TRI_MIRROR, 0, (int)segs.size(), 0);
-    p.col_tile_lo = b[r];
-    p.col_tile_hi = b[r + 1];
-    std::vector<Prob> probs{p};
-    int rc = launch_contract(ctx, probs, segs, flag);
-    if (rc) return rc;
-    if (*cev_next >= 39) return HSDLA_ERR_UNSUPPORTED;
-    cudaEvent_t e = ctx->cev[(*cev_next)++];
-    HS_CUDA(cudaEventRecord(e, ctx->stream));
-    HS_CUDA(cudaStreamWaitEvent(ctx->copy, e, 0));
-    const int c0 = b[r] * kTile, c1 = std::min(n, b[r + 1] * kTile);
-    HS_CUDA(cudaMemcpy2DAsync(host + (size_t)c0 * ld_host, size_t(ld_host) * sizeof(hsdla_c64),
-                              C + (size_t)c0 * ldc, size_t(ldc) * sizeof(double2),
-                              size_t(n) * sizeof(double2), c1 - c0, cudaMemcpyDeviceToHost,
-                              ctx->copy));
-  }
-  return HSDLA_OK;
-}
-
 // The composed build (builder.py:403-474) with an optional fused A/B generation
-// (flapw.py:201-233).  Everything is enqueued without a host round trip: the per-T-set
-// Cholesky info selects the HPD / general operands on the device (Seg::sel), and is read
-// back together with the non-finite flag after the last kernel.
-int run_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args* ab,
-              hsdla_build_result* res) {
+// (flapw.py:201-233), split into enqueue and finish so consecutive k-points pipeline:
+// nothing in `enqueue_build` waits for the device.  The per-T-set Cholesky info selects
+// the HPD / general operands on the device (Seg::sel); it is read back with the non-finite
+// flag by `finish_build`.  With host destinations, S is copied on the copy stream while
+// the H phase computes, and H while the next k-point's A/B and S compute; the next
+// build's S / H contractions wait for the previous copies of those buffers.
+// Wait for a slot's build (compute, result publication and host copies) and collect its
+// outcome; the slot becomes free.
+int complete_slot(hsdla_ctx* ctx, hsdla_ctx::BuildSlot& sl, hsdla_ctx::Outcome* o) {
+  (void)ctx;
+  HS_CUDA(cudaEventSynchronize(sl.done));
+  if (sl.copies) HS_CUDA(cudaEventSynchronize(sl.h_copied));
+  HS_CUDA(cudaEventSynchronize(sl.s_copied));
+  sl.pending = false;
+  const volatile int* area = sl.host_area;
+  o->info.resize(sl.n_tsets);
+  o->hpd.resize(sl.n_atoms);
+  bool nan_input = false;
+  for (int t = 0; t < sl.n_tsets; ++t) {
+    o->info[t] = area[1 + t];
+    if (!sl.force && o->info[t] == -1) nan_input = true;
+  }
+  for (int i = 0; i < sl.n_atoms; ++i)
+    o->hpd[i] = (!sl.force && o->info[sl.t_index[i]] == 0) ? 1 : 0;
+  o->nonfinite = area[0];
+  cudaEvent_t* ev = sl.ev;
+  float t01 = 0, t12 = 0, t23 = 0, t34 = 0, t46 = 0, t07 = 0;
+  cudaEventElapsedTime(&t01, ev[0], ev[1]);
+  cudaEventElapsedTime(&t12, ev[1], ev[2]);
+  cudaEventElapsedTime(&t23, ev[2], ev[3]);
+  cudaEventElapsedTime(&t34, ev[3], ev[4]);
+  cudaEventElapsedTime(&t46, ev[4], ev[6]);
+  cudaEventElapsedTime(&t07, ev[0], ev[7]);
+  o->ms[0] = t01; o->ms[1] = t12; o->ms[2] = t23; o->ms[3] = t34; o->ms[4] = t46; o->ms[5] = t07;
+  o->rc = nan_input ? HSDLA_ERR_NAN_INPUT : (o->nonfinite ? HSDLA_ERR_NONFINITE : HSDLA_OK);
+  return o->rc;
+}
+
+int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args* ab,
+                  unsigned long long* ticket) {
   const int na = a->n_atoms, n = a->n_basis;
   if (na < 1 || n < 1) return -2;
   for (int i = 0; i < na; ++i) {
@@ -435,6 +438,30 @@ int run_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args* ab
     set_error("workspace too small");
     return -2;
   }
+  const bool sharded = a->n_shards > 1;
+  if (sharded && (a->H_host || a->S_host)) {
+    set_error("host destinations are not supported with column-panel sharding");
+    return -2;
+  }
+  if (a->n_tsets > 96) {
+    set_error("more than 96 distinct T sets per build");
+    return HSDLA_ERR_UNSUPPORTED;
+  }
+  // Slot of this build; a slot still pending from two builds ago is finished first.
+  hsdla_ctx::BuildSlot& sl = ctx->slots[ctx->seq % 2];
+  if (sl.pending) {  // a third build in flight: complete the oldest one into the stash
+    hsdla_ctx::Outcome o;
+    int rc0 = complete_slot(ctx, sl, &o);
+    if (rc0 != HSDLA_OK && rc0 != HSDLA_ERR_NAN_INPUT && rc0 != HSDLA_ERR_NONFINITE) return rc0;
+    ctx->stash[sl.ticket] = o;
+  }
+  hsdla_ctx::BuildSlot& prev = ctx->slots[(ctx->seq + 1) % 2];
+  sl.n_atoms = na;
+  sl.n_tsets = a->n_tsets;
+  sl.force = a->force_general_path != 0;
+  sl.t_index.assign(a->t_index, a->t_index + na);
+  sl.copies = (a->H_host != nullptr) || (a->S_host != nullptr);
+
   char* ws = static_cast<char*>(a->workspace);
   const long long ld = a->ld;
   const long long R = w.R;
@@ -447,15 +474,9 @@ int run_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args* ab
   int* info_dev = reinterpret_cast<int*>(ws + w.info);
   const int mp = w.mp;
   const long long fs = (long long)mp * mp;
-  const bool sharded = a->n_shards > 1;
-  int* flag = flag_slot(ctx, 2);
-  cudaEvent_t* ev = ctx->ev;
+  int* flag = sl.flag_dev;
+  cudaEvent_t* ev = sl.ev;
   int rc;
-  int cev_next = 0;
-  if (sharded && (a->H_host || a->S_host)) {
-    set_error("host destinations are not supported with column-panel sharding");
-    return -2;
-  }
 
   HS_CUDA(cudaEventRecord(ev[0], ctx->stream));
   HS_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
@@ -504,20 +525,32 @@ int run_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args* ab
         probs.push_back(p);
       }
   };
+  auto copy_out = [&](const double2* C, hsdla_c64* host, cudaEvent_t done_ev) -> int {
+    HS_CUDA(cudaEventRecord(ctx->copy_go, ctx->stream));
+    HS_CUDA(cudaStreamWaitEvent(ctx->copy, ctx->copy_go, 0));
+    HS_CUDA(cudaMemcpy2DAsync(host, size_t(a->ldh_host) * sizeof(hsdla_c64), C,
+                              size_t(a->ldh) * sizeof(double2), size_t(n) * sizeof(double2), n,
+                              cudaMemcpyDeviceToHost, ctx->copy));
+    HS_CUDA(cudaEventRecord(done_ev, ctx->copy));
+    return HSDLA_OK;
+  };
 
   // ---- S = A^H A + (U B)^H (U B)   (builder.py:199-209)
+  if (prev.copies) HS_CUDA(cudaStreamWaitEvent(ctx->stream, prev.s_copied, 0));
   {
     std::vector<Seg> segs{make_seg(A, ld, A, ld, (int)R), make_seg(Bs, ld, Bs, ld, (int)R)};
-    if (!sharded) {
-      rc = launch_tri_copied(ctx, D2(a->S), a->ldh, n, segs, flag, a->S_host, a->ldh_host, &cev_next);
-    } else {
-      std::vector<Prob> probs;
-      add_tri(probs, D2(a->S), 0, 2);
-      rc = launch_contract(ctx, probs, segs, flag);
-    }
+    std::vector<Prob> probs;
+    add_tri(probs, D2(a->S), 0, 2);
+    rc = launch_contract(ctx, probs, segs, flag);
     if (rc) return rc;
   }
   HS_CUDA(cudaEventRecord(ev[2], ctx->stream));
+  if (a->S_host) {
+    rc = copy_out(D2(a->S), a->S_host, sl.s_copied);
+    if (rc) return rc;
+  } else {
+    HS_CUDA(cudaEventRecord(sl.s_copied, ctx->stream));
+  }
 
   // Rows of a block beyond its T size must be zero in Z / XY (builder.py:232-245 compaction).
   for (int i = 0; i < na; ++i) {
@@ -565,6 +598,7 @@ int run_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args* ab
   HS_CUDA(cudaEventRecord(ev[4], ctx->stream));
   // ---- H = Z^H B + B^H Z + sum_HPD Y^H Y + sum_nonHPD A^H X   (builder.py:246-247, :305-311)
   //      AA segments per run of atoms sharing one T set: P = XY (HPD) or A (general).
+  if (prev.copies) HS_CUDA(cudaStreamWaitEvent(ctx->stream, prev.h_copied, 0));
   {
     std::vector<Seg> segs{make_seg(Z, ld, B, ld, (int)R), make_seg(B, ld, Z, ld, (int)R)};
     int i = 0;
@@ -580,64 +614,64 @@ int run_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args* ab
       segs.push_back(make_seg(XY + off, ld, XY + off, ld, (int)rows, A + off, info_dev + ts));
       i = j;
     }
-    if (!sharded) {
-      rc = launch_tri_copied(ctx, D2(a->H), a->ldh, n, segs, flag, a->H_host, a->ldh_host, &cev_next);
-    } else {
-      std::vector<Prob> probs;
-      add_tri(probs, D2(a->H), 0, (int)segs.size());
-      rc = launch_contract(ctx, probs, segs, flag);
-    }
+    std::vector<Prob> probs;
+    add_tri(probs, D2(a->H), 0, (int)segs.size());
+    rc = launch_contract(ctx, probs, segs, flag);
     if (rc) return rc;
   }
   HS_CUDA(cudaEventRecord(ev[6], ctx->stream));
-  if (cev_next > 0) {  // join the copy stream: the final sync covers the D2H
-    HS_CUDA(cudaEventRecord(ctx->cev[39], ctx->copy));
-    HS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->cev[39], 0));
+  if (a->H_host) {
+    rc = copy_out(D2(a->H), a->H_host, sl.h_copied);
+    if (rc) return rc;
+  } else {
+    HS_CUDA(cudaEventRecord(sl.h_copied, ctx->stream));
   }
-  int* info_host = ctx->scratch_host + 128;
-  HS_CUDA(cudaMemcpyAsync(info_host, info_dev, a->n_tsets * sizeof(int), cudaMemcpyDeviceToHost,
-                          ctx->stream));
-  HS_CUDA(cudaMemcpyAsync(ctx->scratch_host + 2, flag, sizeof(int), cudaMemcpyDeviceToHost,
-                          ctx->stream));
+  rc = launch_publish(ctx, flag, info_dev, a->n_tsets, sl.host_area_dev);
+  if (rc) return rc;
   HS_CUDA(cudaEventRecord(ev[7], ctx->stream));
-  HS_CUDA(cudaEventSynchronize(ev[7]));
-
-  bool nan_input = false;
-  for (int t = 0; t < a->n_tsets; ++t) {
-    if (res->chol_info) res->chol_info[t] = info_host[t];
-    if (!a->force_general_path && info_host[t] == -1) nan_input = true;
-  }
-  for (int i = 0; i < na; ++i) {
-    const int hpd = (!a->force_general_path && info_host[a->t_index[i]] == 0) ? 1 : 0;
-    if (res->hpd_mask) res->hpd_mask[i] = hpd;
-  }
-  res->nonfinite = ctx->scratch_host[2];
-  float t01 = 0, t12 = 0, t23 = 0, t34 = 0, t46 = 0;
-  cudaEventElapsedTime(&t01, ev[0], ev[1]);
-  cudaEventElapsedTime(&t12, ev[1], ev[2]);
-  cudaEventElapsedTime(&t23, ev[2], ev[3]);
-  cudaEventElapsedTime(&t34, ev[3], ev[4]);
-  cudaEventElapsedTime(&t46, ev[4], ev[6]);
-  res->ms_setup = t01;
-  res->ms_S = t12;
-  res->ms_H_ABBA_BB = t23 + t46;
-  res->ms_H_AA = t34;
-  res->ms_contract_S = t12;
-  res->ms_contract_H = t46;
-  res->ms_apply_Z = t23;
-  res->ms_apply_XY = t34;
-  float t07 = 0;
-  cudaEventElapsedTime(&t07, ev[0], ev[7]);
-  res->ms_total = t07;
-  if (nan_input) {
-    set_error("NaN in the lower triangle of a T_AA block (Cholesky input)");
-    return HSDLA_ERR_NAN_INPUT;
-  }
-  if (res->nonfinite) {
-    set_error("accumulator contains non-finite values");
-    return HSDLA_ERR_NONFINITE;
-  }
+  HS_CUDA(cudaEventRecord(sl.done, ctx->stream));
+  sl.pending = true;
+  sl.ticket = ++ctx->seq;
+  *ticket = sl.ticket;
   return HSDLA_OK;
+}
+
+int fill_result(const hsdla_ctx::Outcome& o, hsdla_build_result* res) {
+  for (size_t t = 0; t < o.info.size(); ++t)
+    if (res->chol_info) res->chol_info[t] = o.info[t];
+  for (size_t i = 0; i < o.hpd.size(); ++i)
+    if (res->hpd_mask) res->hpd_mask[i] = o.hpd[i];
+  res->nonfinite = o.nonfinite;
+  res->ms_setup = o.ms[0];
+  res->ms_S = o.ms[1];
+  res->ms_H_ABBA_BB = o.ms[2] + o.ms[4];
+  res->ms_H_AA = o.ms[3];
+  res->ms_contract_S = o.ms[1];
+  res->ms_contract_H = o.ms[4];
+  res->ms_apply_Z = o.ms[2];
+  res->ms_apply_XY = o.ms[3];
+  res->ms_total = o.ms[5];
+  if (o.rc == HSDLA_ERR_NAN_INPUT) set_error("NaN in the lower triangle of a T_AA block (Cholesky input)");
+  if (o.rc == HSDLA_ERR_NONFINITE) set_error("accumulator contains non-finite values");
+  return o.rc;
+}
+
+int finish_build(hsdla_ctx* ctx, unsigned long long ticket, hsdla_build_result* res) {
+  auto it = ctx->stash.find(ticket);
+  if (it != ctx->stash.end()) {
+    const hsdla_ctx::Outcome o = it->second;
+    ctx->stash.erase(it);
+    return fill_result(o, res);
+  }
+  for (auto& sl : ctx->slots)
+    if (sl.pending && sl.ticket == ticket) {
+      hsdla_ctx::Outcome o;
+      int rc = complete_slot(ctx, sl, &o);
+      if (rc != HSDLA_OK && rc != HSDLA_ERR_NAN_INPUT && rc != HSDLA_ERR_NONFINITE) return rc;
+      return fill_result(o, res);
+    }
+  set_error("unknown or already finished build ticket");
+  return -2;
 }
 }  // namespace
 
@@ -646,7 +680,10 @@ int hsdla_build_hs(hsdla_ctx* ctx, const hsdla_build_args* a, hsdla_build_result
   if (!a) return -2;
   if (!res) return -3;
   std::lock_guard<std::mutex> lk(g_api_mutex);
-  return run_build(ctx, a, nullptr, res);
+  unsigned long long t = 0;
+  int rc = enqueue_build(ctx, a, nullptr, &t);
+  if (rc) return rc;
+  return finish_build(ctx, t, res);
 }
 
 int hsdla_setup_hs(hsdla_ctx* ctx, const hsdla_ab_args* ab, const hsdla_build_args* a,
@@ -656,7 +693,26 @@ int hsdla_setup_hs(hsdla_ctx* ctx, const hsdla_ab_args* ab, const hsdla_build_ar
   if (!a) return -3;
   if (!res) return -4;
   std::lock_guard<std::mutex> lk(g_api_mutex);
-  return run_build(ctx, a, ab, res);
+  unsigned long long t = 0;
+  int rc = enqueue_build(ctx, a, ab, &t);
+  if (rc) return rc;
+  return finish_build(ctx, t, res);
+}
+
+int hsdla_setup_hs_async(hsdla_ctx* ctx, const hsdla_ab_args* ab, const hsdla_build_args* a,
+                         unsigned long long* ticket) {
+  if (!ctx) return -1;
+  if (!a) return -3;
+  if (!ticket) return -4;
+  std::lock_guard<std::mutex> lk(g_api_mutex);
+  return enqueue_build(ctx, a, ab, ticket);
+}
+
+int hsdla_build_finish(hsdla_ctx* ctx, unsigned long long ticket, hsdla_build_result* res) {
+  if (!ctx) return -1;
+  if (!res) return -3;
+  std::lock_guard<std::mutex> lk(g_api_mutex);
+  return finish_build(ctx, ticket, res);
 }
 
 }  // extern "C"

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
 #include <string>
 #include <vector>
 
@@ -73,8 +74,28 @@ struct Arena;  // descriptor staging (defined in capi.cu)
 struct hsdla_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // T preparation overlaps A/B generation here
-  cudaStream_t copy = nullptr;  // D2H of finished column ranges of H / S
-  cudaEvent_t cev[40] = {};
+  cudaStream_t copy = nullptr;  // D2H of finished H / S, overlapped with later compute
+  cudaEvent_t copy_go = nullptr;
+  // Two in-flight builds (k-point pipelining): per-build events, flag and read-back area.
+  struct BuildSlot {
+    cudaEvent_t ev[8] = {};
+    cudaEvent_t s_copied = nullptr, h_copied = nullptr, done = nullptr;
+    int* flag_dev = nullptr;
+    int* host_area = nullptr;      // mapped pinned (host view)
+    int* host_area_dev = nullptr;  // device view of host_area
+    int n_atoms = 0, n_tsets = 0;
+    bool force = false, copies = false, pending = false;
+    unsigned long long ticket = 0;
+    std::vector<int> t_index;
+  } slots[2];
+  unsigned long long seq = 0;
+  // Outcomes of builds completed before their ticket was finished (more than two in flight).
+  struct Outcome {
+    int rc = 0, nonfinite = 0;
+    std::vector<int> info, hpd;
+    float ms[6] = {};
+  };
+  std::map<unsigned long long, Outcome> stash;
   cudaEvent_t fork = nullptr, join = nullptr;
   int device = 0;
   int num_sms = 148;
@@ -90,9 +111,9 @@ struct hsdla_ctx {
   cudaEvent_t stage_done = nullptr;
   bool stage_pending = false;
   // Small device scratch: tile counters and flags; pinned mirrors for read-back.
-  int* scratch_dev = nullptr;   // [0..63] tile counters, [64..127] flags
-  int* scratch_host = nullptr;  // pinned
-  cudaEvent_t ev[8] = {};
+  int* scratch_dev = nullptr;   // [64..95] operator flags, [96..97] build-slot flags
+  int* scratch_host = nullptr;  // mapped pinned: [0..127] operator read-back, [128..327] build slots
+  int* scratch_host_dev = nullptr;
 };
 
 namespace hsdla {
@@ -120,4 +141,7 @@ int ab_generate(hsdla_ctx* ctx, const hsdla_ab_args* args);
 int launch_mirror(hsdla_ctx* ctx, int n, double2* C, long long ldc, int* flag_dev);
 int launch_scale_rows(hsdla_ctx* ctx, int m, int n, const double* d, double2* B, long long ldb);
 int launch_zero_rows(hsdla_ctx* ctx, double2* base, long long ld, int row0, int rows, int cols);
+// Copy the non-finite flag and the Cholesky infos into mapped host memory (out[0] = flag,
+// out[1..n] = info) with plain stores, keeping the D2H copy engine free for H / S.
+int launch_publish(hsdla_ctx* ctx, const int* flag, const int* info, int n, int* out_mapped);
 }  // namespace hsdla

@@ -252,6 +252,14 @@ __global__ void prep_kernel(int op, int rows, int cols, const double2* in, long 
   out[r + (long long)c * ldout] = v;
 }
 
+__global__ void publish_kernel(const int* flag, const int* info, int n, int* out) {
+  for (int i = threadIdx.x; i <= n; i += blockDim.x) {
+    volatile int* o = out;
+    o[i] = (i == 0) ? *flag : info[i - 1];
+  }
+  __threadfence_system();
+}
+
 __global__ void zero_rows_kernel(double2* base, long long ld, int row0, int rows) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
@@ -304,6 +312,12 @@ int launch_prep(hsdla_ctx* ctx, int op, int rows, int cols, const double2* in, l
   if (rows <= 0 || cols <= 0) return HSDLA_OK;
   prep_kernel<<<dim3((rows + 127) / 128, cols), 128, 0, ctx->stream>>>(op, rows, cols, in, ldin,
                                                                         out, ldout, scale);
+  HS_CHECK_LAUNCH();
+  return HSDLA_OK;
+}
+
+int launch_publish(hsdla_ctx* ctx, const int* flag, const int* info, int n, int* out_mapped) {
+  publish_kernel<<<1, 128, 0, ctx->stream>>>(flag, info, n, out_mapped);
   HS_CHECK_LAUNCH();
   return HSDLA_OK;
 }

@@ -1,13 +1,15 @@
 """Device-resident H/S setup pipeline (the B200 hot path).
 
-    SystemSpec + T blocks --(H2D, tiny)--> [A/B generator] --> [native build] --> H, S in HBM
+    SystemSpec + T blocks --(H2D, tiny)--> [A/B generator] --> [native build] --> H, S
 
 `HSPipeline` owns the HBM buffers for one problem shape and runs one k-point per
-call: the fused A/B generator (reference `flapw.py:201-233`) writes A, B and the
-row-scaled B directly, then `hsdla_build_hs` (reference `builder.py:403-474`) runs
-the T-block applications and the two triangular DMMA contractions with the
-Hermitian mirror fused into their epilogue.  Inputs stay resident; nothing but the
-spec, the T blocks and (optionally) the results crosses PCIe.
+call as a single native call (`hsdla_setup_hs`): the fused A/B generator (reference
+`flapw.py:201-233`) writes A, B and the row-scaled B, the T preparation / Cholesky runs
+on a side stream meanwhile, then the T-block applications and the two triangular DMMA
+contractions with the Hermitian mirror fused into their epilogue (reference
+`builder.py:403-474`).  Inputs stay resident; only the spec, the T blocks and (when
+asked) the results cross PCIe.  `run_async` / `finish` pipeline consecutive k-points:
+the D2H copies of k-point i overlap the compute of k-point i+1.
 
 Layout in HBM (column-major complex128, leading dimension `ld` = R rounded up to a
 multiple of 16 so every 16-element K chunk starts on a 256-byte boundary):
@@ -31,6 +33,15 @@ def padded_ld(rows: int) -> int:
     return max(LD_ALIGN, (rows + LD_ALIGN - 1) // LD_ALIGN * LD_ALIGN)
 
 
+def _to_device(arrays):
+    """Upload host arrays through pinned staging with asynchronous copies on the current
+    stream (the host does not wait for earlier queued GPU work).  Returns (device
+    tensors, pinned staging tensors that must stay alive until the copies ran)."""
+    t = device.torch()
+    staged = [t.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in arrays]
+    return [s.to("cuda", non_blocking=True) for s in staged], staged
+
+
 @dataclass
 class TPack:
     """Distinct T sets uploaded once: atoms sharing the same T objects share a set."""
@@ -42,6 +53,7 @@ class TPack:
     t_ab: object
     t_bb: object
     h2d_bytes: int
+    _staging: object = None
 
     @property
     def n_tsets(self) -> int:
@@ -49,8 +61,8 @@ class TPack:
 
 
 def pack_tmats(tmats) -> TPack:
-    """Deduplicate per-atom T blocks by identity and upload them (one H2D per family)."""
-    t = device.require_cuda()
+    """Deduplicate per-atom T blocks by identity and upload them (one H2D)."""
+    device.require_cuda()
     keys, index, reps = {}, [], []
     for a in range(tmats.atom_count):
         key = (id(tmats.t_aa[a]), id(tmats.t_ab[a]), id(tmats.t_bb[a]))
@@ -65,88 +77,16 @@ def pack_tmats(tmats) -> TPack:
         m = int(dims[s])
         for f, fam in enumerate((tmats.t_aa, tmats.t_ab, tmats.t_bb)):
             host[f, s, :m, :m] = fam[a].array.T  # (col, row) storage = column-major
-    dev = t.from_numpy(host).to("cuda")
+    (dev,), staged = _to_device([host])
     return TPack(np.array(index, dtype=np.int32), dims, t_ld, dev[0], dev[1], dev[2],
-                 host.nbytes)
-
-
-def build_device(*, n_basis, heights, row_offset, tpack: TPack, A, B, Bs, udot, ld,
-                 force_general_path, H, S, ldh, shard_rank=0, n_shards=1, workspace=None,
-                 ab_args=None, host_out=None):
-    """Run `hsdla_build_hs` (or `hsdla_setup_hs` when `ab_args` is given: A/B generation
-    fused in front) on device buffers; returns (result dict, workspace tensor)."""
-    lib = _native.load()
-    t = device.require_cuda()
-    na = len(heights)
-    h_arr = np.ascontiguousarray(heights, dtype=np.int32)
-    o_arr = np.ascontiguousarray(row_offset, dtype=np.int64)
-    ti = np.ascontiguousarray(tpack.t_index, dtype=np.int32)
-    td = np.ascontiguousarray(tpack.t_dim, dtype=np.int32)
-    args = _native.BuildArgs()
-    args.n_atoms = na
-    args.n_basis = n_basis
-    args.heights = h_arr.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
-    args.row_offset = o_arr.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
-    args.t_index = ti.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
-    args.n_tsets = tpack.n_tsets
-    args.t_dim = td.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
-    args.t_aa = tpack.t_aa.data_ptr()
-    args.t_ab = tpack.t_ab.data_ptr()
-    args.t_bb = tpack.t_bb.data_ptr()
-    args.t_ld = tpack.t_ld
-    args.A = A.data_ptr()
-    args.B = B.data_ptr()
-    args.B_scaled = Bs.data_ptr() if Bs is not None else None
-    args.udot_norms = udot.data_ptr() if udot is not None else None
-    args.ld = ld
-    args.force_general_path = 1 if force_general_path else 0
-    args.H = H.data_ptr()
-    args.S = S.data_ptr()
-    args.ldh = ldh
-    args.shard_rank = shard_rank
-    args.n_shards = n_shards
-    if host_out is not None:  # pinned (n, n) tensors: D2H overlapped inside the native call
-        args.H_host = host_out[0].data_ptr()
-        args.S_host = host_out[1].data_ptr()
-        args.ldh_host = int(host_out[0].shape[1])
-    need = lib.hsdla_build_workspace_size(ctypes.byref(args))
-    if workspace is None or workspace.numel() < need:
-        workspace = t.empty(max(need, 1), dtype=t.uint8, device="cuda")
-    args.workspace = workspace.data_ptr()
-    args.workspace_bytes = workspace.numel()
-    mask = (ctypes.c_int32 * na)()
-    info = (ctypes.c_int32 * tpack.n_tsets)()
-    res = _native.BuildResult()
-    res.hpd_mask = mask
-    res.chol_info = info
-    if ab_args is not None:
-        rc = lib.hsdla_setup_hs(device.ctx(), ctypes.byref(ab_args), ctypes.byref(args),
-                                ctypes.byref(res))
-    else:
-        rc = lib.hsdla_build_hs(device.ctx(), ctypes.byref(args), ctypes.byref(res))
-    if rc == _native.HSDLA_ERR_NAN_INPUT:
-        raise ContractViolationError("NaN in Cholesky input (lower triangle)")
-    if rc == _native.HSDLA_ERR_NONFINITE:
-        raise ContractViolationError("accumulator contains non-finite values")
-    _native.check(rc, "hsdla_build_hs")
-    out = {
-        "hpd_mask": [bool(mask[i]) for i in range(na)],
-        "chol_info": [int(info[i]) for i in range(tpack.n_tsets)],
-        "ms": {"setup": res.ms_setup, "S": res.ms_S, "H_ABBA_BB": res.ms_H_ABBA_BB,
-               "H_AA": res.ms_H_AA},
-        "kernel_ms": {"contract_S": res.ms_contract_S, "contract_H": res.ms_contract_H,
-                      "apply_Z": res.ms_apply_Z, "apply_XY": res.ms_apply_XY},
-        "workspace_bytes": int(need),
-        "ms_total": res.ms_total,
-    }
-    return out, workspace
+                 host.nbytes, staged)
 
 
 class DeviceSpec:
     """A SystemSpec's arrays in HBM (k-vectors, positions, rotations, radii, radial table)."""
 
     def __init__(self, spec):
-        t = device.require_cuda()
+        device.require_cuda()
         self.n_atoms = int(spec.n_atoms)
         self.n_basis = int(spec.n_basis)
         self.l_sph = np.ascontiguousarray(spec.l_sph, dtype=np.int32)
@@ -166,14 +106,13 @@ class DeviceSpec:
             radial[a, :n, 3] = rad.udot_prime[:n]
             radial[a, :n, 4] = rad.udot_norm[:n]
         self.radial_stride = stride
-        host = [np.ascontiguousarray(spec.k_vectors, dtype=np.float64),
-                np.ascontiguousarray(spec.positions, dtype=np.float64),
-                np.ascontiguousarray(np.asarray(spec.rotations, dtype=np.float64).reshape(-1, 9)),
-                np.ascontiguousarray(spec.mt_radius, dtype=np.float64),
-                radial]
+        host = [np.asarray(spec.k_vectors, dtype=np.float64),
+                np.asarray(spec.positions, dtype=np.float64),
+                np.asarray(spec.rotations, dtype=np.float64).reshape(-1, 9),
+                np.asarray(spec.mt_radius, dtype=np.float64), radial]
         self.h2d_bytes = int(sum(h.nbytes for h in host))
-        self.kv, self.pos, self.rot, self.rmt, self.radial = (
-            t.from_numpy(h).to("cuda", non_blocking=False) for h in host)
+        dev, self._staging = _to_device(host)
+        self.kv, self.pos, self.rot, self.rmt, self.radial = dev
         self.omega = float(spec.omega)
 
 
@@ -188,10 +127,8 @@ def make_ab_args(dspec: DeviceSpec, A, B, Bs, ld, udot) -> "_native.AbArgs":
     args.mt_radius = dspec.rmt.data_ptr()
     args.radial = dspec.radial.data_ptr()
     args.radial_stride = dspec.radial_stride
-    l_arr = dspec.l_sph
-    o_arr = dspec.row_offset
-    args.l_sph = l_arr.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
-    args.row_offset = o_arr.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+    args.l_sph = dspec.l_sph.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+    args.row_offset = dspec.row_offset.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
     args.omega = dspec.omega
     args.A = A.data_ptr()
     args.B = B.data_ptr()
@@ -206,6 +143,115 @@ def ab_generate_device(dspec: DeviceSpec, A, B, Bs, ld, udot):
     lib = _native.load()
     args = make_ab_args(dspec, A, B, Bs, ld, udot)
     _native.check(lib.hsdla_ab_generate(device.ctx(), ctypes.byref(args)), "hsdla_ab_generate")
+
+
+class _Call:
+    """Argument blocks of one native build call (kept alive while it is in flight)."""
+
+    def __init__(self, *, n_basis, heights, row_offset, tpack: TPack, A, B, Bs, udot, ld,
+                 force_general_path, H, S, ldh, shard_rank, n_shards, workspace, host_out,
+                 ab_args=None):
+        lib = _native.load()
+        t = device.torch()
+        self.na = len(heights)
+        self.n_tsets = tpack.n_tsets
+        self.keep = [np.ascontiguousarray(heights, dtype=np.int32),
+                     np.ascontiguousarray(row_offset, dtype=np.int64),
+                     np.ascontiguousarray(tpack.t_index, dtype=np.int32),
+                     np.ascontiguousarray(tpack.t_dim, dtype=np.int32), tpack, host_out, ab_args]
+        h_arr, o_arr, ti, td = self.keep[:4]
+        a = _native.BuildArgs()
+        a.n_atoms = self.na
+        a.n_basis = n_basis
+        a.heights = h_arr.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+        a.row_offset = o_arr.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+        a.t_index = ti.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+        a.n_tsets = tpack.n_tsets
+        a.t_dim = td.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+        a.t_aa = tpack.t_aa.data_ptr()
+        a.t_ab = tpack.t_ab.data_ptr()
+        a.t_bb = tpack.t_bb.data_ptr()
+        a.t_ld = tpack.t_ld
+        a.A = A.data_ptr()
+        a.B = B.data_ptr()
+        a.B_scaled = Bs.data_ptr() if Bs is not None else None
+        a.udot_norms = udot.data_ptr() if udot is not None else None
+        a.ld = ld
+        a.force_general_path = 1 if force_general_path else 0
+        a.H = H.data_ptr()
+        a.S = S.data_ptr()
+        a.ldh = ldh
+        a.shard_rank = shard_rank
+        a.n_shards = n_shards
+        if host_out is not None:  # pinned (n, n) tensors, row j = column j
+            a.H_host = host_out[0].data_ptr()
+            a.S_host = host_out[1].data_ptr()
+            a.ldh_host = int(host_out[0].shape[1])
+        self.need = lib.hsdla_build_workspace_size(ctypes.byref(a))
+        if workspace is None or workspace.numel() < self.need:
+            workspace = t.empty(max(self.need, 1), dtype=t.uint8, device="cuda")
+        self.workspace = workspace
+        a.workspace = workspace.data_ptr()
+        a.workspace_bytes = workspace.numel()
+        self.args = a
+        self.ab = ab_args
+        self.mask = (ctypes.c_int32 * self.na)()
+        self.info = (ctypes.c_int32 * self.n_tsets)()
+        self.res = _native.BuildResult()
+        self.res.hpd_mask = self.mask
+        self.res.chol_info = self.info
+
+    def result(self, rc: int) -> dict:
+        if rc == _native.HSDLA_ERR_NAN_INPUT:
+            raise ContractViolationError("NaN in Cholesky input (lower triangle)")
+        if rc == _native.HSDLA_ERR_NONFINITE:
+            raise ContractViolationError("accumulator contains non-finite values")
+        _native.check(rc, "hsdla_build_hs")
+        r = self.res
+        return {
+            "hpd_mask": [bool(self.mask[i]) for i in range(self.na)],
+            "chol_info": [int(self.info[i]) for i in range(self.n_tsets)],
+            "ms": {"setup": r.ms_setup, "S": r.ms_S, "H_ABBA_BB": r.ms_H_ABBA_BB,
+                   "H_AA": r.ms_H_AA},
+            "kernel_ms": {"contract_S": r.ms_contract_S, "contract_H": r.ms_contract_H,
+                          "apply_Z": r.ms_apply_Z, "apply_XY": r.ms_apply_XY},
+            "workspace_bytes": int(self.need),
+            "ms_total": r.ms_total,
+        }
+
+    def run_sync(self) -> dict:
+        lib = _native.load()
+        if self.ab is not None:
+            rc = lib.hsdla_setup_hs(device.ctx(), ctypes.byref(self.ab), ctypes.byref(self.args),
+                                    ctypes.byref(self.res))
+        else:
+            rc = lib.hsdla_build_hs(device.ctx(), ctypes.byref(self.args), ctypes.byref(self.res))
+        return self.result(rc)
+
+    def start(self) -> int:
+        lib = _native.load()
+        ticket = ctypes.c_ulonglong(0)
+        ab = ctypes.byref(self.ab) if self.ab is not None else None
+        _native.check(lib.hsdla_setup_hs_async(device.ctx(), ab, ctypes.byref(self.args),
+                                               ctypes.byref(ticket)), "hsdla_setup_hs_async")
+        return ticket.value
+
+    def finish(self, ticket: int) -> dict:
+        rc = _native.load().hsdla_build_finish(device.ctx(), ctypes.c_ulonglong(ticket),
+                                               ctypes.byref(self.res))
+        return self.result(rc)
+
+
+def build_device(*, n_basis, heights, row_offset, tpack: TPack, A, B, Bs, udot, ld,
+                 force_general_path, H, S, ldh, shard_rank=0, n_shards=1, workspace=None,
+                 ab_args=None, host_out=None):
+    """Synchronous `hsdla_build_hs` (or `hsdla_setup_hs` when `ab_args` is given: A/B
+    generation fused in front); returns (result dict, workspace tensor)."""
+    call = _Call(n_basis=n_basis, heights=heights, row_offset=row_offset, tpack=tpack, A=A, B=B,
+                 Bs=Bs, udot=udot, ld=ld, force_general_path=force_general_path, H=H, S=S,
+                 ldh=ldh, shard_rank=shard_rank, n_shards=n_shards, workspace=workspace,
+                 host_out=host_out, ab_args=ab_args)
+    return call.run_sync(), call.workspace
 
 
 class HSPipeline:
@@ -228,6 +274,7 @@ class HSPipeline:
         self.workspace = None
         self.shard_rank, self.n_shards = shard_rank, n_shards
         self.n_basis = 0
+        self._inflight = {}
 
     @property
     def device_bytes(self) -> int:
@@ -237,46 +284,54 @@ class HSPipeline:
             tot += self.workspace.numel()
         return int(tot)
 
-    def generate(self, dspec: DeviceSpec):
-        if dspec.n_basis > self.n_capacity or dspec.rows != self.rows:
-            raise ContractViolationError("spec shape does not fit the pipeline buffers")
-        self.n_basis = dspec.n_basis
-        ab_generate_device(dspec, self.A, self.B, self.Bs, self.ld, self.udot)
-
-    def build(self, dspec: DeviceSpec, tpack: TPack, force_general_path: bool = False):
-        res, self.workspace = build_device(
-            n_basis=dspec.n_basis, heights=dspec.heights, row_offset=dspec.row_offset, tpack=tpack,
-            A=self.A, B=self.B, Bs=self.Bs, udot=self.udot, ld=self.ld,
-            force_general_path=force_general_path, H=self.H, S=self.S, ldh=self.n_capacity,
-            shard_rank=self.shard_rank, n_shards=self.n_shards, workspace=self.workspace)
-        return res
-
-    def run(self, dspec: DeviceSpec, tpack: TPack, force_general_path: bool = False,
-            host_out=None):
-        """One k-point, spec -> H, S in HBM, as a single native call (`hsdla_setup_hs`).
-        With `host_out` = pinned (n, n) tensors, H and S are also copied to the host with the
-        copies overlapped with the remaining compute."""
+    def _call(self, dspec: DeviceSpec, tpack: TPack, force_general_path: bool, host_out):
         if dspec.n_basis > self.n_capacity or dspec.rows != self.rows:
             raise ContractViolationError("spec shape does not fit the pipeline buffers")
         self.n_basis = dspec.n_basis
         ab = make_ab_args(dspec, self.A, self.B, self.Bs, self.ld, None)
-        res, self.workspace = build_device(
-            n_basis=dspec.n_basis, heights=dspec.heights, row_offset=dspec.row_offset, tpack=tpack,
-            A=self.A, B=self.B, Bs=self.Bs, udot=self.udot, ld=self.ld,
-            force_general_path=force_general_path, H=self.H, S=self.S, ldh=self.n_capacity,
-            shard_rank=self.shard_rank, n_shards=self.n_shards, workspace=self.workspace,
-            ab_args=ab, host_out=host_out)
-        return res
+        call = _Call(n_basis=dspec.n_basis, heights=dspec.heights, row_offset=dspec.row_offset,
+                     tpack=tpack, A=self.A, B=self.B, Bs=self.Bs, udot=self.udot, ld=self.ld,
+                     force_general_path=force_general_path, H=self.H, S=self.S,
+                     ldh=self.n_capacity, shard_rank=self.shard_rank, n_shards=self.n_shards,
+                     workspace=self.workspace, host_out=host_out, ab_args=ab)
+        call.keep.append(dspec)
+        self.workspace = call.workspace
+        return call
+
+    def run(self, dspec: DeviceSpec, tpack: TPack, force_general_path: bool = False,
+            host_out=None) -> dict:
+        """One k-point, spec -> H, S in HBM (and in `host_out` pinned (n, n) tensors when
+        given), as a single synchronous native call (`hsdla_setup_hs`)."""
+        return self._call(dspec, tpack, force_general_path, host_out).run_sync()
+
+    def run_async(self, dspec: DeviceSpec, tpack: TPack, force_general_path: bool = False,
+                  host_out=None) -> int:
+        """Enqueue one k-point and return a ticket at once (`hsdla_setup_hs_async`).  At
+        most two k-points may be in flight; their `host_out` buffers must differ."""
+        call = self._call(dspec, tpack, force_general_path, host_out)
+        ticket = call.start()
+        self._inflight[ticket] = call
+        return ticket
+
+    def finish(self, ticket: int) -> dict:
+        """Wait for a k-point enqueued by `run_async` (compute and host copies)."""
+        return self._inflight.pop(ticket).finish(ticket)
 
     def launches_per_run(self, dspec: DeviceSpec) -> int:
-        """Kernels this pipeline launches per k-point (A/B + row-norm kernel per l group,
-        T prep, S contraction, Z apply, XY apply, H contraction)."""
+        """Kernels this pipeline launches per k-point (A/B per l group, T prep, S
+        contraction, Z apply, XY apply, H contraction)."""
         return len(np.unique(dspec.l_sph)) + 5
 
     def result_views(self):
         """Host-indexable (n, n) views: H[i, j] == tensor[j, i] (column-major storage)."""
         n = self.n_basis
         return self.H[:n, :n], self.S[:n, :n]
+
+
+def _pinned_pair(n: int):
+    t = device.torch()
+    return (t.empty((n, n), dtype=t.complex128, pin_memory=True),
+            t.empty((n, n), dtype=t.complex128, pin_memory=True))
 
 
 def build_hs(spec, tmats, config=None, *, pipeline: HSPipeline | None = None, host_out=None):
@@ -294,14 +349,58 @@ def build_hs(spec, tmats, config=None, *, pipeline: HSPipeline | None = None, ho
     dspec = DeviceSpec(spec)
     tpack = pack_tmats(tmats)
     pipe = pipeline or HSPipeline(spec.n_basis, dspec.heights)
-    t = device.torch()
     n = spec.n_basis
     if host_out is None or tuple(host_out[0].shape) != (n, n):
-        host_out = (t.empty((n, n), dtype=t.complex128, pin_memory=True),
-                    t.empty((n, n), dtype=t.complex128, pin_memory=True))
+        host_out = _pinned_pair(n)
     res = pipe.run(dspec, tpack, config.force_general_path, host_out=host_out)
-    h = ComplexDense(host_out[0].numpy().T)
-    s = ComplexDense(host_out[1].numpy().T)
     res["h2d_bytes"] = dspec.h2d_bytes + tpack.h2d_bytes
     res["d2h_bytes"] = 2 * 16 * n * n
-    return h, s, res
+    return ComplexDense(host_out[0].numpy().T), ComplexDense(host_out[1].numpy().T), res
+
+
+def build_hs_many(specs, tmats, config=None, *, pipeline: HSPipeline | None = None,
+                  on_result=None, host_buffers=None):
+    """A k-point batch (same crystal, T blocks shared): H and S of every k-point land in
+    pinned host memory, with k-point i's D2H copies overlapping k-point i+1's compute.
+
+    `on_result(index, H, S, result)` is called for each k-point as soon as it is complete
+    (H, S are `ComplexDense` views of double-buffered pinned memory, valid until the
+    callback returns).  Every k-point uploads its own spec (H2D) and T blocks are uploaded
+    once per batch.  Returns the list of result dicts."""
+    from .builder import BuildConfig
+    from .matrix import ComplexDense
+
+    config = config or BuildConfig()
+    specs = list(specs)
+    if not specs:
+        return []
+    n_cap = max(s.n_basis for s in specs)
+    tpack = pack_tmats(tmats)
+    first = DeviceSpec(specs[0])
+    pipe = pipeline or HSPipeline(n_cap, first.heights)
+    bufs = host_buffers if host_buffers is not None else {}
+    results = []
+    pending = None  # (index, ticket, host_out, dspec)
+    for i, spec in enumerate(specs):
+        dspec = first if i == 0 else DeviceSpec(spec)
+        n = spec.n_basis
+        key = (i % 2, n)
+        if key not in bufs:
+            bufs[key] = _pinned_pair(n)
+        ticket = pipe.run_async(dspec, tpack, config.force_general_path, host_out=bufs[key])
+        if pending is not None:
+            results.append(_complete(pipe, pending, tpack, on_result, ComplexDense))
+        pending = (i, ticket, bufs[key], dspec)
+    results.append(_complete(pipe, pending, tpack, on_result, ComplexDense))
+    return results
+
+
+def _complete(pipe, pending, tpack, on_result, ComplexDense):
+    i, ticket, host_out, dspec = pending
+    res = pipe.finish(ticket)
+    n = dspec.n_basis
+    res["h2d_bytes"] = dspec.h2d_bytes + (tpack.h2d_bytes if i == 0 else 0)
+    res["d2h_bytes"] = 2 * 16 * n * n
+    if on_result is not None:
+        on_result(i, ComplexDense(host_out[0].numpy().T), ComplexDense(host_out[1].numpy().T), res)
+    return res

@@ -121,6 +121,9 @@ namespace hsdla {
 // the persistent DMMA kernel.  `counter_slot` picks the tile counter to use.
 int launch_contract(hsdla_ctx* ctx, const std::vector<Prob>& probs,
                     const std::vector<Seg>& segs, int* flag_dev);
+// TMA + mbarrier variant (contract_tma.cu); `probs` already tiled (it_base, nchunks set).
+int launch_contract_tma(hsdla_ctx* ctx, const std::vector<Prob>& probs, long long total,
+                        const std::vector<Seg>& segs, int* flag_dev);
 // Arena helpers.
 int arena_begin(hsdla_ctx* ctx, size_t bytes);
 void* arena_push(hsdla_ctx* ctx, const void* src, size_t bytes, void** host_ptr);

@@ -1,0 +1,509 @@
+// TMA-fed variant of the multi-segment DMMA contraction (sm_100a).
+//
+// Same math, tiles, stream-K work split and epilogue as contract.cu (see there), but the
+// operand K-chunks arrive by TMA (cp.async.bulk.tensor, 128-byte swizzle) into a 3-stage
+// ring guarded by mbarriers instead of per-thread cp.async + __syncthreads:
+//   * one elected thread (warp 0, lane 0) is the producer: it issues the four box loads of
+//     chunk j+2 (P/Q x two 16-double k halves, 8 KB each) while chunk j is consumed, across
+//     tile and segment boundaries of the CTA's stream-K range;
+//   * consumer warps wait on the stage's `full` barrier (transaction-count completion) and
+//     release it through its `empty` barrier — no CTA-wide barrier per chunk, so one slow
+//     warp no longer stalls the others, and the DMMA warps execute no load-issue code.
+// Each operand of each segment is a 2-D tensor map over doubles: dim0 = 2k (the segment's
+// K extent, so K tails read as zeros), dim1 = columns (tile edges read as zeros).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <stdint.h>
+
+#include <map>
+#include <tuple>
+
+#include "common.cuh"
+
+namespace hsdla {
+namespace {
+
+constexpr int kT = 128;              // threads: 2x2 warps, 32x32 complex each
+constexpr int kStg = 3;
+constexpr int kBoxBytes = 64 * 128;  // 64 columns x 16 doubles
+constexpr int kStageBytes = 4 * kBoxBytes;
+constexpr size_t kSmemBytes = size_t(kStg) * kStageBytes + 1024 + 128;
+constexpr int kPartial = kTile * kTile * 2;
+constexpr int kIssueStep = 3;  // k'-step after which the producer refills the ring
+
+struct TSeg {
+  int mapP, mapPalt, mapQ;
+  int k;
+  const int* sel;
+};
+
+struct TKParams {
+  const Prob* probs;
+  const TSeg* segs;
+  const CUtensorMap* maps;
+  long long total_it;
+  int nprob;
+  int grid;
+  double* partials;
+  int* ready;
+  int* flag;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)),
+               "r"(bytes));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity));
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ long long range_start(long long total, int grid, int g) {
+  return total * g / grid;
+}
+
+__device__ __forceinline__ int locate_prob(const TKParams& sk, long long it) {
+  int lo = 0, hi = sk.nprob - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (sk.probs[mid].it_base <= it) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void tile_coords(const Prob& pr, int tile, int& tm, int& tn) {
+  if (pr.kind == PROB_GENERAL) {
+    tm = tile % pr.tiles_m;
+    tn = tile / pr.tiles_m;
+  } else {
+    const int nb = pr.tiles_m;
+    tn = pr.col_tile_lo;
+    while (tile >= nb - tn) { tile -= nb - tn; ++tn; }
+    tm = tn + tile;
+  }
+}
+
+// Producer-side walk over the CTA's (tile, chunk) sequence: the segment and K offset of
+// the next chunk to load.  Lives in one thread.
+struct ProdIter {
+  long long it, it_end;
+  int p, tile, c, nch, i0, j0, seg, send, kofs;
+
+  __device__ void seek(const TKParams& sk, long long it0, long long it1) {
+    it = it0;
+    it_end = it1;
+    if (it >= it_end) return;
+    p = locate_prob(sk, it);
+    const Prob& pr = sk.probs[p];
+    nch = pr.nchunks;
+    const long long local = it - pr.it_base;
+    tile = (int)(local / nch);
+    c = (int)(local - (long long)tile * nch);
+    set_tile(sk);
+    // walk segments to chunk c
+    int cb = 0;
+    for (; seg < send; ++seg) {
+      const int ncs = (sk.segs[seg].k + 15) / 16;
+      if (c < cb + ncs) { kofs = (c - cb) * 16; return; }
+      cb += ncs;
+    }
+    seg = pr.seg0;  // empty K: one chunk reading out of bounds (zeros)
+    kofs = 1 << 24;
+  }
+  __device__ void set_tile(const TKParams& sk) {
+    const Prob& pr = sk.probs[p];
+    int tm, tn;
+    tile_coords(pr, tile, tm, tn);
+    i0 = tm * kTile;
+    j0 = tn * kTile;
+    seg = pr.seg0;
+    send = pr.seg0 + pr.nseg;
+    kofs = 0;
+  }
+  __device__ void first_nonempty(const TKParams& sk) {
+    const int s0 = seg;
+    while (seg < send && sk.segs[seg].k <= 0) ++seg;
+    if (seg >= send) { seg = s0; kofs = 1 << 24; }
+  }
+  __device__ void next(const TKParams& sk) {
+    ++it;
+    if (it >= it_end) return;
+    ++c;
+    if (c == nch) {
+      c = 0;
+      ++tile;
+      if (tile == sk.probs[p].ntiles) {
+        ++p;
+        tile = 0;
+        nch = sk.probs[p].nchunks;
+      }
+      set_tile(sk);
+      first_nonempty(sk);
+      return;
+    }
+    kofs += 16;
+    if (kofs >= sk.segs[seg].k) {
+      int nx = seg + 1;
+      while (nx < send && sk.segs[nx].k <= 0) ++nx;
+      if (nx < send) { seg = nx; kofs = 0; }
+    }
+  }
+  __device__ void issue(const TKParams& sk, char* stage, uint64_t* full) {
+    const TSeg s = sk.segs[seg];
+    const int mp = (s.sel && *s.sel != 0) ? s.mapPalt : s.mapP;
+    const CUtensorMap* mP = sk.maps + mp;
+    const CUtensorMap* mQ = sk.maps + s.mapQ;
+    const int kd = 2 * kofs;
+    mbar_expect_tx(full, kStageBytes);
+    tma_load_2d(stage, mP, kd, i0, full);
+    tma_load_2d(stage + kBoxBytes, mP, kd + 16, i0, full);
+    tma_load_2d(stage + 2 * kBoxBytes, mQ, kd, j0, full);
+    tma_load_2d(stage + 3 * kBoxBytes, mQ, kd + 16, j0, full);
+  }
+};
+
+__device__ __forceinline__ bool finite2(double2 v) { return isfinite(v.x) && isfinite(v.y); }
+
+__global__ void __launch_bounds__(kT, 2) contract_tma_kernel(TKParams sk) {
+  extern __shared__ __align__(1024) char smem_raw[];
+  // 1024-byte alignment for the 128B-swizzled TMA boxes; indexing the shared array keeps
+  // the shared address space visible to the compiler (LDS, not generic loads).
+  char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStg * kStageBytes);
+  uint64_t* empty = full + kStg;
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int g = lane >> 2, q = lane & 3;
+  const unsigned sign_hi = (q & 1) ? 0x80000000u : 0u;
+  // K order inside a chunk is free (P and Q use the same one): in k'-step s4 of a 16-double
+  // box, lane q reads double 2*s4 + (q&1) + 8*(q>>1), so a half-warp touches 16 distinct
+  // bank pairs under the TMA 128B swizzle (16-B unit u of row c stored at u ^ (c & 7)).
+  // The re/im partner (double ^ 1) stays in the same 16-B unit: byte offset ^ 8.
+  const int fo = (((4 * (q >> 1)) ^ g) << 4) | ((q & 1) << 3);
+
+  const int cta = blockIdx.x;
+  const long long it0 = range_start(sk.total_it, sk.grid, cta);
+  const long long it_end = range_start(sk.total_it, sk.grid, cta + 1);
+  const long long nchunks_cta = it_end - it0;
+
+  if (tid == 0) {
+    for (int s = 0; s < kStg; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  ProdIter pi;
+  if (tid == 0) {
+    pi.seek(sk, it0, it_end);
+    for (int s = 0; s < kStg - 1 && s < nchunks_cta; ++s) {
+      pi.issue(sk, smem + s * kStageBytes, full + s);
+      pi.next(sk);
+    }
+  }
+
+  long long j = 0;  // chunks consumed by this CTA
+  long long it = it0;
+  while (it < it_end) {
+    const int pidx = locate_prob(sk, it);
+    const Prob pr = sk.probs[pidx];
+    const long long local = it - pr.it_base;
+    const int nch = pr.nchunks;
+    int tile = (int)(local / nch);
+    const int c_lo = (int)(local - (long long)tile * nch);
+    const long long left = it_end - it;
+    const int c_hi = (left < (long long)(nch - c_lo)) ? c_lo + (int)left : nch;
+    const long long tile_it_end = pr.it_base + (long long)(tile + 1) * nch;
+    int tm, tn;
+    tile_coords(pr, tile, tm, tn);
+    const int i0 = tm * kTile, j0 = tn * kTile;
+
+    double accR[4][4][2], accI[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        accR[a][b][0] = accR[a][b][1] = 0.0;
+        accI[a][b][0] = accI[a][b][1] = 0.0;
+      }
+
+    for (int cc = c_lo; cc < c_hi; ++cc, ++j) {
+      const int st = (int)(j % kStg);
+      mbar_wait(full + st, (uint32_t)((j / kStg) & 1));
+      const char* sP = smem + st * kStageBytes + (wm * 32 + g) * 128;
+      const char* sQ = smem + st * kStageBytes + 2 * kBoxBytes + (wn * 32 + g) * 128;
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const int boxo = (s >> 2) * kBoxBytes;
+        const int off = boxo + (fo ^ ((s & 3) << 4));
+        double a[4], br[4], bi[4];
+#pragma unroll
+        for (int ib = 0; ib < 4; ++ib)
+          a[ib] = *reinterpret_cast<const double*>(sP + ib * 8 * 128 + off);
+#pragma unroll
+        for (int jb = 0; jb < 4; ++jb) {
+          br[jb] = *reinterpret_cast<const double*>(sQ + jb * 8 * 128 + off);
+          const double x = *reinterpret_cast<const double*>(sQ + jb * 8 * 128 + (off ^ 8));
+          bi[jb] = __hiloint2double(__double2hiint(x) ^ sign_hi, __double2loint(x));
+        }
+#pragma unroll
+        for (int ib = 0; ib < 4; ++ib)
+#pragma unroll
+          for (int jb = 0; jb < 4; ++jb) {
+            dmma(accR[ib][jb][0], accR[ib][jb][1], a[ib], br[jb]);
+            dmma(accI[ib][jb][0], accI[ib][jb][1], a[ib], bi[jb]);
+          }
+        if (s == kIssueStep && tid == 0) {
+          // Producer, mid-chunk: by now the other warps have released chunk j-1 (whose stage
+          // chunk j+2 reuses), so the empty-barrier wait rarely blocks this warp.
+          const long long x = j + kStg - 1;
+          if (x < nchunks_cta) {
+            const int sx = (int)(x % kStg);
+            if (x >= kStg) mbar_wait(empty + sx, (uint32_t)(((x / kStg) - 1) & 1));
+            pi.issue(sk, smem + sx * kStageBytes, full + sx);
+            pi.next(sk);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + st);
+    }
+    it += c_hi - c_lo;
+
+    if (c_lo != 0) {
+      // Later piece of a split tile: publish the partial for the tile's finishing CTA.
+      double* slot = sk.partials + (long long)cta * kPartial;
+      int r = 0;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            __stcg(slot + (r++) * kT + tid, accR[a][b][v]);
+            __stcg(slot + (r++) * kT + tid, accI[a][b][v]);
+          }
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) atomicExch(sk.ready + cta, 1);
+      continue;
+    }
+    if (c_hi < nch) {
+      for (int jj = cta + 1; jj < sk.grid && range_start(sk.total_it, sk.grid, jj) < tile_it_end; ++jj) {
+        if (tid == 0) {
+          while (atomicAdd(sk.ready + jj, 0) == 0) __nanosleep(100);
+        }
+        __syncthreads();
+        const double* slot = sk.partials + (long long)jj * kPartial;
+        int r = 0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              accR[a][b][v] += __ldcg(slot + (r++) * kT + tid);
+              accI[a][b][v] += __ldcg(slot + (r++) * kT + tid);
+            }
+      }
+    }
+
+    bool bad = false;
+#pragma unroll
+    for (int ib = 0; ib < 4; ++ib) {
+      const int i = i0 + wm * 32 + ib * 8 + g;
+#pragma unroll
+      for (int jb = 0; jb < 4; ++jb) {
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int jcol = j0 + wn * 32 + jb * 8 + 2 * q + v;
+          double2 val = make_double2(accR[ib][jb][v], accI[ib][jb][v]);
+          if (pr.kind == PROB_GENERAL) {
+            if (i < pr.m && jcol < pr.n) {
+              double2* cp = pr.C + i + (long long)jcol * pr.ldC;
+              const double2 al = pr.alpha;
+              double2 out;
+              if (al.x == 1.0 && al.y == 0.0) {
+                out = val;
+              } else {
+                out.x = al.x * val.x - al.y * val.y;
+                out.y = al.x * val.y + al.y * val.x;
+              }
+              if (pr.accumulate) {
+                const double2 old = *cp;
+                const double2 be = pr.beta;
+                out.x += be.x * old.x - be.y * old.y;
+                out.y += be.x * old.y + be.y * old.x;
+              }
+              *cp = out;
+            }
+          } else if (i < pr.n && jcol < pr.n && i >= jcol) {
+            double2* cl = pr.C + i + (long long)jcol * pr.ldC;
+            if (pr.accumulate) {
+              const double2 old = *cl;
+              val.x += old.x;
+              val.y += old.y;
+            }
+            if (pr.kind == PROB_TRI_MIRROR) {
+              if (i == jcol) val.y = 0.0;
+              bad |= !finite2(val);
+              if (i > jcol) pr.C[jcol + (long long)i * pr.ldC] = make_double2(val.x, -val.y);
+            }
+            *cl = val;
+          }
+        }
+      }
+    }
+    if (bad) atomicOr(sk.flag, 1);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+}  // namespace
+
+int launch_contract_tma(hsdla_ctx* ctx, const std::vector<Prob>& probs, long long total,
+                        const std::vector<Seg>& segs, int* flag_dev) {
+  auto encode = get_encoder();
+  if (!encode) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return HSDLA_ERR_UNSUPPORTED;
+  }
+  // Tensor maps, deduplicated by (address, K extent, columns, leading dimension).
+  std::vector<CUtensorMap> maps;
+  std::map<std::tuple<const void*, long long, long long, long long>, int> cache;
+  auto map_of = [&](const double2* base, int k, int cols, long long ld, int* out) -> int {
+    const long long kk = k > 0 ? k : 1;
+    auto key = std::make_tuple((const void*)base, kk, (long long)cols, ld);
+    auto it = cache.find(key);
+    if (it != cache.end()) { *out = it->second; return HSDLA_OK; }
+    CUtensorMap m;
+    cuuint64_t dims[2] = {(cuuint64_t)(2 * kk), (cuuint64_t)cols};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 16};
+    cuuint32_t box[2] = {16, 64};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double2*>(base), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+      return HSDLA_ERR_CUDA;
+    }
+    *out = (int)maps.size();
+    cache[key] = *out;
+    maps.push_back(m);
+    return HSDLA_OK;
+  };
+  std::vector<TSeg> tsegs(segs.size());
+  for (const Prob& p : probs) {
+    for (int s = p.seg0; s < p.seg0 + p.nseg; ++s) {
+      const Seg& sg = segs[s];
+      TSeg& t = tsegs[s];
+      t.k = sg.k;
+      t.sel = sg.sel;
+      int rc = map_of(sg.P, sg.k, p.m, sg.ldP, &t.mapP);
+      if (rc) return rc;
+      t.mapPalt = t.mapP;
+      if (sg.P_alt) {
+        rc = map_of(sg.P_alt, sg.k, p.m, sg.ldP, &t.mapPalt);
+        if (rc) return rc;
+      }
+      rc = map_of(sg.Q, sg.k, p.n, sg.ldQ, &t.mapQ);
+      if (rc) return rc;
+    }
+  }
+  static bool attr = false;
+  if (!attr) {
+    HS_CUDA(cudaFuncSetAttribute(contract_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kSmemBytes));
+    attr = true;
+  }
+  int occ = 0;
+  HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, contract_tma_kernel, kT, kSmemBytes));
+  if (occ < 1) occ = 1;
+  long long grid_ll = (long long)ctx->num_sms * occ;
+  if (grid_ll > total) grid_ll = total;
+  const int grid = (int)grid_ll;
+  if (ctx->partial_slots < grid) {
+    HS_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->partials) cudaFree(ctx->partials);
+    if (ctx->ready) cudaFree(ctx->ready);
+    HS_CUDA(cudaMalloc(&ctx->partials, size_t(grid) * kPartial * sizeof(double)));
+    HS_CUDA(cudaMalloc(&ctx->ready, size_t(grid) * sizeof(int)));
+    ctx->partial_slots = grid;
+  }
+  int rc = arena_begin(ctx, probs.size() * sizeof(Prob) + tsegs.size() * sizeof(TSeg) +
+                                maps.size() * sizeof(CUtensorMap) + 512);
+  if (rc) return rc;
+  Prob* dprobs = static_cast<Prob*>(arena_push(ctx, probs.data(), probs.size() * sizeof(Prob), nullptr));
+  TSeg* dsegs = static_cast<TSeg*>(
+      arena_push(ctx, tsegs.data(), (tsegs.empty() ? 1 : tsegs.size()) * sizeof(TSeg), nullptr));
+  CUtensorMap* dmaps = static_cast<CUtensorMap*>(
+      arena_push(ctx, maps.data(), maps.size() * sizeof(CUtensorMap), nullptr));
+  rc = arena_flush(ctx);
+  if (rc) return rc;
+  HS_CUDA(cudaMemsetAsync(ctx->ready, 0, size_t(grid) * sizeof(int), ctx->stream));
+  TKParams sk;
+  sk.probs = dprobs;
+  sk.segs = dsegs;
+  sk.maps = dmaps;
+  sk.total_it = total;
+  sk.nprob = (int)probs.size();
+  sk.grid = grid;
+  sk.partials = ctx->partials;
+  sk.ready = ctx->ready;
+  sk.flag = flag_dev;
+  void* kargs[] = {&sk};
+  HS_CUDA(cudaLaunchCooperativeKernel((const void*)contract_tma_kernel, dim3(grid), dim3(kT), kargs,
+                                      kSmemBytes, ctx->stream));
+  return HSDLA_OK;
+}
+
+}  // namespace hsdla

@@ -61,11 +61,18 @@ void* arena_push(hsdla_ctx* ctx, const void* src, size_t bytes, void** host_ptr)
   return dev;
 }
 
+// Descriptors go up on a dedicated stream as soon as they are written, so the copy is not
+// queued behind earlier kernels of the compute stream; the compute stream only waits on an
+// event that has long completed by the time it gets there.  Ring regions are reused only
+// after a wrap, which synchronises the compute stream (and thereby every earlier upload).
 int arena_flush(hsdla_ctx* ctx) {
   size_t end = align_up(ctx->desc_off);
-  if (end > g_arena_start)
+  if (end > g_arena_start) {
     HS_CUDA(cudaMemcpyAsync(ctx->desc_dev + g_arena_start, ctx->stage_host + g_arena_start,
-                            end - g_arena_start, cudaMemcpyHostToDevice, ctx->stream));
+                            end - g_arena_start, cudaMemcpyHostToDevice, ctx->upload));
+    HS_CUDA(cudaEventRecord(ctx->upload_done, ctx->upload));
+    HS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->upload_done, 0));
+  }
   ctx->desc_off = end;
   return HSDLA_OK;
 }
@@ -138,6 +145,8 @@ int hsdla_ctx_create(hsdla_ctx** out, void* stream) {
   HS_CUDA(cudaEventCreateWithFlags(&c->stage_done, cudaEventDisableTiming));
   HS_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   HS_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+  HS_CUDA(cudaStreamCreateWithFlags(&c->upload, cudaStreamNonBlocking));
+  HS_CUDA(cudaEventCreateWithFlags(&c->upload_done, cudaEventDisableTiming));
   HS_CUDA(cudaEventCreateWithFlags(&c->copy_go, cudaEventDisableTiming));
   for (int k = 0; k < 2; ++k) {
     auto& sl = c->slots[k];
@@ -149,6 +158,8 @@ int hsdla_ctx_create(hsdla_ctx** out, void* stream) {
     sl.host_area = c->scratch_host + 128 + 100 * k;  // [0] flag, [1..96] info
     sl.host_area_dev = c->scratch_host_dev + 128 + 100 * k;
   }
+  HS_CUDA(cudaEventCreate(&c->epoch));
+  HS_CUDA(cudaEventRecord(c->epoch, c->stream));
   HS_CUDA(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
   HS_CUDA(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
   *out = c;
@@ -176,6 +187,9 @@ int hsdla_ctx_destroy(hsdla_ctx* c) {
   }
   cudaEventDestroy(c->copy_go);
   cudaStreamDestroy(c->copy);
+  cudaStreamSynchronize(c->upload);
+  cudaEventDestroy(c->upload_done);
+  cudaStreamDestroy(c->upload);
   if (c->partials) cudaFree(c->partials);
   if (c->ready) cudaFree(c->ready);
   delete c;
@@ -418,6 +432,15 @@ int complete_slot(hsdla_ctx* ctx, hsdla_ctx::BuildSlot& sl, hsdla_ctx::Outcome* 
   cudaEventElapsedTime(&t46, ev[4], ev[6]);
   cudaEventElapsedTime(&t07, ev[0], ev[7]);
   o->ms[0] = t01; o->ms[1] = t12; o->ms[2] = t23; o->ms[3] = t34; o->ms[4] = t46; o->ms[5] = t07;
+  if (getenv("HSDLA_TIMELINE")) {  // debug: absolute build timeline vs the context epoch
+    float a0 = 0, a7 = 0, a2 = 0, a6 = 0;
+    cudaEventElapsedTime(&a0, ctx->epoch, ev[0]);
+    cudaEventElapsedTime(&a2, ctx->epoch, ev[2]);
+    cudaEventElapsedTime(&a6, ctx->epoch, ev[6]);
+    cudaEventElapsedTime(&a7, ctx->epoch, ev[7]);
+    fprintf(stderr, "build %llu: start %.3f S-done %.3f H-done %.3f end %.3f ms\n", sl.ticket, a0, a2,
+            a6, a7);
+  }
   o->rc = nan_input ? HSDLA_ERR_NAN_INPUT : (o->nonfinite ? HSDLA_ERR_NONFINITE : HSDLA_OK);
   return o->rc;
 }

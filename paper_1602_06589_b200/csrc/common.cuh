@@ -76,6 +76,8 @@ struct hsdla_ctx {
   cudaStream_t side = nullptr;  // T preparation overlaps A/B generation here
   cudaStream_t copy = nullptr;  // D2H of finished H / S, overlapped with later compute
   cudaEvent_t copy_go = nullptr;
+  cudaStream_t upload = nullptr;  // descriptor H2D, ahead of the compute stream
+  cudaEvent_t upload_done = nullptr;
   // Two in-flight builds (k-point pipelining): per-build events, flag and read-back area.
   struct BuildSlot {
     cudaEvent_t ev[8] = {};
@@ -97,6 +99,7 @@ struct hsdla_ctx {
   };
   std::map<unsigned long long, Outcome> stash;
   cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t epoch = nullptr;  // recorded at creation (debug timelines)
   int device = 0;
   int num_sms = 148;
   // stream-K fix-up workspace: per-CTA partial tiles and ready flags

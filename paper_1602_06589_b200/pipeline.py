@@ -33,13 +33,29 @@ def padded_ld(rows: int) -> int:
     return max(LD_ALIGN, (rows + LD_ALIGN - 1) // LD_ALIGN * LD_ALIGN)
 
 
+_UPLOAD = {}
+
+
 def _to_device(arrays):
-    """Upload host arrays through pinned staging with asynchronous copies on the current
-    stream (the host does not wait for earlier queued GPU work).  Returns (device
+    """Upload host arrays through pinned staging on a dedicated upload stream, so the
+    copies run at once instead of queueing behind kernels already enqueued on the compute
+    stream (k-point pipelining); the compute stream waits on an event.  Returns (device
     tensors, pinned staging tensors that must stay alive until the copies ran)."""
     t = device.torch()
+    dev = t.cuda.current_device()
+    up = _UPLOAD.get(dev)
+    if up is None:
+        up = _UPLOAD[dev] = t.cuda.Stream()
+    main = t.cuda.current_stream()
     staged = [t.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in arrays]
-    return [s.to("cuda", non_blocking=True) for s in staged], staged
+    with t.cuda.stream(up):
+        out = [s.to("cuda", non_blocking=True) for s in staged]
+        done = t.cuda.Event()
+        done.record(up)
+    main.wait_event(done)
+    for o in out:
+        o.record_stream(main)
+    return out, staged
 
 
 @dataclass

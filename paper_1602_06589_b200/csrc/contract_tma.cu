@@ -16,6 +16,9 @@
 #include <cudaTypedefs.h>
 #include <stdint.h>
 
+#include <stdlib.h>
+
+#include <algorithm>
 #include <map>
 #include <tuple>
 
@@ -24,12 +27,24 @@
 namespace hsdla {
 namespace {
 
-constexpr int kT = 128;              // threads: 2x2 warps, 32x32 complex each
 constexpr int kStg = 3;
-constexpr int kBoxBytes = 64 * 128;  // 64 columns x 16 doubles
-constexpr int kStageBytes = 4 * kBoxBytes;
-constexpr size_t kSmemBytes = size_t(kStg) * kStageBytes + 1024 + 128;
-constexpr int kPartial = kTile * kTile * 2;
+
+// Tile configuration: WM x WN warps, each 32 rows x 8*JB columns (complex); the output
+// tile is TM x TN.  Cfg<2,2,4> = 64x64 (4 warps, ~250 registers, every triangular problem);
+// Cfg<3,2,2> = 96x32 (6 warps, ~128 registers) for the T applications when 64 < m <= 96
+// (m = 81 at l_sph = 8: 84% of the rows useful instead of 63% with 64-row tiles).
+template <int WM_, int WN_, int JB_>
+struct Cfg {
+  static constexpr int WM = WM_, WN = WN_, JB = JB_;
+  static constexpr int TM = 32 * WM, TN = 8 * JB * WN;
+  static constexpr int kT = 32 * WM * WN;
+  static constexpr int kPBox = TM * 128, kQBox = TN * 128;  // box = columns x 16 doubles
+  static constexpr int kStageBytes = 2 * (kPBox + kQBox);
+  static constexpr size_t kSmemBytes = size_t(kStg) * kStageBytes + 1024 + 128;
+  static constexpr int kPartial = TM * TN * 2;
+};
+using Cfg64 = Cfg<2, 2, 4>;
+using Cfg96 = Cfg<3, 2, 2>;
 constexpr int kIssueStep = 3;  // k'-step after which the producer refills the ring
 
 struct TSeg {
@@ -119,6 +134,7 @@ struct ProdIter {
   long long it, it_end;
   int p, tile, c, nch, i0, j0, seg, send, kofs;
 
+  template <class C>
   __device__ void seek(const TKParams& sk, long long it0, long long it1) {
     it = it0;
     it_end = it1;
@@ -129,7 +145,7 @@ struct ProdIter {
     const long long local = it - pr.it_base;
     tile = (int)(local / nch);
     c = (int)(local - (long long)tile * nch);
-    set_tile(sk);
+    set_tile<C>(sk);
     // walk segments to chunk c
     int cb = 0;
     for (; seg < send; ++seg) {
@@ -140,12 +156,13 @@ struct ProdIter {
     seg = pr.seg0;  // empty K: one chunk reading out of bounds (zeros)
     kofs = 1 << 24;
   }
+  template <class C>
   __device__ void set_tile(const TKParams& sk) {
     const Prob& pr = sk.probs[p];
     int tm, tn;
     tile_coords(pr, tile, tm, tn);
-    i0 = tm * kTile;
-    j0 = tn * kTile;
+    i0 = tm * C::TM;
+    j0 = tn * C::TN;
     seg = pr.seg0;
     send = pr.seg0 + pr.nseg;
     kofs = 0;
@@ -155,6 +172,7 @@ struct ProdIter {
     while (seg < send && sk.segs[seg].k <= 0) ++seg;
     if (seg >= send) { seg = s0; kofs = 1 << 24; }
   }
+  template <class C>
   __device__ void next(const TKParams& sk) {
     ++it;
     if (it >= it_end) return;
@@ -167,7 +185,7 @@ struct ProdIter {
         tile = 0;
         nch = sk.probs[p].nchunks;
       }
-      set_tile(sk);
+      set_tile<C>(sk);
       first_nonempty(sk);
       return;
     }
@@ -178,23 +196,26 @@ struct ProdIter {
       if (nx < send) { seg = nx; kofs = 0; }
     }
   }
+  template <class C>
   __device__ void issue(const TKParams& sk, char* stage, uint64_t* full) {
     const TSeg s = sk.segs[seg];
     const int mp = (s.sel && *s.sel != 0) ? s.mapPalt : s.mapP;
     const CUtensorMap* mP = sk.maps + mp;
     const CUtensorMap* mQ = sk.maps + s.mapQ;
     const int kd = 2 * kofs;
-    mbar_expect_tx(full, kStageBytes);
+    mbar_expect_tx(full, C::kStageBytes);
     tma_load_2d(stage, mP, kd, i0, full);
-    tma_load_2d(stage + kBoxBytes, mP, kd + 16, i0, full);
-    tma_load_2d(stage + 2 * kBoxBytes, mQ, kd, j0, full);
-    tma_load_2d(stage + 3 * kBoxBytes, mQ, kd + 16, j0, full);
+    tma_load_2d(stage + C::kPBox, mP, kd + 16, i0, full);
+    tma_load_2d(stage + 2 * C::kPBox, mQ, kd, j0, full);
+    tma_load_2d(stage + 2 * C::kPBox + C::kQBox, mQ, kd + 16, j0, full);
   }
 };
 
 __device__ __forceinline__ bool finite2(double2 v) { return isfinite(v.x) && isfinite(v.y); }
 
-__global__ void __launch_bounds__(kT, 2) contract_tma_kernel(TKParams sk) {
+template <class C>
+__global__ void __launch_bounds__(C::kT, 2) contract_tma_kernel(TKParams sk) {
+  constexpr int kT = C::kT, JB = C::JB, kStageBytes = C::kStageBytes, kPartial = C::kPartial;
   extern __shared__ __align__(1024) char smem_raw[];
   // 1024-byte alignment for the 128B-swizzled TMA boxes; indexing the shared array keeps
   // the shared address space visible to the compiler (LDS, not generic loads).
@@ -205,7 +226,7 @@ __global__ void __launch_bounds__(kT, 2) contract_tma_kernel(TKParams sk) {
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  const int wm = warp & 1, wn = warp >> 1;
+  const int wm = warp % C::WM, wn = warp / C::WM;
   const int g = lane >> 2, q = lane & 3;
   const unsigned sign_hi = (q & 1) ? 0x80000000u : 0u;
   // K order inside a chunk is free (P and Q use the same one): in k'-step s4 of a 16-double
@@ -222,7 +243,7 @@ __global__ void __launch_bounds__(kT, 2) contract_tma_kernel(TKParams sk) {
   if (tid == 0) {
     for (int s = 0; s < kStg; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, 4);
+      mbar_init(empty + s, C::WM * C::WN);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -231,10 +252,10 @@ __global__ void __launch_bounds__(kT, 2) contract_tma_kernel(TKParams sk) {
 
   ProdIter pi;
   if (tid == 0) {
-    pi.seek(sk, it0, it_end);
+    pi.seek<C>(sk, it0, it_end);
     for (int s = 0; s < kStg - 1 && s < nchunks_cta; ++s) {
-      pi.issue(sk, smem + s * kStageBytes, full + s);
-      pi.next(sk);
+      pi.issue<C>(sk, smem + s * kStageBytes, full + s);
+      pi.next<C>(sk);
     }
   }
 
@@ -252,13 +273,13 @@ __global__ void __launch_bounds__(kT, 2) contract_tma_kernel(TKParams sk) {
     const long long tile_it_end = pr.it_base + (long long)(tile + 1) * nch;
     int tm, tn;
     tile_coords(pr, tile, tm, tn);
-    const int i0 = tm * kTile, j0 = tn * kTile;
+    const int i0 = tm * C::TM, j0 = tn * C::TN;
 
-    double accR[4][4][2], accI[4][4][2];
+    double accR[4][JB][2], accI[4][JB][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
+      for (int b = 0; b < JB; ++b) {
         accR[a][b][0] = accR[a][b][1] = 0.0;
         accI[a][b][0] = accI[a][b][1] = 0.0;
       }
@@ -267,25 +288,26 @@ __global__ void __launch_bounds__(kT, 2) contract_tma_kernel(TKParams sk) {
       const int st = (int)(j % kStg);
       mbar_wait(full + st, (uint32_t)((j / kStg) & 1));
       const char* sP = smem + st * kStageBytes + (wm * 32 + g) * 128;
-      const char* sQ = smem + st * kStageBytes + 2 * kBoxBytes + (wn * 32 + g) * 128;
+      const char* sQ = smem + st * kStageBytes + 2 * C::kPBox + (wn * 8 * JB + g) * 128;
 #pragma unroll
       for (int s = 0; s < 8; ++s) {
-        const int boxo = (s >> 2) * kBoxBytes;
-        const int off = boxo + (fo ^ ((s & 3) << 4));
-        double a[4], br[4], bi[4];
+        const int off = fo ^ ((s & 3) << 4);
+        const char* pA = sP + (s >> 2) * C::kPBox;
+        const char* pB = sQ + (s >> 2) * C::kQBox;
+        double a[4], br[JB], bi[JB];
 #pragma unroll
         for (int ib = 0; ib < 4; ++ib)
-          a[ib] = *reinterpret_cast<const double*>(sP + ib * 8 * 128 + off);
+          a[ib] = *reinterpret_cast<const double*>(pA + ib * 8 * 128 + off);
 #pragma unroll
-        for (int jb = 0; jb < 4; ++jb) {
-          br[jb] = *reinterpret_cast<const double*>(sQ + jb * 8 * 128 + off);
-          const double x = *reinterpret_cast<const double*>(sQ + jb * 8 * 128 + (off ^ 8));
+        for (int jb = 0; jb < JB; ++jb) {
+          br[jb] = *reinterpret_cast<const double*>(pB + jb * 8 * 128 + off);
+          const double x = *reinterpret_cast<const double*>(pB + jb * 8 * 128 + (off ^ 8));
           bi[jb] = __hiloint2double(__double2hiint(x) ^ sign_hi, __double2loint(x));
         }
 #pragma unroll
         for (int ib = 0; ib < 4; ++ib)
 #pragma unroll
-          for (int jb = 0; jb < 4; ++jb) {
+          for (int jb = 0; jb < JB; ++jb) {
             dmma(accR[ib][jb][0], accR[ib][jb][1], a[ib], br[jb]);
             dmma(accI[ib][jb][0], accI[ib][jb][1], a[ib], bi[jb]);
           }
@@ -296,8 +318,8 @@ __global__ void __launch_bounds__(kT, 2) contract_tma_kernel(TKParams sk) {
           if (x < nchunks_cta) {
             const int sx = (int)(x % kStg);
             if (x >= kStg) mbar_wait(empty + sx, (uint32_t)(((x / kStg) - 1) & 1));
-            pi.issue(sk, smem + sx * kStageBytes, full + sx);
-            pi.next(sk);
+            pi.issue<C>(sk, smem + sx * kStageBytes, full + sx);
+            pi.next<C>(sk);
           }
         }
       }
@@ -313,7 +335,7 @@ __global__ void __launch_bounds__(kT, 2) contract_tma_kernel(TKParams sk) {
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
+        for (int b = 0; b < JB; ++b)
 #pragma unroll
           for (int v = 0; v < 2; ++v) {
             __stcg(slot + (r++) * kT + tid, accR[a][b][v]);
@@ -335,7 +357,7 @@ __global__ void __launch_bounds__(kT, 2) contract_tma_kernel(TKParams sk) {
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
-          for (int b = 0; b < 4; ++b)
+          for (int b = 0; b < JB; ++b)
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
               accR[a][b][v] += __ldcg(slot + (r++) * kT + tid);
@@ -349,10 +371,10 @@ __global__ void __launch_bounds__(kT, 2) contract_tma_kernel(TKParams sk) {
     for (int ib = 0; ib < 4; ++ib) {
       const int i = i0 + wm * 32 + ib * 8 + g;
 #pragma unroll
-      for (int jb = 0; jb < 4; ++jb) {
+      for (int jb = 0; jb < JB; ++jb) {
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-          const int jcol = j0 + wn * 32 + jb * 8 + 2 * q + v;
+          const int jcol = j0 + wn * 8 * JB + jb * 8 + 2 * q + v;
           double2 val = make_double2(accR[ib][jb][v], accI[ib][jb][v]);
           if (pr.kind == PROB_GENERAL) {
             if (i < pr.m && jcol < pr.n) {
@@ -408,25 +430,53 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encoder() {
 
 }  // namespace
 
-int launch_contract_tma(hsdla_ctx* ctx, const std::vector<Prob>& probs, long long total,
-                        const std::vector<Seg>& segs, int* flag_dev) {
+namespace {
+template <class C>
+int launch_cfg(hsdla_ctx* ctx, const std::vector<Prob>& probs_in, const std::vector<Seg>& segs,
+               int* flag_dev) {
   auto encode = get_encoder();
   if (!encode) {
     set_error("cuTensorMapEncodeTiled unavailable");
     return HSDLA_ERR_UNSUPPORTED;
   }
-  // Tensor maps, deduplicated by (address, K extent, columns, leading dimension).
+  // Stream-K iteration space with this configuration's tile shape.
+  std::vector<Prob> probs;
+  long long total = 0;
+  for (Prob p : probs_in) {
+    if (p.m <= 0 || p.n <= 0) continue;
+    p.tiles_m = (p.m + C::TM - 1) / C::TM;
+    p.tiles_n = (p.n + C::TN - 1) / C::TN;
+    if (p.kind != PROB_GENERAL) {
+      if (C::TM != C::TN) {
+        set_error("triangular problems need square tiles");
+        return HSDLA_ERR_UNSUPPORTED;
+      }
+      p.tiles_n = p.tiles_m;
+      if (p.col_tile_hi <= 0 || p.col_tile_hi > p.tiles_m) p.col_tile_hi = p.tiles_m;
+      if (p.col_tile_lo < 0) p.col_tile_lo = 0;
+    }
+    p.ntiles = prob_tile_count(p);
+    int nch = 0;
+    for (int s = 0; s < p.nseg; ++s) nch += (segs[p.seg0 + s].k + 15) / 16;
+    p.nchunks = nch > 0 ? nch : 1;
+    p.it_base = total;
+    total += (long long)p.ntiles * p.nchunks;
+    if (p.ntiles > 0) probs.push_back(p);
+  }
+  if (total == 0) return HSDLA_OK;
+  // Tensor maps, deduplicated by (address, K extent, columns, leading dimension, box rows).
   std::vector<CUtensorMap> maps;
-  std::map<std::tuple<const void*, long long, long long, long long>, int> cache;
-  auto map_of = [&](const double2* base, int k, int cols, long long ld, int* out) -> int {
+  std::map<std::tuple<const void*, long long, long long, long long, int>, int> cache;
+  auto map_of = [&](const double2* base, int k, int cols, long long ld, int box_cols,
+                    int* out) -> int {
     const long long kk = k > 0 ? k : 1;
-    auto key = std::make_tuple((const void*)base, kk, (long long)cols, ld);
+    auto key = std::make_tuple((const void*)base, kk, (long long)cols, ld, box_cols);
     auto it = cache.find(key);
     if (it != cache.end()) { *out = it->second; return HSDLA_OK; }
     CUtensorMap m;
     cuuint64_t dims[2] = {(cuuint64_t)(2 * kk), (cuuint64_t)cols};
     cuuint64_t strides[1] = {(cuuint64_t)ld * 16};
-    cuuint32_t box[2] = {16, 64};
+    cuuint32_t box[2] = {16, (cuuint32_t)box_cols};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double2*>(base), dims,
                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -448,34 +498,37 @@ int launch_contract_tma(hsdla_ctx* ctx, const std::vector<Prob>& probs, long lon
       TSeg& t = tsegs[s];
       t.k = sg.k;
       t.sel = sg.sel;
-      int rc = map_of(sg.P, sg.k, p.m, sg.ldP, &t.mapP);
+      int rc = map_of(sg.P, sg.k, p.m, sg.ldP, C::TM, &t.mapP);
       if (rc) return rc;
       t.mapPalt = t.mapP;
       if (sg.P_alt) {
-        rc = map_of(sg.P_alt, sg.k, p.m, sg.ldP, &t.mapPalt);
+        rc = map_of(sg.P_alt, sg.k, p.m, sg.ldP, C::TM, &t.mapPalt);
         if (rc) return rc;
       }
-      rc = map_of(sg.Q, sg.k, p.n, sg.ldQ, &t.mapQ);
+      rc = map_of(sg.Q, sg.k, p.n, sg.ldQ, C::TN, &t.mapQ);
       if (rc) return rc;
     }
   }
   static bool attr = false;
   if (!attr) {
-    HS_CUDA(cudaFuncSetAttribute(contract_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kSmemBytes));
+    HS_CUDA(cudaFuncSetAttribute(contract_tma_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)C::kSmemBytes));
     attr = true;
   }
   int occ = 0;
-  HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, contract_tma_kernel, kT, kSmemBytes));
+  HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, contract_tma_kernel<C>, C::kT,
+                                                        C::kSmemBytes));
   if (occ < 1) occ = 1;
   long long grid_ll = (long long)ctx->num_sms * occ;
   if (grid_ll > total) grid_ll = total;
   const int grid = (int)grid_ll;
+  constexpr int kSlot = kTile * kTile * 2;  // partial slot stride covers every configuration
+  static_assert(C::kPartial <= kSlot, "partial tile larger than a slot");
   if (ctx->partial_slots < grid) {
     HS_CUDA(cudaStreamSynchronize(ctx->stream));
     if (ctx->partials) cudaFree(ctx->partials);
     if (ctx->ready) cudaFree(ctx->ready);
-    HS_CUDA(cudaMalloc(&ctx->partials, size_t(grid) * kPartial * sizeof(double)));
+    HS_CUDA(cudaMalloc(&ctx->partials, size_t(grid) * kSlot * sizeof(double)));
     HS_CUDA(cudaMalloc(&ctx->ready, size_t(grid) * sizeof(int)));
     ctx->partial_slots = grid;
   }
@@ -501,9 +554,30 @@ int launch_contract_tma(hsdla_ctx* ctx, const std::vector<Prob>& probs, long lon
   sk.ready = ctx->ready;
   sk.flag = flag_dev;
   void* kargs[] = {&sk};
-  HS_CUDA(cudaLaunchCooperativeKernel((const void*)contract_tma_kernel, dim3(grid), dim3(kT), kargs,
-                                      kSmemBytes, ctx->stream));
+  HS_CUDA(cudaLaunchCooperativeKernel((const void*)contract_tma_kernel<C>, dim3(grid), dim3(C::kT),
+                                      kargs, C::kSmemBytes, ctx->stream));
   return HSDLA_OK;
+}
+}  // namespace
+
+int launch_contract_tma(hsdla_ctx* ctx, const std::vector<Prob>& probs, long long total,
+                        const std::vector<Seg>& segs, int* flag_dev) {
+  (void)total;
+  // General (T-application) problems with 64 < m <= 96 run on 96 x 32 tiles.
+  static int apply_tile = -1;
+  if (apply_tile < 0) {
+    const char* e = getenv("HSDLA_APPLY_TILE");
+    apply_tile = (e && atoi(e) == 64) ? 64 : 96;
+  }
+  bool general = !probs.empty();
+  int max_m = 0;
+  for (const Prob& p : probs) {
+    general = general && p.kind == PROB_GENERAL;
+    max_m = std::max(max_m, p.m);
+  }
+  if (general && apply_tile == 96 && max_m > 64 && max_m <= 96)
+    return launch_cfg<Cfg96>(ctx, probs, segs, flag_dev);
+  return launch_cfg<Cfg64>(ctx, probs, segs, flag_dev);
 }
 
 }  // namespace hsdla

@@ -1,0 +1,290 @@
+"""GPU tests restating the reference suite's operator and phase contracts
+(pkg/tests/test_kernels.py and test_builder.py) against the B200 implementation, plus the
+column-panel sharded build (the multi-GPU tile partition) emulated rank by rank on one GPU."""
+import numpy as np
+import pytest
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+from conftest import hermitian_from_lower, rand_complex, rel_fro
+from oracle import build as ob
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg(cuda):
+    import paper_1602_06589_b200 as p
+
+    p._native.load()
+    return p
+
+
+# -- operator contracts (test_kernels.py) ----------------------------------------------
+
+def test_herk_single_row_rank_one(pkg):
+    c = pkg.HermitianAccumulator(2)
+    led = pkg.FlopLedger()
+    pkg.get_backend().hermitian_rank_k_update(c, pkg.ComplexDense.from_array([[1.0 + 0j, 1.0j]]),
+                                              led)
+    arr = c.matrix.array
+    assert arr[0, 0] == 1.0 and arr[1, 0] == -1.0j and arr[1, 1] == 1.0
+    assert led.hermitian_rank_k == 4 * 1 * 2 * 2
+
+
+def test_zero_updates_leave_c(pkg):
+    rng = np.random.default_rng(2)
+    c = pkg.HermitianAccumulator(3)
+    vals = np.tril(rand_complex(rng, 3, 3))
+    c.matrix.array[:] = vals
+    be = pkg.get_backend()
+    be.hermitian_rank_k_update(c, pkg.ComplexDense.zeros(4, 3), pkg.FlopLedger())
+    be.hermitian_rank_2k_update(c, pkg.ComplexDense.zeros(4, 3),
+                                pkg.ComplexDense.from_array(rand_complex(rng, 4, 3)),
+                                pkg.FlopLedger())
+    np.testing.assert_array_equal(c.matrix.array, vals)
+
+
+def test_gemm_identity_and_alpha_zero(pkg):
+    rng = np.random.default_rng(11)
+    be = pkg.get_backend()
+    b_vals = rand_complex(rng, 3, 5)
+    c = pkg.ComplexDense.from_array(rand_complex(rng, 3, 5))
+    be.general_product(c, pkg.ComplexDense.from_array(np.eye(3, dtype=complex)),
+                       pkg.ComplexDense.from_array(b_vals), False, 1.0, 0.0, pkg.FlopLedger())
+    np.testing.assert_allclose(c.array, b_vals, rtol=1e-15)
+    c0 = rand_complex(rng, 2, 3)
+    c = pkg.ComplexDense.from_array(c0)
+    be.general_product(c, pkg.ComplexDense.from_array(rand_complex(rng, 2, 4)),
+                       pkg.ComplexDense.from_array(rand_complex(rng, 4, 3)), False, 0.0, 1.0,
+                       pkg.FlopLedger())
+    np.testing.assert_allclose(c.array, c0, rtol=1e-15)
+
+
+def test_hemm_empty_non_accumulate_zeroes_and_diag(pkg):
+    be = pkg.get_backend()
+    d = np.array([2.0, -1.0, 0.5])
+    a = np.array([[1.0 + 1.0j], [2.0 - 1.0j], [3.0 + 0.5j]])
+    x = pkg.ComplexDense.zeros(3, 1)
+    be.hermitian_product(x, pkg.ComplexDense.from_array(np.diag(d)), pkg.ComplexDense.from_array(a),
+                         False, 1.0, pkg.FlopLedger())
+    np.testing.assert_allclose(x.array, d[:, None] * a, rtol=1e-15)
+    x = pkg.ComplexDense.from_array(np.ones((3, 0), dtype=complex))
+    led = pkg.FlopLedger()
+    be.hermitian_product(x, pkg.ComplexDense.from_array(np.eye(3) + 0j),
+                         pkg.ComplexDense.from_array(np.ones((3, 0), dtype=complex)), False, 1.0, led)
+    assert led.hermitian_product == 0
+
+
+def test_trmm_one_by_one_conjugates(pkg):
+    c00 = 2.0 - 3.0j
+    a = np.array([[1.0 + 1.0j, -2.0j]])
+    y = pkg.ComplexDense.zeros(1, 2)
+    pkg.get_backend().triangular_product(y, pkg.ComplexDense.from_array([[c00]]),
+                                         pkg.ComplexDense.from_array(a), True, pkg.FlopLedger())
+    np.testing.assert_allclose(y.array, np.conj(c00) * a, rtol=1e-15)
+
+
+def test_cholesky_failure_preserves_input_and_charges_nothing(pkg):
+    rng = np.random.default_rng(15)
+    bad = hermitian_from_lower(rand_complex(rng, 4, 4)) - 10 * np.eye(4)
+    t = pkg.ComplexDense.from_array(bad)
+    led = pkg.FlopLedger()
+    with pytest.raises(pkg.NotHPDError):
+        pkg.get_backend().cholesky_factor(t, led)
+    np.testing.assert_array_equal(t.array, bad)
+    assert led.cholesky == 0
+    with pytest.raises(pkg.NotHPDError) as e:
+        pkg.get_backend().cholesky_factor(pkg.ComplexDense.from_array([[-1.0 + 0j]]), led)
+    assert e.value.pivot == 0
+
+
+def test_cholesky_ignores_poisoned_upper_and_perturbation(pkg):
+    rng = np.random.default_rng(16)
+    g = rand_complex(rng, 6, 6)
+    t_vals = g @ g.conj().T + np.eye(6)
+    t = pkg.ComplexDense.from_array(t_vals)
+    t.array[np.triu_indices(6, 1)] = np.nan
+    c = pkg.get_backend().cholesky_factor(t, pkg.FlopLedger())
+    assert rel_fro(c.array @ c.array.conj().T, t_vals) <= 1e-13
+
+
+def test_ledger_scripted_sequence(pkg):
+    rng = np.random.default_rng(20)
+    led = pkg.FlopLedger()
+    be = pkg.get_backend()
+    cd = pkg.ComplexDense.from_array
+    be.hermitian_rank_k_update(pkg.HermitianAccumulator(64), cd(rand_complex(rng, 98, 64)), led)
+    be.hermitian_rank_2k_update(pkg.HermitianAccumulator(8), cd(rand_complex(rng, 12, 8)),
+                                cd(rand_complex(rng, 12, 8)), led)
+    be.general_product(pkg.ComplexDense.zeros(4, 5), cd(rand_complex(rng, 4, 3)),
+                       cd(rand_complex(rng, 3, 5)), False, 1.0, 0.0, led)
+    be.hermitian_product(pkg.ComplexDense.zeros(5, 7), cd(hermitian_from_lower(rand_complex(rng, 5, 5))),
+                         cd(rand_complex(rng, 5, 7)), False, 1.0, led)
+    be.triangular_product(pkg.ComplexDense.zeros(6, 4), cd(np.tril(rand_complex(rng, 6, 6))),
+                          cd(rand_complex(rng, 6, 4)), False, led)
+    g = rand_complex(rng, 5, 5)
+    be.cholesky_factor(cd(g @ g.conj().T + np.eye(5)), led)
+    pkg.scale_rows(cd(rand_complex(rng, 4, 3)), np.ones(4), led)
+    expected = [4 * 98 * 64 * 64, 8 * 12 * 8 * 8, 8 * 4 * 5 * 3, 8 * 5 * 5 * 7, 4 * 6 * 6 * 4,
+                4 * 125 // 3, 2 * 4 * 3]
+    assert [led.hermitian_rank_k, led.hermitian_rank_2k, led.general_product,
+            led.hermitian_product, led.triangular_product, led.cholesky, led.row_scale] == expected
+    assert led.total == sum(expected)
+
+
+@settings(max_examples=20, deadline=None)
+@given(m=st.integers(1, 70), n=st.integers(1, 70), seed=st.integers(0, 10_000))
+def test_property_herk_random_shapes(pkg, m, n, seed):
+    rng = np.random.default_rng(seed)
+    a = rand_complex(rng, m, n)
+    c = pkg.HermitianAccumulator(n)
+    pkg.get_backend().hermitian_rank_k_update(c, pkg.ComplexDense.from_array(a), pkg.FlopLedger())
+    assert rel_fro(np.tril(c.matrix.array), np.tril(a.conj().T @ a)) <= 1e-13
+
+
+@settings(max_examples=20, deadline=None)
+@given(m=st.integers(1, 70), n=st.integers(1, 70), k=st.integers(1, 40),
+       seed=st.integers(0, 10_000))
+def test_property_gemm_random_shapes(pkg, m, n, k, seed):
+    rng = np.random.default_rng(seed)
+    a, b = rand_complex(rng, m, k), rand_complex(rng, k, n)
+    c = pkg.ComplexDense.zeros(m, n)
+    pkg.get_backend().general_product(c, pkg.ComplexDense.from_array(a), pkg.ComplexDense.from_array(b),
+                                      False, 1.0, 0.0, pkg.FlopLedger())
+    assert rel_fro(c.array, a @ b) <= 1e-13
+
+
+# -- phase contracts (test_builder.py) ----------------------------------------------------
+
+def _coeffs(pkg, seed, heights, n_g, cap=None):
+    rng = np.random.default_rng(seed)
+    lay = pkg.AtomBlockLayout(tuple(heights), cap or max(heights))
+    r = lay.total_rows
+    a = pkg.ComplexDense.zeros(r, n_g, capacity_rows=lay.capacity_rows)
+    b = pkg.ComplexDense.zeros(r, n_g, capacity_rows=lay.capacity_rows)
+    a.array[:] = rand_complex(rng, r, n_g)
+    b.array[:] = rand_complex(rng, r, n_g)
+    return pkg.StackedCoefficients(a, b, lay, rng.uniform(0.5, 2.0, r))
+
+
+def test_build_s_overwrites_b_and_matches_naive(pkg):
+    co = _coeffs(pkg, 42, (4, 4), 8)
+    a0, b0, u = co.A_star.array.copy(), co.B_star.array.copy(), co.udot_norms.copy()
+    led = pkg.FlopLedger()
+    s = pkg.build_S(co, led, pkg.get_backend()).mirror_to_full()
+    assert rel_fro(s.array, ob.naive_S(a0, b0, u)) <= 1e-13
+    np.testing.assert_array_equal(co.B_star.array, b0 * u[:, None])
+    r = co.layout.total_rows
+    assert led.hermitian_rank_k == 2 * 4 * r * 64 and led.row_scale == 2 * r * 8
+
+
+def test_h_phases_match_naive_with_smaller_t_and_mixed_hpd(pkg):
+    rng = np.random.default_rng(13)
+    heights = (9, 4, 9, 4)
+    co = _coeffs(pkg, 13, heights, 14, cap=9)
+    a0, b0 = co.A_star.array.copy(), co.B_star.array.copy()
+    sizes = (4, 4, 9, 4)  # T may couple only the first rows of a taller block
+    cd = pkg.ComplexDense.from_array
+    t_aa, t_ab, t_bb = [], [], []
+    for i, m in enumerate(sizes):
+        g = rand_complex(rng, m, m)
+        t_aa.append(cd(g.conj().T @ g + np.eye(m) if i % 2 == 0 else
+                       hermitian_from_lower(g) - 4 * np.eye(m)))
+        t_ab.append(cd(rand_complex(rng, m, m)))
+        t_bb.append(cd(hermitian_from_lower(rand_complex(rng, m, m))))
+    tm = pkg.TMatrixSet(t_aa, t_ab, t_bb, [0] * 4, [0] * 4)
+    h = pkg.HermitianAccumulator(14)
+    led = pkg.FlopLedger()
+    rep = pkg.BuildReport()
+    be = pkg.get_backend()
+    pkg.build_H_ABBA_BB(co, tm, h, led, be)
+    co.A_star.array[:] = a0
+    co.B_star.array[:] = b0
+    pkg.build_H_AA(co, tm, h, pkg.BuildConfig(), led, rep, be)
+    want = ob.naive_H(a0, b0, heights, [t.array for t in t_aa], [t.array for t in t_ab],
+                      [t.array for t in t_bb])
+    assert rel_fro(h.mirror_to_full().array, want) <= 1e-12
+    assert rep.hpd_mask == [True, False, True, False]
+    # the fused native build agrees (T smaller than blocks -> zero rows in Z / XY)
+    co2 = pkg.StackedCoefficients(pkg.ComplexDense.from_array(a0), pkg.ComplexDense.from_array(b0),
+                                  co.layout, co.udot_norms)
+    h2, _, rep2 = pkg.build_all(co2, tm, pkg.BuildConfig())
+    assert rel_fro(h2.array, want) <= 1e-12
+    assert rep2.ledger == pkg.build_ledger(heights, sizes, 14, rep2.hpd_mask, False)
+
+
+def test_forced_general_path_equals_dynamic(pkg):
+    from paper_1602_06589_b200 import configs
+
+    inst = configs.make_instance("C1")
+    co = pkg.compute_AB(inst.spec)
+    h1, s1, r1 = pkg.build_all(co.copy(), inst.tmats, pkg.BuildConfig())
+    h2, s2, r2 = pkg.build_all(co.copy(), inst.tmats, pkg.BuildConfig(force_general_path=True))
+    assert r1.hpd_atom_count == 4 and r2.hpd_atom_count == 0
+    assert rel_fro(h2.array, h1.array) <= 1e-12 and rel_fro(s2.array, s1.array) <= 1e-14
+
+
+def test_nan_t_aa_is_contract_violation(pkg):
+    co = _coeffs(pkg, 3, (4,), 6)
+    t = np.eye(4, dtype=complex)
+    t[2, 1] = np.nan
+    cd = pkg.ComplexDense.from_array
+    tm = pkg.TMatrixSet([cd(t)], [cd(np.eye(4) + 0j)], [cd(np.eye(4) + 0j)], [1], [1])
+    with pytest.raises(pkg.ContractViolationError):
+        pkg.build_all(co, tm, pkg.BuildConfig())
+
+
+def test_report_json_flat(pkg):
+    import json
+
+    from paper_1602_06589_b200 import configs
+
+    inst = configs.make_instance("C1")
+    _, _, rep = pkg.build_all(pkg.compute_AB(inst.spec), inst.tmats, pkg.BuildConfig())
+    doc = rep.to_json_dict()
+    assert {"time_setup_s", "time_S_s", "time_H_ABBA_BB_s", "time_H_AA_s"} <= set(doc)
+    assert doc["flops_total"] == rep.ledger.total and json.loads(json.dumps(doc)) == doc
+    assert rep.predicted_bytes == pkg.estimate_memory(4, 49, inst.spec.n_basis, True)
+
+
+# -- multi-GPU column-panel partition, emulated rank by rank ---------------------------
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_panels_reassemble_full_build(pkg, world):
+    """Each rank computes the lower tiles of its column panels (hsdla_build_args.shard_rank
+    / n_shards); copying every rank's owned panels together and mirroring gives the
+    unsharded H and S.  The NCCL gather itself is covered by the gloo test."""
+    import torch
+
+    from paper_1602_06589_b200 import configs
+    from paper_1602_06589_b200.pipeline import DeviceSpec, HSPipeline, pack_tmats
+    from paper_1602_06589_b200.shard import PANEL, owned_panels
+
+    inst = configs.make_instance("C1")
+    spec = inst.spec
+    n = spec.n_basis
+    dspec = DeviceSpec(spec)
+    tp = pack_tmats(inst.tmats)
+    full = HSPipeline(n, dspec.heights)
+    full.run(dspec, tp)
+    h_ref, s_ref = (m.cpu().numpy().T for m in full.result_views())
+    h_asm = torch.zeros((n, n), dtype=torch.complex128, device="cuda")
+    s_asm = torch.zeros((n, n), dtype=torch.complex128, device="cuda")
+    for r in range(world):
+        pipe = HSPipeline(n, dspec.heights, shard_rank=r, n_shards=world)
+        pipe.run(dspec, tp)
+        for j in owned_panels(n, world, r):
+            sl = slice(j * PANEL, min(n, (j + 1) * PANEL))
+            h_asm[sl] = pipe.H[sl, :n]
+            s_asm[sl] = pipe.S[sl, :n]
+    import ctypes
+
+    lib = pkg._native.load()
+    from paper_1602_06589_b200 import device
+
+    for m in (h_asm, s_asm):
+        flag = ctypes.c_int32(0)
+        assert lib.hsdla_mirror_lower(device.ctx(), n, device.ptr(m), n, ctypes.byref(flag)) == 0
+    h, s = h_asm.cpu().numpy().T, s_asm.cpu().numpy().T
+    assert rel_fro(h, h_ref) <= 1e-14 and rel_fro(s, s_ref) <= 1e-14

@@ -127,6 +127,8 @@ int launch_contract(hsdla_ctx* ctx, const std::vector<Prob>& probs,
 // TMA + mbarrier variant (contract_tma.cu); `probs` already tiled (it_base, nchunks set).
 int launch_contract_tma(hsdla_ctx* ctx, const std::vector<Prob>& probs, long long total,
                         const std::vector<Seg>& segs, int* flag_dev);
+// True when the TMA path has a better tile shape for these problems (96-row T applications).
+bool tma_wants(const std::vector<Prob>& probs);
 // Arena helpers.
 int arena_begin(hsdla_ctx* ctx, size_t bytes);
 void* arena_push(hsdla_ctx* ctx, const void* src, size_t bytes, void** host_ptr);

@@ -372,12 +372,15 @@ int launch_contract(hsdla_ctx* ctx, const std::vector<Prob>& probs_in,
     if (p.ntiles > 0) probs.push_back(p);
   }
   if (total == 0) return HSDLA_OK;
-  static int use_tma = -1;
-  if (use_tma < 0) {
+  // Feed path: HSDLA_CONTRACT = auto (default: TMA 96x32 tiles for T applications with
+  // 64 < m <= 96, cp.async 64x64 otherwise) | tma (all TMA) | cpasync (all cp.async).
+  static int mode = -1;
+  if (mode < 0) {
     const char* e = getenv("HSDLA_CONTRACT");
-    use_tma = (e && std::string(e) == "cpasync") ? 0 : 1;  // TMA + mbarrier ring by default
+    mode = (e && std::string(e) == "tma") ? 1 : (e && std::string(e) == "cpasync") ? 2 : 0;
   }
-  if (use_tma) return launch_contract_tma(ctx, probs, total, segs, flag_dev);
+  if (mode == 1 || (mode == 0 && tma_wants(probs)))
+    return launch_contract_tma(ctx, probs, total, segs, flag_dev);
   // Variant selection (HSDLA_WARP_COLS = 32 | 16, HSDLA_SMEM_PAD = 0 | 1) for A/B tests.
   static int variant = -1, pad = -1;
   if (variant < 0) {

@@ -45,7 +45,6 @@ struct Cfg {
 };
 using Cfg64 = Cfg<2, 2, 4>;
 using Cfg96 = Cfg<3, 2, 2>;
-constexpr int kIssueStep = 3;  // k'-step after which the producer refills the ring
 
 struct TSeg {
   int mapP, mapPalt, mapQ;
@@ -87,6 +86,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(b)),
       "r"(parity));
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity));
+  return ok != 0;
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
                                             uint64_t* bar) {
@@ -311,7 +322,7 @@ __global__ void __launch_bounds__(C::kT, 2) contract_tma_kernel(TKParams sk) {
             dmma(accR[ib][jb][0], accR[ib][jb][1], a[ib], br[jb]);
             dmma(accI[ib][jb][0], accI[ib][jb][1], a[ib], bi[jb]);
           }
-        if (s == kIssueStep && tid == 0) {
+        if (s == 3 && tid == 0) {
           // Producer, mid-chunk: by now the other warps have released chunk j-1 (whose stage
           // chunk j+2 reuses), so the empty-barrier wait rarely blocks this warp.
           const long long x = j + kStg - 1;
@@ -560,9 +571,7 @@ int launch_cfg(hsdla_ctx* ctx, const std::vector<Prob>& probs_in, const std::vec
 }
 }  // namespace
 
-int launch_contract_tma(hsdla_ctx* ctx, const std::vector<Prob>& probs, long long total,
-                        const std::vector<Seg>& segs, int* flag_dev) {
-  (void)total;
+bool tma_wants(const std::vector<Prob>& probs) {
   // General (T-application) problems with 64 < m <= 96 run on 96 x 32 tiles.
   static int apply_tile = -1;
   if (apply_tile < 0) {
@@ -575,8 +584,13 @@ int launch_contract_tma(hsdla_ctx* ctx, const std::vector<Prob>& probs, long lon
     general = general && p.kind == PROB_GENERAL;
     max_m = std::max(max_m, p.m);
   }
-  if (general && apply_tile == 96 && max_m > 64 && max_m <= 96)
-    return launch_cfg<Cfg96>(ctx, probs, segs, flag_dev);
+  return general && apply_tile == 96 && max_m > 64 && max_m <= 96;
+}
+
+int launch_contract_tma(hsdla_ctx* ctx, const std::vector<Prob>& probs, long long total,
+                        const std::vector<Seg>& segs, int* flag_dev) {
+  (void)total;
+  if (tma_wants(probs)) return launch_cfg<Cfg96>(ctx, probs, segs, flag_dev);
   return launch_cfg<Cfg64>(ctx, probs, segs, flag_dev);
 }
 

@@ -9,6 +9,6 @@ CFG=${CFG:-C2}
 timeout 600 python bench.py --config $CFG > gpurun_out/bench_$CFG.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_$CFG.log
 cat gpurun_out/bench_$CFG.log
 python bench.py --config $CFG --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/plain_short.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"contract_kernel" -s 4 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:"contract" -s 4 -c 1 \
     -o gpurun_out/prof_contractS_$CFG python bench.py --config $CFG --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
 echo "ncu full rc=$?"

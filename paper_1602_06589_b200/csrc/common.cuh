@@ -125,6 +125,8 @@ namespace hsdla {
 int launch_contract(hsdla_ctx* ctx, const std::vector<Prob>& probs,
                     const std::vector<Seg>& segs, int* flag_dev);
 // TMA + mbarrier variant (contract_tma.cu); `probs` already tiled (it_base, nchunks set).
+void plan_dp_waves(const std::vector<Prob>& probs, long long total, int grid, int* waves,
+                   int* nch, long long* dp_it);
 int launch_contract_tma(hsdla_ctx* ctx, const std::vector<Prob>& probs, long long total,
                         const std::vector<Seg>& segs, int* flag_dev);
 // True when the TMA path has a better tile shape for these problems (96-row T applications).

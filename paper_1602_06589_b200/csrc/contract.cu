@@ -52,6 +52,9 @@ struct SKParams {
   const Prob* probs;
   const Seg* segs;
   long long total_it;
+  long long dp_it;    // iterations [0, dp_it) are whole tiles dealt round-robin (dp_waves waves)
+  int dp_waves;
+  int dp_nch;         // chunks per tile (uniform across problems when dp_waves > 0)
   int nprob;
   int grid;
   double* partials;
@@ -80,6 +83,10 @@ __device__ __forceinline__ bool finite2(double2 v) { return isfinite(v.x) && isf
 
 __device__ __forceinline__ long long range_start(long long total, int grid, int g) {
   return total * g / grid;
+}
+// First iteration of CTA g's stream-K range (the part after the data-parallel waves).
+__device__ __forceinline__ long long sk_start(const SKParams& sk, int g) {
+  return sk.dp_it + range_start(sk.total_it - sk.dp_it, sk.grid, g);
 }
 
 __device__ __forceinline__ Seg load_seg(const Seg* s) {
@@ -114,8 +121,18 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), 2) contract_kernel(SKParams
   const int dst_lane = PAD ? lp * 2 : ((((lp >> 1) ^ (lc & 7)) << 2) + (lp & 1) * 2);
 
   const int cta = blockIdx.x;
-  long long it = range_start(sk.total_it, sk.grid, cta);
-  const long long it_end = range_start(sk.total_it, sk.grid, cta + 1);
+  // Work order: dp_waves waves of whole tiles (CTA g takes tile g + w*grid, so the CTAs of
+  // a wave start together and walk K in step over neighbouring tiles: the live operand
+  // set stays L2-resident), then an even stream-K split of the remaining iterations.
+  for (int ph = 0; ph <= sk.dp_waves; ++ph) {
+  long long it, it_end;
+  if (ph < sk.dp_waves) {
+    it = (long long)(cta + ph * sk.grid) * sk.dp_nch;
+    it_end = it + sk.dp_nch;
+  } else {
+    it = sk_start(sk, cta);
+    it_end = sk_start(sk, cta + 1);
+  }
 
   while (it < it_end) {
     // ---- locate (problem, tile, chunk range) of the next piece
@@ -271,7 +288,7 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), 2) contract_kernel(SKParams
     }
     if (c_hi < nch) {
       // Head piece of a split tile: add the later pieces in CTA order (deterministic).
-      for (int j = cta + 1; j < sk.grid && range_start(sk.total_it, sk.grid, j) < tile_it_end; ++j) {
+      for (int j = cta + 1; j < sk.grid && sk_start(sk, j) < tile_it_end; ++j) {
         if (tid == 0) {
           while (atomicAdd(sk.ready + j, 0) == 0) __nanosleep(100);
         }
@@ -339,6 +356,7 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), 2) contract_kernel(SKParams
     }
     if (bad) atomicOr(sk.flag, 1);
   }
+  }
 }
 
 }  // namespace
@@ -348,6 +366,33 @@ int prob_tile_count(const Prob& p) {
   int cnt = 0;
   for (int tn = p.col_tile_lo; tn < p.col_tile_hi; ++tn) cnt += p.tiles_m - tn;
   return cnt;
+}
+
+// Data-parallel waves ahead of the stream-K split (HSDLA_SK_DP=0 disables): only when all
+// problems share one chunk count, so a whole tile is the same work everywhere.  The
+// stream-K remainder is kept at >= 8 chunks per CTA (else one wave moves back into it)
+// to avoid long split-tile fix-up chains.
+void plan_dp_waves(const std::vector<Prob>& probs, long long total, int grid, int* waves,
+                   int* nch, long long* dp_it) {
+  static int enabled = -1;
+  if (enabled < 0) {
+    const char* e = getenv("HSDLA_SK_DP");
+    enabled = (e && std::string(e) == "0") ? 0 : 1;
+  }
+  *waves = 0;
+  *nch = 1;
+  *dp_it = 0;
+  if (!enabled || probs.empty()) return;
+  const int n0 = probs[0].nchunks;
+  for (const Prob& p : probs)
+    if (p.nchunks != n0) return;
+  const long long tiles = total / n0;
+  long long w = tiles / grid;
+  const long long rem = tiles - w * grid;
+  if (w > 0 && rem > 0 && rem * n0 < 8LL * grid) --w;
+  *waves = (int)w;
+  *nch = n0;
+  *dp_it = w * grid * n0;
 }
 
 int launch_contract(hsdla_ctx* ctx, const std::vector<Prob>& probs_in,
@@ -429,6 +474,7 @@ int launch_contract(hsdla_ctx* ctx, const std::vector<Prob>& probs_in,
   sk.total_it = total;
   sk.nprob = (int)probs.size();
   sk.grid = grid;
+  plan_dp_waves(probs, total, grid, &sk.dp_waves, &sk.dp_nch, &sk.dp_it);
   sk.partials = ctx->partials;
   sk.ready = ctx->ready;
   sk.flag = flag_dev;

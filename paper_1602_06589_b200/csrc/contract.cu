@@ -41,7 +41,7 @@ constexpr int kChunk = 16;                       // complex K per stage
 // consecutive doubles per half-warp phase) is conflict-free with compile-time offsets.
 // PAD = 0 instead keeps 256-B columns with a 32-byte XOR swizzle (k-chunk index ^ column&7).
 template <int PAD> struct Layout {
-  static constexpr int kColDoubles = 2 * kChunk + (PAD ? 4 : 0);
+  static constexpr int kColDoubles = 2 * kChunk + (PAD == 1 ? 4 : 0);
   static constexpr int kOpDoubles = kTile * kColDoubles;
   static constexpr int kStageDoubles = 2 * kOpDoubles;
   static constexpr size_t kSmemBytes = size_t(kStages) * kStageDoubles * sizeof(double);
@@ -55,6 +55,7 @@ struct SKParams {
   long long dp_it;    // iterations [0, dp_it) are whole tiles dealt round-robin (dp_waves waves)
   int dp_waves;
   int dp_nch;         // chunks per tile (uniform across problems when dp_waves > 0)
+  int spread;         // issue cp.async rounds between DMMA steps (HSDLA_CP_SPREAD=1; default 0)
   int nprob;
   int grid;
   double* partials;
@@ -72,6 +73,15 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, int
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc),
                "r"(src_bytes));
+}
+// Zero-filling variant with the PTX ignore-src predicate: when !valid no global access is
+// made (src may then point anywhere) and the 16 bytes are written as zeros.
+__device__ __forceinline__ void cp_async16_zfill(void* smem_dst, const void* gsrc, bool valid) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile(
+      "{\n .reg .pred ign;\n setp.eq.u32 ign, %2, 0;\n"
+      " cp.async.cg.shared.global [%0], [%1], 16, ign;\n}\n" ::"r"(s),
+      "l"(gsrc), "r"((unsigned)valid));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
 template <int N>
@@ -118,7 +128,9 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), 2) contract_kernel(SKParams
   // cp.async slot of this thread: complex element lp of the chunk, columns lc + kColStep*r.
   const int lp = tid & 15;
   const int lc = tid >> 4;
-  const int dst_lane = PAD ? lp * 2 : ((((lp >> 1) ^ (lc & 7)) << 2) + (lp & 1) * 2);
+  const int dst_lane = PAD == 1 ? lp * 2
+                       : PAD == 2 ? ((((lp >> 1) ^ ((lc & 1) << 1)) << 2) + (lp & 1) * 2)
+                                  : ((((lp >> 1) ^ (lc & 7)) << 2) + (lp & 1) * 2);
 
   const int cta = blockIdx.x;
   // Work order: dp_waves waves of whole tiles (CTA g takes tile g + w*grid, so the CTAs of
@@ -185,21 +197,24 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), 2) contract_kernel(SKParams
     const double2* bQ = cur.Q + (long long)(j0 + lc) * cur.ldQ + lp;
     long long stP = (long long)kColStep * cur.ldP, stQ = (long long)kColStep * cur.ldQ;
 
-    auto issue = [&](int stage) {
+    // cp.async rounds [r0, r1) of the chunk at iko into `stage` (round r = columns
+    // lc + kColStep*r of both operands), then advance() moves iko to the next chunk.
+    auto issue_rounds = [&](int stage, int r0, int r1) {
       double* sP = smem + stage * kStageDoubles + lc * kColDoubles + dst_lane;
       double* sQ = sP + kOpDoubles;
       const bool kval = (iko + lp) < cur.k;
-      const double2* p = bP + iko;
-      const double2* qq = bQ + iko;
+      const int limP = kval ? nvP : 0, limQ = kval ? nvQ : 0;
+      const double2* p = bP + iko + r0 * stP;
+      const double2* qq = bQ + iko + r0 * stQ;
 #pragma unroll
-      for (int r = 0; r < kRounds; ++r) {
-        const bool vp = kval && r < nvP;
-        cp_async16(sP + r * kColStep * kColDoubles, vp ? p : cur.Q, vp ? 16 : 0);
-        const bool vq = kval && r < nvQ;
-        cp_async16(sQ + r * kColStep * kColDoubles, vq ? qq : cur.Q, vq ? 16 : 0);
+      for (int r = r0; r < r1; ++r) {
+        cp_async16_zfill(sP + r * kColStep * kColDoubles, p, r < limP);
+        cp_async16_zfill(sQ + r * kColStep * kColDoubles, qq, r < limQ);
         p += stP;
         qq += stQ;
       }
+    };
+    auto advance = [&]() {
       iko += kChunk;
       if (iko >= cur.k) {
         int nx = isi + 1;
@@ -214,6 +229,10 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), 2) contract_kernel(SKParams
           stQ = (long long)kColStep * cur.ldQ;
         }
       }
+    };
+    auto issue = [&](int stage) {
+      issue_rounds(stage, 0, kRounds);
+      advance();
     };
 
     double accR[4][JB][2], accI[4][JB][2];
@@ -236,15 +255,63 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), 2) contract_kernel(SKParams
       cp_async_wait<kStages - 2>();
       __syncthreads();
       const int nc = c + kStages - 1;
-      if (nc < nchunks) issue(nc % kStages);
-      cp_async_commit();
+      const bool more = nc < nchunks;
+      const int nstage = nc % kStages;
+      // spread: the next-but-one chunk's loads are issued a round at a time between the
+      // DMMA steps instead of as one block after the barrier.
+      if (!sk.spread) {
+        if (more) issue(nstage);
+        cp_async_commit();
+      }
 
       const double* sP = smem + (c % kStages) * kStageDoubles;
       const double* sQ = sP + kOpDoubles;
       const double* pa = sP + (wm * 32 + g) * kColDoubles;
       const double* pb = sQ + (wn * kWarpCols + g) * kColDoubles;
+      if constexpr (PAD == 2) {
+        // Paired K steps: lane q takes complex element 4j+q whole (one 16-byte load per
+        // fragment) and uses its real part at step 2j, its imaginary part at step 2j+1.
+        // The K order of the real embedding is free as long as P and Q share it:
+        //   step 2j:   Re += p_re q_re   Im += p_re q_im
+        //   step 2j+1: Re += p_im q_im   Im += p_im (-q_re)
+        // 32-byte units of odd columns are swapped in pairs (unit ^ 2), so the two
+        // columns of a quarter-warp's 128-bit load fall in opposite 64-byte bank halves.
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (sk.spread && more) issue_rounds(nstage, j * kRounds / 4, (j + 1) * kRounds / 4);
+          const int off = (((2 * j + (q >> 1)) ^ ((g & 1) << 1)) << 2) + ((q & 1) << 1);
+          double2 av[4], bv[JB];
+#pragma unroll
+          for (int ib = 0; ib < 4; ++ib)
+            av[ib] = *reinterpret_cast<const double2*>(pa + ib * 8 * kColDoubles + off);
+#pragma unroll
+          for (int jb = 0; jb < JB; ++jb)
+            bv[jb] = *reinterpret_cast<const double2*>(pb + jb * 8 * kColDoubles + off);
+#pragma unroll
+          for (int ib = 0; ib < 4; ++ib)
+#pragma unroll
+            for (int jb = 0; jb < JB; ++jb) {
+              dmma(accR[ib][jb][0], accR[ib][jb][1], av[ib].x, bv[jb].x);
+              dmma(accI[ib][jb][0], accI[ib][jb][1], av[ib].x, bv[jb].y);
+            }
+          double nb[JB];
+#pragma unroll
+          for (int jb = 0; jb < JB; ++jb)
+            nb[jb] = __hiloint2double(__double2hiint(bv[jb].x) ^ 0x80000000u,
+                                      __double2loint(bv[jb].x));
+#pragma unroll
+          for (int ib = 0; ib < 4; ++ib)
+#pragma unroll
+            for (int jb = 0; jb < JB; ++jb) {
+              dmma(accR[ib][jb][0], accR[ib][jb][1], av[ib].y, bv[jb].y);
+              dmma(accI[ib][jb][0], accI[ib][jb][1], av[ib].y, nb[jb]);
+            }
+        }
+      } else {
 #pragma unroll
       for (int s = 0; s < 8; ++s) {
+        if (sk.spread && more && s % (8 / kRounds) == 0)
+          issue_rounds(nstage, s / (8 / kRounds), s / (8 / kRounds) + 1);
         const int off = PAD ? (s << 2) : ((s ^ g) << 2);
         double a[4], br[JB], bi[JB];
 #pragma unroll
@@ -262,6 +329,11 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), 2) contract_kernel(SKParams
             dmma(accR[ib][jb][0], accR[ib][jb][1], a[ib], br[jb]);
             dmma(accI[ib][jb][0], accI[ib][jb][1], a[ib], bi[jb]);
           }
+      }
+      }
+      if (sk.spread) {
+        if (more) advance();
+        cp_async_commit();
       }
     }
     cp_async_wait<0>();
@@ -427,12 +499,14 @@ int launch_contract(hsdla_ctx* ctx, const std::vector<Prob>& probs_in,
   if (mode == 1 || (mode == 0 && tma_wants(probs)))
     return launch_contract_tma(ctx, probs, total, segs, flag_dev);
   // Variant selection (HSDLA_WARP_COLS = 32 | 16, HSDLA_SMEM_PAD = 0 | 1) for A/B tests.
+  // Shared-memory layout / fragment path: HSDLA_CP_LAYOUT = pair (default: paired K steps,
+  // 128-bit fragment loads) | xor (32-byte XOR swizzle, 64-bit loads) | pad (288-byte columns).
   static int variant = -1, pad = -1;
   if (variant < 0) {
     const char* e = getenv("HSDLA_WARP_COLS");
     variant = (e && atoi(e) == 16) ? 2 : 4;
-    const char* p = getenv("HSDLA_SMEM_PAD");
-    pad = (p && atoi(p) == 1) ? 1 : 0;
+    const char* p = getenv("HSDLA_CP_LAYOUT");
+    pad = (p && std::string(p) == "pad") ? 1 : (p && std::string(p) == "xor") ? 0 : 2;
     HS_CUDA(cudaFuncSetAttribute(contract_kernel<4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)Layout<0>::kSmemBytes));
     HS_CUDA(cudaFuncSetAttribute(contract_kernel<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -441,10 +515,16 @@ int launch_contract(hsdla_ctx* ctx, const std::vector<Prob>& probs_in,
                                  (int)Layout<1>::kSmemBytes));
     HS_CUDA(cudaFuncSetAttribute(contract_kernel<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)Layout<1>::kSmemBytes));
+    HS_CUDA(cudaFuncSetAttribute(contract_kernel<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)Layout<2>::kSmemBytes));
+    HS_CUDA(cudaFuncSetAttribute(contract_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)Layout<2>::kSmemBytes));
   }
-  const void* kfn = variant == 4 ? (pad ? (const void*)contract_kernel<4, 1> : (const void*)contract_kernel<4, 0>)
-                                 : (pad ? (const void*)contract_kernel<2, 1> : (const void*)contract_kernel<2, 0>);
-  const size_t kSmemBytes = pad ? Layout<1>::kSmemBytes : Layout<0>::kSmemBytes;
+  const void* kfns[2][3] = {
+      {(const void*)contract_kernel<2, 0>, (const void*)contract_kernel<2, 1>, (const void*)contract_kernel<2, 2>},
+      {(const void*)contract_kernel<4, 0>, (const void*)contract_kernel<4, 1>, (const void*)contract_kernel<4, 2>}};
+  const void* kfn = kfns[variant == 4 ? 1 : 0][pad];
+  const size_t kSmemBytes = pad == 1 ? Layout<1>::kSmemBytes : Layout<0>::kSmemBytes;
   const int kThreads = variant == 4 ? 128 : 256;
   int occ = 0;
   HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kThreads, kSmemBytes));
@@ -475,6 +555,12 @@ int launch_contract(hsdla_ctx* ctx, const std::vector<Prob>& probs_in,
   sk.nprob = (int)probs.size();
   sk.grid = grid;
   plan_dp_waves(probs, total, grid, &sk.dp_waves, &sk.dp_nch, &sk.dp_it);
+  static int spread = -1;
+  if (spread < 0) {
+    const char* e = getenv("HSDLA_CP_SPREAD");
+    spread = (e && std::string(e) == "1") ? 1 : 0;
+  }
+  sk.spread = spread;
   sk.partials = ctx->partials;
   sk.ready = ctx->ready;
   sk.flag = flag_dev;

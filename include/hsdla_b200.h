@@ -101,6 +101,12 @@ int hsdla_potrf_lower_batched(hsdla_ctx* ctx, int n, int batch, const hsdla_c64*
  * finite (synchronises).  Replaces HermitianAccumulator.mirror_to_full (matrix.py:216-226). */
 int hsdla_mirror_lower(hsdla_ctx* ctx, int n, hsdla_c64* C, int64_t ldc, int32_t* nonfinite_host);
 
+/* *nonfinite_host = 1 if any element of the m x n window A (DEVICE, column-major, lda)
+ * is NaN or Inf, else 0; synchronises the stream.  The guard of write_hsm1
+ * (matrix.py:242-246), run in HBM before an HSM1 file is streamed out. */
+int hsdla_check_finite(hsdla_ctx* ctx, int m, int n, const hsdla_c64* A, int64_t lda,
+                       int32_t* nonfinite_host);
+
 /* B[i, :] *= d[i] (d real, DEVICE).  Replaces scale_rows (matrix.py:229-239). */
 int hsdla_scale_rows(hsdla_ctx* ctx, int m, int n, const double* d, hsdla_c64* B, int64_t ldb);
 

@@ -96,6 +96,7 @@ SIGNATURES = {
     "hsdla_potrf_lower_batched": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _i64, _i64,
                                                  _vp, _i64, _i64, _P_i32]),
     "hsdla_mirror_lower": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _i64, _P_i32]),
+    "hsdla_check_finite": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _i64, _P_i32]),
     "hsdla_scale_rows": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _i64]),
     "hsdla_ab_generate": (ctypes.c_int, [_vp, ctypes.POINTER(AbArgs)]),
     "hsdla_build_workspace_size": (ctypes.c_size_t, [ctypes.POINTER(BuildArgs)]),

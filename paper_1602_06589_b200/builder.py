@@ -454,6 +454,15 @@ def build_all(coeffs: StackedCoefficients, tmats: TMatrixSet, config: BuildConfi
     s_full = ComplexDense(s_host[0])
     wall = time.perf_counter() - t0
 
+    fill_report(report, res, layout, sizes, n, config, wall,
+                int(sum(x.numel() * x.element_size() for x in (a_d, b_d, udot, h_d, s_d))
+                    + ws.numel()))
+    return h_full, s_full, report
+
+
+def fill_report(report: BuildReport, res: dict, layout: AtomBlockLayout, sizes, n: int,
+                config: BuildConfig, wall: float, device_bytes: int) -> BuildReport:
+    """Ledger, branch statistics and phase timings of one native build (`builder.py:436-474`)."""
     mask = res["hpd_mask"]
     report.ledger = build_ledger(layout.block_heights, sizes, n, mask, config.force_general_path)
     report.hpd_mask = list(mask)
@@ -462,9 +471,8 @@ def build_all(coeffs: StackedCoefficients, tmats: TMatrixSet, config: BuildConfi
     ms = res["ms"]
     report.timings = {k: v / 1e3 for k, v in ms.items()}
     report.timings["setup"] = max(wall - sum(v / 1e3 for k, v in ms.items() if k != "setup"), 0.0)
-    report.peak_observed_bytes = int(sum(x.numel() * x.element_size()
-                                         for x in (a_d, b_d, udot, h_d, s_d)) + ws.numel())
-    return h_full, s_full, report
+    report.peak_observed_bytes = device_bytes
+    return report
 
 
 def _pinned_square(n: int):

@@ -343,6 +343,25 @@ int hsdla_mirror_lower(hsdla_ctx* ctx, int n, hsdla_c64* C, int64_t ldc, int32_t
   return HSDLA_OK;
 }
 
+int hsdla_check_finite(hsdla_ctx* ctx, int m, int n, const hsdla_c64* A, int64_t lda,
+                       int32_t* nonfinite_host) {
+  if (!ctx) return -1;
+  if (m < 0) return -2;
+  if (n < 0) return -3;
+  if (!A && m > 0 && n > 0) return -4;
+  if (lda < (m > 1 ? m : 1)) return -5;
+  std::lock_guard<std::mutex> lk(g_api_mutex);
+  int* flag = flag_slot(ctx, 1);
+  HS_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+  int rc = launch_finite_check(ctx, m, n, reinterpret_cast<const double2*>(A), lda, flag);
+  if (rc) return rc;
+  HS_CUDA(cudaMemcpyAsync(ctx->scratch_host + 1, flag, sizeof(int), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  HS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (nonfinite_host) *nonfinite_host = ctx->scratch_host[1];
+  return HSDLA_OK;
+}
+
 int hsdla_scale_rows(hsdla_ctx* ctx, int m, int n, const double* d, hsdla_c64* B, int64_t ldb) {
   if (!ctx) return -1;
   std::lock_guard<std::mutex> lk(g_api_mutex);

@@ -151,6 +151,7 @@ int ab_generate(hsdla_ctx* ctx, const hsdla_ab_args* args);
 int launch_mirror(hsdla_ctx* ctx, int n, double2* C, long long ldc, int* flag_dev);
 int launch_scale_rows(hsdla_ctx* ctx, int m, int n, const double* d, double2* B, long long ldb);
 int launch_zero_rows(hsdla_ctx* ctx, double2* base, long long ld, int row0, int rows, int cols);
+int launch_finite_check(hsdla_ctx* ctx, int m, int n, const double2* A, long long lda, int* flag);
 // Copy the non-finite flag and the Cholesky infos into mapped host memory (out[0] = flag,
 // out[1..n] = info) with plain stores, keeping the D2H copy engine free for H / S.
 int launch_publish(hsdla_ctx* ctx, const int* flag, const int* info, int n, int* out_mapped);

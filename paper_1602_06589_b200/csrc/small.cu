@@ -322,6 +322,28 @@ int launch_publish(hsdla_ctx* ctx, const int* flag, const int* info, int n, int*
   return HSDLA_OK;
 }
 
+// flag |= 1 if any element of the m x n window is NaN/Inf (write_hsm1's guard,
+// matrix.py:244-246).  Rows are the fast index: one coalesced 16-byte load per thread.
+__global__ void finite_kernel(int m, int n, const double2* __restrict__ A, long long lda,
+                              int* flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  bool bad = false;
+  if (i < m)
+    for (int j = blockIdx.y; j < n; j += gridDim.y) {
+      const double2 v = A[i + (long long)j * lda];
+      bad |= !(isfinite(v.x) && isfinite(v.y));
+    }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+int launch_finite_check(hsdla_ctx* ctx, int m, int n, const double2* A, long long lda, int* flag) {
+  if (m <= 0 || n <= 0) return HSDLA_OK;
+  const int gy = n < 4096 ? n : 4096;
+  finite_kernel<<<dim3((m + 255) / 256, gy), 256, 0, ctx->stream>>>(m, n, A, lda, flag);
+  HS_CHECK_LAUNCH();
+  return HSDLA_OK;
+}
+
 int launch_zero_rows(hsdla_ctx* ctx, double2* base, long long ld, int row0, int rows, int cols) {
   if (rows <= 0 || cols <= 0) return HSDLA_OK;
   zero_rows_kernel<<<dim3((rows + 127) / 128, cols), 128, 0, ctx->stream>>>(base, ld, row0, rows);

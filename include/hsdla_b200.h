@@ -131,6 +131,30 @@ typedef struct {
 } hsdla_ab_args;
 int hsdla_ab_generate(hsdla_ctx* ctx, const hsdla_ab_args* args);
 
+/* Radial match factors f_A, f_B (flapw.py:179-198 match_factors) on the device: row
+ * f_row[a] + l (l <= l_sph[a]) of f_a / f_b (DEVICE, row-major, row stride ld_f >= n_basis)
+ * receives the factors of atom a for every K-vector.  Uses n_atoms, n_basis, k_vectors,
+ * mt_radius, radial, radial_stride and l_sph of `spec`; f_b may be NULL. */
+int hsdla_match_factors(hsdla_ctx* ctx, const hsdla_ab_args* spec, const int64_t* f_row,
+                        double* f_a, double* f_b, int64_t ld_f);
+
+/* ---- Legendre-reduced A-side overlap (oracle.py:159-216 reduced_S_AA) ----- */
+typedef struct {
+  int32_t n_atoms;
+  int32_t n_basis;
+  const double* k_vectors;    /* DEVICE n_basis x 3 */
+  const double* positions;    /* DEVICE n_atoms x 3 */
+  const double* f;            /* DEVICE match factors, row f_row[a] + l, row stride ld_f */
+  int64_t ld_f;
+  const int64_t* f_row;       /* HOST n_atoms */
+  const int32_t* l_top;       /* HOST n_atoms: rows l = 0..l_top[a] of atom a (<= HSDLA_MAX_LSPH) */
+  const double* coef;         /* DEVICE per f row: (2l+1) / (4 pi) / W_l^2 */
+  double scale;               /* (4 pi)^2 / Omega */
+  hsdla_c64* S;               /* DEVICE out n_basis x n_basis, column-major, full (exactly Hermitian) */
+  int64_t lds;
+} hsdla_reduced_args;
+int hsdla_reduced_s_aa(hsdla_ctx* ctx, const hsdla_reduced_args* args);
+
 /* ---- the composed build (builder.py:403-474 build_all) ------------------- */
 typedef struct {
   int32_t n_atoms;

@@ -49,6 +49,15 @@ class AbArgs(ctypes.Structure):
     ]
 
 
+class ReducedArgs(ctypes.Structure):
+    _fields_ = [
+        ("n_atoms", _i32), ("n_basis", _i32),
+        ("k_vectors", _vp), ("positions", _vp), ("f", _vp), ("ld_f", _i64),
+        ("f_row", _P_i64), ("l_top", _P_i32), ("coef", _vp), ("scale", ctypes.c_double),
+        ("S", _vp), ("lds", _i64),
+    ]
+
+
 class BuildArgs(ctypes.Structure):
     _fields_ = [
         ("n_atoms", _i32), ("n_basis", _i32),
@@ -99,6 +108,8 @@ SIGNATURES = {
     "hsdla_check_finite": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _i64, _P_i32]),
     "hsdla_scale_rows": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _i64]),
     "hsdla_ab_generate": (ctypes.c_int, [_vp, ctypes.POINTER(AbArgs)]),
+    "hsdla_match_factors": (ctypes.c_int, [_vp, ctypes.POINTER(AbArgs), _P_i64, _vp, _vp, _i64]),
+    "hsdla_reduced_s_aa": (ctypes.c_int, [_vp, ctypes.POINTER(ReducedArgs)]),
     "hsdla_build_workspace_size": (ctypes.c_size_t, [ctypes.POINTER(BuildArgs)]),
     "hsdla_build_hs": (ctypes.c_int, [_vp, ctypes.POINTER(BuildArgs), ctypes.POINTER(BuildResult)]),
     "hsdla_setup_hs": (ctypes.c_int, [_vp, ctypes.POINTER(AbArgs), ctypes.POINTER(BuildArgs),

@@ -375,6 +375,23 @@ int hsdla_ab_generate(hsdla_ctx* ctx, const hsdla_ab_args* args) {
   return ab_generate(ctx, args);
 }
 
+int hsdla_match_factors(hsdla_ctx* ctx, const hsdla_ab_args* spec, const int64_t* f_row,
+                        double* f_a, double* f_b, int64_t ld_f) {
+  if (!ctx) return -1;
+  if (!spec) return -2;
+  if (!f_row) return -3;
+  if (!f_a && !f_b) return -4;
+  std::lock_guard<std::mutex> lk(g_api_mutex);
+  return match_factors(ctx, spec, f_row, f_a, f_b, ld_f);
+}
+
+int hsdla_reduced_s_aa(hsdla_ctx* ctx, const hsdla_reduced_args* args) {
+  if (!ctx) return -1;
+  if (!args || !args->f_row || !args->l_top || !args->S) return -2;
+  std::lock_guard<std::mutex> lk(g_api_mutex);
+  return reduced_s_aa(ctx, args);
+}
+
 // ---- composed build ------------------------------------------------------------------
 namespace {
 struct WsLayout {

@@ -148,6 +148,9 @@ int launch_tprep(hsdla_ctx* ctx, cudaStream_t stream, int n_tsets, const int* td
                  const double2* taa, const double2* tab, const double2* tbb, long long t_ld,
                  double2* forms, int do_chol, int* info_dev);
 int ab_generate(hsdla_ctx* ctx, const hsdla_ab_args* args);
+int match_factors(hsdla_ctx* ctx, const hsdla_ab_args* s, const int64_t* f_row, double* fa,
+                  double* fb, int64_t ldf);
+int reduced_s_aa(hsdla_ctx* ctx, const hsdla_reduced_args* r);
 int launch_mirror(hsdla_ctx* ctx, int n, double2* C, long long ldc, int* flag_dev);
 int launch_scale_rows(hsdla_ctx* ctx, int m, int n, const double* d, double2* B, long long ldb);
 int launch_zero_rows(hsdla_ctx* ctx, double2* base, long long ld, int row0, int rows, int cols);

@@ -8,6 +8,9 @@ and writes small .npz fixtures next to this script:
 * special.npz   — spherical_bessel_all / spherical_harmonics_all values (special.py:104-179)
 * ab_small.npz  — compute_AB on a small spec with random rotations, mixed l_sph and a
                   K = 0 vector, full A*/B* (flapw.py:201-233)
+* ab_high.npz   — compute_AB at l_sph 12..14 (the supported maximum), x = |K| r up to ~21
+* reduced.npz   — reduced_overlap_inputs + reduced_S_AA on the small spec (full) and on
+                  C1 (projections, diagonal, first column)
 * ab_c1.npz     — compute_AB on BASELINE C1: sampled columns + projections A* V
 * build_small.npz — build_all (optimized backend) on small mixed-HPD / varying-height
                   instances: inputs and full H, S, ledger, hpd mask (builder.py:403-474)
@@ -114,6 +117,53 @@ def ab_small():
     np.savez_compressed(os.path.join(HERE, "ab_small.npz"), **out)
 
 
+def ab_high():
+    """compute_AB at the largest supported l (HSDLA_MAX_LSPH = 14) with |K| r_MT up to ~21,
+    so all three Bessel regimes (series, Miller, upward) occur at l = 12..14."""
+    rng = np.random.default_rng(9)
+    l_sph = np.array([12, 14, 13])
+    n_atoms = len(l_sph)
+    pos = rng.uniform(0, 1, (n_atoms, 3)) * 6.0
+    rots = np.array([np.eye(3), np.linalg.qr(rng.standard_normal((3, 3)))[0], np.eye(3)])
+    kv = rng.standard_normal((60, 3))
+    kv *= (rng.uniform(0.0, 8.5, 60) / np.linalg.norm(kv, axis=1))[:, None]
+    kv[0] = 0.0
+    kv[1] = (0.0, 0.0, 0.05)
+    radial = []
+    for a in range(n_atoms):
+        n = l_sph[a] + 1
+        radial.append(hsdla.RadialBoundaryData(
+            u=rng.uniform(0.1, 1, n), u_prime=rng.uniform(0.1, 1, n), udot=rng.uniform(0.1, 1, n),
+            udot_prime=rng.uniform(0.1, 1, n), energy=np.zeros(n),
+            udot_norm=np.sqrt(rng.uniform(0.01, 0.1, n))))
+    spec = hsdla.SystemSpec(positions=pos, rotations=rots, mt_radius=np.array([2.5, 2.2, 1.8]),
+                            l_sph=l_sph, l_nonsph=l_sph, k_point=np.zeros(3), k_vectors=kv,
+                            omega=216.0, radial=radial)
+    c = hsdla.compute_AB(spec)
+    out = spec_arrays(spec)
+    out.update(A=c.A_star.array, B=c.B_star.array, udot_norms=c.udot_norms)
+    np.savez_compressed(os.path.join(HERE, "ab_high.npz"), **out)
+
+
+def reduced():
+    """reduced_overlap_inputs + reduced_S_AA (flapw.py:236-250, oracle.py:159-216): the small
+    mixed-l spec in full, C1 through projections."""
+    out = {}
+    spec = small_spec()
+    inp = hsdla.reduced_overlap_inputs(spec)
+    out.update(spec_arrays(spec))
+    for a, (f, w) in enumerate(zip(inp.f, inp.wronskians)):
+        out[f"small_f_{a}"], out[f"small_w_{a}"] = f, w
+    out["small_S"] = hsdla.reduced_S_AA(inp).array
+    c1spec = ref_spec(configs.make_instance("C1").spec)
+    inp = hsdla.reduced_overlap_inputs(c1spec)
+    s = hsdla.reduced_S_AA(inp).array
+    v = projections(s.shape[0], seed=78)
+    out.update(c1_f_0=inp.f[0], c1_V=v, c1_SV=s @ v, c1_diag=np.diag(s).copy(),
+               c1_col0=s[:, 0].copy(), c1_fro=np.linalg.norm(s))
+    np.savez_compressed(os.path.join(HERE, "reduced.npz"), **out)
+
+
 def projections(n, k=6, seed=77):
     rng = np.random.default_rng(seed)
     return rng.standard_normal((n, k)) + 1j * rng.standard_normal((n, k))
@@ -182,10 +232,10 @@ def build_small():
 
 
 if __name__ == "__main__":
-    special()
-    ab_small()
-    build_small()
-    c1()
+    steps = {"special": special, "ab_small": ab_small, "ab_high": ab_high,
+             "build_small": build_small, "c1": c1, "reduced": reduced}
+    for name in (sys.argv[1:] or list(steps)):  # e.g. `make_golden.py ab_high`
+        steps[name]()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

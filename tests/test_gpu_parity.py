@@ -146,6 +146,23 @@ def test_compute_ab_small_vs_reference_golden(pkg):
     assert c.A_star.leading_dimension == c.layout.capacity_rows
 
 
+def test_compute_ab_high_l_vs_reference_golden(pkg):
+    """l_sph 12, 14 (HSDLA_MAX_LSPH), 13 with x = |K| r up to ~21: every Bessel regime at
+    high order; checked per (atom, l) block so no block hides behind larger ones."""
+    d = golden("ab_high.npz")
+    c = pkg.compute_AB(spec_from_golden(d))
+    a, b = c.A_star.array, c.B_star.array
+    assert rel_fro(a, d["A"]) <= 1e-13
+    assert rel_fro(b, d["B"]) <= 1e-13
+    r0 = 0
+    for l_max in d["spec_l_sph"]:
+        for l in range(int(l_max) + 1):
+            rows = slice(r0 + l * l, r0 + (l + 1) ** 2)
+            assert rel_fro(a[rows], d["A"][rows]) <= 1e-12, (l_max, l)
+            assert rel_fro(b[rows], d["B"][rows]) <= 1e-12, (l_max, l)
+        r0 += (int(l_max) + 1) ** 2
+
+
 def test_compute_ab_c1_vs_reference_golden(pkg):
     from paper_1602_06589_b200 import configs
 

@@ -60,6 +60,14 @@ def test_compute_ab_small_matches_reference():
     np.testing.assert_array_equal(norms, d["udot_norms"])
 
 
+def test_compute_ab_high_l_matches_reference():
+    d = golden("ab_high.npz")
+    a, b, norms, _ = of.compute_ab(spec_from_golden(d))
+    assert rel_fro(a, d["A"]) <= 1e-13
+    assert rel_fro(b, d["B"]) <= 1e-13
+    np.testing.assert_array_equal(norms, d["udot_norms"])
+
+
 def test_compute_ab_c1_matches_reference():
     d = golden("ab_c1.npz")
     inst = configs.make_instance("C1")
@@ -118,3 +126,22 @@ def test_predict_flops_and_memory_kats():
     assert ob.estimate_memory(384, 81, 29144, True) == 71_605_642_240
     led = ob.predict_flops([1], 1, [True])
     assert led["hermitian_rank_k"] == 12 and led["cholesky"] == 1
+
+
+def test_reduced_overlap_matches_reference():
+    """oracle/reduced.py vs the reference's reduced_overlap_inputs + reduced_S_AA."""
+    from oracle import reduced as orr
+
+    d = golden("reduced.npz")
+    spec = spec_from_golden(d)
+    f, w = orr.reduced_inputs(spec)
+    for a in range(len(f)):
+        assert rel_fro(f[a], d[f"small_f_{a}"]) <= 1e-14
+        np.testing.assert_array_equal(w[a], d[f"small_w_{a}"])
+    s = orr.reduced_s_aa(f, w, spec.positions, spec.k_vectors, spec.omega)
+    assert rel_fro(s, d["small_S"]) <= 1e-13
+    inst = configs.make_instance("C1")
+    f, w = orr.reduced_inputs(inst.spec)
+    s = orr.reduced_s_aa(f, w, inst.spec.positions, inst.spec.k_vectors, inst.spec.omega)
+    assert rel_fro(s @ d["c1_V"], d["c1_SV"]) <= 1e-13
+    assert rel_fro(np.diag(s), d["c1_diag"]) <= 1e-13

@@ -87,94 +87,132 @@ __global__ void rs_prep_kernel(int n, int n_atoms, const double* __restrict__ kv
 }
 
 struct RsParams {
-  int n, n_types, tiles;
+  int n, tiles;
   const double4* unit;       // n: K^ and 1 (0 for K = 0)
   const double2* phase;      // n_atoms x n: e^{i K.x_a}
-  const double* f;           // match-factor rows, stride ldf
+  const double* f;           // this type's match-factor rows l = 0..ltop, stride ldf
   long long ldf;
-  const long long* trow;     // per type: first f row
-  const int* tltop;          // per type: l_top
-  const int* tatoms;         // atoms grouped by type
-  const int* tbegin;         // n_types + 1
-  const double* coef;        // per f row: (2l+1) / (4 pi) / W^2
+  int ltop;
+  const double* coef;        // this type's (2l+1) / (4 pi) / W_l^2
+  const int* atoms;          // atoms of this type
+  int n_type_atoms;
+  int accumulate;            // add to the lower triangle already in S (earlier types)
   double scale;              // (4 pi)^2 / Omega
   double2* S;
   long long lds;
 };
 
-// One CTA per lower 32 x 32 tile, 128 threads, each thread a 2 x 4 micro-tile (rows
-// i0 + tx + 16 r, columns j0 + ty + 8 s).  Atoms that share match factors (one type) share
-// the radial sum, so per element the work is
-//   types x (l+1) x (Legendre step + FMA)  +  atoms x 2 complex FMAs (structure factor),
-// against 8 (l+1)^2 flops per atom of the stacked A*^H A*.  The tile's strict lower part
-// is mirrored as conj into the upper triangle and the diagonal's imaginary part is 0, so the
-// result is exactly Hermitian (as the reference's is).
-template <int LMAX>
-__global__ void __launch_bounds__(128) rs_kernel(RsParams p) {
+__device__ __forceinline__ void cp_async16_rs(void* smem_dst, const void* gsrc) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_commit_rs() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_rs() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+constexpr int kRsTile = 64;
+constexpr int kRsAtomChunk = 8;
+
+// One CTA per lower 64 x 64 tile and atom type, 256 threads, each thread a 4 x 4 micro-tile
+// (rows i0 + tx + 16 r, columns j0 + ty + 16 s):
+//   radial(i, j) = sum_l coef_l f_l(i) f_l(j) P_l(K^_i . K^_j)      (Legendre recurrence)
+//   sf(i, j)     = sum_{a in type} conj(p_a(i)) p_a(j)               (phases staged in smem)
+//   S(i, j)     (+)= scale * sf * radial
+// Per element: (l+1) x (recurrence + FMA) + atoms x 4 FMAs, against 8 (l+1)^2 flops per
+// atom of the stacked A*^H A*.  The strict lower part is mirrored as conj and the diagonal's
+// imaginary part is 0, so the result is exactly Hermitian (as the reference's is).
+__global__ void __launch_bounds__(256) rs_kernel(RsParams p) {
+  constexpr int MR = 4, MS = 4;
+  __shared__ __align__(16) double2 sEi[2][kRsAtomChunk][kRsTile];
+  __shared__ __align__(16) double2 sEj[2][kRsAtomChunk][kRsTile];
   int t = blockIdx.x, tj = 0;
   while (t >= p.tiles - tj) { t -= p.tiles - tj; ++tj; }
   const int ti = tj + t;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // ty < 8
-  constexpr int MR = 2, MS = 4;
-  int gi[MR], gj[MS];
-  double4 ui[MR], uj[MS];
-#pragma unroll
-  for (int r = 0; r < MR; ++r) {
-    gi[r] = ti * 32 + tx + 16 * r;
-    ui[r] = p.unit[min(gi[r], p.n - 1)];
-  }
-#pragma unroll
-  for (int s = 0; s < MS; ++s) {
-    gj[s] = tj * 32 + ty + 8 * s;
-    uj[s] = p.unit[min(gj[s], p.n - 1)];
-  }
-  double c[MR][MS];
-#pragma unroll
-  for (int r = 0; r < MR; ++r)
-#pragma unroll
-    for (int s = 0; s < MS; ++s) {
-      double v = 1.0;  // a zero K-vector is parallel to everything (oracle.py:199-201)
-      if (ui[r].w != 0.0 && uj[s].w != 0.0)
-        v = fmin(fmax(__fma_rn(ui[r].x, uj[s].x, __fma_rn(ui[r].y, uj[s].y, __dmul_rn(ui[r].z, uj[s].z))),
-                      -1.0), 1.0);
-      c[r][s] = v;
+  const int i0 = ti * kRsTile, j0 = tj * kRsTile;
+  // cp.async of chunk q's phases (kRsAtomChunk atoms x 64 rows/columns) into buffer q & 1
+  auto stage = [&](int q) {
+    const int a0 = q * kRsAtomChunk;
+    const int na = min(kRsAtomChunk, p.n_type_atoms - a0);
+    for (int e = threadIdx.x; e < na * kRsTile; e += blockDim.x) {
+      const int k = e / kRsTile, x = e - k * kRsTile;
+      const double2* ph = p.phase + (long long)p.atoms[a0 + k] * p.n;
+      cp_async16_rs(&sEi[q & 1][k][x], ph + min(i0 + x, p.n - 1));
+      cp_async16_rs(&sEj[q & 1][k][x], ph + min(j0 + x, p.n - 1));
     }
-  double ar[MR][MS] = {}, ai[MR][MS] = {};
-  for (int ty_ = 0; ty_ < p.n_types; ++ty_) {
-    const double* fr = p.f + p.trow[ty_] * p.ldf;
-    const double* cf = p.coef + p.trow[ty_];
-    const int lt = p.tltop[ty_];
-    double rad[MR][MS] = {}, p0[MR][MS], p1[MR][MS];
+  };
+  if (p.n_type_atoms > 0) stage(0);
+  cp_async_commit_rs();
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  int ci[MR], cj[MS];  // clamped indices (edge tiles compute duplicates, never stored)
+#pragma unroll
+  for (int r = 0; r < MR; ++r) ci[r] = min(i0 + tx + 16 * r, p.n - 1);
+#pragma unroll
+  for (int s = 0; s < MS; ++s) cj[s] = min(j0 + ty + 16 * s, p.n - 1);
+  // ---- radial part
+  double rad[MR][MS] = {};
+  {
+    double c[MR][MS], p0[MR][MS], p1[MR][MS];
+    double4 ui[MR], uj[MS];
+#pragma unroll
+    for (int r = 0; r < MR; ++r) ui[r] = p.unit[ci[r]];
+#pragma unroll
+    for (int s = 0; s < MS; ++s) uj[s] = p.unit[cj[s]];
+#pragma unroll
+    for (int r = 0; r < MR; ++r)
+#pragma unroll
+      for (int s = 0; s < MS; ++s) {
+        double v = 1.0;  // a zero K-vector is parallel to everything (oracle.py:199-201)
+        if (ui[r].w != 0.0 && uj[s].w != 0.0)
+          v = fmin(fmax(__fma_rn(ui[r].x, uj[s].x, __fma_rn(ui[r].y, uj[s].y, __dmul_rn(ui[r].z, uj[s].z))),
+                        -1.0), 1.0);
+        c[r][s] = v;
+        p0[r][s] = 0.0;
+        p1[r][s] = 0.0;
+      }
 #pragma unroll 1
-    for (int l = 0; l <= lt; ++l) {
+    for (int l = 0; l <= p.ltop; ++l) {
       const double tl = (double)(2 * l - 1), ml = (double)(l - 1), il = 1.0 / (double)l;
+      const double cl = p.coef[l];
+      const double* fr = p.f + l * p.ldf;
       double hi[MR], fj[MS];
 #pragma unroll
-      for (int r = 0; r < MR; ++r) hi[r] = __dmul_rn(cf[l], __ldg(fr + l * p.ldf + min(gi[r], p.n - 1)));
+      for (int r = 0; r < MR; ++r) hi[r] = __dmul_rn(cl, __ldg(fr + ci[r]));
 #pragma unroll
-      for (int s = 0; s < MS; ++s) fj[s] = __ldg(fr + l * p.ldf + min(gj[s], p.n - 1));
+      for (int s = 0; s < MS; ++s) fj[s] = __ldg(fr + cj[s]);
 #pragma unroll
       for (int r = 0; r < MR; ++r)
 #pragma unroll
         for (int s = 0; s < MS; ++s) {
-          double pl;  // P_l(c), special.py:22-38 recurrence
+          double pl;  // P_l, special.py:22-38 recurrence
           if (l == 0) pl = 1.0;
           else if (l == 1) pl = c[r][s];
           else pl = __dmul_rn(__fma_rn(__dmul_rn(tl, c[r][s]), p1[r][s], -__dmul_rn(ml, p0[r][s])), il);
-          if (l > 0) p0[r][s] = p1[r][s];
+          p0[r][s] = p1[r][s];
           p1[r][s] = pl;
           rad[r][s] = __fma_rn(__dmul_rn(hi[r], fj[s]), pl, rad[r][s]);
         }
     }
-    // structure factor of the type: sum_a conj(p_a(i)) p_a(j)
-    double sr[MR][MS] = {}, si[MR][MS] = {};
-    for (int k = p.tbegin[ty_]; k < p.tbegin[ty_ + 1]; ++k) {
-      const double2* ph = p.phase + (long long)p.tatoms[k] * p.n;
+  }
+  // ---- structure factor of the type: phases of kRsAtomChunk atoms at a time, double-
+  // buffered in smem by cp.async (chunk 0 was issued before the radial loop)
+  double sr[MR][MS] = {}, si[MR][MS] = {};
+  const int nchunk = (p.n_type_atoms + kRsAtomChunk - 1) / kRsAtomChunk;
+  for (int q = 0; q < nchunk; ++q) {
+    if (q + 1 < nchunk) stage(q + 1);
+    cp_async_commit_rs();
+    cp_async_wait_rs<1>();
+    __syncthreads();
+    const int na = min(kRsAtomChunk, p.n_type_atoms - q * kRsAtomChunk);
+    const int b = q & 1;
+#pragma unroll 2
+    for (int k = 0; k < na; ++k) {
       double2 pi_[MR], pj[MS];
 #pragma unroll
-      for (int r = 0; r < MR; ++r) pi_[r] = __ldg(ph + min(gi[r], p.n - 1));
+      for (int r = 0; r < MR; ++r) pi_[r] = sEi[b][k][tx + 16 * r];
 #pragma unroll
-      for (int s = 0; s < MS; ++s) pj[s] = __ldg(ph + min(gj[s], p.n - 1));
+      for (int s = 0; s < MS; ++s) pj[s] = sEj[b][k][ty + 16 * s];
 #pragma unroll
       for (int r = 0; r < MR; ++r)
 #pragma unroll
@@ -183,32 +221,27 @@ __global__ void __launch_bounds__(128) rs_kernel(RsParams p) {
           si[r][s] = __fma_rn(pi_[r].x, pj[s].y, __fma_rn(-pi_[r].y, pj[s].x, si[r][s]));
         }
     }
-#pragma unroll
-    for (int r = 0; r < MR; ++r)
-#pragma unroll
-      for (int s = 0; s < MS; ++s) {
-        ar[r][s] = __fma_rn(sr[r][s], rad[r][s], ar[r][s]);
-        ai[r][s] = __fma_rn(si[r][s], rad[r][s], ai[r][s]);
-      }
+    __syncthreads();  // buffer b is refilled by the stage() of iteration q + 1
   }
+  // ---- epilogue: lower tile + conjugate mirror
 #pragma unroll
   for (int r = 0; r < MR; ++r)
 #pragma unroll
     for (int s = 0; s < MS; ++s) {
-      const int i = gi[r], j = gj[s];
+      const int i = i0 + tx + 16 * r, j = j0 + ty + 16 * s;
       if (i >= p.n || j >= p.n || i < j) continue;
-      const double re = __dmul_rn(ar[r][s], p.scale);
-      const double im = (i == j) ? 0.0 : __dmul_rn(ai[r][s], p.scale);
-      p.S[i + (long long)j * p.lds] = make_double2(re, im);
+      double re = __dmul_rn(__dmul_rn(sr[r][s], rad[r][s]), p.scale);
+      double im = (i == j) ? 0.0 : __dmul_rn(__dmul_rn(si[r][s], rad[r][s]), p.scale);
+      double2* lo = p.S + i + (long long)j * p.lds;
+      if (p.accumulate) {
+        const double2 old = *lo;
+        re = __dadd_rn(re, old.x);
+        im = (i == j) ? 0.0 : __dadd_rn(im, old.y);
+      }
+      *lo = make_double2(re, im);
       if (i != j) p.S[j + (long long)i * p.lds] = make_double2(re, -im);
     }
 }
-
-typedef void (*rs_kernel_t)(RsParams);
-const rs_kernel_t kRsKernels[HSDLA_MAX_LSPH + 1] = {
-    rs_kernel<0>, rs_kernel<1>, rs_kernel<2>, rs_kernel<3>, rs_kernel<4>,
-    rs_kernel<5>, rs_kernel<6>, rs_kernel<7>, rs_kernel<8>, rs_kernel<9>,
-    rs_kernel<10>, rs_kernel<11>, rs_kernel<12>, rs_kernel<13>, rs_kernel<14>};
 
 }  // namespace
 
@@ -253,13 +286,11 @@ int reduced_s_aa(hsdla_ctx* ctx, const hsdla_reduced_args* r) {
   std::vector<long long> trow;
   std::vector<int> tlt, tatoms, tbegin;
   std::vector<int> type_of(na, -1);
-  int lmax = 0;
   for (int a = 0; a < na; ++a) {
     if (r->l_top[a] < 0 || r->l_top[a] > HSDLA_MAX_LSPH) {
       set_error("l above HSDLA_MAX_LSPH");
       return HSDLA_ERR_UNSUPPORTED;
     }
-    lmax = r->l_top[a] > lmax ? r->l_top[a] : lmax;
     for (size_t k = 0; k < trow.size(); ++k)
       if (trow[k] == r->f_row[a] && tlt[k] == r->l_top[a]) type_of[a] = (int)k;
     if (type_of[a] < 0) {
@@ -282,10 +313,7 @@ int reduced_s_aa(hsdla_ctx* ctx, const hsdla_reduced_args* r) {
   int rc = arena_begin(ctx, trow.size() * (sizeof(long long) + sizeof(int)) +
                                 (tatoms.size() + tbegin.size()) * sizeof(int) + 256);
   if (rc) return rc;
-  long long* dtrow = static_cast<long long*>(arena_push(ctx, trow.data(), trow.size() * sizeof(long long), nullptr));
-  int* dtlt = static_cast<int*>(arena_push(ctx, tlt.data(), tlt.size() * sizeof(int), nullptr));
   int* dtat = static_cast<int*>(arena_push(ctx, tatoms.data(), tatoms.size() * sizeof(int), nullptr));
-  int* dtb = static_cast<int*>(arena_push(ctx, tbegin.data(), tbegin.size() * sizeof(int), nullptr));
   rc = arena_flush(ctx);
   if (rc) return rc;
   rs_prep_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(n, na, r->k_vectors, r->positions,
@@ -293,23 +321,25 @@ int reduced_s_aa(hsdla_ctx* ctx, const hsdla_reduced_args* r) {
   HS_CHECK_LAUNCH();
   RsParams p;
   p.n = n;
-  p.n_types = (int)trow.size();
-  p.tiles = (n + 31) / 32;
+  p.tiles = (n + kRsTile - 1) / kRsTile;
   p.unit = unit;
   p.phase = phase;
-  p.f = r->f;
   p.ldf = r->ld_f;
-  p.trow = dtrow;
-  p.tltop = dtlt;
-  p.tatoms = dtat;
-  p.tbegin = dtb;
-  p.coef = r->coef;
   p.scale = r->scale;
   p.S = reinterpret_cast<double2*>(r->S);
   p.lds = r->lds;
   const long long ntile = (long long)p.tiles * (p.tiles + 1) / 2;
-  kRsKernels[lmax]<<<(unsigned)ntile, 128, 0, ctx->stream>>>(p);
-  HS_CHECK_LAUNCH();
+  // one launch per atom type; later types accumulate into the lower triangle
+  for (size_t k = 0; k < trow.size(); ++k) {
+    p.f = r->f + trow[k] * r->ld_f;
+    p.coef = r->coef + trow[k];
+    p.ltop = tlt[k];
+    p.atoms = dtat + tbegin[k];
+    p.n_type_atoms = tbegin[k + 1] - tbegin[k];
+    p.accumulate = k > 0;
+    rs_kernel<<<(unsigned)ntile, 256, 0, ctx->stream>>>(p);
+    HS_CHECK_LAUNCH();
+  }
   HS_CUDA(cudaFreeAsync(scratch, ctx->stream));
   return HSDLA_OK;
 }

@@ -42,6 +42,10 @@ def parse():
     p.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--mode", default="kpoints", choices=["kpoints", "panels"],
+                   help="kpoints: one k-point per GPU per step (weak scaling, default); "
+                        "panels: ONE k-point split over all GPUs by column panels, tiles "
+                        "stored into rank 0's H/S over NVLink peer memory (strong scaling)")
     return p.parse_args()
 
 
@@ -339,10 +343,107 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_panels(args):
+    """One k-point per step, column panels over all ranks (SURVEY §8e, C3/C4 strong scaling):
+    every rank regenerates A*/B* locally, computes its owned lower tiles and stores them and
+    their mirror straight into rank 0's symmetric-memory H and S (shard.P2PShardedBuild)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1602_06589_b200 import configs
+    from paper_1602_06589_b200.pipeline import DeviceSpec, pack_tmats
+    from paper_1602_06589_b200.shard import P2PShardedBuild
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if "MASTER_ADDR" not in os.environ:  # single process without torchrun
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(sk.getsockname()[1]),
+                              RANK="0", WORLD_SIZE="1")
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    inst = configs.make_instance(args.config)
+    spec = inst.spec
+    n = spec.n_basis
+    dspec = DeviceSpec(spec)
+    tpack = pack_tmats(inst.tmats)
+    sb = P2PShardedBuild(n, dspec.heights)
+    out = None
+    for _ in range(max(args.warmup, 3)):
+        out = sb.run(dspec, tpack)
+    kern = {"contract_S": [], "contract_H": [], "apply_Z": [], "apply_XY": []}
+    stream = torch.cuda.current_stream()
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            res = sb.pipe.run(dspec, tpack)
+            torch.cuda.synchronize()
+            dist.barrier()
+            for k, v in res["kernel_ms"].items():
+                kern[k].append(v)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    mask = res["hpd_mask"]
+    flops_step = configs.nominal_flops(spec, mask)
+    value = flops_step * args.steps / (float(ms.item()) / 1e3) / 1e12
+    # e2e: spec upload + sharded build + full H, S read back to pinned host on rank 0
+    hh = torch.empty((n, n), dtype=torch.complex128, pin_memory=True)
+    hs = torch.empty((n, n), dtype=torch.complex128, pin_memory=True)
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        out = sb.run(DeviceSpec(spec), tpack)
+        if out is not None:
+            hh.copy_(out[0], non_blocking=True)
+            hs.copy_(out[1], non_blocking=True)
+            torch.cuda.synchronize()
+    e2e = torch.tensor([(time.perf_counter() - t0) * 1e3 / args.steps], device="cuda")
+    dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        rows = dspec.rows
+        hpd_rows = int(sum(h for h, m in zip(dspec.heights, mask) if m))
+        kc = statistics.mean(kern["contract_S"]) + statistics.mean(kern["contract_H"])
+        fc = contract_flops(n, rows, hpd_rows) / world  # this rank's share of the tiles
+        line = {
+            "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": round(float(ms.item()) / args.steps, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: N_G={n}, R={rows}, one k-point split over "
+                                   f"{world} GPU(s) by column panels",
+                       "n_basis": n, "rows": rows, "ledger_flops_per_step": flops_step,
+                       "parallelism": f"panels-p2p{world}",
+                       "l2": "operands and H, S exceed the 126 MB L2; no flush"},
+            "fp64_peak_frac": round(value / world / FP64_PEAK_TFLOPS, 4),
+            "roofline": {"bound": "tensor", "achieved": round(fc / (kc / 1e3) / 1e12, 3),
+                         "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": round(fc / (kc / 1e3) / 1e12 / FP64_PEAK_TFLOPS, 4),
+                         "traffic": None,
+                         "kernel_ms": {k: round(statistics.mean(v), 4) for k, v in kern.items()}},
+            "e2e": {"value": round(flops_step / (float(e2e.item()) / 1e3) / 1e12, 4), "unit": UNIT,
+                    "h2d_bytes_per_step": int(dspec.h2d_bytes), "d2h_bytes_per_step": 32 * n * n,
+                    "ms_per_step": round(float(e2e.item()), 3),
+                    "api": "paper_1602_06589_b200.shard.P2PShardedBuild.run + D2H of H, S"},
+            "gpu_launches": args.steps * sb.pipe.launches_per_run(dspec),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.mode == "panels":
+        run_panels(args)
     else:
         run_ours(args)
 

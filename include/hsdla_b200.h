@@ -188,6 +188,11 @@ typedef struct {
   hsdla_c64* H_host;
   hsdla_c64* S_host;
   int64_t ldh_host;
+  /* With sharding: 1 = write the owned tiles together with their conjugate mirror, so H / S
+   * must be full n_basis x n_basis matrices shared by all shards — e.g. the consumer rank's
+   * buffers mapped into every rank through NVLink peer memory: the contraction epilogue then
+   * is the gather (no separate collective, no mirror pass).  0 = lower tiles only. */
+  int32_t shard_mirror;
 } hsdla_build_args;
 
 typedef struct {

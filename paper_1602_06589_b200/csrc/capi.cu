@@ -578,7 +578,8 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     }
     for (int j = 0; j < nb; ++j)
       if (hsdla_panel_owner(nb, a->n_shards, j) == a->shard_rank) {
-        Prob p = make_prob(C, a->ldh, n, n, PROB_TRI_LOWER, seg0, nseg, 0);
+        Prob p = make_prob(C, a->ldh, n, n, a->shard_mirror ? PROB_TRI_MIRROR : PROB_TRI_LOWER,
+                           seg0, nseg, 0);
         p.col_tile_lo = j;
         p.col_tile_hi = j + 1;
         probs.push_back(p);

@@ -166,7 +166,7 @@ class _Call:
 
     def __init__(self, *, n_basis, heights, row_offset, tpack: TPack, A, B, Bs, udot, ld,
                  force_general_path, H, S, ldh, shard_rank, n_shards, workspace, host_out,
-                 ab_args=None):
+                 ab_args=None, shard_mirror=False):
         lib = _native.load()
         t = device.torch()
         self.na = len(heights)
@@ -199,6 +199,7 @@ class _Call:
         a.ldh = ldh
         a.shard_rank = shard_rank
         a.n_shards = n_shards
+        a.shard_mirror = 1 if shard_mirror else 0
         if host_out is not None:  # pinned (n, n) tensors, row j = column j
             a.H_host = host_out[0].data_ptr()
             a.S_host = host_out[1].data_ptr()
@@ -274,7 +275,10 @@ class HSPipeline:
     """Reusable HBM buffers for up to `n_capacity` basis functions and one atom layout;
     `run` = one k-point (any N_G <= n_capacity, e.g. a k-point batch with varying G-sets)."""
 
-    def __init__(self, n_capacity: int, heights, *, shard_rank: int = 0, n_shards: int = 1):
+    def __init__(self, n_capacity: int, heights, *, shard_rank: int = 0, n_shards: int = 1,
+                 out=None, shard_mirror: bool = False):
+        """`out` = (H, S) device (n_capacity, ld) tensors to write instead of own buffers
+        (e.g. a peer rank's, mapped through NVLink); `shard_mirror` see hsdla_build_args."""
         t = device.require_cuda()
         self.n_capacity = int(n_capacity)
         self.heights = np.asarray(heights, dtype=np.int32)
@@ -285,10 +289,16 @@ class HSPipeline:
         self.B = device.empty_matrix(self.ld, n, self.ld, zero=True)
         self.Bs = device.empty_matrix(self.ld, n, self.ld, zero=True)
         self.udot = t.zeros(self.ld, dtype=t.float64, device="cuda")
-        self.H = device.empty_matrix(n, n, n)
-        self.S = device.empty_matrix(n, n, n)
+        if out is None:
+            self.H = device.empty_matrix(n, n, n)
+            self.S = device.empty_matrix(n, n, n)
+        else:
+            self.H, self.S = out
+            if tuple(self.H.shape) != (n, n) or tuple(self.S.shape) != (n, n):
+                raise ContractViolationError("output buffers must be (n_capacity, n_capacity)")
         self.workspace = None
         self.shard_rank, self.n_shards = shard_rank, n_shards
+        self.shard_mirror = bool(shard_mirror)
         self.n_basis = 0
         self._inflight = {}
 
@@ -309,7 +319,8 @@ class HSPipeline:
                      tpack=tpack, A=self.A, B=self.B, Bs=self.Bs, udot=self.udot, ld=self.ld,
                      force_general_path=force_general_path, H=self.H, S=self.S,
                      ldh=self.n_capacity, shard_rank=self.shard_rank, n_shards=self.n_shards,
-                     workspace=self.workspace, host_out=host_out, ab_args=ab)
+                     workspace=self.workspace, host_out=host_out, ab_args=ab,
+                     shard_mirror=self.shard_mirror)
         call.keep.append(dspec)
         self.workspace = call.workspace
         return call

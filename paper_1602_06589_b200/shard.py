@@ -65,10 +65,22 @@ def gather_panels(mat, n: int, world: int, rank: int, dst: int = 0, group=None):
     return mat
 
 
-def build_hs_sharded(spec, tmats, config=None, *, dst: int = 0, group=None):
+def build_hs_sharded(spec, tmats, config=None, *, dst: int = 0, group=None,
+                     transport: str = "nccl"):
     """One k-point's H and S computed by all ranks of the process group (column panels),
-    gathered and mirrored on rank `dst`; returns device (H, S, result) on `dst`, None
-    elsewhere.  Every rank must call it (collective)."""
+    assembled on rank `dst`; returns device (H, S, result) on `dst`, None elsewhere.
+    Every rank must call it (collective).
+
+    transport="nccl": each rank writes its panels locally, then `gather_panels` moves them
+    to `dst` (batched NCCL send/recv) and `dst` runs the Hermitian mirror.
+    transport="p2p": H and S live in symmetric memory; every rank's contraction epilogue
+    stores its owned tiles and their conjugate mirror straight into `dst`'s buffers over
+    NVLink (hsdla_build_args.shard_mirror), so compute and gather are one kernel and no
+    mirror pass is left."""
+    if transport == "p2p":
+        return _build_hs_sharded_p2p(spec, tmats, config, dst=dst, group=group)
+    if transport != "nccl":
+        raise ValueError(f"unknown transport {transport!r}")
     import ctypes
 
     import torch.distributed as dist
@@ -97,3 +109,60 @@ def build_hs_sharded(spec, tmats, config=None, *, dst: int = 0, group=None):
         if flag.value:
             raise ContractViolationError("accumulator contains non-finite values")
     return pipe.H[:n, :n], pipe.S[:n, :n], res
+
+
+class P2PShardedBuild:
+    """Reusable state of the P2P panel-sharded build of one k-point shape: H and S in torch
+    symmetric memory (mapped into every rank), the consumer's buffers as every rank's
+    output, and an HSPipeline per rank writing its owned tiles + mirror there."""
+
+    def __init__(self, n: int, heights, *, dst: int = 0, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        from .pipeline import HSPipeline
+
+        self.group = group or dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        self.dst = dst
+        self.n = n
+        self.local = [symm_mem.empty((n, n), dtype=torch.complex128, device="cuda")
+                      for _ in range(2)]
+        peers = []
+        for buf in self.local:
+            hdl = symm_mem.rendezvous(buf, self.group.group_name)
+            peers.append(hdl.get_buffer(dst, (n, n), torch.complex128))
+        self.pipe = HSPipeline(n, heights, shard_rank=self.rank, n_shards=self.world,
+                               out=tuple(peers), shard_mirror=True)
+
+    def run(self, dspec, tpack, force_general_path: bool = False):
+        """All ranks: build; returns (H, S, result) device views on dst, None elsewhere."""
+        import torch
+        import torch.distributed as dist
+
+        from .errors import ContractViolationError
+
+        try:
+            res, bad = self.pipe.run(dspec, tpack, force_general_path), 0
+        except ContractViolationError:
+            res, bad = None, 1
+        torch.cuda.synchronize()  # this rank's remote stores are complete
+        flag = torch.tensor([bad], device="cuda")
+        dist.all_reduce(flag, group=self.group)  # orders every rank's stores before dst reads
+        if int(flag.item()):
+            raise ContractViolationError("accumulator contains non-finite values")
+        if self.rank != self.dst:
+            return None
+        return self.local[0], self.local[1], res
+
+
+def _build_hs_sharded_p2p(spec, tmats, config=None, *, dst: int = 0, group=None):
+    from .builder import BuildConfig
+    from .pipeline import DeviceSpec, pack_tmats
+
+    config = config or BuildConfig()
+    dspec = DeviceSpec(spec)
+    return P2PShardedBuild(spec.n_basis, dspec.heights, dst=dst, group=group).run(
+        dspec, pack_tmats(tmats), config.force_general_path)

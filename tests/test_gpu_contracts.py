@@ -288,3 +288,62 @@ def test_sharded_panels_reassemble_full_build(pkg, world):
         assert lib.hsdla_mirror_lower(device.ctx(), n, device.ptr(m), n, ctypes.byref(flag)) == 0
     h, s = h_asm.cpu().numpy().T, s_asm.cpu().numpy().T
     assert rel_fro(h, h_ref) <= 1e-14 and rel_fro(s, s_ref) <= 1e-14
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_shard_mirror_into_one_shared_buffer(pkg, world):
+    """The P2P transport's data path on one GPU: every shard writes its owned tiles and their
+    conjugate mirror (hsdla_build_args.shard_mirror) into ONE full buffer, as the ranks do
+    into the consumer's symmetric-memory buffer over NVLink; no gather or mirror pass."""
+    import torch
+
+    from paper_1602_06589_b200 import configs
+    from paper_1602_06589_b200.pipeline import DeviceSpec, HSPipeline, pack_tmats
+
+    inst = configs.make_instance("C1")
+    spec = inst.spec
+    n = spec.n_basis
+    dspec = DeviceSpec(spec)
+    tp = pack_tmats(inst.tmats)
+    full = HSPipeline(n, dspec.heights)
+    full.run(dspec, tp)
+    h_ref, s_ref = (m.cpu().numpy().T for m in full.result_views())
+    shared = (torch.full((n, n), complex("nan"), dtype=torch.complex128, device="cuda"),
+              torch.full((n, n), complex("nan"), dtype=torch.complex128, device="cuda"))
+    for r in range(world):
+        HSPipeline(n, dspec.heights, shard_rank=r, n_shards=world, out=shared,
+                   shard_mirror=True).run(dspec, tp)
+    h, s = (m.cpu().numpy().T for m in shared)
+    assert np.isfinite(h).all() and np.isfinite(s).all()     # every element written once
+    assert rel_fro(h, h_ref) <= 1e-14 and rel_fro(s, s_ref) <= 1e-14
+    np.testing.assert_array_equal(h, h.conj().T)
+
+
+def test_build_hs_sharded_p2p_single_rank(pkg):
+    """build_hs_sharded(transport="p2p") end to end through torch symmetric memory on a
+    one-rank NCCL group (the only GPU count this suite has): rendezvous, peer-buffer
+    mapping, epilogue stores, flag all-reduce."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1602_06589_b200 import configs
+    from paper_1602_06589_b200.pipeline import build_hs
+    from paper_1602_06589_b200.shard import build_hs_sharded
+
+    inst = configs.make_instance("C1")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        h_d, s_d, res = build_hs_sharded(inst.spec, inst.tmats, transport="p2p")
+        h, s = h_d.cpu().numpy().T, s_d.cpu().numpy().T
+    finally:
+        dist.destroy_process_group()
+    h_ref, s_ref, _ = build_hs(inst.spec, inst.tmats)
+    assert rel_fro(h, h_ref.array) <= 1e-14 and rel_fro(s, s_ref.array) <= 1e-14
+    np.testing.assert_array_equal(h, h.conj().T)

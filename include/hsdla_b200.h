@@ -193,6 +193,11 @@ typedef struct {
    * buffers mapped into every rank through NVLink peer memory: the contraction epilogue then
    * is the gather (no separate collective, no mirror pass).  0 = lower tiles only. */
   int32_t shard_mirror;
+  /* 1 = the T sets (t_aa/t_ab/t_bb contents) are unchanged since the previous build on this
+   * context: the T forms and Cholesky factors still in `workspace` are reused and the T
+   * preparation is skipped (T does not depend on the k-point).  Honoured only when the
+   * workspace, T pointers, t_ld, t_dim and force_general_path also match that build. */
+  int32_t reuse_t;
 } hsdla_build_args;
 
 typedef struct {

@@ -72,6 +72,14 @@ struct Arena;  // descriptor staging (defined in capi.cu)
 }  // namespace hsdla
 
 struct hsdla_ctx {
+  // Key of the T preparation whose results sit in a build workspace (hsdla_build_args.reuse_t).
+  struct TKey {
+    const void* ws = nullptr;
+    const void *taa = nullptr, *tab = nullptr, *tbb = nullptr;
+    long long t_ld = 0;
+    int force = -1;
+    std::vector<int> tdim;
+  } tkey;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // T preparation overlaps A/B generation here
   cudaStream_t copy = nullptr;  // D2H of finished H / S, overlapped with later compute

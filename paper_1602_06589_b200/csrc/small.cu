@@ -96,7 +96,6 @@ __device__ void chol_packed(int n, const double2* __restrict__ T, long long ldt,
                             long long ldf, int* info) {
   extern __shared__ double2 Lp[];
   __shared__ int s_bad;
-  __shared__ double s_ljj;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int tx = tid & 31, ty = tid >> 5, nty = nt >> 5;
   if (tid == 0) s_bad = 0;
@@ -115,34 +114,28 @@ __device__ void chol_packed(int n, const double2* __restrict__ T, long long ldt,
     if (tid == 0) *info = -1;
     return;
   }
+  // Right-looking, one barrier per column: every thread reads the pivot and forms
+  // 1/L[j][j] itself; column j stays unscaled in shared memory (its scaled values go
+  // straight to F), so the trailing update can scale on the fly without a second pass.
   for (int j = 0; j < n; ++j) {
-    if (tid == 0) {
-      const double d = Lp[packed_idx(j, j)].x;
-      if (!(d > 0.0) || !isfinite(d)) {
-        s_bad = j + 1;
-      } else {
-        s_ljj = sqrt(d);
-        Lp[packed_idx(j, j)] = make_double2(s_ljj, 0.0);
-      }
-    }
-    __syncthreads();
-    if (s_bad) {
-      if (tid == 0) *info = s_bad;
+    const double d = Lp[packed_idx(j, j)].x;
+    if (!(d > 0.0) || !isfinite(d)) {  // uniform across the block
+      if (tid == 0) *info = j + 1;
       return;
     }
-    const double ljj = s_ljj;
-    for (int i = j + 1 + tid; i < n; i += nt) {
-      const double2 v = Lp[packed_idx(i, j)];
-      Lp[packed_idx(i, j)] = make_double2(v.x / ljj, v.y / ljj);
-    }
-    __syncthreads();
-    // trailing update L[i][k] -= L[i][j] conj(L[k][j]), j < k <= i: a warp per row i,
-    // lanes along k (consecutive packed addresses), L[i][j] broadcast within the warp.
+    const double ljj = sqrt(d);
+    const double inv = 1.0 / ljj;
+    if (tid == 0) F[j + (long long)j * ldf] = make_double2(ljj, 0.0);
+    // trailing update L[i][k] -= L[i][j] conj(L[k][j]) / L[j][j]^2, j < k <= i: a warp per
+    // row i, lanes along k (consecutive packed addresses), L[i][j] broadcast in the warp.
     for (int i = j + 1 + ty; i < n; i += nty) {
       const int pi = packed_idx(i, 0);
-      const double2 a = Lp[pi + j];
+      const double2 a0 = Lp[pi + j];
+      const double2 a = make_double2(a0.x * inv, a0.y * inv);
+      if (tx == 0) F[i + (long long)j * ldf] = a;
       for (int k = j + 1 + tx; k <= i; k += 32) {
-        const double2 b = Lp[packed_idx(k, j)];
+        const double2 b0 = Lp[packed_idx(k, j)];
+        const double2 b = make_double2(b0.x * inv, b0.y * inv);
         double2 v = Lp[pi + k];
         v.x -= a.x * b.x + a.y * b.y;
         v.y -= a.y * b.x - a.x * b.y;
@@ -153,7 +146,7 @@ __device__ void chol_packed(int n, const double2* __restrict__ T, long long ldt,
   }
   for (long long e = tid; e < (long long)n * n; e += nt) {
     const int r = (int)(e % n), c = (int)(e / n);
-    F[r + c * ldf] = (r >= c) ? Lp[packed_idx(r, c)] : make_double2(0.0, 0.0);
+    if (r < c) F[r + c * ldf] = make_double2(0.0, 0.0);
   }
   if (tid == 0) *info = 0;
 }

@@ -166,7 +166,7 @@ class _Call:
 
     def __init__(self, *, n_basis, heights, row_offset, tpack: TPack, A, B, Bs, udot, ld,
                  force_general_path, H, S, ldh, shard_rank, n_shards, workspace, host_out,
-                 ab_args=None, shard_mirror=False):
+                 ab_args=None, shard_mirror=False, reuse_t=False):
         lib = _native.load()
         t = device.torch()
         self.na = len(heights)
@@ -200,6 +200,7 @@ class _Call:
         a.shard_rank = shard_rank
         a.n_shards = n_shards
         a.shard_mirror = 1 if shard_mirror else 0
+        a.reuse_t = 1 if reuse_t else 0
         if host_out is not None:  # pinned (n, n) tensors, row j = column j
             a.H_host = host_out[0].data_ptr()
             a.S_host = host_out[1].data_ptr()
@@ -299,6 +300,7 @@ class HSPipeline:
         self.workspace = None
         self.shard_rank, self.n_shards = shard_rank, n_shards
         self.shard_mirror = bool(shard_mirror)
+        self._last_t = None  # (TPack, force) of the previous call: T forms reusable
         self.n_basis = 0
         self._inflight = {}
 
@@ -315,14 +317,19 @@ class HSPipeline:
             raise ContractViolationError("spec shape does not fit the pipeline buffers")
         self.n_basis = dspec.n_basis
         ab = make_ab_args(dspec, self.A, self.B, self.Bs, self.ld, None)
+        # A TPack is an immutable device copy, so the same object means the same T: its
+        # forms and Cholesky factors from the previous call are still in the workspace.
+        last = self._last_t
+        reuse = last is not None and last[0] is tpack and last[1] == bool(force_general_path)
         call = _Call(n_basis=dspec.n_basis, heights=dspec.heights, row_offset=dspec.row_offset,
                      tpack=tpack, A=self.A, B=self.B, Bs=self.Bs, udot=self.udot, ld=self.ld,
                      force_general_path=force_general_path, H=self.H, S=self.S,
                      ldh=self.n_capacity, shard_rank=self.shard_rank, n_shards=self.n_shards,
                      workspace=self.workspace, host_out=host_out, ab_args=ab,
-                     shard_mirror=self.shard_mirror)
+                     shard_mirror=self.shard_mirror, reuse_t=reuse)
         call.keep.append(dspec)
         self.workspace = call.workspace
+        self._last_t = (tpack, bool(force_general_path))
         return call
 
     def run(self, dspec: DeviceSpec, tpack: TPack, force_general_path: bool = False,

@@ -76,6 +76,14 @@ __global__ void __launch_bounds__(kAbThreads) ab_kernel(AbParams p, const int* _
   const int tc = live ? t : p.n_basis - 1;
   const int a = atoms[blockIdx.y];
   const long long off = row_off[blockIdx.y];
+  // This atom's radial table (u, u', udot, udot', ||udot|| per l) staged in shared memory at
+  // entry (the load overlaps the Bessel recurrences): uniform per CTA, read once instead of
+  // an L2 round trip inside every l iteration.
+  __shared__ double rad[5 * (L + 1)];
+  {
+    const double* src = p.radial + (long long)a * p.radial_stride * 5;
+    for (int e = threadIdx.x; e < 5 * (L + 1); e += blockDim.x) rad[e] = src[e];
+  }
 
   const double kx = p.kv[3 * tc + 0], ky = p.kv[3 * tc + 1], kz = p.kv[3 * tc + 2];
   const double kn = sqrt(kx * kx + ky * ky + kz * kz);
@@ -106,7 +114,7 @@ __global__ void __launch_bounds__(kAbThreads) ab_kernel(AbParams p, const int* _
   sincos(th, &phs, &phc);
   const double sqo = sqrt(p.omega);
   const double fourpi = 4.0 * 3.141592653589793;
-  const double* rad = p.radial + (long long)a * p.radial_stride * 5;
+  __syncthreads();  // rad[] staged at kernel entry
 
   // e^{i m phi} for m <= L (running product as the reference's expphi**m)
   double emr[L + 1], emi[L + 1];

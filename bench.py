@@ -190,6 +190,25 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ GPU arm
 
+def hbm_peak_gbs():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, KeyError, ValueError):
+        return 6550.0, "SURVEY.md 8d measured copy bandwidth"
+
+
+def ab_gen_line(ms, rows, n):
+    """A/B generation against the HBM-write roofline: the generator writes A*,
+    B* and ||udot|| B* (48 R N bytes; the reference's Bytes_AB counts A*, B* = 32 R N)."""
+    peak, src = hbm_peak_gbs()
+    written = 48 * rows * n
+    gbs = written / (ms / 1e3) / 1e9
+    return {"ms": round(ms, 4), "bytes_written": written, "bytes_ab_ref": 32 * rows * n,
+            "achieved_gbs": round(gbs, 1), "peak_gbs": peak, "peak_source": src,
+            "frac": round(gbs / peak, 4)}
+
+
 def contract_flops(n, rows, hpd_rows):
     """F_contract of the two triangular contractions: 8RN^2 (S) +
     8RN^2 (ZHER2K) + 4 R_hpd N^2 + 8 R_nonhpd N^2 — the ledger's share of the DMMA kernels."""
@@ -236,15 +255,21 @@ def run_ours(args):
         # k-points back to back through the pipelined native path: step i+1 is enqueued
         # before step i is collected, so host-side enqueue never idles the GPU.
         prev = None
+        ab_ms = []
+
+        def collect(ticket):
+            r = pipe.finish(ticket)
+            for k, v in r["kernel_ms"].items():
+                kern[k].append(v)
+            ab_ms.append(r["ms"]["setup"])  # A/B generation (T preparation reused)
+
         for _ in range(args.steps):
             ticket = pipe.run_async(dspec, tpack)
             if prev is not None:
-                for k, v in pipe.finish(prev)["kernel_ms"].items():
-                    kern[k].append(v)
+                collect(prev)
             prev = ticket
         e1.record(stream)
-        for k, v in pipe.finish(prev)["kernel_ms"].items():
-            kern[k].append(v)
+        collect(prev)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -320,6 +345,7 @@ def run_ours(args):
                 "algorithmic_flops_per_step": fc,
                 "kernel_ms": {k: round(statistics.mean(v), 4) for k, v in kern.items()},
             },
+            "ab_gen": ab_gen_line(statistics.mean(ab_ms), rows, n),
             "e2e": {"value": round(e2e_value, 4), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
                     "ms_per_step": round(float(e2e_t[0].item()), 3),

@@ -33,9 +33,10 @@ constexpr int kStg = 3;
 // tile is TM x TN.  Cfg<2,2,4> = 64x64 (4 warps, ~250 registers, every triangular problem);
 // Cfg<3,2,2> = 96x32 (6 warps, ~128 registers) for the T applications when 64 < m <= 96
 // (m = 81 at l_sph = 8: 84% of the rows useful instead of 63% with 64-row tiles).
-template <int WM_, int WN_, int JB_>
+template <int WM_, int WN_, int JB_, bool PAIR_ = false>
 struct Cfg {
   static constexpr int WM = WM_, WN = WN_, JB = JB_;
+  static constexpr bool PAIR = PAIR_;
   static constexpr int TM = 32 * WM, TN = 8 * JB * WN;
   static constexpr int kT = 32 * WM * WN;
   static constexpr int kPBox = TM * 128, kQBox = TN * 128;  // box = columns x 16 doubles
@@ -45,6 +46,14 @@ struct Cfg {
 };
 using Cfg64 = Cfg<2, 2, 4>;
 using Cfg96 = Cfg<3, 2, 2>;
+// PAIR: 128-bit fragment loads (lane q takes complex element 4j+q whole; real part at DMMA
+// step 2j, imaginary part at 2j+1, as contract.cu's "pair" layout).  Under the TMA 128-byte
+// swizzle (16-B unit u of row c at u ^ (c & 7)) the two rows of a quarter-warp must differ
+// in bit 2 of (c & 7), so fragment row g reads tile column pi(g) = (g >> 1) | ((g & 1) << 2)
+// inside each 8-column block; the epilogue maps rows and columns through pi.
+using Cfg64P = Cfg<2, 2, 4, true>;
+using Cfg96P = Cfg<3, 2, 2, true>;
+__device__ __forceinline__ int pair_perm(int g) { return (g >> 1) | ((g & 1) << 2); }
 
 struct TSeg {
   int mapP, mapPalt, mapQ;
@@ -298,6 +307,52 @@ __global__ void __launch_bounds__(C::kT, 2) contract_tma_kernel(TKParams sk) {
     for (int cc = c_lo; cc < c_hi; ++cc, ++j) {
       const int st = (int)(j % kStg);
       mbar_wait(full + st, (uint32_t)((j / kStg) & 1));
+      if constexpr (C::PAIR) {
+        const int pg = pair_perm(g);
+        const char* sP = smem + st * kStageBytes + (wm * 32 + pg) * 128;
+        const char* sQ = smem + st * kStageBytes + 2 * C::kPBox + (wn * 8 * JB + pg) * 128;
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int off = ((((jj & 1) << 2) + q) ^ pg) << 4;
+          const char* pA = sP + (jj >> 1) * C::kPBox + off;
+          const char* pB = sQ + (jj >> 1) * C::kQBox + off;
+          double2 av[4], bv[JB];
+#pragma unroll
+          for (int ib = 0; ib < 4; ++ib) av[ib] = *reinterpret_cast<const double2*>(pA + ib * 8 * 128);
+#pragma unroll
+          for (int jb = 0; jb < JB; ++jb) bv[jb] = *reinterpret_cast<const double2*>(pB + jb * 8 * 128);
+#pragma unroll
+          for (int ib = 0; ib < 4; ++ib)
+#pragma unroll
+            for (int jb = 0; jb < JB; ++jb) {
+              dmma(accR[ib][jb][0], accR[ib][jb][1], av[ib].x, bv[jb].x);
+              dmma(accI[ib][jb][0], accI[ib][jb][1], av[ib].x, bv[jb].y);
+            }
+          double nb[JB];
+#pragma unroll
+          for (int jb = 0; jb < JB; ++jb)
+            nb[jb] = __hiloint2double(__double2hiint(bv[jb].x) ^ 0x80000000u, __double2loint(bv[jb].x));
+#pragma unroll
+          for (int ib = 0; ib < 4; ++ib)
+#pragma unroll
+            for (int jb = 0; jb < JB; ++jb) {
+              dmma(accR[ib][jb][0], accR[ib][jb][1], av[ib].y, bv[jb].y);
+              dmma(accI[ib][jb][0], accI[ib][jb][1], av[ib].y, nb[jb]);
+            }
+          if (jj == 1 && tid == 0) {
+            const long long x = j + kStg - 1;
+            if (x < nchunks_cta) {
+              const int sx = (int)(x % kStg);
+              if (x >= kStg) mbar_wait(empty + sx, (uint32_t)(((x / kStg) - 1) & 1));
+              pi.issue<C>(sk, smem + sx * kStageBytes, full + sx);
+              pi.next<C>(sk);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + st);
+        continue;
+      }
       const char* sP = smem + st * kStageBytes + (wm * 32 + g) * 128;
       const char* sQ = smem + st * kStageBytes + 2 * C::kPBox + (wn * 8 * JB + g) * 128;
 #pragma unroll
@@ -380,12 +435,12 @@ __global__ void __launch_bounds__(C::kT, 2) contract_tma_kernel(TKParams sk) {
     bool bad = false;
 #pragma unroll
     for (int ib = 0; ib < 4; ++ib) {
-      const int i = i0 + wm * 32 + ib * 8 + g;
+      const int i = i0 + wm * 32 + ib * 8 + (C::PAIR ? pair_perm(g) : g);
 #pragma unroll
       for (int jb = 0; jb < JB; ++jb) {
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-          const int jcol = j0 + wn * 8 * JB + jb * 8 + 2 * q + v;
+          const int jcol = j0 + wn * 8 * JB + jb * 8 + (C::PAIR ? pair_perm(2 * q + v) : 2 * q + v);
           double2 val = make_double2(accR[ib][jb][v], accI[ib][jb][v]);
           if (pr.kind == PROB_GENERAL) {
             if (i < pr.m && jcol < pr.n) {
@@ -590,8 +645,17 @@ bool tma_wants(const std::vector<Prob>& probs) {
 int launch_contract_tma(hsdla_ctx* ctx, const std::vector<Prob>& probs, long long total,
                         const std::vector<Seg>& segs, int* flag_dev) {
   (void)total;
-  if (tma_wants(probs)) return launch_cfg<Cfg96>(ctx, probs, segs, flag_dev);
-  return launch_cfg<Cfg64>(ctx, probs, segs, flag_dev);
+  // HSDLA_TMA_PAIR=0 selects the 64-bit fragment-load variant.
+  static int pair = -1;
+  if (pair < 0) {
+    const char* e = getenv("HSDLA_TMA_PAIR");
+    pair = (e && atoi(e) == 0) ? 0 : 1;
+  }
+  if (tma_wants(probs))
+    return pair ? launch_cfg<Cfg96P>(ctx, probs, segs, flag_dev)
+                : launch_cfg<Cfg96>(ctx, probs, segs, flag_dev);
+  return pair ? launch_cfg<Cfg64P>(ctx, probs, segs, flag_dev)
+              : launch_cfg<Cfg64>(ctx, probs, segs, flag_dev);
 }
 
 }  // namespace hsdla

@@ -197,11 +197,8 @@ int launch_ab_l(hsdla_ctx* ctx, const AbParams& p, const int* atoms_dev, const l
                 int count) {
   constexpr int S = 2 * L + 1;
   const size_t smem = size_t(2) * kAbThreads * S * sizeof(double2);
-  static bool attr = false;
-  if (!attr && smem > 48 * 1024) {
+  if (smem > 48 * 1024 && first_on_device((const void*)ab_kernel<L>))
     HS_CUDA(cudaFuncSetAttribute(ab_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
   dim3 grid((p.n_basis + kAbThreads - 1) / kAbThreads, count);
   ab_kernel<L><<<grid, kAbThreads, smem, ctx->stream>>>(p, atoms_dev, off_dev);
   HS_CHECK_LAUNCH();

@@ -6,11 +6,25 @@
 
 #include <map>
 #include <string>
+#include <mutex>
+#include <set>
+#include <utility>
 #include <vector>
 
 #include "../../include/hsdla_b200.h"
 
 namespace hsdla {
+
+// True the first time it is called for (key, current device): per-device one-time setup
+// such as cudaFuncSetAttribute (function attributes are per device).
+inline bool first_on_device(const void* key) {
+  static std::mutex m;
+  static std::set<std::pair<const void*, int>> seen;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(m);
+  return seen.insert({key, dev}).second;
+}
 
 void set_error(const std::string& msg);
 

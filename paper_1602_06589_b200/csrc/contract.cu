@@ -517,24 +517,14 @@ int launch_contract(hsdla_ctx* ctx, const std::vector<Prob>& probs_in,
     variant = (e && atoi(e) == 16) ? 2 : 4;
     const char* p = getenv("HSDLA_CP_LAYOUT");
     pad = (p && std::string(p) == "pad") ? 1 : (p && std::string(p) == "xor") ? 0 : 2;
-    HS_CUDA(cudaFuncSetAttribute(contract_kernel<4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)Layout<0>::kSmemBytes));
-    HS_CUDA(cudaFuncSetAttribute(contract_kernel<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)Layout<0>::kSmemBytes));
-    HS_CUDA(cudaFuncSetAttribute(contract_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)Layout<1>::kSmemBytes));
-    HS_CUDA(cudaFuncSetAttribute(contract_kernel<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)Layout<1>::kSmemBytes));
-    HS_CUDA(cudaFuncSetAttribute(contract_kernel<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)Layout<2>::kSmemBytes));
-    HS_CUDA(cudaFuncSetAttribute(contract_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)Layout<2>::kSmemBytes));
   }
   const void* kfns[2][3] = {
       {(const void*)contract_kernel<2, 0>, (const void*)contract_kernel<2, 1>, (const void*)contract_kernel<2, 2>},
       {(const void*)contract_kernel<4, 0>, (const void*)contract_kernel<4, 1>, (const void*)contract_kernel<4, 2>}};
   const void* kfn = kfns[variant == 4 ? 1 : 0][pad];
   const size_t kSmemBytes = pad == 1 ? Layout<1>::kSmemBytes : Layout<0>::kSmemBytes;
+  if (first_on_device(kfn))
+    HS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
   const int kThreads = variant == 4 ? 128 : 256;
   int occ = 0;
   HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kThreads, kSmemBytes));

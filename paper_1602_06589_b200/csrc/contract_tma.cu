@@ -575,12 +575,9 @@ int launch_cfg(hsdla_ctx* ctx, const std::vector<Prob>& probs_in, const std::vec
       if (rc) return rc;
     }
   }
-  static bool attr = false;
-  if (!attr) {
+  if (first_on_device((const void*)contract_tma_kernel<C>))
     HS_CUDA(cudaFuncSetAttribute(contract_tma_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)C::kSmemBytes));
-    attr = true;
-  }
   int occ = 0;
   HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, contract_tma_kernel<C>, C::kT,
                                                         C::kSmemBytes));

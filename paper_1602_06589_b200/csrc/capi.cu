@@ -623,12 +623,6 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     if (rc) return rc;
   }
   HS_CUDA(cudaEventRecord(ev[2], ctx->stream));
-  if (a->S_host) {
-    rc = copy_out(D2(a->S), a->S_host, sl.s_copied);
-    if (rc) return rc;
-  } else {
-    HS_CUDA(cudaEventRecord(sl.s_copied, ctx->stream));
-  }
 
   // Rows of a block beyond its T size must be zero in Z / XY (builder.py:232-245 compaction).
   for (int i = 0; i < na; ++i) {
@@ -674,6 +668,15 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     if (rc) return rc;
   }
   HS_CUDA(cudaEventRecord(ev[4], ctx->stream));
+  // S leaves for the host now, under the H contraction (4/3 of S's time): started right
+  // after S it would contend with the bandwidth-heavier T applications (measured +25% on
+  // them), and the previous k-point's H copy already overlaps this one's A/B + S phase.
+  if (a->S_host) {
+    rc = copy_out(D2(a->S), a->S_host, sl.s_copied);
+    if (rc) return rc;
+  } else {
+    HS_CUDA(cudaEventRecord(sl.s_copied, ctx->stream));
+  }
   // ---- H = Z^H B + B^H Z + sum_HPD Y^H Y + sum_nonHPD A^H X   (builder.py:246-247, :305-311)
   //      AA segments per run of atoms sharing one T set: P = XY (HPD) or A (general).
   if (prev.copies) HS_CUDA(cudaStreamWaitEvent(ctx->stream, prev.h_copied, 0));

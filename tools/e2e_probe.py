@@ -22,3 +22,13 @@ for rep in range(2):
     print(f"total {1e3*(t1-t0)/30:.3f} ms/kpt; first completion {1e3*(stamps[0]-t0):.2f} ms; "
           f"steady interval median {statistics.median(iv):.3f} ms (min {min(iv):.3f}, max {max(iv):.3f}); "
           f"device ms_total median {statistics.median(r['ms_total'] for r in rr):.3f}")
+ks = {}
+for r in rr[2:]:
+    for k, v in r["kernel_ms"].items():
+        ks.setdefault(k, []).append(v)
+print("kernel_ms during the batch:", {k: round(statistics.median(v), 4) for k, v in ks.items()})
+ticket_ms = []
+for _ in range(10):
+    r = pipe.run(DeviceSpec(spec), rr and __import__("paper_1602_06589_b200.pipeline", fromlist=["x"]).pack_tmats(inst.tmats))
+    ticket_ms.append(r["kernel_ms"])
+print("kernel_ms without host copies:", {k: round(statistics.median(x[k] for x in ticket_ms), 4) for k in ticket_ms[0]})

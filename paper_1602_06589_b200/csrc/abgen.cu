@@ -205,6 +205,17 @@ int launch_ab_l(hsdla_ctx* ctx, const AbParams& p, const int* atoms_dev, const l
   return HSDLA_OK;
 }
 
+template <int L>
+int preload_ab_l() {
+  constexpr int S = 2 * L + 1;
+  const size_t smem = size_t(2) * kAbThreads * S * sizeof(double2);
+  cudaFuncAttributes at;
+  HS_CUDA(cudaFuncGetAttributes(&at, (const void*)ab_kernel<L>));
+  if (smem > 48 * 1024 && first_on_device((const void*)ab_kernel<L>))
+    HS_CUDA(cudaFuncSetAttribute(ab_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  return HSDLA_OK;
+}
+
 typedef int (*ab_launcher)(hsdla_ctx*, const AbParams&, const int*, const long long*, int);
 
 const ab_launcher kAbLaunchers[HSDLA_MAX_LSPH + 1] = {
@@ -246,6 +257,29 @@ int upload_ylm_tables() {
   HS_CUDA(cudaMemcpyToSymbol(c_b, b, sizeof(b)));
   if (dev < 64) done[dev] = true;
   return HSDLA_OK;
+}
+
+int preload_abgen() {
+  int rc = HSDLA_OK;
+  rc = rc ? rc : preload_ab_l<0>();
+  rc = rc ? rc : preload_ab_l<1>();
+  rc = rc ? rc : preload_ab_l<2>();
+  rc = rc ? rc : preload_ab_l<3>();
+  rc = rc ? rc : preload_ab_l<4>();
+  rc = rc ? rc : preload_ab_l<5>();
+  rc = rc ? rc : preload_ab_l<6>();
+  rc = rc ? rc : preload_ab_l<7>();
+  rc = rc ? rc : preload_ab_l<8>();
+  rc = rc ? rc : preload_ab_l<9>();
+  rc = rc ? rc : preload_ab_l<10>();
+  rc = rc ? rc : preload_ab_l<11>();
+  rc = rc ? rc : preload_ab_l<12>();
+  rc = rc ? rc : preload_ab_l<13>();
+  rc = rc ? rc : preload_ab_l<14>();
+  if (rc) return rc;
+  cudaFuncAttributes at;
+  HS_CUDA(cudaFuncGetAttributes(&at, (const void*)udot_rows_kernel));
+  return upload_ylm_tables();
 }
 
 int ab_generate(hsdla_ctx* ctx, const hsdla_ab_args* args) {

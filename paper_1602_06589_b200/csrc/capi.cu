@@ -138,6 +138,18 @@ int hsdla_ctx_create(hsdla_ctx** out, void* stream) {
   HS_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
   HS_CUDA(cudaMalloc(&c->scratch_dev, 512 * sizeof(int)));
   HS_CUDA(cudaMemset(c->scratch_dev, 0, 512 * sizeof(int)));
+  // Stream-K partial tiles and ready flags for every co-resident CTA of any configuration
+  // (at most 2 CTAs per SM; 4 for headroom), allocated once: an allocation inside a build
+  // could synchronise the device while the copy stream waits on the build's own kernels.
+  c->partial_slots = 4 * c->num_sms;
+  HS_CUDA(cudaMalloc(&c->partials, size_t(c->partial_slots) * kTile * kTile * 2 * sizeof(double)));
+  HS_CUDA(cudaMalloc(&c->ready, size_t(c->partial_slots) * sizeof(int)));
+  // Descriptor arena sized up front for the same reason (a build uses a few KB to ~100 KB).
+  if (int rc = arena_begin(c, size_t(1) << 20)) return rc;
+  if (int rc = preload_contract()) return rc;
+  if (int rc = preload_contract_tma()) return rc;
+  if (int rc = preload_abgen()) return rc;
+  if (int rc = preload_small()) return rc;
   // Mapped pinned memory: build results are published by a kernel store, not a DMA copy,
   // so they never queue behind the large H / S copies on the D2H engine.
   HS_CUDA(cudaHostAlloc(&c->scratch_host, 512 * sizeof(int), cudaHostAllocMapped));
@@ -180,6 +192,7 @@ int hsdla_ctx_destroy(hsdla_ctx* c) {
   cudaStreamDestroy(c->side);
   cudaStreamSynchronize(c->copy);
   for (auto& sl : c->slots) {
+    if (sl.panel_cnt) cudaFree(sl.panel_cnt);
     for (auto& e : sl.ev) cudaEventDestroy(e);
     cudaEventDestroy(sl.s_copied);
     cudaEventDestroy(sl.h_copied);
@@ -392,6 +405,27 @@ int hsdla_reduced_s_aa(hsdla_ctx* ctx, const hsdla_reduced_args* args) {
   return reduced_s_aa(ctx, args);
 }
 
+// ---- streamed copies: cuStreamWaitValue32 through the driver entry point --------------
+namespace {
+typedef int (*WaitValueFn)(cudaStream_t, unsigned long long, unsigned int, unsigned int);
+WaitValueFn wait_value_fn() {
+  static WaitValueFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    const char* e = getenv("HSDLA_STREAM_COPIES");
+    if (!(e && atoi(e) == 0) &&
+        cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<WaitValueFn>(p);
+  }
+  return fn;
+}
+constexpr unsigned kWaitGeq = 0x0;  // CU_STREAM_WAIT_VALUE_GEQ
+}  // namespace
+
 // ---- composed build ------------------------------------------------------------------
 namespace {
 struct WsLayout {
@@ -481,8 +515,11 @@ int complete_slot(hsdla_ctx* ctx, hsdla_ctx::BuildSlot& sl, hsdla_ctx::Outcome* 
   return o->rc;
 }
 
+// stream_copies: copy H out panel by panel while the H contraction runs (synchronous calls,
+// where nothing follows that the copy could overlap instead); pipelined builds copy H whole
+// under the next k-point, which measured faster per k-point.
 int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args* ab,
-                  unsigned long long* ticket) {
+                  unsigned long long* ticket, bool stream_copies) {
   const int na = a->n_atoms, n = a->n_basis;
   if (na < 1 || n < 1) return -2;
   for (int i = 0; i < na; ++i) {
@@ -612,13 +649,53 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     HS_CUDA(cudaEventRecord(done_ev, ctx->copy));
     return HSDLA_OK;
   };
+  // Streamed variant, enqueued BEFORE the contraction that produces C: the copy stream waits
+  // (cuStreamWaitValue32) for each 64-column panel's tile counter to reach nb and copies the
+  // finished panel while the kernel is still computing the rest (the contraction epilogue
+  // publishes finished tiles, Prob::panel_done).
+  const int nbp = (n + kTile - 1) / kTile;
+  WaitValueFn waitv = (sharded || !sl.copies || !stream_copies) ? nullptr : wait_value_fn();
+  if (waitv && sl.panel_cap < nbp) {
+    if (sl.panel_cnt) {
+      HS_CUDA(cudaDeviceSynchronize());
+      cudaFree(sl.panel_cnt);
+    }
+    HS_CUDA(cudaMalloc(&sl.panel_cnt, size_t(2) * nbp * sizeof(int)));
+    sl.panel_cap = nbp;
+  }
+  auto stream_out = [&](const double2* C, hsdla_c64* host, int* cnt, cudaEvent_t done_ev) -> int {
+    HS_CUDA(cudaMemsetAsync(cnt, 0, size_t(nbp) * sizeof(int), ctx->stream));
+    HS_CUDA(cudaEventRecord(ctx->copy_go, ctx->stream));
+    HS_CUDA(cudaStreamWaitEvent(ctx->copy, ctx->copy_go, 0));
+    for (int p = 0; p < nbp; ++p) {
+      const int c0 = p * kTile, nc = std::min(kTile, n - c0);
+      if (waitv(ctx->copy, reinterpret_cast<unsigned long long>(cnt + p), (unsigned)nbp, kWaitGeq) != 0) {
+        set_error("cuStreamWaitValue32 failed");
+        return HSDLA_ERR_CUDA;
+      }
+      HS_CUDA(cudaMemcpy2DAsync(host + (long long)c0 * a->ldh_host, size_t(a->ldh_host) * sizeof(hsdla_c64),
+                                C + (long long)c0 * a->ldh, size_t(a->ldh) * sizeof(double2),
+                                size_t(n) * sizeof(double2), nc, cudaMemcpyDeviceToHost, ctx->copy));
+    }
+    HS_CUDA(cudaEventRecord(done_ev, ctx->copy));
+    return HSDLA_OK;
+  };
 
   // ---- S = A^H A + (U B)^H (U B)   (builder.py:199-209)
   if (prev.copies) HS_CUDA(cudaStreamWaitEvent(ctx->stream, prev.s_copied, 0));
+  // S is copied whole after the T applications (below): streaming it during its own
+  // contraction pushed its tail copies under the T applications (measured slower per
+  // k-point); H is streamed during the H contraction.
+  const bool s_streamed = false;
+  if (s_streamed) {
+    rc = stream_out(D2(a->S), a->S_host, sl.panel_cnt, sl.s_copied);
+    if (rc) return rc;
+  }
   {
     std::vector<Seg> segs{make_seg(A, ld, A, ld, (int)R), make_seg(Bs, ld, Bs, ld, (int)R)};
     std::vector<Prob> probs;
     add_tri(probs, D2(a->S), 0, 2);
+    if (s_streamed) probs[0].panel_done = sl.panel_cnt;
     rc = launch_contract(ctx, probs, segs, flag);
     if (rc) return rc;
   }
@@ -671,7 +748,9 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
   // S leaves for the host now, under the H contraction (4/3 of S's time): started right
   // after S it would contend with the bandwidth-heavier T applications (measured +25% on
   // them), and the previous k-point's H copy already overlaps this one's A/B + S phase.
-  if (a->S_host) {
+  if (s_streamed) {
+    // S is on its way already (streamed during its own contraction)
+  } else if (a->S_host) {
     rc = copy_out(D2(a->S), a->S_host, sl.s_copied);
     if (rc) return rc;
   } else {
@@ -680,6 +759,11 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
   // ---- H = Z^H B + B^H Z + sum_HPD Y^H Y + sum_nonHPD A^H X   (builder.py:246-247, :305-311)
   //      AA segments per run of atoms sharing one T set: P = XY (HPD) or A (general).
   if (prev.copies) HS_CUDA(cudaStreamWaitEvent(ctx->stream, prev.h_copied, 0));
+  const bool h_streamed = waitv && a->H_host;
+  if (h_streamed) {
+    rc = stream_out(D2(a->H), a->H_host, sl.panel_cnt + nbp, sl.h_copied);
+    if (rc) return rc;
+  }
   {
     std::vector<Seg> segs{make_seg(Z, ld, B, ld, (int)R), make_seg(B, ld, Z, ld, (int)R)};
     int i = 0;
@@ -697,11 +781,14 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     }
     std::vector<Prob> probs;
     add_tri(probs, D2(a->H), 0, (int)segs.size());
+    if (h_streamed) probs[0].panel_done = sl.panel_cnt + nbp;
     rc = launch_contract(ctx, probs, segs, flag);
     if (rc) return rc;
   }
   HS_CUDA(cudaEventRecord(ev[6], ctx->stream));
-  if (a->H_host) {
+  if (h_streamed) {
+    // H streamed during its contraction
+  } else if (a->H_host) {
     rc = copy_out(D2(a->H), a->H_host, sl.h_copied);
     if (rc) return rc;
   } else {
@@ -762,7 +849,7 @@ int hsdla_build_hs(hsdla_ctx* ctx, const hsdla_build_args* a, hsdla_build_result
   if (!res) return -3;
   std::lock_guard<std::mutex> lk(g_api_mutex);
   unsigned long long t = 0;
-  int rc = enqueue_build(ctx, a, nullptr, &t);
+  int rc = enqueue_build(ctx, a, nullptr, &t, true);
   if (rc) return rc;
   return finish_build(ctx, t, res);
 }
@@ -775,7 +862,7 @@ int hsdla_setup_hs(hsdla_ctx* ctx, const hsdla_ab_args* ab, const hsdla_build_ar
   if (!res) return -4;
   std::lock_guard<std::mutex> lk(g_api_mutex);
   unsigned long long t = 0;
-  int rc = enqueue_build(ctx, a, ab, &t);
+  int rc = enqueue_build(ctx, a, ab, &t, true);
   if (rc) return rc;
   return finish_build(ctx, t, res);
 }
@@ -786,7 +873,7 @@ int hsdla_setup_hs_async(hsdla_ctx* ctx, const hsdla_ab_args* ab, const hsdla_bu
   if (!a) return -3;
   if (!ticket) return -4;
   std::lock_guard<std::mutex> lk(g_api_mutex);
-  return enqueue_build(ctx, a, ab, ticket);
+  return enqueue_build(ctx, a, ab, ticket, false);
 }
 
 int hsdla_build_finish(hsdla_ctx* ctx, unsigned long long ticket, hsdla_build_result* res) {

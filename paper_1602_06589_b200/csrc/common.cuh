@@ -74,6 +74,10 @@ struct Prob {
   long long it_base;     // first stream-K iteration (tile-chunk) of this problem
   int col_tile_lo, col_tile_hi;  // tri only: restrict to tile columns [lo, hi) (sharding)
   double2 alpha, beta;
+  // TRI_MIRROR only, or nullptr: per 64-column panel, the count of finished tiles that wrote
+  // into it (tile (i, j) writes panel j and, mirrored, panel i).  Panel p is complete at
+  // tiles_m; a copy stream streams finished panels to the host while the kernel runs.
+  int* panel_done;
 };
 
 constexpr int kTile = 64;  // complex outputs per CTA tile edge
@@ -105,6 +109,8 @@ struct hsdla_ctx {
     cudaEvent_t ev[8] = {};
     cudaEvent_t s_copied = nullptr, h_copied = nullptr, done = nullptr;
     int* flag_dev = nullptr;
+    int* panel_cnt = nullptr;      // 2 x panel_cap counters (S, H) for streamed copies
+    int panel_cap = 0;
     int* host_area = nullptr;      // mapped pinned (host view)
     int* host_area_dev = nullptr;  // device view of host_area
     int n_atoms = 0, n_tsets = 0;
@@ -177,6 +183,13 @@ int launch_mirror(hsdla_ctx* ctx, int n, double2* C, long long ldc, int* flag_de
 int launch_scale_rows(hsdla_ctx* ctx, int m, int n, const double* d, double2* B, long long ldb);
 int launch_zero_rows(hsdla_ctx* ctx, double2* base, long long ld, int row0, int rows, int cols);
 int launch_finite_check(hsdla_ctx* ctx, int m, int n, const double2* A, long long lda, int* flag);
+// Load every kernel a build may launch and set its shared-memory limit, at context creation:
+// with lazy module loading a first launch inside a build could load (and allocate for) the
+// module while the copy stream waits on that build's own kernels (streamed copies).
+int preload_contract();
+int preload_contract_tma();
+int preload_abgen();
+int preload_small();
 // Copy the non-finite flag and the Cholesky infos into mapped host memory (out[0] = flag,
 // out[1..n] = info) with plain stores, keeping the D2H copy engine free for H / S.
 int launch_publish(hsdla_ctx* ctx, const int* flag, const int* info, int n, int* out_mapped);

@@ -437,6 +437,16 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), 2) contract_kernel(SKParams
       }
     }
     if (bad) atomicOr(sk.flag, 1);
+    if (pr.panel_done) {
+      // Publish the finished tile to the streaming copy: the barrier orders every thread's
+      // stores before thread 0's system-scope fence (cumulative), then the panel counters.
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence_system();
+        atomicAdd(pr.panel_done + tn, 1);
+        if (tm != tn) atomicAdd(pr.panel_done + tm, 1);
+      }
+    }
   }
   }
 }
@@ -475,6 +485,21 @@ void plan_dp_waves(const std::vector<Prob>& probs, long long total, int grid, in
   *waves = (int)w;
   *nch = n0;
   *dp_it = w * grid * n0;
+}
+
+int preload_contract() {
+  const void* fns[] = {(const void*)contract_kernel<2, 0>, (const void*)contract_kernel<2, 1>,
+                       (const void*)contract_kernel<2, 2>, (const void*)contract_kernel<4, 0>,
+                       (const void*)contract_kernel<4, 1>, (const void*)contract_kernel<4, 2>};
+  const size_t smem[] = {Layout<0>::kSmemBytes, Layout<1>::kSmemBytes, Layout<2>::kSmemBytes,
+                         Layout<0>::kSmemBytes, Layout<1>::kSmemBytes, Layout<2>::kSmemBytes};
+  for (int i = 0; i < 6; ++i) {
+    cudaFuncAttributes at;
+    HS_CUDA(cudaFuncGetAttributes(&at, fns[i]));
+    if (first_on_device(fns[i]))
+      HS_CUDA(cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem[i]));
+  }
+  return HSDLA_OK;
 }
 
 int launch_contract(hsdla_ctx* ctx, const std::vector<Prob>& probs_in,

@@ -479,6 +479,14 @@ __global__ void __launch_bounds__(C::kT, 2) contract_tma_kernel(TKParams sk) {
       }
     }
     if (bad) atomicOr(sk.flag, 1);
+    if (pr.panel_done) {  // streamed copy-out, see Prob::panel_done and contract.cu
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence_system();
+        atomicAdd(pr.panel_done + tn, 1);
+        if (tm != tn) atomicAdd(pr.panel_done + tm, 1);
+      }
+    }
   }
 }
 
@@ -622,6 +630,25 @@ int launch_cfg(hsdla_ctx* ctx, const std::vector<Prob>& probs_in, const std::vec
   return HSDLA_OK;
 }
 }  // namespace
+
+namespace {
+template <class C>
+int preload_cfg() {
+  cudaFuncAttributes at;
+  HS_CUDA(cudaFuncGetAttributes(&at, (const void*)contract_tma_kernel<C>));
+  if (first_on_device((const void*)contract_tma_kernel<C>))
+    HS_CUDA(cudaFuncSetAttribute(contract_tma_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)C::kSmemBytes));
+  return HSDLA_OK;
+}
+}  // namespace
+
+int preload_contract_tma() {
+  if (int rc = preload_cfg<Cfg64>()) return rc;
+  if (int rc = preload_cfg<Cfg96>()) return rc;
+  if (int rc = preload_cfg<Cfg64P>()) return rc;
+  return preload_cfg<Cfg96P>();
+}
 
 bool tma_wants(const std::vector<Prob>& probs) {
   // General (T-application) problems with 64 < m <= 96 run on 96 x 32 tiles.

@@ -277,8 +277,7 @@ int launch_tprep(hsdla_ctx* ctx, cudaStream_t stream, int n_tsets, const int* td
   if (n_tsets <= 0) return HSDLA_OK;
   size_t smem = (mp <= kPackedMaxN) ? size_t(mp) * (mp + 1) / 2 * sizeof(double2)
                                     : size_t(mp) * sizeof(double2);
-  if (smem > 48 * 1024)
-    HS_CUDA(cudaFuncSetAttribute(tprep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // smem limit set once per device in preload_small()
   tprep_kernel<<<n_tsets, 512, smem, stream>>>(tdim_dev, mp, taa, tab, tbb, t_ld, forms, do_chol,
                                                info_dev);
   HS_CHECK_LAUNCH();
@@ -341,6 +340,21 @@ int launch_zero_rows(hsdla_ctx* ctx, double2* base, long long ld, int row0, int 
   if (rows <= 0 || cols <= 0) return HSDLA_OK;
   zero_rows_kernel<<<dim3((rows + 127) / 128, cols), 128, 0, ctx->stream>>>(base, ld, row0, rows);
   HS_CHECK_LAUNCH();
+  return HSDLA_OK;
+}
+
+int preload_small() {
+  const void* fns[] = {(const void*)potrf_batched_kernel, (const void*)tprep_kernel,
+                       (const void*)mirror_kernel, (const void*)scale_rows_kernel,
+                       (const void*)prep_kernel, (const void*)publish_kernel,
+                       (const void*)zero_rows_kernel, (const void*)finite_kernel};
+  for (const void* f : fns) {
+    cudaFuncAttributes at;
+    HS_CUDA(cudaFuncGetAttributes(&at, f));
+  }
+  if (first_on_device((const void*)tprep_kernel))
+    HS_CUDA(cudaFuncSetAttribute(tprep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(size_t(kPackedMaxN) * (kPackedMaxN + 1) / 2 * sizeof(double2))));
   return HSDLA_OK;
 }
 

@@ -290,11 +290,15 @@ def run_ours(args):
     bufs = {}
     n_e2e = max(3, args.steps)
     build_hs_many([spec] * args.warmup, inst.tmats, BuildConfig(), pipeline=pipe, host_buffers=bufs)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    rr = build_hs_many([spec] * n_e2e, inst.tmats, BuildConfig(), pipeline=pipe, host_buffers=bufs)
-    torch.cuda.synchronize()
-    e2e_step_ms = (time.perf_counter() - t0) * 1e3 / n_e2e
+    batch_ms = []
+    for _ in range(3):  # median of three batches: the host wall clock is noisier than events
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rr = build_hs_many([spec] * n_e2e, inst.tmats, BuildConfig(), pipeline=pipe,
+                           host_buffers=bufs)
+        torch.cuda.synchronize()
+        batch_ms.append((time.perf_counter() - t0) * 1e3 / n_e2e)
+    e2e_step_ms = statistics.median(batch_ms)
     h2d = sum(r["h2d_bytes"] for r in rr) / n_e2e
     d2h = rr[0]["d2h_bytes"]
     single_ms = []

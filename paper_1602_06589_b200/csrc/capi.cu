@@ -587,6 +587,8 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
   // when the caller vouches that T is unchanged and the previous results are still here.
   hsdla_ctx::TKey key;
   key.ws = a->workspace;
+  key.forms_off = (long long)w.forms;
+  key.info_off = (long long)w.info;
   key.taa = a->t_aa;
   key.tab = a->t_ab;
   key.tbb = a->t_bb;
@@ -594,7 +596,8 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
   key.force = a->force_general_path ? 1 : 0;
   key.tdim.assign(a->t_dim, a->t_dim + a->n_tsets);
   const hsdla_ctx::TKey& old = ctx->tkey;
-  const bool reuse = a->reuse_t && old.ws == key.ws && old.taa == key.taa && old.tab == key.tab &&
+  const bool reuse = a->reuse_t && old.ws == key.ws && old.forms_off == key.forms_off &&
+                     old.info_off == key.info_off && old.taa == key.taa && old.tab == key.tab &&
                      old.tbb == key.tbb && old.t_ld == key.t_ld && old.force == key.force &&
                      old.tdim == key.tdim;
   HS_CUDA(cudaEventRecord(ctx->fork, ctx->stream));

@@ -93,6 +93,7 @@ struct hsdla_ctx {
   // Key of the T preparation whose results sit in a build workspace (hsdla_build_args.reuse_t).
   struct TKey {
     const void* ws = nullptr;
+    long long forms_off = -1, info_off = -1;  // workspace offsets (depend on n_basis, ld)
     const void *taa = nullptr, *tab = nullptr, *tbb = nullptr;
     long long t_ld = 0;
     int force = -1;

@@ -1,0 +1,111 @@
+"""Edge shapes of the composed build and compute_AB on the GPU, against the oracle
+(which is pinned to the reference's goldens): tile and K-chunk boundaries (N_G and block
+heights at 1, 15/16/17, 63/64/65), single atoms, l = 0 blocks, T smaller than its block,
+mixed HPD, a K = 0 vector, and k-point batches whose N_G varies."""
+import numpy as np
+import pytest
+
+from conftest import rand_complex, rel_fro
+from oracle import build as ob
+from oracle import flapw as of
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def pkg(cuda):
+    import paper_1602_06589_b200 as p
+
+    p._native.load()
+    return p
+
+
+def _hermitian(rng, m, shift):
+    x = rand_complex(rng, m, m)
+    return (x + x.conj().T) / (2 * m) + shift * np.eye(m)
+
+
+def _case(pkg, seed, heights, n_g, t_sizes=None, shifts=None):
+    rng = np.random.default_rng(seed)
+    lay = pkg.AtomBlockLayout(tuple(heights))
+    r = lay.total_rows
+    a = pkg.ComplexDense.zeros(r, n_g, capacity_rows=lay.capacity_rows)
+    b = pkg.ComplexDense.zeros(r, n_g, capacity_rows=lay.capacity_rows)
+    a.array[:] = rand_complex(rng, r, n_g)
+    b.array[:] = rand_complex(rng, r, n_g)
+    u = rng.uniform(0.2, 1.5, r)
+    co = pkg.StackedCoefficients(a, b, lay, u)
+    t_sizes = t_sizes or list(heights)
+    shifts = shifts or [2.0] * len(heights)
+    taa = [_hermitian(rng, m, s) for m, s in zip(t_sizes, shifts)]
+    tbb = [_hermitian(rng, m, 1.0) for m in t_sizes]
+    tab = [rand_complex(rng, m, m) / m for m in t_sizes]
+    cd = pkg.ComplexDense.from_array
+    tm = pkg.TMatrixSet([cd(t) for t in taa], [cd(t) for t in tab], [cd(t) for t in tbb],
+                        [0] * len(heights), [0] * len(heights))
+    return co, tm, (a.array.copy(), b.array.copy(), u.copy(), taa, tab, tbb)
+
+
+@pytest.mark.parametrize("heights,n_g", [((1,), 1), ((1,), 2), ((4,), 63), ((4,), 64), ((4,), 65),
+                                         ((16,), 17), ((15, 17), 129), ((1, 64, 3), 64),
+                                         ((9, 9, 9, 9, 9, 9, 9), 200)])
+def test_build_all_edge_shapes(pkg, heights, n_g):
+    co, tm, (a, b, u, taa, tab, tbb) = _case(pkg, sum(heights) * 7 + n_g, heights, n_g)
+    h, s, rep = pkg.build_all(co, tm, pkg.BuildConfig())
+    want = ob.build_all(a, b, u, list(heights), taa, tab, tbb)
+    assert rel_fro(s.array, want[1]) <= TOL
+    assert rel_fro(h.array, want[0]) <= TOL
+    np.testing.assert_array_equal(h.array, h.array.conj().T)
+    np.testing.assert_array_equal(s.array, s.array.conj().T)
+    assert rep.hpd_mask == list(want[3])
+
+
+def test_build_all_small_t_and_non_hpd(pkg):
+    """T smaller than its block (rows beyond m contribute nothing) and a non-HPD T_AA next
+    to HPD ones (device-side branch selection)."""
+    heights = (16, 9, 25)
+    co, tm, (a, b, u, taa, tab, tbb) = _case(pkg, 5, heights, 97, t_sizes=[9, 9, 16],
+                                             shifts=[2.0, -2.0, 2.0])
+    h, s, rep = pkg.build_all(co, tm, pkg.BuildConfig())
+    want = ob.build_all(a, b, u, list(heights), taa, tab, tbb)
+    assert rel_fro(h.array, want[0]) <= TOL and rel_fro(s.array, want[1]) <= TOL
+    assert rep.hpd_mask == [True, False, True] == list(want[3])
+
+
+def test_compute_ab_single_atom_l0_and_zero_k(pkg):
+    from paper_1602_06589_b200 import RadialBoundaryData, SystemSpec
+
+    rng = np.random.default_rng(4)
+    kv = rng.standard_normal((5, 3))
+    kv[0] = 0.0
+    rad = [RadialBoundaryData(u=np.array([0.5]), u_prime=np.array([0.7]), udot=np.array([0.3]),
+                              udot_prime=np.array([0.9]), energy=np.zeros(1),
+                              udot_norm=np.array([0.2]))]
+    spec = SystemSpec(positions=np.zeros((1, 3)), rotations=np.eye(3)[None], mt_radius=np.array([2.0]),
+                      l_sph=np.array([0]), l_nonsph=np.array([0]), k_point=np.zeros(3),
+                      k_vectors=kv, omega=100.0, radial=rad)
+    c = pkg.compute_AB(spec)
+    a, b, norms, _ = of.compute_ab(spec)
+    assert c.A_star.rows == 1 and c.n_basis == 5
+    assert rel_fro(c.A_star.array, a) <= 1e-14 and rel_fro(c.B_star.array, b) <= 1e-14
+    np.testing.assert_array_equal(c.udot_norms, norms)
+
+
+def test_kpoint_batch_with_varying_basis_sizes(pkg):
+    """build_hs_many over k-points whose G-sets differ in size (one pipeline sized to the
+    largest), each result equal to its own single build."""
+    from paper_1602_06589_b200 import configs
+    from paper_1602_06589_b200.pipeline import build_hs, build_hs_many
+
+    inst = configs.make_instance("C1")
+    specs = [configs.kpoint_variant(inst, r) for r in range(3)]
+    assert len({s.n_basis for s in specs}) > 1
+    got = {}
+    build_hs_many(specs, inst.tmats, on_result=lambda i, h, s, r: got.__setitem__(
+        i, (h.array.copy(), s.array.copy())))
+    for i, sp in enumerate(specs):
+        h, s, _ = build_hs(sp, inst.tmats)
+        assert got[i][0].shape == (sp.n_basis, sp.n_basis)
+        assert rel_fro(got[i][0], h.array) <= 1e-14 and rel_fro(got[i][1], s.array) <= 1e-14

@@ -109,3 +109,31 @@ def test_kpoint_batch_with_varying_basis_sizes(pkg):
         h, s, _ = build_hs(sp, inst.tmats)
         assert got[i][0].shape == (sp.n_basis, sp.n_basis)
         assert rel_fro(got[i][0], h.array) <= 1e-14 and rel_fro(got[i][1], s.array) <= 1e-14
+
+
+def test_async_builds_three_in_flight_out_of_order(pkg):
+    """hsdla_setup_hs_async with three k-points in flight (the oldest is completed into the
+    stash when the third is enqueued) and finished out of order; each host result equals a
+    synchronous build, and a finished ticket cannot be finished twice."""
+    import torch
+
+    from paper_1602_06589_b200 import NativeLibraryError, configs
+    from paper_1602_06589_b200.pipeline import DeviceSpec, HSPipeline, build_hs, pack_tmats
+
+    inst = configs.make_instance("C1")
+    specs = [configs.kpoint_variant(inst, r) for r in range(3)]
+    n_cap = max(s.n_basis for s in specs)
+    tp = pack_tmats(inst.tmats)
+    pipe = HSPipeline(n_cap, DeviceSpec(specs[0]).heights)
+    outs = [(torch.empty((s.n_basis, s.n_basis), dtype=torch.complex128, pin_memory=True),
+             torch.empty((s.n_basis, s.n_basis), dtype=torch.complex128, pin_memory=True))
+            for s in specs]
+    tickets = [pipe.run_async(DeviceSpec(s), tp, host_out=o) for s, o in zip(specs, outs)]
+    for k in (2, 0, 1):
+        res = pipe.finish(tickets[k])
+        assert res["hpd_mask"] == [True] * specs[k].n_atoms
+    for s, (h, sm) in zip(specs, outs):
+        h1, s1, _ = build_hs(s, inst.tmats)
+        assert rel_fro(h.numpy().T, h1.array) <= 1e-14 and rel_fro(sm.numpy().T, s1.array) <= 1e-14
+    with pytest.raises((NativeLibraryError, KeyError)):
+        pipe.finish(tickets[0])

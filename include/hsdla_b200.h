@@ -155,6 +155,17 @@ typedef struct {
 } hsdla_reduced_args;
 int hsdla_reduced_s_aa(hsdla_ctx* ctx, const hsdla_reduced_args* args);
 
+/* ---- per-type phase factorisation ---------------
+ * When the atoms of a type share rotation, radial data, muffin-tin radius and T, every
+ * coefficient block is its type's template times a column phase: A_a = A^_t diag(e_a), so
+ * S and H are sums over types of (phase Gram) o (template Gram). */
+/* E[a + t*lde] = exp(i K_t . x_a) (DEVICE k_vectors n_basis x 3, positions n_atoms x 3). */
+int hsdla_phase_matrix(hsdla_ctx* ctx, int n_basis, int n_atoms, const double* k_vectors,
+                       const double* positions, hsdla_c64* E, int64_t lde);
+/* lower(C) (+)= W o G elementwise on i >= j (all DEVICE, column-major). */
+int hsdla_hadamard_lower(hsdla_ctx* ctx, int n, const hsdla_c64* W, int64_t ldw,
+                         const hsdla_c64* G, int64_t ldg, hsdla_c64* C, int64_t ldc, int accumulate);
+
 /* ---- the composed build (builder.py:403-474 build_all) ------------------- */
 typedef struct {
   int32_t n_atoms;

@@ -111,6 +111,9 @@ SIGNATURES = {
     "hsdla_ab_generate": (ctypes.c_int, [_vp, ctypes.POINTER(AbArgs)]),
     "hsdla_match_factors": (ctypes.c_int, [_vp, ctypes.POINTER(AbArgs), _P_i64, _vp, _vp, _i64]),
     "hsdla_reduced_s_aa": (ctypes.c_int, [_vp, ctypes.POINTER(ReducedArgs)]),
+    "hsdla_phase_matrix": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _i64]),
+    "hsdla_hadamard_lower": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _i64, _vp, _i64, _vp, _i64,
+                                            ctypes.c_int]),
     "hsdla_build_workspace_size": (ctypes.c_size_t, [ctypes.POINTER(BuildArgs)]),
     "hsdla_build_hs": (ctypes.c_int, [_vp, ctypes.POINTER(BuildArgs), ctypes.POINTER(BuildResult)]),
     "hsdla_setup_hs": (ctypes.c_int, [_vp, ctypes.POINTER(AbArgs), ctypes.POINTER(BuildArgs),

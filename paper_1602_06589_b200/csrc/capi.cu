@@ -398,6 +398,27 @@ int hsdla_match_factors(hsdla_ctx* ctx, const hsdla_ab_args* spec, const int64_t
   return match_factors(ctx, spec, f_row, f_a, f_b, ld_f);
 }
 
+int hsdla_phase_matrix(hsdla_ctx* ctx, int n_basis, int n_atoms, const double* k_vectors,
+                       const double* positions, hsdla_c64* E, int64_t lde) {
+  if (!ctx) return -1;
+  if (n_basis < 0) return -2;
+  if (n_atoms < 0) return -3;
+  if (lde < (n_atoms > 1 ? n_atoms : 1)) return -7;
+  std::lock_guard<std::mutex> lk(g_api_mutex);
+  return phase_matrix(ctx, n_basis, n_atoms, k_vectors, positions, D2(E), lde);
+}
+
+int hsdla_hadamard_lower(hsdla_ctx* ctx, int n, const hsdla_c64* W, int64_t ldw,
+                         const hsdla_c64* G, int64_t ldg, hsdla_c64* C, int64_t ldc, int accumulate) {
+  if (!ctx) return -1;
+  if (n < 0) return -2;
+  if (ldw < (n > 1 ? n : 1)) return -4;
+  if (ldg < (n > 1 ? n : 1)) return -6;
+  if (ldc < (n > 1 ? n : 1)) return -8;
+  std::lock_guard<std::mutex> lk(g_api_mutex);
+  return hadamard_lower(ctx, n, D2(W), ldw, D2(G), ldg, D2(C), ldc, accumulate);
+}
+
 int hsdla_reduced_s_aa(hsdla_ctx* ctx, const hsdla_reduced_args* args) {
   if (!ctx) return -1;
   if (!args || !args->f_row || !args->l_top || !args->S) return -2;

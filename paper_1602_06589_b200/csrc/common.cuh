@@ -180,6 +180,10 @@ int ab_generate(hsdla_ctx* ctx, const hsdla_ab_args* args);
 int match_factors(hsdla_ctx* ctx, const hsdla_ab_args* s, const int64_t* f_row, double* fa,
                   double* fb, int64_t ldf);
 int reduced_s_aa(hsdla_ctx* ctx, const hsdla_reduced_args* r);
+int phase_matrix(hsdla_ctx* ctx, int n, int n_atoms, const double* kv, const double* pos,
+                 double2* E, long long lde);
+int hadamard_lower(hsdla_ctx* ctx, int n, const double2* W, long long ldw, const double2* G,
+                   long long ldg, double2* C, long long ldc, int accumulate);
 int launch_mirror(hsdla_ctx* ctx, int n, double2* C, long long ldc, int* flag_dev);
 int launch_scale_rows(hsdla_ctx* ctx, int m, int n, const double* d, double2* B, long long ldb);
 int launch_zero_rows(hsdla_ctx* ctx, double2* base, long long ld, int row0, int rows, int cols);

@@ -86,6 +86,40 @@ __global__ void rs_prep_kernel(int n, int n_atoms, const double* __restrict__ kv
   }
 }
 
+// E[a + t * lde] = e^{i K_t . x_a}: the phase matrix of the per-type factorised build
+// (same expression and rounding as the A/B generator's phase).
+__global__ void phase_matrix_kernel(int n, int n_atoms, const double* __restrict__ kv,
+                                    const double* __restrict__ pos, double2* E, long long lde) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const double kx = kv[3 * t + 0], ky = kv[3 * t + 1], kz = kv[3 * t + 2];
+  for (int a = 0; a < n_atoms; ++a) {
+    const double th = kx * pos[3 * a + 0] + ky * pos[3 * a + 1] + kz * pos[3 * a + 2];
+    double sn, cs;
+    sincos(th, &sn, &cs);
+    E[a + (long long)t * lde] = make_double2(cs, sn);
+  }
+}
+
+// C (+)= W o G on the lower triangle (i >= j): the Hadamard combine of a type's phase Gram
+// W with its template Gram G.
+__global__ void hadamard_lower_kernel(int n, const double2* __restrict__ W, long long ldw,
+                                      const double2* __restrict__ G, long long ldg, double2* C,
+                                      long long ldc, int accumulate) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  if (i >= n || i < j) return;
+  const double2 w = W[i + (long long)j * ldw], g = G[i + (long long)j * ldg];
+  double2 v = make_double2(__fma_rn(w.x, g.x, -__dmul_rn(w.y, g.y)), __fma_rn(w.x, g.y, __dmul_rn(w.y, g.x)));
+  double2* c = C + i + (long long)j * ldc;
+  if (accumulate) {
+    const double2 o = *c;
+    v.x = __dadd_rn(v.x, o.x);
+    v.y = __dadd_rn(v.y, o.y);
+  }
+  *c = v;
+}
+
 struct RsParams {
   int n, tiles;
   const double4* unit;       // n: K^ and 1 (0 for K = 0)
@@ -244,6 +278,23 @@ __global__ void __launch_bounds__(256) rs_kernel(RsParams p) {
 }
 
 }  // namespace
+
+int phase_matrix(hsdla_ctx* ctx, int n, int n_atoms, const double* kv, const double* pos,
+                 double2* E, long long lde) {
+  if (n <= 0 || n_atoms <= 0) return HSDLA_OK;
+  phase_matrix_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(n, n_atoms, kv, pos, E, lde);
+  HS_CHECK_LAUNCH();
+  return HSDLA_OK;
+}
+
+int hadamard_lower(hsdla_ctx* ctx, int n, const double2* W, long long ldw, const double2* G,
+                   long long ldg, double2* C, long long ldc, int accumulate) {
+  if (n <= 0) return HSDLA_OK;
+  hadamard_lower_kernel<<<dim3((n + 127) / 128, n), 128, 0, ctx->stream>>>(n, W, ldw, G, ldg, C,
+                                                                          ldc, accumulate);
+  HS_CHECK_LAUNCH();
+  return HSDLA_OK;
+}
 
 int match_factors(hsdla_ctx* ctx, const hsdla_ab_args* s, const int64_t* f_row, double* fa,
                   double* fb, int64_t ldf) {

@@ -194,8 +194,10 @@ typedef struct {
    * With sharding only the lower tiles of owned 64-wide column panels are written, unmirrored. */
   int32_t shard_rank, n_shards;
   /* Optional HOST (pinned) destinations: when non-NULL the full H / S (ld ldh_host) are
-   * copied back on a copy stream, overlapped with later compute (S during the H phase, H
-   * during the next pipelined k-point).  Not with sharding. */
+   * copied back on a copy stream, overlapped with compute: S during the H phase; H during
+   * the next k-point (pipelined builds) or, for the synchronous calls, panel by panel during
+   * its own contraction (cuStreamWaitValue32 on per-panel tile counters; set
+   * HSDLA_STREAM_COPIES=0 to copy H whole after its kernel).  Not with sharding. */
   hsdla_c64* H_host;
   hsdla_c64* S_host;
   int64_t ldh_host;

@@ -429,12 +429,11 @@ def build_all(coeffs: StackedCoefficients, tmats: TMatrixSet, config: BuildConfi
     t0 = time.perf_counter()
     t = device.require_cuda()
     r = layout.total_rows
-    ld = padded_ld(r)
-    a_d = device.upload_window(coeffs.A_star.array, ld)
-    b_d = device.upload_window(coeffs.B_star.array, ld)
-    if r < ld:
-        a_d[:, r:] = 0
-        b_d[:, r:] = 0
+    # K loops read rows < r only, so padding rows of the device stacks need no zeroing
+    a_d, ld = device.upload_stack(coeffs.A_star, padded_ld(r))
+    b_d, ldb = device.upload_stack(coeffs.B_star, padded_ld(r))
+    if ldb != ld:
+        b_d = device.upload_window(coeffs.B_star.array, ld)
     udot = t.zeros(ld, dtype=t.float64, device="cuda")
     udot[:r] = t.from_numpy(np.ascontiguousarray(coeffs.udot_norms)).to("cuda")
     tpack: TPack = pack_tmats(tmats)

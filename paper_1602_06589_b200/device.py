@@ -82,6 +82,31 @@ def upload_window(host: np.ndarray, ld: int | None = None, pinned: bool = False)
     return dev
 
 
+def pinned_stack(rows: int, cols: int, capacity_rows: int):
+    """Host column-major (capacity_rows x cols) complex128 allocation in pinned memory (torch's
+    caching host allocator), as the F-ordered numpy base of a `ComplexDense` window of `rows`
+    rows, plus its (cols, capacity_rows) tensor view for whole-buffer copies."""
+    t = torch()
+    buf = t.empty((max(cols, 1), max(capacity_rows, 1)), dtype=t.complex128, pin_memory=True)
+    return buf.numpy().T[:capacity_rows, :cols], buf
+
+
+def upload_stack(window, ld_min: int | None = None):
+    """Device (cols, ld) copy of a stacked-coefficient window.  A window at the top of an
+    F-ordered allocation (the layout `compute_AB` returns) goes up as one contiguous copy of
+    the whole allocation (ld = its capacity height; pinned memory makes it a DMA at full
+    PCIe speed); anything else is packed first (ld = `ld_min` or the window height)."""
+    t = require_cuda()
+    base = window.base
+    rows, cols = window.shape
+    if (window.row_offset == 0 and base.flags.f_contiguous and base.shape[1] == cols
+            and base.shape[0] >= max(rows, 1) and (ld_min is None or base.shape[0] >= rows)):
+        dev = t.from_numpy(base.T).to("cuda", non_blocking=True)
+        return dev, int(base.shape[0])
+    ld = ld_min or max(rows, 1)
+    return upload_window(window.array, ld), ld
+
+
 def download_window(dev, out: np.ndarray):
     """Copy the device (cols, ld) tensor's leading rows into the numpy window `out`."""
     rows, cols = out.shape

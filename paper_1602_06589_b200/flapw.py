@@ -150,14 +150,18 @@ def compute_AB(spec: SystemSpec) -> StackedCoefficients:
     layout = spec.layout()
     dspec = DeviceSpec(spec)
     n = spec.n_basis
-    ld = padded_ld(dspec.rows)
-    a_dev = device.empty_matrix(ld, n, ld, zero=True)
-    b_dev = device.empty_matrix(ld, n, ld, zero=True)
-    udot = t.zeros(ld, dtype=t.float64, device="cuda")
-    ab_generate_device(dspec, a_dev, b_dev, None, ld, udot)
-    a_star = ComplexDense.zeros(layout.total_rows, n, capacity_rows=layout.capacity_rows)
-    b_star = ComplexDense.zeros(layout.total_rows, n, capacity_rows=layout.capacity_rows)
-    device.download_window(a_dev, a_star.array)
-    device.download_window(b_dev, b_star.array)
+    # Generated with the host allocation's leading dimension (capacity rows, flapw.py:209-212),
+    # so each stack comes back as one contiguous DMA into pinned memory.
+    cap = layout.capacity_rows
+    a_dev = device.empty_matrix(cap, n, cap, zero=True)
+    b_dev = device.empty_matrix(cap, n, cap, zero=True)
+    udot = t.zeros(cap, dtype=t.float64, device="cuda")
+    ab_generate_device(dspec, a_dev, b_dev, None, cap, udot)
+    a_base, a_buf = device.pinned_stack(layout.total_rows, n, cap)
+    b_base, b_buf = device.pinned_stack(layout.total_rows, n, cap)
+    if n and cap:
+        a_buf.copy_(a_dev)
+        b_buf.copy_(b_dev)
     norms = udot[: layout.total_rows].cpu().numpy().copy()
-    return StackedCoefficients(a_star, b_star, layout, norms)
+    return StackedCoefficients(ComplexDense(a_base, 0, layout.total_rows),
+                               ComplexDense(b_base, 0, layout.total_rows), layout, norms)

@@ -111,7 +111,10 @@ def download_window(dev, out: np.ndarray):
     """Copy the device (cols, ld) tensor's leading rows into the numpy window `out`."""
     rows, cols = out.shape
     if rows and cols:
-        out[...] = dev[:cols, :rows].cpu().numpy().T
+        if out.flags.f_contiguous and out.dtype == np.complex128:
+            torch().from_numpy(out.T).copy_(dev[:cols, :rows])  # one copy, straight into `out`
+        else:
+            out[...] = dev[:cols, :rows].cpu().numpy().T
 
 
 def upload_real(vec) -> object:

@@ -190,6 +190,21 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ GPU arm
 
+def fp64_ceilings(sm_mhz):
+    """the DMMA peak at boost clock and at the clock measured during the run, and
+    the measured cuBLAS ZGEMM ceiling on the S-contraction shape (profiles/r01_fp64_peaks.json)."""
+    out = {"dmma_peak_boost_tflops": FP64_PEAK_TFLOPS}
+    if sm_mhz:
+        out["dmma_peak_at_measured_clock_tflops"] = round(148 * 128 * float(sm_mhz) * 1e6 / 1e12, 2)
+    try:
+        with open(os.path.join(REPO, "profiles", "r01_fp64_peaks.json")) as f:
+            z = json.load(f)["cublas_zgemm_tflops"]
+        out["cublas_zgemm_3000x3000x2592_tflops"] = z.get("3000x3000x2592")
+    except (OSError, KeyError, ValueError):
+        pass
+    return out
+
+
 def hbm_peak_gbs():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
@@ -346,6 +361,7 @@ def run_ours(args):
                 "kernel": "contract_kernel (S + H triangular DMMA contractions)",
                 "peak_source": "measured FP64 DMMA ceiling, profiles/r01_fp64_peaks.json "
                                "(MEASURED_PEAKS.json has no FP64 entry)",
+                "ceilings": fp64_ceilings(clk.summary().get("sm_mhz")),
                 "algorithmic_flops_per_step": fc,
                 "kernel_ms": {k: round(statistics.mean(v), 4) for k, v in kern.items()},
             },

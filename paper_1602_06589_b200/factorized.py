@@ -13,9 +13,10 @@ phase Gram and a template Gram multiplied elementwise:
     H = sum_t Phi_t o (Z^_t^H B^_t + B^_t^H Z^_t + Y^_t^H Y^_t   [or A^_t^H X^_t, non-HPD])
     Phi_t[G, G'] = sum_{a in t} conj(e_a(G)) e_a(G')
 
-The work drops from O(N_A N_L N_G^2) to O(N_types (N_L + N_A/N_types) N_G^2): every Gram is
-the same sm_100a DMMA contraction (`hsdla_herk_lower` / `her2k` / `gemm`), the phases come
-from `hsdla_phase_matrix` and the combine is `hsdla_hadamard_lower`.  Atoms are grouped into
+The work drops from O(N_A N_L N_G^2) to O(N_types (N_L + N_A/N_types) N_G^2): the template
+Grams are the S and H of a one-atom system, built by the stacked pipeline itself; Phi_t is one
+more DMMA contraction; the phases come from `hsdla_phase_matrix` and the combine is
+`hsdla_hadamard_lower`.  Atoms are grouped into
 types by exact equality of everything the coefficients depend on, so the result is always
 the stacked build's (a system with no shared types gets one rank-1 phase Gram per atom).
 This is an alternative evaluation, not `build_all`: the benchmark metric counts the
@@ -89,8 +90,14 @@ def build_hs_factorized(spec, tmats, config: BuildConfig | None = None):
 
 def build_hs_factorized_device(spec, tmats, config: BuildConfig | None = None):
     """Device part of `build_hs_factorized`: (H, S) as (n, n) device tensors (row j = column
-    j, full Hermitian), the HPD mask per atom and the device bytes used."""
-    from .pipeline import DeviceSpec, ab_generate_device, padded_ld
+    j, full Hermitian), the HPD mask per atom and the device bytes used.
+
+    Each type's template Grams come from the stacked pipeline run on a one-atom system (the
+    type's atom at the origin): its S and H are exactly A^^H A^ + (U B^)^H (U B^) and
+    Z^^H B^ + B^^H Z^ + Y^^H Y^ (or A^^H X^), with the T preparation, Cholesky dispatch and
+    fused contractions of `hsdla_setup_hs`."""
+    from .builder import TMatrixSet
+    from .pipeline import DeviceSpec, HSPipeline, pack_tmats
 
     config = config or BuildConfig()
     t = device.require_cuda()
@@ -98,20 +105,6 @@ def build_hs_factorized_device(spec, tmats, config: BuildConfig | None = None):
     c = device.ctx()
     n = int(spec.n_basis)
     groups = atom_types(spec, tmats)
-    reps = [g[0] for g in groups]
-    # templates: one atom per type at the origin (same rotation / radial data / radius)
-    tspec = SystemSpec(positions=np.zeros((len(reps), 3)),
-                       rotations=np.asarray(spec.rotations)[reps],
-                       mt_radius=np.asarray(spec.mt_radius)[reps],
-                       l_sph=np.asarray(spec.l_sph)[reps], l_nonsph=np.asarray(spec.l_nonsph)[reps],
-                       k_point=spec.k_point, k_vectors=spec.k_vectors, omega=spec.omega,
-                       radial=[spec.radial[a] for a in reps])
-    ds = DeviceSpec(tspec)
-    ld = padded_ld(ds.rows)
-    a_d = device.empty_matrix(ld, n, ld, zero=True)
-    b_d = device.empty_matrix(ld, n, ld, zero=True)
-    bs_d = device.empty_matrix(ld, n, ld, zero=True)
-    ab_generate_device(ds, a_d, b_d, bs_d, ld, None)
     # phases, atoms in type order
     order = [a for g in groups for a in g]
     lde = max(16, -(-len(order) // 16) * 16)
@@ -123,75 +116,42 @@ def build_hs_factorized_device(spec, tmats, config: BuildConfig | None = None):
     h_d = device.empty_matrix(n, n, n, zero=True)
     s_d = device.empty_matrix(n, n, n, zero=True)
     phi = device.empty_matrix(n, n, n)
-    gram = device.empty_matrix(n, n, n)
+    pipes = {}
     mask = [False] * spec.n_atoms
     e_row = 0
-    for ti, g in enumerate(groups):
+    for g in groups:
         rep = g[0]
-        h = int(ds.heights[ti])
-        r0 = int(ds.row_offset[ti])
-        m = int(tmats.t_aa[rep].rows)
-        # Phi_t = E_t^H E_t
+        tspec = SystemSpec(positions=np.zeros((1, 3)),
+                           rotations=np.asarray(spec.rotations)[[rep]],
+                           mt_radius=np.asarray(spec.mt_radius)[[rep]],
+                           l_sph=np.asarray(spec.l_sph)[[rep]],
+                           l_nonsph=np.asarray(spec.l_nonsph)[[rep]], k_point=spec.k_point,
+                           k_vectors=spec.k_vectors, omega=spec.omega, radial=[spec.radial[rep]])
+        ttm = TMatrixSet([tmats.t_aa[rep]], [tmats.t_ab[rep]], [tmats.t_bb[rep]],
+                         [tmats.l_sph[rep]], [tmats.l_nonsph[rep]])
+        ds = DeviceSpec(tspec)
+        key = int(ds.heights[0])
+        if key not in pipes:
+            pipes[key] = HSPipeline(n, ds.heights)
+        pipe = pipes[key]
+        res = pipe.run(ds, pack_tmats(ttm), config.force_general_path)
+        for a in g:
+            mask[a] = bool(res["hpd_mask"][0])
+        # Phi_t = E_t^H E_t, then H += Phi_t o H_t, S += Phi_t o S_t (lower)
         phi.zero_()
         _native.check(lib.hsdla_herk_lower(c, n, len(g), _p(e_d, e_row), lde, device.ptr(phi), n),
                       "hsdla_herk_lower")
         e_row += len(g)
-        # S: A^^H A^ + (U B^)^H (U B^)
-        gram.zero_()
-        _native.check(lib.hsdla_herk_lower(c, n, h, _p(a_d, r0), ld, device.ptr(gram), n), "herk")
-        _native.check(lib.hsdla_herk_lower(c, n, h, _p(bs_d, r0), ld, device.ptr(gram), n), "herk")
-        _native.check(lib.hsdla_hadamard_lower(c, n, device.ptr(phi), n, device.ptr(gram), n,
-                                               device.ptr(s_d), n, 1), "hsdla_hadamard_lower")
-        if m == 0:
-            continue
-        # H: Z^ = T_AB^H A^ + 1/2 T_BB B^ on the first m rows, then Z^^H B^ + B^^H Z^
-        tab = device.upload_window(tmats.t_ab[rep].array)
-        tbb = device.upload_window(tmats.t_bb[rep].array)
-        taa = device.upload_window(tmats.t_aa[rep].array)
-        ws = device.empty_matrix(m, m)
-        z_d = device.empty_matrix(m, n, m)
-        _native.check(lib.hsdla_gemm(c, 1, m, n, m, _native.c64(1.0), device.ptr(tab), tab.shape[1],
-                                     _p(a_d, r0), ld, _native.c64(0.0), device.ptr(z_d), m, None),
-                      "hsdla_gemm")
-        _native.check(lib.hsdla_hemm_lower(c, m, n, _native.c64(0.5), device.ptr(tbb), tbb.shape[1],
-                                           _p(b_d, r0), ld, 1, device.ptr(z_d), m, device.ptr(ws)),
-                      "hsdla_hemm_lower")
-        gram.zero_()
-        _native.check(lib.hsdla_her2k_lower(c, n, m, device.ptr(z_d), m, _p(b_d, r0), ld,
-                                            device.ptr(gram), n), "hsdla_her2k_lower")
-        # AA: Cholesky per type (builder.py:274-315): Y^ = C^H A^ (HPD) or X^ = T_AA A^
-        fac = device.empty_matrix(m, m)
-        info = (ctypes.c_int32 * 1)()
-        hpd = False
-        if not config.force_general_path:
-            _native.check(lib.hsdla_potrf_lower_batched(c, m, 1, device.ptr(taa), taa.shape[1], 0,
-                                                        device.ptr(fac), m, 0, info), "potrf")
-            if info[0] == -1:
-                raise ContractViolationError("NaN in Cholesky input (lower triangle)")
-            hpd = info[0] == 0
-        xy = device.empty_matrix(m, n, m)
-        if hpd:
-            _native.check(lib.hsdla_trmm_lower(c, 1, m, n, device.ptr(fac), m, _p(a_d, r0), ld,
-                                               device.ptr(xy), m, device.ptr(ws)), "hsdla_trmm_lower")
-            _native.check(lib.hsdla_herk_lower(c, n, m, device.ptr(xy), m, device.ptr(gram), n),
-                          "hsdla_herk_lower")
-        else:
-            _native.check(lib.hsdla_hemm_lower(c, m, n, _native.c64(1.0), device.ptr(taa),
-                                               taa.shape[1], _p(a_d, r0), ld, 0, device.ptr(xy), m,
-                                               device.ptr(ws)), "hsdla_hemm_lower")
-            _native.check(lib.hsdla_gemm(c, 1, n, n, m, _native.c64(1.0), _p(a_d, r0), ld,
-                                         device.ptr(xy), m, _native.c64(1.0), device.ptr(gram), n,
-                                         None), "hsdla_gemm")
-        for a in g:
-            mask[a] = hpd
-        _native.check(lib.hsdla_hadamard_lower(c, n, device.ptr(phi), n, device.ptr(gram), n,
-                                               device.ptr(h_d), n, 1), "hsdla_hadamard_lower")
+        for tmpl, acc in ((pipe.H, h_d), (pipe.S, s_d)):
+            _native.check(lib.hsdla_hadamard_lower(c, n, device.ptr(phi), n, device.ptr(tmpl),
+                                                   int(tmpl.shape[1]), device.ptr(acc), n, 1),
+                          "hsdla_hadamard_lower")
     flag = ctypes.c_int32(0)
     for mat in (h_d, s_d):
         _native.check(lib.hsdla_mirror_lower(c, n, device.ptr(mat), n, ctypes.byref(flag)),
                       "hsdla_mirror_lower")
         if flag.value:
             raise ContractViolationError("accumulator contains non-finite values")
-    nbytes = int(sum(x.numel() * x.element_size()
-                     for x in (a_d, b_d, bs_d, e_d, h_d, s_d, phi, gram)))
+    nbytes = int(sum(x.numel() * x.element_size() for x in (e_d, h_d, s_d, phi)) +
+                 sum(p.device_bytes for p in pipes.values()))
     return h_d, s_d, mask, nbytes

@@ -211,6 +211,11 @@ typedef struct {
    * preparation is skipped (T does not depend on the k-point).  Honoured only when the
    * workspace, T pointers, t_ld, t_dim and force_general_path also match that build. */
   int32_t reuse_t;
+  /* H copy scheduling for host destinations: 0 = default (synchronous calls stream H panel
+   * by panel during its contraction, pipelined calls copy it whole under the next k-point),
+   * 1 = stream (e.g. the last k-point of a batch, which has no successor to hide under),
+   * -1 = copy whole after the contraction. */
+  int32_t stream_h_copy;
 } hsdla_build_args;
 
 typedef struct {

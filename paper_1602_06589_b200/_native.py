@@ -70,7 +70,7 @@ class BuildArgs(ctypes.Structure):
         ("workspace", _vp), ("workspace_bytes", ctypes.c_size_t),
         ("shard_rank", _i32), ("n_shards", _i32),
         ("H_host", _vp), ("S_host", _vp), ("ldh_host", _i64),
-        ("shard_mirror", _i32), ("reuse_t", _i32),
+        ("shard_mirror", _i32), ("reuse_t", _i32), ("stream_h_copy", _i32),
     ]
 
 

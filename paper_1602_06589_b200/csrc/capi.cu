@@ -678,7 +678,8 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
   // finished panel while the kernel is still computing the rest (the contraction epilogue
   // publishes finished tiles, Prob::panel_done).
   const int nbp = (n + kTile - 1) / kTile;
-  WaitValueFn waitv = (sharded || !sl.copies || !stream_copies) ? nullptr : wait_value_fn();
+  const bool want_stream = a->stream_h_copy > 0 || (a->stream_h_copy == 0 && stream_copies);
+  WaitValueFn waitv = (sharded || !sl.copies || !want_stream) ? nullptr : wait_value_fn();
   if (waitv && sl.panel_cap < nbp) {
     if (sl.panel_cnt) {
       HS_CUDA(cudaDeviceSynchronize());

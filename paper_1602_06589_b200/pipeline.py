@@ -166,7 +166,7 @@ class _Call:
 
     def __init__(self, *, n_basis, heights, row_offset, tpack: TPack, A, B, Bs, udot, ld,
                  force_general_path, H, S, ldh, shard_rank, n_shards, workspace, host_out,
-                 ab_args=None, shard_mirror=False, reuse_t=False):
+                 ab_args=None, shard_mirror=False, reuse_t=False, stream_h_copy=0):
         lib = _native.load()
         t = device.torch()
         self.na = len(heights)
@@ -201,6 +201,7 @@ class _Call:
         a.n_shards = n_shards
         a.shard_mirror = 1 if shard_mirror else 0
         a.reuse_t = 1 if reuse_t else 0
+        a.stream_h_copy = int(stream_h_copy)
         if host_out is not None:  # pinned (n, n) tensors, row j = column j
             a.H_host = host_out[0].data_ptr()
             a.S_host = host_out[1].data_ptr()
@@ -312,7 +313,8 @@ class HSPipeline:
             tot += self.workspace.numel()
         return int(tot)
 
-    def _call(self, dspec: DeviceSpec, tpack: TPack, force_general_path: bool, host_out):
+    def _call(self, dspec: DeviceSpec, tpack: TPack, force_general_path: bool, host_out,
+              stream_h_copy: int = 0):
         if dspec.n_basis > self.n_capacity or dspec.rows != self.rows:
             raise ContractViolationError("spec shape does not fit the pipeline buffers")
         self.n_basis = dspec.n_basis
@@ -326,7 +328,7 @@ class HSPipeline:
                      force_general_path=force_general_path, H=self.H, S=self.S,
                      ldh=self.n_capacity, shard_rank=self.shard_rank, n_shards=self.n_shards,
                      workspace=self.workspace, host_out=host_out, ab_args=ab,
-                     shard_mirror=self.shard_mirror, reuse_t=reuse)
+                     shard_mirror=self.shard_mirror, reuse_t=reuse, stream_h_copy=stream_h_copy)
         call.keep.append(dspec)
         self.workspace = call.workspace
         self._last_t = (tpack, bool(force_general_path))
@@ -339,10 +341,11 @@ class HSPipeline:
         return self._call(dspec, tpack, force_general_path, host_out).run_sync()
 
     def run_async(self, dspec: DeviceSpec, tpack: TPack, force_general_path: bool = False,
-                  host_out=None) -> int:
+                  host_out=None, last: bool = False) -> int:
         """Enqueue one k-point and return a ticket at once (`hsdla_setup_hs_async`).  At
-        most two k-points may be in flight; their `host_out` buffers must differ."""
-        call = self._call(dspec, tpack, force_general_path, host_out)
+        most two k-points may be in flight; their `host_out` buffers must differ.  `last`:
+        no k-point follows, so H is streamed to the host during its own contraction."""
+        call = self._call(dspec, tpack, force_general_path, host_out, 1 if last else 0)
         ticket = call.start()
         self._inflight[ticket] = call
         return ticket
@@ -421,7 +424,8 @@ def build_hs_many(specs, tmats, config=None, *, pipeline: HSPipeline | None = No
         key = (i % 2, n)
         if key not in bufs:
             bufs[key] = _pinned_pair(n)
-        ticket = pipe.run_async(dspec, tpack, config.force_general_path, host_out=bufs[key])
+        ticket = pipe.run_async(dspec, tpack, config.force_general_path, host_out=bufs[key],
+                                last=(i == len(specs) - 1))
         if pending is not None:
             results.append(_complete(pipe, pending, tpack, on_result, ComplexDense))
         pending = (i, ticket, bufs[key], dspec)

@@ -131,6 +131,17 @@ typedef struct {
 } hsdla_ab_args;
 int hsdla_ab_generate(hsdla_ctx* ctx, const hsdla_ab_args* args);
 
+/* Spherical Bessel j_0..j_lmax and j'_0..j'_lmax at n arguments x >= 0 (DEVICE), row l of
+ * j / jp = order l ((l_max+1) x n row-major): special.py:104-131 spherical_bessel_all on the
+ * A/B generator's device code (same regimes and rounding).  l_max <= HSDLA_MAX_LSPH. */
+int hsdla_spherical_bessel(hsdla_ctx* ctx, int l_max, int n, const double* x, double* j,
+                           double* jp);
+/* Y_lm, rows l^2+l+m, at n unit directions (DEVICE n x 3): special.py:139-179
+ * spherical_harmonics_all on the generator's Legendre recurrence; Y is (l_max+1)^2 x n
+ * row-major complex. */
+int hsdla_spherical_harmonics(hsdla_ctx* ctx, int l_max, int n, const double* directions,
+                              hsdla_c64* Y);
+
 /* Radial match factors f_A, f_B (flapw.py:179-198 match_factors) on the device: row
  * f_row[a] + l (l <= l_sph[a]) of f_a / f_b (DEVICE, row-major, row stride ld_f >= n_basis)
  * receives the factors of atom a for every K-vector.  Uses n_atoms, n_basis, k_vectors,

@@ -111,6 +111,8 @@ SIGNATURES = {
     "hsdla_ab_generate": (ctypes.c_int, [_vp, ctypes.POINTER(AbArgs)]),
     "hsdla_match_factors": (ctypes.c_int, [_vp, ctypes.POINTER(AbArgs), _P_i64, _vp, _vp, _i64]),
     "hsdla_reduced_s_aa": (ctypes.c_int, [_vp, ctypes.POINTER(ReducedArgs)]),
+    "hsdla_spherical_bessel": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]),
+    "hsdla_spherical_harmonics": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp]),
     "hsdla_phase_matrix": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _i64]),
     "hsdla_hadamard_lower": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _i64, _vp, _i64, _vp, _i64,
                                             ctypes.c_int]),

@@ -205,6 +205,76 @@ int launch_ab_l(hsdla_ctx* ctx, const AbParams& p, const int* atoms_dev, const l
   return HSDLA_OK;
 }
 
+// Standalone special functions (special.py:104-179) on the same device code as the A/B
+// generator: j_l, j'_l at many x, and Y_lm at many unit directions.
+template <int L>
+__global__ void bessel_all_kernel(int n, const double* __restrict__ x, double* j, double* jp) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double jv[L + 2], jd[L + 1];
+  bessel::bessel_jd<L>(x[i], jv, jd);
+#pragma unroll
+  for (int l = 0; l <= L; ++l) {
+    j[(long long)l * n + i] = jv[l];
+    jp[(long long)l * n + i] = jd[l];
+  }
+}
+
+template <int L>
+__global__ void ylm_all_kernel(int n, const double* __restrict__ d, double2* Y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double ct = fmin(fmax(d[3 * i + 2], -1.0), 1.0);
+  const double st = sqrt(fmax(0.0, 1.0 - ct * ct));
+  double ephr, ephi;
+  sincos(atan2(d[3 * i + 1], d[3 * i + 0]), &ephi, &ephr);
+  double emr[L + 1], emi[L + 1];
+  emr[0] = 1.0;
+  emi[0] = 0.0;
+#pragma unroll
+  for (int m = 1; m <= L; ++m) {
+    emr[m] = emr[m - 1] * ephr - emi[m - 1] * ephi;
+    emi[m] = emr[m - 1] * ephi + emi[m - 1] * ephr;
+  }
+  double p1[L + 1], p2[L + 1];
+#pragma unroll
+  for (int l = 0; l <= L; ++l) {
+    double pl[L + 1];
+#pragma unroll
+    for (int m = 0; m <= l; ++m) {
+      if (m == l) pl[m] = (l == 0) ? 0.28209479177387814 : -c_sect[m] * st * p1[m - (l > 0 ? 1 : 0)];
+      else if (m == l - 1) pl[m] = c_sub[m] * ct * p1[m];
+      else pl[m] = c_a[l][m] * (ct * p1[m] - c_b[l][m] * p2[m]);
+    }
+#pragma unroll
+    for (int m = 0; m <= l; ++m) {
+      const double yr = pl[m] * emr[m], yi = pl[m] * emi[m];
+      Y[(long long)(l * l + l + m) * n + i] = make_double2(yr, yi);
+      if (m > 0) {
+        const double sg = (m & 1) ? -1.0 : 1.0;
+        Y[(long long)(l * l + l - m) * n + i] = make_double2(sg * yr, -(sg * yi));
+      }
+    }
+#pragma unroll
+    for (int m = 0; m <= l; ++m) { p2[m] = p1[m]; p1[m] = pl[m]; }
+  }
+}
+
+template <int L>
+int launch_special_l(hsdla_ctx* ctx, int kind, int n, const double* in, double* o1, double* o2) {
+  const int grid = (n + 127) / 128;
+  if (kind == 0) bessel_all_kernel<L><<<grid, 128, 0, ctx->stream>>>(n, in, o1, o2);
+  else ylm_all_kernel<L><<<grid, 128, 0, ctx->stream>>>(n, in, reinterpret_cast<double2*>(o1));
+  HS_CHECK_LAUNCH();
+  return HSDLA_OK;
+}
+typedef int (*special_launcher)(hsdla_ctx*, int, int, const double*, double*, double*);
+const special_launcher kSpecialLaunchers[HSDLA_MAX_LSPH + 1] = {
+    &launch_special_l<0>, &launch_special_l<1>, &launch_special_l<2>, &launch_special_l<3>,
+    &launch_special_l<4>, &launch_special_l<5>, &launch_special_l<6>, &launch_special_l<7>,
+    &launch_special_l<8>, &launch_special_l<9>, &launch_special_l<10>, &launch_special_l<11>,
+    &launch_special_l<12>, &launch_special_l<13>, &launch_special_l<14>};
+
 template <int L>
 int preload_ab_l() {
   constexpr int S = 2 * L + 1;
@@ -280,6 +350,18 @@ int preload_abgen() {
   cudaFuncAttributes at;
   HS_CUDA(cudaFuncGetAttributes(&at, (const void*)udot_rows_kernel));
   return upload_ylm_tables();
+}
+
+int special_functions(hsdla_ctx* ctx, int kind, int l_max, int n, const double* in, double* o1,
+                      double* o2) {
+  if (l_max < 0 || l_max > HSDLA_MAX_LSPH) {
+    set_error("l_max above HSDLA_MAX_LSPH");
+    return HSDLA_ERR_UNSUPPORTED;
+  }
+  if (n <= 0) return HSDLA_OK;
+  int rc = upload_ylm_tables();
+  if (rc) return rc;
+  return kSpecialLaunchers[l_max](ctx, kind, n, in, o1, o2);
 }
 
 int ab_generate(hsdla_ctx* ctx, const hsdla_ab_args* args) {

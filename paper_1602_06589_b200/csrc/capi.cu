@@ -388,6 +388,24 @@ int hsdla_ab_generate(hsdla_ctx* ctx, const hsdla_ab_args* args) {
   return ab_generate(ctx, args);
 }
 
+int hsdla_spherical_bessel(hsdla_ctx* ctx, int l_max, int n, const double* x, double* j,
+                           double* jp) {
+  if (!ctx) return -1;
+  if (n < 0) return -3;
+  if (n > 0 && (!x || !j || !jp)) return -4;
+  std::lock_guard<std::mutex> lk(g_api_mutex);
+  return special_functions(ctx, 0, l_max, n, x, j, jp);
+}
+
+int hsdla_spherical_harmonics(hsdla_ctx* ctx, int l_max, int n, const double* directions,
+                              hsdla_c64* Y) {
+  if (!ctx) return -1;
+  if (n < 0) return -3;
+  if (n > 0 && (!directions || !Y)) return -4;
+  std::lock_guard<std::mutex> lk(g_api_mutex);
+  return special_functions(ctx, 1, l_max, n, directions, reinterpret_cast<double*>(Y), nullptr);
+}
+
 int hsdla_match_factors(hsdla_ctx* ctx, const hsdla_ab_args* spec, const int64_t* f_row,
                         double* f_a, double* f_b, int64_t ld_f) {
   if (!ctx) return -1;

@@ -177,6 +177,10 @@ int launch_tprep(hsdla_ctx* ctx, cudaStream_t stream, int n_tsets, const int* td
                  const double2* taa, const double2* tab, const double2* tbb, long long t_ld,
                  double2* forms, int do_chol, int* info_dev);
 int ab_generate(hsdla_ctx* ctx, const hsdla_ab_args* args);
+// kind 0: o1/o2 = j_l(x), j'_l(x), (l_max+1) x n row-major; kind 1: o1 = Y_lm (complex,
+// (l_max+1)^2 x n row-major) at unit directions in (n x 3).
+int special_functions(hsdla_ctx* ctx, int kind, int l_max, int n, const double* in, double* o1,
+                      double* o2);
 int match_factors(hsdla_ctx* ctx, const hsdla_ab_args* s, const int64_t* f_row, double* fa,
                   double* fb, int64_t ldf);
 int reduced_s_aa(hsdla_ctx* ctx, const hsdla_reduced_args* r);

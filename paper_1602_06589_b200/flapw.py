@@ -165,3 +165,35 @@ def compute_AB(spec: SystemSpec) -> StackedCoefficients:
     norms = udot[: layout.total_rows].cpu().numpy().copy()
     return StackedCoefficients(ComplexDense(a_base, 0, layout.total_rows),
                                ComplexDense(b_base, 0, layout.total_rows), layout, norms)
+
+
+def match_factors(spec: SystemSpec, atom: int):
+    """Real radial match factors (f_A, f_B), each (l_sph+1, N_G), of one atom on the GPU
+    (`flapw.py:179-198`; `hsdla_match_factors`, same Bessel code as `compute_AB`)."""
+    import ctypes
+
+    from . import _native, device
+    from .pipeline import DeviceSpec
+
+    t = device.require_cuda()
+    if not 0 <= atom < spec.n_atoms:
+        raise ContractViolationError(f"atom index {atom} out of range")
+    ds = DeviceSpec(spec)
+    n = ds.n_basis
+    l_top = ds.l_sph.astype(np.int32)
+    f_row = np.concatenate(([0], np.cumsum(l_top.astype(np.int64) + 1)[:-1])).astype(np.int64)
+    rows = int((l_top + 1).sum())
+    fa = t.empty((rows, max(n, 1)), dtype=t.float64, device="cuda")
+    fb = t.empty((rows, max(n, 1)), dtype=t.float64, device="cuda")
+    args = _native.AbArgs()
+    args.n_atoms, args.n_basis = ds.n_atoms, n
+    args.k_vectors, args.positions = ds.kv.data_ptr(), ds.pos.data_ptr()
+    args.rotations, args.mt_radius = ds.rot.data_ptr(), ds.rmt.data_ptr()
+    args.radial, args.radial_stride = ds.radial.data_ptr(), ds.radial_stride
+    args.l_sph = l_top.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+    args.omega = ds.omega
+    _native.check(_native.load().hsdla_match_factors(
+        device.ctx(), ctypes.byref(args), f_row.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+        device.ptr(fa), device.ptr(fb), max(n, 1)), "hsdla_match_factors")
+    r0, r1 = int(f_row[atom]), int(f_row[atom]) + int(l_top[atom]) + 1
+    return fa[r0:r1, :n].cpu().numpy(), fb[r0:r1, :n].cpu().numpy()

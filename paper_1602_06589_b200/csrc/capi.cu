@@ -455,7 +455,15 @@ WaitValueFn wait_value_fn() {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     const char* e = getenv("HSDLA_STREAM_COPIES");
-    if (!(e && atoi(e) == 0) &&
+    // Under a profiler that serialises kernels (Nsight Compute / injection libraries) a copy
+    // stream waiting on a not-yet-launched kernel would wait forever: copy H whole instead.
+    bool profiled = false;
+    for (const char* v : {"CUDA_INJECTION64_PATH", "NV_NSIGHT_INJECTION_TRANSPORT_TYPE",
+                          "NV_COMPUTE_PROFILER_PERFWORKS_DIR"}) {
+      const char* x = getenv(v);
+      profiled = profiled || (x && *x);
+    }
+    if (!(e && atoi(e) == 0) && !profiled &&
         cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
       fn = reinterpret_cast<WaitValueFn>(p);

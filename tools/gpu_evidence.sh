@@ -17,13 +17,13 @@ for c in C3 C4 C5; do
   tail -1 gpurun_out/bench_$c.log | cut -c1-400
 done
 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/plain_short.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_C2.csv \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_C2.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
 echo "ncu launch rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:"contract" -s 4 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"contract" -s 4 -c 1 \
     -o gpurun_out/prof_contractS_C2 python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
 echo "ncu full rc=$?"
-ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
     -k regex:"contract" --csv --log-file gpurun_out/traffic_C2.csv \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_t.log 2>&1
 echo "ncu traffic rc=$?"

@@ -1,0 +1,40 @@
+"""bench.py's output contract on CPU: the reference arm (`--impl reference`, the oracle port
+timed on the host) prints one JSON line with the driver's keys; the GPU arm's helpers
+(ledger flops, FP64 ceilings, A/B-generation roofline) compute what DESIGN.md says."""
+import json
+import os
+import subprocess
+import sys
+
+from conftest import REPO
+
+
+def test_reference_arm_json_line():
+    out = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--impl", "reference",
+                          "--config", "C1", "--steps", "1", "--warmup", "1"],
+                         capture_output=True, text=True, timeout=600, cwd=REPO)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+                "cpu_baseline", "e2e"):
+        assert key in d, key
+    assert d["impl"] == "reference" and d["unit"] == "TFLOP/s" and d["higher_is_better"] is True
+    assert d["value"] > 0 and d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+
+
+def test_bench_helpers():
+    sys.path.insert(0, REPO)
+    import bench
+
+    n, r = 3000, 1296
+    assert bench.contract_flops(n, r, r) == 16 * r * n * n + 4 * r * n * n
+    assert bench.contract_flops(n, r, 0) == 24 * r * n * n
+    c = bench.fp64_ceilings(1965.0)
+    assert c["dmma_peak_boost_tflops"] == 37.2
+    assert abs(c["dmma_peak_at_measured_clock_tflops"] - 37.22) < 0.01
+    g = bench.ab_gen_line(0.1, r, n)
+    assert g["bytes_written"] == 48 * r * n and 0 < g["frac"] < 1

@@ -118,7 +118,7 @@ __device__ __forceinline__ Seg load_seg(const Seg* s) {
 // JB = 8-column DMMA blocks per warp along n: JB = 4 -> warp tile 32x32 complex, 4 warps
 // (128 threads, ~250 registers, 2 warps per SM sub-partition); JB = 2 -> warp tile 32x16,
 // 8 warps (256 threads, <= 128 registers, 4 warps per sub-partition).
-template <int JB, int PAD>
+template <int JB, int PAD, bool G3 = false>
 __global__ void __launch_bounds__(32 * 2 * (8 / JB), 2) contract_kernel(SKParams sk) {
   extern __shared__ __align__(128) double smem[];
   constexpr int kColDoubles = Layout<PAD>::kColDoubles;
@@ -245,13 +245,17 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), 2) contract_kernel(SKParams
       advance();
     };
 
-    double accR[4][JB][2], accI[4][JB][2];
+    // G3 (three-product complex multiply): accR = sum p_re q_re, accX = sum p_im q_im,
+    // accI = sum (p_re - p_im)(q_re + q_im); combined after the K loop into
+    // Re = accR + accX, Im = accI - accR + accX.  Otherwise accR / accI hold Re / Im.
+    double accR[4][JB][2], accI[4][JB][2], accX[G3 ? 4 : 1][G3 ? JB : 1][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < JB; ++b) {
         accR[a][b][0] = accR[a][b][1] = 0.0;
         accI[a][b][0] = accI[a][b][1] = 0.0;
+        if constexpr (G3) accX[a][b][0] = accX[a][b][1] = 0.0;
       }
 
     const int nchunks = c_hi - c_lo;
@@ -297,6 +301,26 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), 2) contract_kernel(SKParams
 #pragma unroll
           for (int jb = 0; jb < JB; ++jb)
             bv[jb] = *reinterpret_cast<const double2*>(pb + jb * 8 * kColDoubles + off);
+          if constexpr (G3) {
+            // Three DMMAs per (block pair, complex-K group) instead of four.
+#pragma unroll
+            for (int ib = 0; ib < 4; ++ib)
+#pragma unroll
+              for (int jb = 0; jb < JB; ++jb) {
+                dmma(accR[ib][jb][0], accR[ib][jb][1], av[ib].x, bv[jb].x);
+                dmma(accX[ib][jb][0], accX[ib][jb][1], av[ib].y, bv[jb].y);
+              }
+            double sa[4], sb[JB];
+#pragma unroll
+            for (int ib = 0; ib < 4; ++ib) sa[ib] = av[ib].x - av[ib].y;
+#pragma unroll
+            for (int jb = 0; jb < JB; ++jb) sb[jb] = bv[jb].x + bv[jb].y;
+#pragma unroll
+            for (int ib = 0; ib < 4; ++ib)
+#pragma unroll
+              for (int jb = 0; jb < JB; ++jb)
+                dmma(accI[ib][jb][0], accI[ib][jb][1], sa[ib], sb[jb]);
+          } else {
 #pragma unroll
           for (int ib = 0; ib < 4; ++ib)
 #pragma unroll
@@ -316,6 +340,7 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), 2) contract_kernel(SKParams
               dmma(accR[ib][jb][0], accR[ib][jb][1], av[ib].y, bv[jb].y);
               dmma(accI[ib][jb][0], accI[ib][jb][1], av[ib].y, nb[jb]);
             }
+          }
         }
       } else {
 #pragma unroll
@@ -349,6 +374,18 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), 2) contract_kernel(SKParams
     cp_async_wait<0>();
     __syncthreads();
     it += nchunks;
+    if constexpr (G3) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < JB; ++b)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const double t1 = accR[a][b][v], t2 = accX[a][b][v];
+            accR[a][b][v] = t1 + t2;
+            accI[a][b][v] = (accI[a][b][v] - t1) + t2;
+          }
+    }
 
     if (c_lo != 0) {
       // Later piece of a split tile: publish the partial for the tile's finishing CTA.
@@ -490,10 +527,13 @@ void plan_dp_waves(const std::vector<Prob>& probs, long long total, int grid, in
 int preload_contract() {
   const void* fns[] = {(const void*)contract_kernel<2, 0>, (const void*)contract_kernel<2, 1>,
                        (const void*)contract_kernel<2, 2>, (const void*)contract_kernel<4, 0>,
-                       (const void*)contract_kernel<4, 1>, (const void*)contract_kernel<4, 2>};
+                       (const void*)contract_kernel<4, 1>, (const void*)contract_kernel<4, 2>,
+                       (const void*)contract_kernel<2, 2, true>,
+                       (const void*)contract_kernel<4, 2, true>};
   const size_t smem[] = {Layout<0>::kSmemBytes, Layout<1>::kSmemBytes, Layout<2>::kSmemBytes,
-                         Layout<0>::kSmemBytes, Layout<1>::kSmemBytes, Layout<2>::kSmemBytes};
-  for (int i = 0; i < 6; ++i) {
+                         Layout<0>::kSmemBytes, Layout<1>::kSmemBytes, Layout<2>::kSmemBytes,
+                         Layout<2>::kSmemBytes, Layout<2>::kSmemBytes};
+  for (int i = 0; i < 8; ++i) {
     cudaFuncAttributes at;
     HS_CUDA(cudaFuncGetAttributes(&at, fns[i]));
     if (first_on_device(fns[i]))
@@ -536,17 +576,23 @@ int launch_contract(hsdla_ctx* ctx, const std::vector<Prob>& probs_in,
   // Variant selection (HSDLA_WARP_COLS = 32 | 16, HSDLA_SMEM_PAD = 0 | 1) for A/B tests.
   // Shared-memory layout / fragment path: HSDLA_CP_LAYOUT = pair (default: paired K steps,
   // 128-bit fragment loads) | xor (32-byte XOR swizzle, 64-bit loads) | pad (288-byte columns).
-  static int variant = -1, pad = -1;
+  // Complex multiply: HSDLA_CMUL = 3 (default: three DMMA products per complex MAC, pair
+  // layout only) | 4 (four, the real embedding).
+  static int variant = -1, pad = -1, cmul = -1;
   if (variant < 0) {
     const char* e = getenv("HSDLA_WARP_COLS");
     variant = (e && atoi(e) == 16) ? 2 : 4;
     const char* p = getenv("HSDLA_CP_LAYOUT");
     pad = (p && std::string(p) == "pad") ? 1 : (p && std::string(p) == "xor") ? 0 : 2;
+    const char* m = getenv("HSDLA_CMUL");
+    cmul = (m && atoi(m) == 4) ? 4 : 3;
   }
-  const void* kfns[2][3] = {
-      {(const void*)contract_kernel<2, 0>, (const void*)contract_kernel<2, 1>, (const void*)contract_kernel<2, 2>},
-      {(const void*)contract_kernel<4, 0>, (const void*)contract_kernel<4, 1>, (const void*)contract_kernel<4, 2>}};
-  const void* kfn = kfns[variant == 4 ? 1 : 0][pad];
+  const void* kfns[2][4] = {
+      {(const void*)contract_kernel<2, 0>, (const void*)contract_kernel<2, 1>, (const void*)contract_kernel<2, 2>,
+       (const void*)contract_kernel<2, 2, true>},
+      {(const void*)contract_kernel<4, 0>, (const void*)contract_kernel<4, 1>, (const void*)contract_kernel<4, 2>,
+       (const void*)contract_kernel<4, 2, true>}};
+  const void* kfn = kfns[variant == 4 ? 1 : 0][(pad == 2 && cmul == 3) ? 3 : pad];
   const size_t kSmemBytes = pad == 1 ? Layout<1>::kSmemBytes : Layout<0>::kSmemBytes;
   if (first_on_device(kfn))
     HS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));

@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <map>
 #include <string>
@@ -27,6 +28,18 @@ inline bool first_on_device(const void* key) {
 }
 
 void set_error(const std::string& msg);
+
+// Complex multiply of the DMMA contractions: 3 (default) = three real products per complex
+// MAC (Re = P_re Q_re + P_im Q_im, Im = (P_re - P_im)(Q_re + Q_im) - P_re Q_re + P_im Q_im);
+// 4 = the real embedding's four.  HSDLA_CMUL=4 selects the latter (A/B measurements).
+inline int cmul_mode() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("HSDLA_CMUL");
+    m = (e && e[0] == '4' && e[1] == 0) ? 4 : 3;
+  }
+  return m;
+}
 
 #define HS_CUDA(call)                                                                  \
   do {                                                                                 \

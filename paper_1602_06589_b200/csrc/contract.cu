@@ -118,8 +118,10 @@ __device__ __forceinline__ Seg load_seg(const Seg* s) {
 // JB = 8-column DMMA blocks per warp along n: JB = 4 -> warp tile 32x32 complex, 4 warps
 // (128 threads, ~250 registers, 2 warps per SM sub-partition); JB = 2 -> warp tile 32x16,
 // 8 warps (256 threads, <= 128 registers, 4 warps per sub-partition).
+// G3 with JB = 2 keeps three accumulator sets in 255 registers at one 8-warp CTA per SM.
 template <int JB, int PAD, bool G3 = false>
-__global__ void __launch_bounds__(32 * 2 * (8 / JB), 2) contract_kernel(SKParams sk) {
+__global__ void __launch_bounds__(32 * 2 * (8 / JB), (G3 && JB == 2) ? 1 : 2)
+    contract_kernel(SKParams sk) {
   extern __shared__ __align__(128) double smem[];
   constexpr int kColDoubles = Layout<PAD>::kColDoubles;
   constexpr int kOpDoubles = Layout<PAD>::kOpDoubles;
@@ -576,16 +578,15 @@ int launch_contract(hsdla_ctx* ctx, const std::vector<Prob>& probs_in,
   // Variant selection (HSDLA_WARP_COLS = 32 | 16, HSDLA_SMEM_PAD = 0 | 1) for A/B tests.
   // Shared-memory layout / fragment path: HSDLA_CP_LAYOUT = pair (default: paired K steps,
   // 128-bit fragment loads) | xor (32-byte XOR swizzle, 64-bit loads) | pad (288-byte columns).
-  // Complex multiply: HSDLA_CMUL = 3 (default: three DMMA products per complex MAC, pair
-  // layout only) | 4 (four, the real embedding).
+  // Complex multiply (cmul_mode, HSDLA_CMUL): 3 (default) uses the three-product kernel, pair
+  // layout only.
   static int variant = -1, pad = -1, cmul = -1;
   if (variant < 0) {
     const char* e = getenv("HSDLA_WARP_COLS");
     variant = (e && atoi(e) == 16) ? 2 : 4;
     const char* p = getenv("HSDLA_CP_LAYOUT");
     pad = (p && std::string(p) == "pad") ? 1 : (p && std::string(p) == "xor") ? 0 : 2;
-    const char* m = getenv("HSDLA_CMUL");
-    cmul = (m && atoi(m) == 4) ? 4 : 3;
+    cmul = cmul_mode();
   }
   const void* kfns[2][4] = {
       {(const void*)contract_kernel<2, 0>, (const void*)contract_kernel<2, 1>, (const void*)contract_kernel<2, 2>,

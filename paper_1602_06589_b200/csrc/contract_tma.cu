@@ -33,10 +33,11 @@ constexpr int kStg = 3;
 // tile is TM x TN.  Cfg<2,2,4> = 64x64 (4 warps, ~250 registers, every triangular problem);
 // Cfg<3,2,2> = 96x32 (6 warps, ~128 registers) for the T applications when 64 < m <= 96
 // (m = 81 at l_sph = 8: 84% of the rows useful instead of 63% with 64-row tiles).
-template <int WM_, int WN_, int JB_, bool PAIR_ = false>
+template <int WM_, int WN_, int JB_, bool PAIR_ = false, bool G3_ = false>
 struct Cfg {
   static constexpr int WM = WM_, WN = WN_, JB = JB_;
   static constexpr bool PAIR = PAIR_;
+  static constexpr bool G3 = G3_;  // three-product complex multiply (PAIR only), see contract.cu
   static constexpr int TM = 32 * WM, TN = 8 * JB * WN;
   static constexpr int kT = 32 * WM * WN;
   static constexpr int kPBox = TM * 128, kQBox = TN * 128;  // box = columns x 16 doubles
@@ -53,6 +54,8 @@ using Cfg96 = Cfg<3, 2, 2>;
 // inside each 8-column block; the epilogue maps rows and columns through pi.
 using Cfg64P = Cfg<2, 2, 4, true>;
 using Cfg96P = Cfg<3, 2, 2, true>;
+using Cfg64G = Cfg<2, 2, 4, true, true>;
+using Cfg96G = Cfg<3, 2, 2, true, true>;
 __device__ __forceinline__ int pair_perm(int g) { return (g >> 1) | ((g & 1) << 2); }
 
 struct TSeg {
@@ -295,13 +298,16 @@ __global__ void __launch_bounds__(C::kT, 2) contract_tma_kernel(TKParams sk) {
     tile_coords(pr, tile, tm, tn);
     const int i0 = tm * C::TM, j0 = tn * C::TN;
 
-    double accR[4][JB][2], accI[4][JB][2];
+    // G3: accR = sum p_re q_re, accX = sum p_im q_im, accI = sum (p_re - p_im)(q_re + q_im),
+    // combined after the K loop (Re = accR + accX, Im = accI - accR + accX).
+    double accR[4][JB][2], accI[4][JB][2], accX[C::G3 ? 4 : 1][C::G3 ? JB : 1][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < JB; ++b) {
         accR[a][b][0] = accR[a][b][1] = 0.0;
         accI[a][b][0] = accI[a][b][1] = 0.0;
+        if constexpr (C::G3) accX[a][b][0] = accX[a][b][1] = 0.0;
       }
 
     for (int cc = c_lo; cc < c_hi; ++cc, ++j) {
@@ -321,6 +327,25 @@ __global__ void __launch_bounds__(C::kT, 2) contract_tma_kernel(TKParams sk) {
           for (int ib = 0; ib < 4; ++ib) av[ib] = *reinterpret_cast<const double2*>(pA + ib * 8 * 128);
 #pragma unroll
           for (int jb = 0; jb < JB; ++jb) bv[jb] = *reinterpret_cast<const double2*>(pB + jb * 8 * 128);
+          if constexpr (C::G3) {
+#pragma unroll
+            for (int ib = 0; ib < 4; ++ib)
+#pragma unroll
+              for (int jb = 0; jb < JB; ++jb) {
+                dmma(accR[ib][jb][0], accR[ib][jb][1], av[ib].x, bv[jb].x);
+                dmma(accX[ib][jb][0], accX[ib][jb][1], av[ib].y, bv[jb].y);
+              }
+            double sa[4], sb[JB];
+#pragma unroll
+            for (int ib = 0; ib < 4; ++ib) sa[ib] = av[ib].x - av[ib].y;
+#pragma unroll
+            for (int jb = 0; jb < JB; ++jb) sb[jb] = bv[jb].x + bv[jb].y;
+#pragma unroll
+            for (int ib = 0; ib < 4; ++ib)
+#pragma unroll
+              for (int jb = 0; jb < JB; ++jb)
+                dmma(accI[ib][jb][0], accI[ib][jb][1], sa[ib], sb[jb]);
+          } else {
 #pragma unroll
           for (int ib = 0; ib < 4; ++ib)
 #pragma unroll
@@ -339,6 +364,7 @@ __global__ void __launch_bounds__(C::kT, 2) contract_tma_kernel(TKParams sk) {
               dmma(accR[ib][jb][0], accR[ib][jb][1], av[ib].y, bv[jb].y);
               dmma(accI[ib][jb][0], accI[ib][jb][1], av[ib].y, nb[jb]);
             }
+          }
           if (jj == 1 && tid == 0) {
             const long long x = j + kStg - 1;
             if (x < nchunks_cta) {
@@ -393,6 +419,18 @@ __global__ void __launch_bounds__(C::kT, 2) contract_tma_kernel(TKParams sk) {
       if (lane == 0) mbar_arrive(empty + st);
     }
     it += c_hi - c_lo;
+    if constexpr (C::G3) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < JB; ++b)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const double t1 = accR[a][b][v], t2 = accX[a][b][v];
+            accR[a][b][v] = t1 + t2;
+            accI[a][b][v] = (accI[a][b][v] - t1) + t2;
+          }
+    }
 
     if (c_lo != 0) {
       // Later piece of a split tile: publish the partial for the tile's finishing CTA.
@@ -647,7 +685,9 @@ int preload_contract_tma() {
   if (int rc = preload_cfg<Cfg64>()) return rc;
   if (int rc = preload_cfg<Cfg96>()) return rc;
   if (int rc = preload_cfg<Cfg64P>()) return rc;
-  return preload_cfg<Cfg96P>();
+  if (int rc = preload_cfg<Cfg96P>()) return rc;
+  if (int rc = preload_cfg<Cfg64G>()) return rc;
+  return preload_cfg<Cfg96G>();
 }
 
 bool tma_wants(const std::vector<Prob>& probs) {
@@ -675,11 +715,14 @@ int launch_contract_tma(hsdla_ctx* ctx, const std::vector<Prob>& probs, long lon
     const char* e = getenv("HSDLA_TMA_PAIR");
     pair = (e && atoi(e) == 0) ? 0 : 1;
   }
+  const bool g3 = pair && cmul_mode() == 3;
   if (tma_wants(probs))
-    return pair ? launch_cfg<Cfg96P>(ctx, probs, segs, flag_dev)
-                : launch_cfg<Cfg96>(ctx, probs, segs, flag_dev);
-  return pair ? launch_cfg<Cfg64P>(ctx, probs, segs, flag_dev)
-              : launch_cfg<Cfg64>(ctx, probs, segs, flag_dev);
+    return g3     ? launch_cfg<Cfg96G>(ctx, probs, segs, flag_dev)
+           : pair ? launch_cfg<Cfg96P>(ctx, probs, segs, flag_dev)
+                  : launch_cfg<Cfg96>(ctx, probs, segs, flag_dev);
+  return g3     ? launch_cfg<Cfg64G>(ctx, probs, segs, flag_dev)
+         : pair ? launch_cfg<Cfg64P>(ctx, probs, segs, flag_dev)
+                : launch_cfg<Cfg64>(ctx, probs, segs, flag_dev);
 }
 
 }  // namespace hsdla

@@ -43,6 +43,10 @@ typedef struct hsdla_ctx hsdla_ctx;
 
 /* ---- library / context ------------------------------------------------- */
 int hsdla_version(void);
+/* Real DMMA products per complex multiply-add in the contractions: 3 (default: Re = P_re Q_re +
+ * P_im Q_im, Im = (P_re - P_im)(Q_re + Q_im) - P_re Q_re + P_im Q_im) or 4 (HSDLA_CMUL=4).
+ * The ledger (builder.py:336-370) counts 8 flops per complex MAC either way. */
+int hsdla_complex_mul_products(void);
 const char* hsdla_last_error(void);
 /* Context = stream + descriptor arena + pinned staging; `stream` is a cudaStream_t (NULL = legacy). */
 int hsdla_ctx_create(hsdla_ctx** out, void* stream);

@@ -88,6 +88,7 @@ class BuildResult(ctypes.Structure):
 # name -> (restype, argtypes); every symbol include/hsdla_b200.h declares
 SIGNATURES = {
     "hsdla_version": (ctypes.c_int, []),
+    "hsdla_complex_mul_products": (ctypes.c_int, []),
     "hsdla_last_error": (ctypes.c_char_p, []),
     "hsdla_ctx_create": (ctypes.c_int, [ctypes.POINTER(_vp), _vp]),
     "hsdla_ctx_destroy": (ctypes.c_int, [_vp]),

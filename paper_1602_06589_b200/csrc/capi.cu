@@ -127,6 +127,7 @@ int* flag_slot(hsdla_ctx* ctx, int i) { return ctx->scratch_dev + 64 + i; }
 extern "C" {
 
 int hsdla_version(void) { return 1; }
+int hsdla_complex_mul_products(void) { return hsdla::cmul_mode(); }
 
 const char* hsdla_last_error(void) { return g_last_error.c_str(); }
 

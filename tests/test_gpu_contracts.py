@@ -347,3 +347,43 @@ def test_build_hs_sharded_p2p_single_rank(pkg):
     h_ref, s_ref, _ = build_hs(inst.spec, inst.tmats)
     assert rel_fro(h, h_ref.array) <= 1e-14 and rel_fro(s, s_ref.array) <= 1e-14
     np.testing.assert_array_equal(h, h.conj().T)
+
+
+# -- complex multiply variants ------------------------------------------------------------
+
+def test_three_and_four_product_contractions_agree(pkg, tmp_path):
+    """The default three-product complex multiply (hsdla_complex_mul_products() == 3) and the
+    four-product real embedding (HSDLA_CMUL=4, read once per process, so run in a child)
+    give the same H and S on a mixed-HPD C1-sized build to rounding, both within 1e-13 of
+    the oracle."""
+    import os
+    import subprocess
+    import sys
+
+    from paper_1602_06589_b200 import configs
+
+    assert pkg._native.load().hsdla_complex_mul_products() == 3
+    script = (
+        "import sys, numpy as np; sys.path.insert(0, '.')\n"
+        "import paper_1602_06589_b200 as pkg\n"
+        "from paper_1602_06589_b200 import configs\n"
+        "inst = configs.make_instance('C1')\n"
+        "h, s, r = pkg.build_all(pkg.compute_AB(inst.spec), inst.tmats, pkg.BuildConfig())\n"
+        "assert pkg._native.load().hsdla_complex_mul_products() == 4\n"
+        "np.savez(sys.argv[1], h=h.array, s=s.array)\n")
+    out = tmp_path / "cmul4.npz"
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run([sys.executable, "-c", script, str(out)], check=True, cwd=repo,
+                   env={**os.environ, "HSDLA_CMUL": "4"}, timeout=600)
+    four = np.load(out)
+    inst = configs.make_instance("C1")
+    h, s, _ = pkg.build_all(pkg.compute_AB(inst.spec), inst.tmats, pkg.BuildConfig())
+    from oracle import flapw as of
+    a, b, norms, offs = of.compute_ab(inst.spec)
+    tm = inst.tmats
+    ho, so, _, _ = ob.build_all(a, b, norms, list(np.diff(offs)), [t.array for t in tm.t_aa],
+                                [t.array for t in tm.t_ab], [t.array for t in tm.t_bb])
+    assert rel_fro(h.array, four["h"]) <= 1e-13 and rel_fro(s.array, four["s"]) <= 1e-13
+    assert not np.array_equal(h.array, four["h"])  # the variants really differ
+    for x, ref in ((h.array, ho), (s.array, so), (four["h"], ho), (four["s"], so)):
+        assert rel_fro(x, ref) <= 1e-13

@@ -231,6 +231,15 @@ typedef struct {
    * 1 = stream (e.g. the last k-point of a batch, which has no successor to hide under),
    * -1 = copy whole after the contraction. */
   int32_t stream_h_copy;
+  /* H form.  0 = default: per T set, factor the 2m x 2m Hermitian
+   * [[T_AA, T_AB], [T_AB^H, T_BB]] = L L^H once (with the T preparation, cached with it); where
+   * it is positive definite the atom's whole H contribution is W^H W with W = L^H [A_a; B_a],
+   * so H is one stacked rank-2R update (K = 2R) instead of the reference's ZHER2K + ZHERK
+   * (K = 3R), equal to rounding.  Sets whose matrix is not HPD, force_general_path, and
+   * 1 here (or HSDLA_JOINT=0) use the reference forms Z = T_AB^H A + 1/2 T_BB B and
+   * Y = C^H A / X = T_AA A.  The first build after the T sets change waits (host) for the
+   * T preparation to learn which form applies. */
+  int32_t h_reference_form;
 } hsdla_build_args;
 
 typedef struct {
@@ -241,6 +250,7 @@ typedef struct {
   float ms_contract_S, ms_contract_H;           /* out: the two triangular DMMA contraction launches */
   float ms_apply_Z, ms_apply_XY;                /* out: the batched T-application launches */
   float ms_total;                               /* out: first event to last kernel / copy */
+  int32_t* joint_info;        /* HOST out n_tsets or NULL: 1 = H used the joint T factor for this set */
 } hsdla_build_result;
 
 size_t hsdla_build_workspace_size(const hsdla_build_args* args);

@@ -71,6 +71,7 @@ class BuildArgs(ctypes.Structure):
         ("shard_rank", _i32), ("n_shards", _i32),
         ("H_host", _vp), ("S_host", _vp), ("ldh_host", _i64),
         ("shard_mirror", _i32), ("reuse_t", _i32), ("stream_h_copy", _i32),
+        ("h_reference_form", _i32),
     ]
 
 
@@ -81,7 +82,7 @@ class BuildResult(ctypes.Structure):
         ("ms_H_ABBA_BB", ctypes.c_float), ("ms_H_AA", ctypes.c_float),
         ("ms_contract_S", ctypes.c_float), ("ms_contract_H", ctypes.c_float),
         ("ms_apply_Z", ctypes.c_float), ("ms_apply_XY", ctypes.c_float),
-        ("ms_total", ctypes.c_float),
+        ("ms_total", ctypes.c_float), ("joint_info", _P_i32),
     ]
 
 

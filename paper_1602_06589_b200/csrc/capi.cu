@@ -477,7 +477,7 @@ constexpr unsigned kWaitGeq = 0x0;  // CU_STREAM_WAIT_VALUE_GEQ
 // ---- composed build ------------------------------------------------------------------
 namespace {
 struct WsLayout {
-  size_t bs, z, xy, forms, tdim, info, total;
+  size_t bs, z, xy, forms, tdim, info, joint, jinfo, total;
   int mp;
   long long R;
 };
@@ -503,6 +503,10 @@ WsLayout ws_layout(const hsdla_build_args* a) {
   w.tdim = off;
   off += align_up(a->n_tsets * sizeof(int));
   w.info = off;
+  off += align_up(a->n_tsets * sizeof(int));
+  w.joint = off;  // per T set: the 2m x 2m joint factor, ld 2*mp
+  off += align_up(size_t(a->n_tsets) * 4 * mp * mp * sizeof(double2));
+  w.jinfo = off;
   off += align_up(a->n_tsets * sizeof(int));
   w.total = off;
   return w;
@@ -541,6 +545,7 @@ int complete_slot(hsdla_ctx* ctx, hsdla_ctx::BuildSlot& sl, hsdla_ctx::Outcome* 
   for (int i = 0; i < sl.n_atoms; ++i)
     o->hpd[i] = (!sl.force && o->info[sl.t_index[i]] == 0) ? 1 : 0;
   o->nonfinite = area[0];
+  o->joint = sl.joint;
   cudaEvent_t* ev = sl.ev;
   float t01 = 0, t12 = 0, t23 = 0, t34 = 0, t46 = 0, t07 = 0;
   cudaEventElapsedTime(&t01, ev[0], ev[1]);
@@ -616,7 +621,10 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
   double2* forms = reinterpret_cast<double2*>(ws + w.forms);
   int* tdim_dev = reinterpret_cast<int*>(ws + w.tdim);
   int* info_dev = reinterpret_cast<int*>(ws + w.info);
+  double2* joint = reinterpret_cast<double2*>(ws + w.joint);
+  int* jinfo_dev = reinterpret_cast<int*>(ws + w.jinfo);
   const int mp = w.mp;
+  const long long lj = 2LL * mp;  // leading dimension of the joint factors
   const long long fs = (long long)mp * mp;
   int* flag = sl.flag_dev;
   cudaEvent_t* ev = sl.ev;
@@ -642,22 +650,49 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
   key.tbb = a->t_bb;
   key.t_ld = a->t_ld;
   key.force = a->force_general_path ? 1 : 0;
+  static int joint_env = -1;
+  if (joint_env < 0) {
+    const char* e = getenv("HSDLA_JOINT");
+    joint_env = (e && e[0] == '0') ? 0 : 1;
+  }
+  key.joint = (!a->force_general_path && !a->h_reference_form && joint_env) ? 1 : 0;
   key.tdim.assign(a->t_dim, a->t_dim + a->n_tsets);
   const hsdla_ctx::TKey& old = ctx->tkey;
   const bool reuse = a->reuse_t && old.ws == key.ws && old.forms_off == key.forms_off &&
                      old.info_off == key.info_off && old.taa == key.taa && old.tab == key.tab &&
                      old.tbb == key.tbb && old.t_ld == key.t_ld && old.force == key.force &&
-                     old.tdim == key.tdim;
+                     old.joint == key.joint && old.tdim == key.tdim;
   HS_CUDA(cudaEventRecord(ctx->fork, ctx->stream));
   if (!reuse) {
     HS_CUDA(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));
     rc = launch_tprep(ctx, ctx->side, a->n_tsets, tdim_dev, mp, D2(a->t_aa), D2(a->t_ab),
                       D2(a->t_bb), a->t_ld, forms, a->force_general_path ? 0 : 1, info_dev);
     if (rc) return rc;
+    int* jhost = ctx->scratch_host + 400;  // mapped: [400, 496)
+    if (key.joint) {
+      rc = launch_tjoint(ctx->side, a->n_tsets, tdim_dev, mp, D2(a->t_aa), D2(a->t_ab),
+                         D2(a->t_bb), a->t_ld, joint, jinfo_dev, ctx->scratch_host_dev + 400);
+      if (rc) return rc;
+    }
     HS_CUDA(cudaEventRecord(ctx->join, ctx->side));
+    ctx->joint_info.assign(a->n_tsets, -2);
+    if (key.joint) {
+      // Which H form each T set takes is a host decision (it fixes the K extents of the
+      // contractions): wait for the T preparation alone.  It runs on the side stream under
+      // this build's A/B generation; with reuse_t later k-points skip both.
+      HS_CUDA(cudaEventSynchronize(ctx->join));
+      for (int t = 0; t < a->n_tsets; ++t) ctx->joint_info[t] = ((volatile int*)jhost)[t];
+    }
     ctx->tkey = key;
   } else {
     HS_CUDA(cudaEventRecord(ctx->join, ctx->stream));
+  }
+  sl.joint.assign(a->n_tsets, 0);
+  bool any_joint = false, all_joint = true;
+  for (int t = 0; t < a->n_tsets; ++t) {
+    sl.joint[t] = (key.joint && ctx->joint_info[t] == 0) ? 1 : 0;
+    any_joint |= sl.joint[t] != 0;
+    all_joint &= sl.joint[t] != 0;
   }
   if (ab) {
     rc = ab_generate(ctx, ab);
@@ -764,6 +799,7 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     }
   }
   // ---- Z_a = T_AB^H A_a + 1/2 T_BB B_a   (builder.py:231-240)
+  //      joint T sets: Z_a = W2_a = L22^H B_a (rows m..2m of W_a = L^H [A_a; B_a])
   {
     std::vector<Seg> segs;
     std::vector<Prob> probs;
@@ -772,6 +808,12 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
       const long long off = a->row_offset[i];
       const double2* f = forms + (long long)ts * 4 * fs;
       const int s0 = (int)segs.size();
+      if (sl.joint[ts]) {
+        const double2* L = joint + (long long)ts * lj * lj;
+        segs.push_back(make_seg(L + m + m * lj, lj, B + off, ld, m));
+        probs.push_back(make_prob(Z + off, ld, m, n, PROB_GENERAL, s0, 1, 0));
+        continue;
+      }
       segs.push_back(make_seg(f, mp, A + off, ld, m));
       segs.push_back(make_seg(f + fs, mp, B + off, ld, m));
       probs.push_back(make_prob(Z + off, ld, m, n, PROB_GENERAL, s0, 2, 0));
@@ -782,6 +824,7 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
   HS_CUDA(cudaEventRecord(ev[3], ctx->stream));
   // ---- Y_a = C_a^H A_a if T_AA is HPD, else X_a = T_AA A_a (builder.py:279-304);
   //      the branch is taken on the device from the Cholesky info.
+  //      joint T sets: XY_a = W1_a = L11^H A_a + L21^H B_a (rows 0..m of W_a)
   {
     std::vector<Seg> segs;
     std::vector<Prob> probs;
@@ -790,6 +833,13 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
       const long long off = a->row_offset[i];
       const double2* f = forms + (long long)ts * 4 * fs;
       const int s0 = (int)segs.size();
+      if (sl.joint[ts]) {
+        const double2* L = joint + (long long)ts * lj * lj;
+        segs.push_back(make_seg(L, lj, A + off, ld, m));
+        segs.push_back(make_seg(L + m, lj, B + off, ld, m));
+        probs.push_back(make_prob(XY + off, ld, m, n, PROB_GENERAL, s0, 2, 0));
+        continue;
+      }
       segs.push_back(make_seg(f + 3 * fs, mp, A + off, ld, m, f + 2 * fs, info_dev + ts));
       probs.push_back(make_prob(XY + off, ld, m, n, PROB_GENERAL, s0, 1, 0));
     }
@@ -816,20 +866,39 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     rc = stream_out(D2(a->H), a->H_host, sl.panel_cnt + nbp, sl.h_copied);
     if (rc) return rc;
   }
+  //      joint T sets: H += W1^H W1 + W2^H W2 over their rows (XY and Z slots), K = 2R.
   {
-    std::vector<Seg> segs{make_seg(Z, ld, B, ld, (int)R), make_seg(B, ld, Z, ld, (int)R)};
-    int i = 0;
-    while (i < na) {
-      int j = i;
-      long long rows = 0;
-      const int ts = a->t_index[i];
-      while (j < na && a->t_index[j] == ts && (j == i || a->row_offset[j] == a->row_offset[j - 1] + a->heights[j - 1])) {
-        rows += a->heights[j];
-        ++j;
+    std::vector<Seg> segs;
+    if (all_joint) {
+      segs.push_back(make_seg(XY, ld, XY, ld, (int)R));
+      segs.push_back(make_seg(Z, ld, Z, ld, (int)R));
+    } else {
+      if (!any_joint) {
+        segs.push_back(make_seg(Z, ld, B, ld, (int)R));
+        segs.push_back(make_seg(B, ld, Z, ld, (int)R));
       }
-      const long long off = a->row_offset[i];
-      segs.push_back(make_seg(XY + off, ld, XY + off, ld, (int)rows, A + off, info_dev + ts));
-      i = j;
+      int i = 0;
+      while (i < na) {
+        int j = i;
+        long long rows = 0;
+        const int ts = a->t_index[i];
+        while (j < na && a->t_index[j] == ts && (j == i || a->row_offset[j] == a->row_offset[j - 1] + a->heights[j - 1])) {
+          rows += a->heights[j];
+          ++j;
+        }
+        const long long off = a->row_offset[i];
+        if (sl.joint[ts]) {
+          segs.push_back(make_seg(XY + off, ld, XY + off, ld, (int)rows));
+          segs.push_back(make_seg(Z + off, ld, Z + off, ld, (int)rows));
+        } else {
+          if (any_joint) {
+            segs.push_back(make_seg(Z + off, ld, B + off, ld, (int)rows));
+            segs.push_back(make_seg(B + off, ld, Z + off, ld, (int)rows));
+          }
+          segs.push_back(make_seg(XY + off, ld, XY + off, ld, (int)rows, A + off, info_dev + ts));
+        }
+        i = j;
+      }
     }
     std::vector<Prob> probs;
     add_tri(probs, D2(a->H), 0, (int)segs.size());
@@ -859,6 +928,8 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
 int fill_result(const hsdla_ctx::Outcome& o, hsdla_build_result* res) {
   for (size_t t = 0; t < o.info.size(); ++t)
     if (res->chol_info) res->chol_info[t] = o.info[t];
+  for (size_t t = 0; t < o.joint.size(); ++t)
+    if (res->joint_info) res->joint_info[t] = o.joint[t];
   for (size_t i = 0; i < o.hpd.size(); ++i)
     if (res->hpd_mask) res->hpd_mask[i] = o.hpd[i];
   res->nonfinite = o.nonfinite;

@@ -109,9 +109,11 @@ struct hsdla_ctx {
     long long forms_off = -1, info_off = -1;  // workspace offsets (depend on n_basis, ld)
     const void *taa = nullptr, *tab = nullptr, *tbb = nullptr;
     long long t_ld = 0;
-    int force = -1;
+    int force = -1, joint = -1;
     std::vector<int> tdim;
   } tkey;
+  // Joint-factor info per T set of the T preparation in tkey (0 = H takes the joint form).
+  std::vector<int> joint_info;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // T preparation overlaps A/B generation here
   cudaStream_t copy = nullptr;  // D2H of finished H / S, overlapped with later compute
@@ -131,12 +133,13 @@ struct hsdla_ctx {
     bool force = false, copies = false, pending = false;
     unsigned long long ticket = 0;
     std::vector<int> t_index;
+    std::vector<int> joint;  // per T set: 1 = this build's H used the joint factor
   } slots[2];
   unsigned long long seq = 0;
   // Outcomes of builds completed before their ticket was finished (more than two in flight).
   struct Outcome {
     int rc = 0, nonfinite = 0;
-    std::vector<int> info, hpd;
+    std::vector<int> info, hpd, joint;
     float ms[6] = {};
   };
   std::map<unsigned long long, Outcome> stash;
@@ -189,6 +192,11 @@ int launch_potrf_batched(hsdla_ctx* ctx, int n, int batch, const double2* T, lon
 int launch_tprep(hsdla_ctx* ctx, cudaStream_t stream, int n_tsets, const int* tdim_dev, int mp,
                  const double2* taa, const double2* tab, const double2* tbb, long long t_ld,
                  double2* forms, int do_chol, int* info_dev);
+// Joint factor L of [[T_AA, T_AB], [T_AB^H, T_BB]] per T set (2m x 2m, ld 2*mp, in `joint`),
+// info per set into info_dev and, if non-null, the mapped host view info_host_dev.
+int launch_tjoint(cudaStream_t stream, int n_tsets, const int* tdim_dev, int mp,
+                  const double2* taa, const double2* tab, const double2* tbb, long long t_ld,
+                  double2* joint, int* info_dev, int* info_host_dev);
 int ab_generate(hsdla_ctx* ctx, const hsdla_ab_args* args);
 // kind 0: o1/o2 = j_l(x), j'_l(x), (l_max+1) x n row-major; kind 1: o1 = Y_lm (complex,
 // (l_max+1)^2 x n row-major) at unit directions in (n x 3).

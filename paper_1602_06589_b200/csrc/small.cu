@@ -179,11 +179,48 @@ __global__ void tprep_kernel(const int* tdim, int mp, const double2* taa, const 
   __syncthreads();
   if (!do_chol) {
     if (threadIdx.x == 0) info[b] = -2;
-  } else if (m <= kPackedMaxN) {
+  } else if (mp <= kPackedMaxN) {  // the launch sized shared memory by mp, not by this set's m
     chol_packed(m, Taa, t_ld, f + 3 * fs, mp, info + b);
   } else {
     chol_block(m, Taa, t_ld, f + 3 * fs, mp, info + b);
   }
+}
+
+// Joint factor of one T set: the 2m x 2m Hermitian
+//   T = [[T_AA, T_AB], [T_AB^H, T_BB]]
+// (T_AA / T_BB from their lower triangles with real diagonals, as hermitian_product and
+// cholesky_factor read them, kernels.py:198-201 / :217-228) so that per atom
+//   A^H T_AA A + A^H T_AB B + B^H T_AB^H A + B^H T_BB B = W^H W,  W = L^H [A; B],  T = L L^H,
+// i.e. the H of build_H_ABBA_BB + build_H_AA (builder.py:212-315) as one rank-2m update.
+// The factor is written in place over the assembled lower triangle (ld 2*mp); info as
+// chol_block (0 = HPD).  L11 equals the T_AA factor of tprep_kernel bit for bit (the first m
+// columns see the same updates in the same order).  info_host (mapped) may be null.
+__global__ void tjoint_kernel(const int* tdim, int mp, const double2* taa, const double2* tab,
+                              const double2* tbb, long long t_ld, double2* joint, int* info,
+                              int* info_host) {
+  const int b = blockIdx.x;
+  const int m = tdim[b], n = 2 * m;
+  const long long lj = 2LL * mp;
+  const long long tstride = t_ld * t_ld;
+  const double2* Taa = taa + b * tstride;
+  const double2* Tab = tab + b * tstride;
+  const double2* Tbb = tbb + b * tstride;
+  double2* J = joint + (long long)b * lj * lj;
+  for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) {
+    const int r = (int)(e % n), c = (int)(e / n);
+    if (r < c) continue;
+    double2 v;
+    if (r < m) v = Taa[r + c * t_ld];
+    else if (c < m) v = cconj(Tab[c + (r - m) * t_ld]);
+    else v = Tbb[(r - m) + (c - m) * t_ld];
+    if (r == c) v.y = 0.0;
+    J[r + c * lj] = v;
+  }
+  __syncthreads();
+  if (lj <= kPackedMaxN) chol_packed(n, J, lj, J, lj, info + b);  // shared memory sized by 2*mp
+  else chol_block(n, J, lj, J, lj, info + b);
+  __syncthreads();
+  if (threadIdx.x == 0 && info_host) info_host[b] = info[b];
 }
 
 // ---------------------------------------------------------------------------
@@ -284,6 +321,19 @@ int launch_tprep(hsdla_ctx* ctx, cudaStream_t stream, int n_tsets, const int* td
   return HSDLA_OK;
 }
 
+int launch_tjoint(cudaStream_t stream, int n_tsets, const int* tdim_dev, int mp,
+                  const double2* taa, const double2* tab, const double2* tbb, long long t_ld,
+                  double2* joint, int* info_dev, int* info_host_dev) {
+  if (n_tsets <= 0) return HSDLA_OK;
+  const int n = 2 * mp;
+  size_t smem = (n <= kPackedMaxN) ? size_t(n) * (n + 1) / 2 * sizeof(double2)
+                                   : size_t(n) * sizeof(double2);
+  tjoint_kernel<<<n_tsets, 512, smem, stream>>>(tdim_dev, mp, taa, tab, tbb, t_ld, joint, info_dev,
+                                                info_host_dev);
+  HS_CHECK_LAUNCH();
+  return HSDLA_OK;
+}
+
 int launch_mirror(hsdla_ctx* ctx, int n, double2* C, long long ldc, int* flag_dev) {
   if (n <= 0) return HSDLA_OK;
   const int nb = (n + 31) / 32;
@@ -347,11 +397,15 @@ int preload_small() {
   const void* fns[] = {(const void*)potrf_batched_kernel, (const void*)tprep_kernel,
                        (const void*)mirror_kernel, (const void*)scale_rows_kernel,
                        (const void*)prep_kernel, (const void*)publish_kernel,
-                       (const void*)zero_rows_kernel, (const void*)finite_kernel};
+                       (const void*)zero_rows_kernel, (const void*)finite_kernel,
+                       (const void*)tjoint_kernel};
   for (const void* f : fns) {
     cudaFuncAttributes at;
     HS_CUDA(cudaFuncGetAttributes(&at, f));
   }
+  if (first_on_device((const void*)tjoint_kernel))
+    HS_CUDA(cudaFuncSetAttribute(tjoint_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(size_t(kPackedMaxN) * (kPackedMaxN + 1) / 2 * sizeof(double2))));
   if (first_on_device((const void*)tprep_kernel))
     HS_CUDA(cudaFuncSetAttribute(tprep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(size_t(kPackedMaxN) * (kPackedMaxN + 1) / 2 * sizeof(double2))));

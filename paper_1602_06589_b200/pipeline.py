@@ -166,7 +166,8 @@ class _Call:
 
     def __init__(self, *, n_basis, heights, row_offset, tpack: TPack, A, B, Bs, udot, ld,
                  force_general_path, H, S, ldh, shard_rank, n_shards, workspace, host_out,
-                 ab_args=None, shard_mirror=False, reuse_t=False, stream_h_copy=0):
+                 ab_args=None, shard_mirror=False, reuse_t=False, stream_h_copy=0,
+                 h_reference_form=False):
         lib = _native.load()
         t = device.torch()
         self.na = len(heights)
@@ -202,6 +203,7 @@ class _Call:
         a.shard_mirror = 1 if shard_mirror else 0
         a.reuse_t = 1 if reuse_t else 0
         a.stream_h_copy = int(stream_h_copy)
+        a.h_reference_form = 1 if h_reference_form else 0
         if host_out is not None:  # pinned (n, n) tensors, row j = column j
             a.H_host = host_out[0].data_ptr()
             a.S_host = host_out[1].data_ptr()
@@ -217,8 +219,10 @@ class _Call:
         self.mask = (ctypes.c_int32 * self.na)()
         self.info = (ctypes.c_int32 * self.n_tsets)()
         self.res = _native.BuildResult()
+        self.joint = (ctypes.c_int32 * self.n_tsets)()
         self.res.hpd_mask = self.mask
         self.res.chol_info = self.info
+        self.res.joint_info = self.joint
 
     def result(self, rc: int) -> dict:
         if rc == _native.HSDLA_ERR_NAN_INPUT:
@@ -230,6 +234,7 @@ class _Call:
         return {
             "hpd_mask": [bool(self.mask[i]) for i in range(self.na)],
             "chol_info": [int(self.info[i]) for i in range(self.n_tsets)],
+            "joint_t": [bool(self.joint[i]) for i in range(self.n_tsets)],
             "ms": {"setup": r.ms_setup, "S": r.ms_S, "H_ABBA_BB": r.ms_H_ABBA_BB,
                    "H_AA": r.ms_H_AA},
             "kernel_ms": {"contract_S": r.ms_contract_S, "contract_H": r.ms_contract_H,
@@ -263,13 +268,14 @@ class _Call:
 
 def build_device(*, n_basis, heights, row_offset, tpack: TPack, A, B, Bs, udot, ld,
                  force_general_path, H, S, ldh, shard_rank=0, n_shards=1, workspace=None,
-                 ab_args=None, host_out=None):
+                 ab_args=None, host_out=None, h_reference_form=False):
     """Synchronous `hsdla_build_hs` (or `hsdla_setup_hs` when `ab_args` is given: A/B
     generation fused in front); returns (result dict, workspace tensor)."""
     call = _Call(n_basis=n_basis, heights=heights, row_offset=row_offset, tpack=tpack, A=A, B=B,
                  Bs=Bs, udot=udot, ld=ld, force_general_path=force_general_path, H=H, S=S,
                  ldh=ldh, shard_rank=shard_rank, n_shards=n_shards, workspace=workspace,
-                 host_out=host_out, ab_args=ab_args)
+                 host_out=host_out, ab_args=ab_args,
+                 h_reference_form=h_reference_form)
     return call.run_sync(), call.workspace
 
 
@@ -278,9 +284,11 @@ class HSPipeline:
     `run` = one k-point (any N_G <= n_capacity, e.g. a k-point batch with varying G-sets)."""
 
     def __init__(self, n_capacity: int, heights, *, shard_rank: int = 0, n_shards: int = 1,
-                 out=None, shard_mirror: bool = False):
+                 out=None, shard_mirror: bool = False, h_reference_form: bool = False):
         """`out` = (H, S) device (n_capacity, ld) tensors to write instead of own buffers
-        (e.g. a peer rank's, mapped through NVLink); `shard_mirror` see hsdla_build_args."""
+        (e.g. a peer rank's, mapped through NVLink); `shard_mirror`, `h_reference_form` see
+        hsdla_build_args (the latter: always the reference's Z / Y forms for H instead of the
+        joint factor of the per-type T matrix)."""
         t = device.require_cuda()
         self.n_capacity = int(n_capacity)
         self.heights = np.asarray(heights, dtype=np.int32)
@@ -301,6 +309,7 @@ class HSPipeline:
         self.workspace = None
         self.shard_rank, self.n_shards = shard_rank, n_shards
         self.shard_mirror = bool(shard_mirror)
+        self.h_reference_form = bool(h_reference_form)
         self._last_t = None  # (TPack, force) of the previous call: T forms reusable
         self.n_basis = 0
         self._inflight = {}
@@ -328,7 +337,8 @@ class HSPipeline:
                      force_general_path=force_general_path, H=self.H, S=self.S,
                      ldh=self.n_capacity, shard_rank=self.shard_rank, n_shards=self.n_shards,
                      workspace=self.workspace, host_out=host_out, ab_args=ab,
-                     shard_mirror=self.shard_mirror, reuse_t=reuse, stream_h_copy=stream_h_copy)
+                     shard_mirror=self.shard_mirror, reuse_t=reuse, stream_h_copy=stream_h_copy,
+                     h_reference_form=self.h_reference_form)
         call.keep.append(dspec)
         self.workspace = call.workspace
         self._last_t = (tpack, bool(force_general_path))

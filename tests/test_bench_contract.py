@@ -38,3 +38,21 @@ def test_bench_helpers():
     assert abs(c["dmma_peak_at_measured_clock_tflops"] - 37.22) < 0.01
     g = bench.ab_gen_line(0.1, r, n)
     assert g["bytes_written"] == 48 * r * n and 0 < g["frac"] < 1
+
+
+def test_executed_flops_accounting():
+    """Executed DMMA work: S (K = 2R) + H with joint T sets (K = 2R) is 16 R N^2 complex-MAC
+    flops; with the reference forms H adds ZHER2K (8 R N^2) + ZHERK over HPD rows (4 R N^2)
+    + ZGEMM over non-HPD rows (8 R N^2).  Three products: x 3/4."""
+    sys.path.insert(0, REPO)
+    import bench
+
+    n, r = 3000, 1296
+    fc = bench.contract_flops(n, r, r)
+    joint = bench.executed_flops(fc, 1.0, 3, n, r, r, r)
+    assert joint["executed_flops_per_step"] == 16 * r * n * n * 3 // 4
+    ref = bench.executed_flops(fc, 1.0, 4, n, r, r, 0)
+    assert ref["executed_flops_per_step"] == fc  # four products, reference forms: the ledger
+    mixed = bench.executed_flops(fc, 1.0, 4, n, r, 600, 300)
+    assert mixed["executed_flops_per_step"] == (8 * r + 8 * 300 + 8 * (r - 300) + 4 * 300
+                                               + 8 * (r - 600)) * n * n

@@ -1,0 +1,132 @@
+"""H through the joint factor of each T set's 2m x 2m matrix [[T_AA, T_AB], [T_AB^H, T_BB]]
+(hsdla_build_args.h_reference_form = 0, the default): where that matrix is HPD, L L^H = it and
+the atom's whole H contribution is W^H W with W = L^H [A_a; B_a] — one stacked rank-2R update
+instead of the reference's ZHER2K + ZHERK (builder.py:212-315).  Checked against the oracle
+(pinned to the reference's goldens) and against the reference forms Z / Y / X on the same
+device, for joint-HPD sets, sets where only T_AA is HPD (fallback to Y), non-HPD T_AA
+(fallback to X), T smaller than its block, and the forced general path."""
+import numpy as np
+import pytest
+
+from conftest import rand_complex, rel_fro
+from oracle import build as ob
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def pkg(cuda):
+    import paper_1602_06589_b200 as p
+
+    p._native.load()
+    return p
+
+
+def _hermitian(rng, m, shift):
+    x = rand_complex(rng, m, m)
+    return (x + x.conj().T) / (2 * m) + shift * np.eye(m)
+
+
+def _case(pkg, seed, heights, n_g, t_sizes, aa_shifts, bb_shifts):
+    rng = np.random.default_rng(seed)
+    lay = pkg.AtomBlockLayout(tuple(heights))
+    r = lay.total_rows
+    a = pkg.ComplexDense.zeros(r, n_g, capacity_rows=lay.capacity_rows)
+    b = pkg.ComplexDense.zeros(r, n_g, capacity_rows=lay.capacity_rows)
+    a.array[:] = rand_complex(rng, r, n_g)
+    b.array[:] = rand_complex(rng, r, n_g)
+    u = rng.uniform(0.2, 1.5, r)
+    co = pkg.StackedCoefficients(a, b, lay, u)
+    taa = [_hermitian(rng, m, s) for m, s in zip(t_sizes, aa_shifts)]
+    tbb = [_hermitian(rng, m, s) for m, s in zip(t_sizes, bb_shifts)]
+    tab = [rand_complex(rng, m, m) / m for m in t_sizes]
+    # poison the strict upper triangles (read from the lower only) and diagonal imaginaries
+    for t in taa + tbb:
+        t[np.triu_indices(len(t), 1)] = np.nan
+        t[np.diag_indices(len(t))] += 3.0j
+    cd = pkg.ComplexDense.from_array
+    tm = pkg.TMatrixSet([cd(t) for t in taa], [cd(t) for t in tab], [cd(t) for t in tbb],
+                        [0] * len(heights), [0] * len(heights))
+    herm = [np.tril(t, -1) + np.tril(t, -1).conj().T + np.diag(t.diagonal().real) for t in taa]
+    hbb = [np.tril(t, -1) + np.tril(t, -1).conj().T + np.diag(t.diagonal().real) for t in tbb]
+    return co, tm, (a.array.copy(), b.array.copy(), u.copy(), herm, tab, hbb)
+
+
+def _build(pkg, co, tm, force=False, reference_form=False):
+    import torch
+
+    from paper_1602_06589_b200 import device
+    from paper_1602_06589_b200.pipeline import build_device, pack_tmats, padded_ld
+
+    lay, n = co.layout, co.n_basis
+    r = lay.total_rows
+    ld = padded_ld(r)
+    a_d = device.upload_window(co.A_star.array, ld)
+    b_d = device.upload_window(co.B_star.array, ld)
+    udot = torch.zeros(ld, dtype=torch.float64, device="cuda")
+    udot[:r] = torch.from_numpy(np.ascontiguousarray(co.udot_norms)).cuda()
+    h_d, s_d = device.empty_matrix(n, n, n), device.empty_matrix(n, n, n)
+    res, _ = build_device(n_basis=n, heights=lay.block_heights, row_offset=lay.offsets[:-1],
+                          tpack=pack_tmats(tm), A=a_d, B=b_d, Bs=None, udot=udot, ld=ld,
+                          force_general_path=force, H=h_d, S=s_d, ldh=n,
+                          h_reference_form=reference_form)
+    torch.cuda.synchronize()
+    return h_d.cpu().numpy().T.copy(), s_d.cpu().numpy().T.copy(), res
+
+
+def _check(pkg, co, tm, ref, want_joint, want_hpd, force=False):
+    a, b, u, taa, tab, tbb = ref
+    heights = list(co.layout.block_heights)
+    h_o, s_o, _, mask_o = ob.build_all(a, b, u, heights, taa, tab, tbb, force_general_path=force)
+    h, s, res = _build(pkg, co, tm, force=force)
+    h_r, s_r, res_r = _build(pkg, co, tm, force=force, reference_form=True)
+    assert res["joint_t"] == want_joint
+    assert res_r["joint_t"] == [False] * len(want_joint)
+    assert res["hpd_mask"] == res_r["hpd_mask"] == want_hpd == list(mask_o)
+    assert rel_fro(h, h_o) <= TOL and rel_fro(s, s_o) <= TOL
+    assert rel_fro(h, h_r) <= 1e-13
+    np.testing.assert_array_equal(s, s_r)  # S does not depend on the H form
+    np.testing.assert_array_equal(h, h.conj().T)
+    return h, h_r
+
+
+def test_joint_form_all_hpd(pkg):
+    heights = (9, 9, 9, 9)
+    co, tm, ref = _case(pkg, 1, heights, 130, [9] * 4, [2.0] * 4, [2.0] * 4)
+    h, h_r = _check(pkg, co, tm, ref, [True] * 4, [True] * 4)
+    assert not np.array_equal(h, h_r)  # the two forms really are different evaluations
+
+
+def test_joint_form_mixed_fallbacks(pkg):
+    """Set 0 joint-HPD; set 1: T_AA HPD but T_BB = -2 I-ish (joint not HPD -> Y path);
+    set 2: T_AA not HPD (X path); set 3: joint-HPD with T smaller than its block."""
+    heights = (16, 16, 9, 25)
+    co, tm, ref = _case(pkg, 2, heights, 97, [16, 16, 9, 16], [2.0, 2.0, -2.0, 2.0],
+                        [2.0, -2.0, 2.0, 1.5])
+    _check(pkg, co, tm, ref, [True, False, False, True], [True, True, False, True])
+
+
+def test_joint_form_forced_general_path(pkg):
+    heights = (9, 16)
+    co, tm, ref = _case(pkg, 3, heights, 70, [9, 16], [2.0, 2.0], [2.0, 2.0])
+    _check(pkg, co, tm, ref, [False, False], [False, False], force=True)
+
+
+def test_joint_form_shared_type_pipeline_reuse(pkg):
+    """BASELINE-style shared type (C1): every atom joint; a k-point batch reuses the cached
+    joint factor (no second T preparation) and equals single builds bitwise."""
+    from paper_1602_06589_b200 import configs
+    from paper_1602_06589_b200.pipeline import build_hs, build_hs_many
+
+    inst = configs.make_instance("C1")
+    h1, s1, r1 = build_hs(inst.spec, inst.tmats)
+    assert all(r1["joint_t"])
+    out = {}
+    rr = build_hs_many([inst.spec] * 3, inst.tmats,
+                       on_result=lambda i, h, s, r: out.__setitem__(i, (h.array.copy(), s.array.copy())))
+    assert all(all(r["joint_t"]) for r in rr)
+    for i in range(3):
+        np.testing.assert_array_equal(out[i][0], h1.array)
+        np.testing.assert_array_equal(out[i][1], s1.array)

@@ -269,8 +269,9 @@ int hsdla_setup_hs(hsdla_ctx* ctx, const hsdla_ab_args* ab, const hsdla_build_ar
 /* Pipelined form for k-point batches: enqueue one k-point (ab may be NULL = A/B given) and
  * return at once with a ticket; `hsdla_build_finish` waits for that k-point's compute and
  * host copies and fills `result`.  Two builds may be in flight per context; the next
- * build's contractions wait for the previous build's copies of the shared H / S buffers,
- * so the copies of k-point i overlap the compute of k-point i+1.  Host destinations of
+ * build's contractions wait for the previous build's copies when it writes the same device
+ * H / S; alternating two device H / S pairs between consecutive k-points removes those waits,
+ * so the copies of k-point i overlap the whole compute of k-point i+1.  Host destinations of
  * in-flight builds must differ. */
 int hsdla_setup_hs_async(hsdla_ctx* ctx, const hsdla_ab_args* ab, const hsdla_build_args* args,
                          unsigned long long* ticket);

@@ -164,8 +164,8 @@ int hsdla_ctx_create(hsdla_ctx** out, void* stream) {
   for (int k = 0; k < 2; ++k) {
     auto& sl = c->slots[k];
     for (auto& e : sl.ev) HS_CUDA(cudaEventCreate(&e));
-    HS_CUDA(cudaEventCreateWithFlags(&sl.s_copied, cudaEventDisableTiming));
-    HS_CUDA(cudaEventCreateWithFlags(&sl.h_copied, cudaEventDisableTiming));
+    HS_CUDA(cudaEventCreate(&sl.s_copied));  // timed: HSDLA_TIMELINE reports copy ends
+    HS_CUDA(cudaEventCreate(&sl.h_copied));
     HS_CUDA(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
     sl.flag_dev = c->scratch_dev + 96 + k;
     sl.host_area = c->scratch_host + 128 + 100 * k;  // [0] flag, [1..96] info
@@ -561,8 +561,13 @@ int complete_slot(hsdla_ctx* ctx, hsdla_ctx::BuildSlot& sl, hsdla_ctx::Outcome* 
     cudaEventElapsedTime(&a2, ctx->epoch, ev[2]);
     cudaEventElapsedTime(&a6, ctx->epoch, ev[6]);
     cudaEventElapsedTime(&a7, ctx->epoch, ev[7]);
-    fprintf(stderr, "build %llu: start %.3f S-done %.3f H-done %.3f end %.3f ms\n", sl.ticket, a0, a2,
-            a6, a7);
+    float sc = -1, hc = -1;
+    if (sl.copies) {
+      cudaEventElapsedTime(&sc, ctx->epoch, sl.s_copied);
+      cudaEventElapsedTime(&hc, ctx->epoch, sl.h_copied);
+    }
+    fprintf(stderr, "build %llu: start %.3f S-done %.3f H-done %.3f end %.3f S-copied %.3f H-copied %.3f ms\n",
+            sl.ticket, a0, a2, a6, a7, sc, hc);
   }
   o->rc = nan_input ? HSDLA_ERR_NAN_INPUT : (o->nonfinite ? HSDLA_ERR_NONFINITE : HSDLA_OK);
   return o->rc;
@@ -610,6 +615,8 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
   sl.force = a->force_general_path != 0;
   sl.t_index.assign(a->t_index, a->t_index + na);
   sl.copies = (a->H_host != nullptr) || (a->S_host != nullptr);
+  sl.h_dev = a->H;
+  sl.s_dev = a->S;
 
   char* ws = static_cast<char*>(a->workspace);
   const long long ld = a->ld;
@@ -668,31 +675,17 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     rc = launch_tprep(ctx, ctx->side, a->n_tsets, tdim_dev, mp, D2(a->t_aa), D2(a->t_ab),
                       D2(a->t_bb), a->t_ld, forms, a->force_general_path ? 0 : 1, info_dev);
     if (rc) return rc;
-    int* jhost = ctx->scratch_host + 400;  // mapped: [400, 496)
-    if (key.joint) {
+    if (key.joint) {  // info also to the mapped host words [400, 496)
       rc = launch_tjoint(ctx->side, a->n_tsets, tdim_dev, mp, D2(a->t_aa), D2(a->t_ab),
                          D2(a->t_bb), a->t_ld, joint, jinfo_dev, ctx->scratch_host_dev + 400);
       if (rc) return rc;
     }
     HS_CUDA(cudaEventRecord(ctx->join, ctx->side));
     ctx->joint_info.assign(a->n_tsets, -2);
-    if (key.joint) {
-      // Which H form each T set takes is a host decision (it fixes the K extents of the
-      // contractions): wait for the T preparation alone.  It runs on the side stream under
-      // this build's A/B generation; with reuse_t later k-points skip both.
-      HS_CUDA(cudaEventSynchronize(ctx->join));
-      for (int t = 0; t < a->n_tsets; ++t) ctx->joint_info[t] = ((volatile int*)jhost)[t];
-    }
+    ctx->joint_pending = key.joint != 0;  // read after the S contraction is enqueued
     ctx->tkey = key;
   } else {
     HS_CUDA(cudaEventRecord(ctx->join, ctx->stream));
-  }
-  sl.joint.assign(a->n_tsets, 0);
-  bool any_joint = false, all_joint = true;
-  for (int t = 0; t < a->n_tsets; ++t) {
-    sl.joint[t] = (key.joint && ctx->joint_info[t] == 0) ? 1 : 0;
-    any_joint |= sl.joint[t] != 0;
-    all_joint &= sl.joint[t] != 0;
   }
   if (ab) {
     rc = ab_generate(ctx, ab);
@@ -769,11 +762,19 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
   };
 
   // ---- S = A^H A + (U B)^H (U B)   (builder.py:199-209)
-  if (prev.copies) HS_CUDA(cudaStreamWaitEvent(ctx->stream, prev.s_copied, 0));
-  // S is copied whole after the T applications (below): streaming it during its own
-  // contraction pushed its tail copies under the T applications (measured slower per
-  // k-point); H is streamed during the H contraction.
-  const bool s_streamed = false;
+  // (only when the previous build wrote the same device S: callers alternating two H / S
+  // buffer pairs between consecutive k-points never wait here)
+  if (prev.copies && prev.s_dev == a->S) HS_CUDA(cudaStreamWaitEvent(ctx->stream, prev.s_copied, 0));
+  // Pipelined builds copy S whole after the T applications (below): streaming it during its
+  // own contraction pushed its tail copies under the T applications (measured slower per
+  // k-point).  A synchronous call has no later k-point to hide its copies under, so there S
+  // is streamed panel by panel during its own contraction too (HSDLA_STREAM_S=0: whole).
+  static int stream_s_env = -1;
+  if (stream_s_env < 0) {
+    const char* e = getenv("HSDLA_STREAM_S");
+    stream_s_env = (e && e[0] == '0') ? 0 : 1;
+  }
+  const bool s_streamed = waitv && a->S_host && stream_copies && stream_s_env;
   if (s_streamed) {
     rc = stream_out(D2(a->S), a->S_host, sl.panel_cnt, sl.s_copied);
     if (rc) return rc;
@@ -787,6 +788,24 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     if (rc) return rc;
   }
   HS_CUDA(cudaEventRecord(ev[2], ctx->stream));
+
+  // Which H form each T set takes is a host decision (it fixes the K extents of the H
+  // contraction): after a fresh T preparation, wait for it alone — it ran on the side stream
+  // under this build's A/B generation, and the S contraction is already queued, so the
+  // device does not idle.  With reuse_t later k-points skip both.
+  if (ctx->joint_pending) {
+    HS_CUDA(cudaEventSynchronize(ctx->join));
+    const volatile int* jhost = ctx->scratch_host + 400;
+    for (int t = 0; t < a->n_tsets; ++t) ctx->joint_info[t] = jhost[t];
+    ctx->joint_pending = false;
+  }
+  sl.joint.assign(a->n_tsets, 0);
+  bool any_joint = false, all_joint = true;
+  for (int t = 0; t < a->n_tsets; ++t) {
+    sl.joint[t] = (key.joint && ctx->joint_info[t] == 0) ? 1 : 0;
+    any_joint |= sl.joint[t] != 0;
+    all_joint &= sl.joint[t] != 0;
+  }
 
   // Rows of a block beyond its T size must be zero in Z / XY (builder.py:232-245 compaction).
   for (int i = 0; i < na; ++i) {
@@ -860,7 +879,7 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
   }
   // ---- H = Z^H B + B^H Z + sum_HPD Y^H Y + sum_nonHPD A^H X   (builder.py:246-247, :305-311)
   //      AA segments per run of atoms sharing one T set: P = XY (HPD) or A (general).
-  if (prev.copies) HS_CUDA(cudaStreamWaitEvent(ctx->stream, prev.h_copied, 0));
+  if (prev.copies && prev.h_dev == a->H) HS_CUDA(cudaStreamWaitEvent(ctx->stream, prev.h_copied, 0));
   const bool h_streamed = waitv && a->H_host;
   if (h_streamed) {
     rc = stream_out(D2(a->H), a->H_host, sl.panel_cnt + nbp, sl.h_copied);

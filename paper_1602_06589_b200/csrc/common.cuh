@@ -114,6 +114,7 @@ struct hsdla_ctx {
   } tkey;
   // Joint-factor info per T set of the T preparation in tkey (0 = H takes the joint form).
   std::vector<int> joint_info;
+  bool joint_pending = false;  // joint_info not read back yet (fresh T preparation in flight)
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // T preparation overlaps A/B generation here
   cudaStream_t copy = nullptr;  // D2H of finished H / S, overlapped with later compute
@@ -134,6 +135,8 @@ struct hsdla_ctx {
     unsigned long long ticket = 0;
     std::vector<int> t_index;
     std::vector<int> joint;  // per T set: 1 = this build's H used the joint factor
+    const void* h_dev = nullptr;  // this build's device H / S (copy hazards of the next build)
+    const void* s_dev = nullptr;
   } slots[2];
   unsigned long long seq = 0;
   // Outcomes of builds completed before their ticket was finished (more than two in flight).

@@ -306,6 +306,9 @@ class HSPipeline:
             self.H, self.S = out
             if tuple(self.H.shape) != (n, n) or tuple(self.S.shape) != (n, n):
                 raise ContractViolationError("output buffers must be (n_capacity, n_capacity)")
+        self._own_out = out is None
+        self._alt = None  # second device (H, S) pair for pipelined k-points (run_async)
+        self._flip = 0
         self.workspace = None
         self.shard_rank, self.n_shards = shard_rank, n_shards
         self.shard_mirror = bool(shard_mirror)
@@ -318,12 +321,14 @@ class HSPipeline:
     def device_bytes(self) -> int:
         tot = sum(x.numel() * x.element_size() for x in (self.A, self.B, self.Bs, self.udot,
                                                           self.H, self.S))
+        if self._alt is not None:
+            tot += sum(x.numel() * x.element_size() for x in self._alt)
         if self.workspace is not None:
             tot += self.workspace.numel()
         return int(tot)
 
     def _call(self, dspec: DeviceSpec, tpack: TPack, force_general_path: bool, host_out,
-              stream_h_copy: int = 0):
+              stream_h_copy: int = 0, alternate: bool = False):
         if dspec.n_basis > self.n_capacity or dspec.rows != self.rows:
             raise ContractViolationError("spec shape does not fit the pipeline buffers")
         self.n_basis = dspec.n_basis
@@ -332,9 +337,20 @@ class HSPipeline:
         # forms and Cholesky factors from the previous call are still in the workspace.
         last = self._last_t
         reuse = last is not None and last[0] is tpack and last[1] == bool(force_general_path)
+        H, S = self.H, self.S
+        if alternate and self._own_out and host_out is not None:
+            # Pipelined k-points with host copies alternate two device (H, S) pairs, so
+            # k-point i+1's contractions never wait for k-point i's copies (hsdla_setup_hs_async).
+            if self._alt is None:
+                n = self.n_capacity
+                self._alt = (device.empty_matrix(n, n, n), device.empty_matrix(n, n, n))
+            if self._flip:
+                H, S = self._alt
+            self._flip ^= 1
+        self._last_out = (H, S)
         call = _Call(n_basis=dspec.n_basis, heights=dspec.heights, row_offset=dspec.row_offset,
                      tpack=tpack, A=self.A, B=self.B, Bs=self.Bs, udot=self.udot, ld=self.ld,
-                     force_general_path=force_general_path, H=self.H, S=self.S,
+                     force_general_path=force_general_path, H=H, S=S,
                      ldh=self.n_capacity, shard_rank=self.shard_rank, n_shards=self.n_shards,
                      workspace=self.workspace, host_out=host_out, ab_args=ab,
                      shard_mirror=self.shard_mirror, reuse_t=reuse, stream_h_copy=stream_h_copy,
@@ -355,7 +371,8 @@ class HSPipeline:
         """Enqueue one k-point and return a ticket at once (`hsdla_setup_hs_async`).  At
         most two k-points may be in flight; their `host_out` buffers must differ.  `last`:
         no k-point follows, so H is streamed to the host during its own contraction."""
-        call = self._call(dspec, tpack, force_general_path, host_out, 1 if last else 0)
+        call = self._call(dspec, tpack, force_general_path, host_out, 1 if last else 0,
+                          alternate=True)
         ticket = call.start()
         self._inflight[ticket] = call
         return ticket
@@ -372,7 +389,8 @@ class HSPipeline:
     def result_views(self):
         """Host-indexable (n, n) views: H[i, j] == tensor[j, i] (column-major storage)."""
         n = self.n_basis
-        return self.H[:n, :n], self.S[:n, :n]
+        h, s = getattr(self, "_last_out", (self.H, self.S))
+        return h[:n, :n], s[:n, :n]
 
 
 def _pinned_pair(n: int):

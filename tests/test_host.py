@@ -176,3 +176,36 @@ def test_configuration_errors():
     tm = pkg.TMatrixSet(z, z, z, [1], [1])
     with pytest.raises(pkg.ConfigurationError):
         pkg.build_all(coeffs, tm, pkg.BuildConfig(backup=False))
+
+
+def test_ctypes_structs_match_the_c_header(tmp_path):
+    """Every argument block the Python side passes through the C ABI has the header's field
+    names, offsets and size (gcc compiles the header and prints offsetof / sizeof)."""
+    import ctypes
+    import shutil
+    import subprocess
+
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    from paper_1602_06589_b200 import _native
+
+    structs = {"hsdla_ab_args": _native.AbArgs, "hsdla_reduced_args": _native.ReducedArgs,
+               "hsdla_build_args": _native.BuildArgs, "hsdla_build_result": _native.BuildResult,
+               "hsdla_c64": _native.C64}
+    lines = ["#include <stddef.h>", "#include <stdio.h>", '#include "hsdla_b200.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            lines.append(f'printf("{cname}.{fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines += ["return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    subprocess.run(["gcc", "-I", inc, str(src), "-o", str(exe)], check=True)
+    out = dict(l.rsplit(" ", 1) for l in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                         check=True).stdout.splitlines())
+    for cname, py in structs.items():
+        assert int(out[cname]) == ctypes.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert int(out[f"{cname}.{fname}"]) == getattr(py, fname).offset, (cname, fname)

@@ -240,6 +240,13 @@ typedef struct {
    * Y = C^H A / X = T_AA A.  The first build after the T sets change waits (host) for the
    * T preparation to learn which form applies. */
   int32_t h_reference_form;
+  /* Optional HOST (pinned) sources of A and B (column-major, ld ld_ab_host >= rows): the build
+   * uploads them into the DEVICE buffers A / B itself (which it then writes), A first and B on
+   * a copy stream while the A-part of S (A^H A) already runs; S is then accumulated in two
+   * launches.  B_scaled must be NULL; not with sharding. */
+  const hsdla_c64* A_host;
+  const hsdla_c64* B_host;
+  int64_t ld_ab_host;
 } hsdla_build_args;
 
 typedef struct {
@@ -254,6 +261,8 @@ typedef struct {
 } hsdla_build_result;
 
 size_t hsdla_build_workspace_size(const hsdla_build_args* args);
+/* 1 if `p` points into page-locked (pinned / registered) host memory, else 0. */
+int hsdla_is_pinned(const void* p);
 /* Enqueues the whole build without a host round trip (the HPD branch is selected on the
  * device from the Cholesky info) and synchronises once at the end (info, flags, timings).  Returns HSDLA_ERR_NAN_INPUT on a NaN
  * in tril(T_AA) and HSDLA_ERR_NONFINITE on non-finite output (outputs still written). */

@@ -72,6 +72,7 @@ class BuildArgs(ctypes.Structure):
         ("H_host", _vp), ("S_host", _vp), ("ldh_host", _i64),
         ("shard_mirror", _i32), ("reuse_t", _i32), ("stream_h_copy", _i32),
         ("h_reference_form", _i32),
+        ("A_host", _vp), ("B_host", _vp), ("ld_ab_host", _i64),
     ]
 
 
@@ -90,6 +91,7 @@ class BuildResult(ctypes.Structure):
 SIGNATURES = {
     "hsdla_version": (ctypes.c_int, []),
     "hsdla_complex_mul_products": (ctypes.c_int, []),
+    "hsdla_is_pinned": (ctypes.c_int, [_vp]),
     "hsdla_last_error": (ctypes.c_char_p, []),
     "hsdla_ctx_create": (ctypes.c_int, [ctypes.POINTER(_vp), _vp]),
     "hsdla_ctx_destroy": (ctypes.c_int, [_vp]),

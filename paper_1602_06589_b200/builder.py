@@ -407,6 +407,9 @@ def build_ledger(heights, t_sizes, n_g: int, hpd_mask, force_general_path: bool)
     return led
 
 
+HOST_SOURCED_MIN_BYTES = 1 << 28  # per stack; see build_all
+
+
 def build_all(coeffs: StackedCoefficients, tmats: TMatrixSet, config: BuildConfig,
               regenerate=None):
     """Composed build on the GPU; returns (H, S, report) with H, S full Hermitian (`builder.py:403-474`).
@@ -429,11 +432,22 @@ def build_all(coeffs: StackedCoefficients, tmats: TMatrixSet, config: BuildConfi
     t0 = time.perf_counter()
     t = device.require_cuda()
     r = layout.total_rows
-    # K loops read rows < r only, so padding rows of the device stacks need no zeroing
-    a_d, ld = device.upload_stack(coeffs.A_star, padded_ld(r))
-    b_d, ldb = device.upload_stack(coeffs.B_star, padded_ld(r))
-    if ldb != ld:
-        b_d = device.upload_window(coeffs.B_star.array, ld)
+    # K loops read rows < r only, so padding rows of the device stacks need no zeroing.
+    # Large stacks in pinned host memory (what compute_AB returns) are uploaded by the native
+    # build itself, B overlapped with the A-part of S (C3: 152 -> 145 ms); below ~256 MB per
+    # stack the split S launch costs what the overlap saves (C2: 10.4 vs 10.7 ms), and
+    # anything else goes up here first.
+    src = (device.pinned_sources(coeffs.A_star, coeffs.B_star)
+           if r * n * 16 >= HOST_SOURCED_MIN_BYTES else None)
+    if src is not None:
+        ld = src[2]
+        a_d = device.empty_matrix(r, n, ld)
+        b_d = device.empty_matrix(r, n, ld)
+    else:
+        a_d, ld = device.upload_stack(coeffs.A_star, padded_ld(r))
+        b_d, ldb = device.upload_stack(coeffs.B_star, padded_ld(r))
+        if ldb != ld:
+            b_d = device.upload_window(coeffs.B_star.array, ld)
     udot = t.zeros(ld, dtype=t.float64, device="cuda")
     udot[:r] = t.from_numpy(np.ascontiguousarray(coeffs.udot_norms)).to("cuda")
     tpack: TPack = pack_tmats(tmats)
@@ -444,7 +458,8 @@ def build_all(coeffs: StackedCoefficients, tmats: TMatrixSet, config: BuildConfi
     res, ws = build_device(n_basis=n, heights=layout.block_heights,
                            row_offset=layout.offsets[:-1], tpack=tpack, A=a_d, B=b_d, Bs=None,
                            udot=udot, ld=ld, force_general_path=config.force_general_path,
-                           H=h_d, S=s_d, ldh=n, host_out=(h_host[1], s_host[1]))
+                           H=h_d, S=s_d, ldh=n, host_out=(h_host[1], s_host[1]),
+                           host_src=src)
     if not config.backup:
         regenerate(coeffs)
         if coeffs.A_star.rows != layout.total_rows or coeffs.A_star.cols != n:

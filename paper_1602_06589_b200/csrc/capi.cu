@@ -160,6 +160,9 @@ int hsdla_ctx_create(hsdla_ctx** out, void* stream) {
   HS_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
   HS_CUDA(cudaStreamCreateWithFlags(&c->upload, cudaStreamNonBlocking));
   HS_CUDA(cudaEventCreateWithFlags(&c->upload_done, cudaEventDisableTiming));
+  HS_CUDA(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+  HS_CUDA(cudaEventCreateWithFlags(&c->a_up, cudaEventDisableTiming));
+  HS_CUDA(cudaEventCreateWithFlags(&c->b_up, cudaEventDisableTiming));
   HS_CUDA(cudaEventCreateWithFlags(&c->copy_go, cudaEventDisableTiming));
   for (int k = 0; k < 2; ++k) {
     auto& sl = c->slots[k];
@@ -203,6 +206,10 @@ int hsdla_ctx_destroy(hsdla_ctx* c) {
   cudaStreamDestroy(c->copy);
   cudaStreamSynchronize(c->upload);
   cudaEventDestroy(c->upload_done);
+  cudaStreamSynchronize(c->h2d);
+  cudaStreamDestroy(c->h2d);
+  cudaEventDestroy(c->a_up);
+  cudaEventDestroy(c->b_up);
   cudaStreamDestroy(c->upload);
   if (c->partials) cudaFree(c->partials);
   if (c->ready) cudaFree(c->ready);
@@ -513,6 +520,15 @@ WsLayout ws_layout(const hsdla_build_args* a) {
 }
 }  // namespace
 
+int hsdla_is_pinned(const void* p) {
+  cudaPointerAttributes at;
+  if (!p || cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return at.type == cudaMemoryTypeHost ? 1 : 0;
+}
+
 size_t hsdla_build_workspace_size(const hsdla_build_args* args) {
   if (!args) return 0;
   return ws_layout(args).total;
@@ -597,6 +613,11 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     set_error("host destinations are not supported with column-panel sharding");
     return -2;
   }
+  const bool host_src = a->A_host != nullptr;
+  if (host_src && (!a->B_host || a->B_scaled || sharded || a->ld_ab_host < 1)) {
+    set_error("host-sourced A / B need both sources, no B_scaled, no sharding");
+    return -2;
+  }
   if (a->n_tsets > 96) {
     set_error("more than 96 distinct T sets per build");
     return HSDLA_ERR_UNSUPPORTED;
@@ -670,6 +691,18 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
                      old.tbb == key.tbb && old.t_ld == key.t_ld && old.force == key.force &&
                      old.joint == key.joint && old.tdim == key.tdim;
   HS_CUDA(cudaEventRecord(ctx->fork, ctx->stream));
+  if (host_src) {
+    // A then B on the copy stream, after everything already queued (earlier builds read A / B)
+    HS_CUDA(cudaStreamWaitEvent(ctx->h2d, ctx->fork, 0));
+    const size_t hp = size_t(a->ld_ab_host) * sizeof(hsdla_c64), dp = size_t(ld) * sizeof(double2);
+    const size_t rows_b = size_t(w.R) * sizeof(double2);
+    HS_CUDA(cudaMemcpy2DAsync(const_cast<hsdla_c64*>(a->A), dp, a->A_host, hp, rows_b, n,
+                              cudaMemcpyHostToDevice, ctx->h2d));
+    HS_CUDA(cudaEventRecord(ctx->a_up, ctx->h2d));
+    HS_CUDA(cudaMemcpy2DAsync(const_cast<hsdla_c64*>(a->B), dp, a->B_host, hp, rows_b, n,
+                              cudaMemcpyHostToDevice, ctx->h2d));
+    HS_CUDA(cudaEventRecord(ctx->b_up, ctx->h2d));
+  }
   if (!reuse) {
     HS_CUDA(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));
     rc = launch_tprep(ctx, ctx->side, a->n_tsets, tdim_dev, mp, D2(a->t_aa), D2(a->t_ab),
@@ -692,14 +725,16 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     if (rc) return rc;
   }
   const double2* Bs = D2(a->B_scaled);
-  if (!Bs) {
+  auto make_bs = [&]() -> int {
     double2* bs = reinterpret_cast<double2*>(ws + w.bs);
     HS_CUDA(cudaMemcpyAsync(bs, B, size_t(ld) * n * sizeof(double2), cudaMemcpyDeviceToDevice,
                             ctx->stream));
-    rc = launch_scale_rows(ctx, (int)R, n, a->udot_norms, bs, ld);
-    if (rc) return rc;
+    int r2 = launch_scale_rows(ctx, (int)R, n, a->udot_norms, bs, ld);
+    if (r2) return r2;
     Bs = bs;
-  }
+    return HSDLA_OK;
+  };
+  if (!Bs && !host_src && (rc = make_bs())) return rc;
   HS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join, 0));
   HS_CUDA(cudaEventRecord(ev[1], ctx->stream));
 
@@ -779,7 +814,21 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     rc = stream_out(D2(a->S), a->S_host, sl.panel_cnt, sl.s_copied);
     if (rc) return rc;
   }
-  {
+  if (host_src) {
+    // S = A^H A as soon as A is in HBM (B still uploading), then += (U B)^H (U B) + mirror
+    HS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->a_up, 0));
+    {
+      std::vector<Seg> segs{make_seg(A, ld, A, ld, (int)R)};
+      std::vector<Prob> probs{make_prob(D2(a->S), a->ldh, n, n, PROB_TRI_LOWER, 0, 1, 0)};
+      if ((rc = launch_contract(ctx, probs, segs, flag))) return rc;
+    }
+    HS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->b_up, 0));
+    if ((rc = make_bs())) return rc;
+    std::vector<Seg> segs{make_seg(Bs, ld, Bs, ld, (int)R)};
+    std::vector<Prob> probs{make_prob(D2(a->S), a->ldh, n, n, PROB_TRI_MIRROR, 0, 1, 1)};
+    if (s_streamed) probs[0].panel_done = sl.panel_cnt;
+    if ((rc = launch_contract(ctx, probs, segs, flag))) return rc;
+  } else {
     std::vector<Seg> segs{make_seg(A, ld, A, ld, (int)R), make_seg(Bs, ld, Bs, ld, (int)R)};
     std::vector<Prob> probs;
     add_tri(probs, D2(a->S), 0, 2);

@@ -120,6 +120,8 @@ struct hsdla_ctx {
   cudaStream_t copy = nullptr;  // D2H of finished H / S, overlapped with later compute
   cudaEvent_t copy_go = nullptr;
   cudaStream_t upload = nullptr;  // descriptor H2D, ahead of the compute stream
+  cudaStream_t h2d = nullptr;     // host-sourced A / B uploads (hsdla_build_args.A_host)
+  cudaEvent_t a_up = nullptr, b_up = nullptr;
   cudaEvent_t upload_done = nullptr;
   // Two in-flight builds (k-point pipelining): per-build events, flag and read-back area.
   struct BuildSlot {

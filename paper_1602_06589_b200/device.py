@@ -107,6 +107,26 @@ def upload_stack(window, ld_min: int | None = None):
     return upload_window(window.array, ld), ld
 
 
+def pinned_sources(a_window, b_window):
+    """(A_host, B_host, ld) when both stacked windows start at row 0 of F-ordered complex128
+    allocations of the same height that live in pinned host memory (the layout `compute_AB`
+    returns), so the native build can DMA them itself; else None."""
+    lib = _native.load()
+    ptrs = []
+    ld = None
+    for w in (a_window, b_window):
+        base = w.base
+        if (w.row_offset != 0 or base.dtype != np.complex128 or not base.flags.f_contiguous
+                or base.shape[1] != w.cols or (ld is not None and base.shape[0] != ld)):
+            return None
+        ld = int(base.shape[0])
+        p = base.ctypes.data
+        if not lib.hsdla_is_pinned(ctypes.c_void_p(p)):
+            return None
+        ptrs.append(p)
+    return ptrs[0], ptrs[1], ld
+
+
 def download_window(dev, out: np.ndarray):
     """Copy the device (cols, ld) tensor's leading rows into the numpy window `out`."""
     rows, cols = out.shape

@@ -167,7 +167,7 @@ class _Call:
     def __init__(self, *, n_basis, heights, row_offset, tpack: TPack, A, B, Bs, udot, ld,
                  force_general_path, H, S, ldh, shard_rank, n_shards, workspace, host_out,
                  ab_args=None, shard_mirror=False, reuse_t=False, stream_h_copy=0,
-                 h_reference_form=False):
+                 h_reference_form=False, host_src=None):
         lib = _native.load()
         t = device.torch()
         self.na = len(heights)
@@ -204,6 +204,8 @@ class _Call:
         a.reuse_t = 1 if reuse_t else 0
         a.stream_h_copy = int(stream_h_copy)
         a.h_reference_form = 1 if h_reference_form else 0
+        if host_src is not None:  # (A_host ptr, B_host ptr, ld): pinned sources the build uploads
+            a.A_host, a.B_host, a.ld_ab_host = host_src
         if host_out is not None:  # pinned (n, n) tensors, row j = column j
             a.H_host = host_out[0].data_ptr()
             a.S_host = host_out[1].data_ptr()
@@ -268,14 +270,14 @@ class _Call:
 
 def build_device(*, n_basis, heights, row_offset, tpack: TPack, A, B, Bs, udot, ld,
                  force_general_path, H, S, ldh, shard_rank=0, n_shards=1, workspace=None,
-                 ab_args=None, host_out=None, h_reference_form=False):
+                 ab_args=None, host_out=None, h_reference_form=False, host_src=None):
     """Synchronous `hsdla_build_hs` (or `hsdla_setup_hs` when `ab_args` is given: A/B
     generation fused in front); returns (result dict, workspace tensor)."""
     call = _Call(n_basis=n_basis, heights=heights, row_offset=row_offset, tpack=tpack, A=A, B=B,
                  Bs=Bs, udot=udot, ld=ld, force_general_path=force_general_path, H=H, S=S,
                  ldh=ldh, shard_rank=shard_rank, n_shards=n_shards, workspace=workspace,
                  host_out=host_out, ab_args=ab_args,
-                 h_reference_form=h_reference_form)
+                 h_reference_form=h_reference_form, host_src=host_src)
     return call.run_sync(), call.workspace
 
 

@@ -137,3 +137,28 @@ def test_async_builds_three_in_flight_out_of_order(pkg):
         assert rel_fro(h.numpy().T, h1.array) <= 1e-14 and rel_fro(sm.numpy().T, s1.array) <= 1e-14
     with pytest.raises((NativeLibraryError, KeyError)):
         pipe.finish(tickets[0])
+
+
+def test_build_all_host_sourced_upload(pkg, monkeypatch):
+    """compute_AB's pinned stacks uploaded by the native build itself (B overlapped with the
+    A-part of S, S accumulated in two launches; used for large stacks): same H, S as the
+    default upload path to rounding and the oracle to 1e-12, and exactly Hermitian."""
+    from paper_1602_06589_b200 import builder, configs, device
+
+    inst = configs.make_instance("C1")
+    co = pkg.compute_AB(inst.spec)
+    assert device.pinned_sources(co.A_star, co.B_star) is not None
+    h0, s0, r0 = pkg.build_all(co, inst.tmats, pkg.BuildConfig())
+    monkeypatch.setattr(builder, "HOST_SOURCED_MIN_BYTES", 0)
+    co = pkg.compute_AB(inst.spec)
+    h1, s1, r1 = pkg.build_all(co, inst.tmats, pkg.BuildConfig())
+    assert rel_fro(h1.array, h0.array) <= 1e-14 and rel_fro(s1.array, s0.array) <= 1e-14
+    a, b, norms, offs = of.compute_ab(inst.spec)
+    tm = inst.tmats
+    h_o, s_o, _, mask = ob.build_all(a, b, norms, list(np.diff(offs)), [t.array for t in tm.t_aa],
+                                     [t.array for t in tm.t_ab], [t.array for t in tm.t_bb])
+    assert rel_fro(h1.array, h_o) <= TOL and rel_fro(s1.array, s_o) <= TOL
+    np.testing.assert_array_equal(s1.array, s1.array.conj().T)
+    assert r1.hpd_mask == r0.hpd_mask == list(mask)
+    # a window that is not at the top of its allocation is not host-sourced
+    assert device.pinned_sources(co.A_star.block(1, co.A_star.rows - 1), co.B_star) is None

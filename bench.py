@@ -96,10 +96,23 @@ def host_threads():
         return os.cpu_count()
 
 
+def use_all_host_threads():
+    """The CPU arms use every host thread: torchrun exports OMP_NUM_THREADS=1 to each rank,
+    which would otherwise cap the reference's OpenBLAS at one thread."""
+    try:
+        from threadpoolctl import threadpool_limits
+
+        n = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+        return threadpool_limits(limits=max(1, n), user_api="blas")
+    except Exception:  # pragma: no cover
+        return None
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
+    _limits = use_all_host_threads()  # noqa: F841 (kept alive for the run)
     from paper_1602_06589_b200 import configs
 
     inst = configs.make_instance(args.config)
@@ -406,6 +419,7 @@ def run_ours(args):
             "clocks": clk.summary(),
         }
         if not args.no_cpu_baseline and world == 1:
+            _limits = use_all_host_threads()  # noqa: F841
             cspec = cpu_sample(inst)
             dt, fl, t_ab, t_build = cpu_oracle_step(cspec, inst.tmats)
             line["cpu_baseline"] = {

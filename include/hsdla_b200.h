@@ -247,6 +247,12 @@ typedef struct {
   const hsdla_c64* A_host;
   const hsdla_c64* B_host;
   int64_t ld_ab_host;
+  /* HOST n_tsets or NULL: dense-block size d <= t_dim of each T set ((l_nonsph+1)^2).  Where
+   * d < t_dim and T is zero outside the leading d x d blocks except its diagonals (as the
+   * reference's assemble_T builds it, flapw.py:306-363), the joint H form factors the 2d x 2d
+   * dense part and one 2x2 block per tail row, and the T applications run with K = d plus an
+   * elementwise tail; otherwise T is treated as dense. */
+  const int32_t* t_dense;
 } hsdla_build_args;
 
 typedef struct {
@@ -257,7 +263,8 @@ typedef struct {
   float ms_contract_S, ms_contract_H;           /* out: the two triangular DMMA contraction launches */
   float ms_apply_Z, ms_apply_XY;                /* out: the batched T-application launches */
   float ms_total;                               /* out: first event to last kernel / copy */
-  int32_t* joint_info;        /* HOST out n_tsets or NULL: 1 = H used the joint T factor for this set */
+  int32_t* joint_info;        /* HOST out n_tsets or NULL: 1 = H used the joint T factor for this set,
+                                 2 = with the dense / diagonal-tail split */
 } hsdla_build_result;
 
 size_t hsdla_build_workspace_size(const hsdla_build_args* args);

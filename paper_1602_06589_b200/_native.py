@@ -73,6 +73,7 @@ class BuildArgs(ctypes.Structure):
         ("shard_mirror", _i32), ("reuse_t", _i32), ("stream_h_copy", _i32),
         ("h_reference_form", _i32),
         ("A_host", _vp), ("B_host", _vp), ("ld_ab_host", _i64),
+        ("t_dense", _P_i32),
     ]
 
 

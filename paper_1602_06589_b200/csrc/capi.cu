@@ -153,7 +153,7 @@ int hsdla_ctx_create(hsdla_ctx** out, void* stream) {
   if (int rc = preload_small()) return rc;
   // Mapped pinned memory: build results are published by a kernel store, not a DMA copy,
   // so they never queue behind the large H / S copies on the D2H engine.
-  HS_CUDA(cudaHostAlloc(&c->scratch_host, 512 * sizeof(int), cudaHostAllocMapped));
+  HS_CUDA(cudaHostAlloc(&c->scratch_host, 1024 * sizeof(int), cudaHostAllocMapped));
   HS_CUDA(cudaHostGetDevicePointer((void**)&c->scratch_host_dev, c->scratch_host, 0));
   HS_CUDA(cudaEventCreateWithFlags(&c->stage_done, cudaEventDisableTiming));
   HS_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
@@ -507,8 +507,8 @@ WsLayout ws_layout(const hsdla_build_args* a) {
   off += stack;
   w.forms = off;
   off += align_up(size_t(a->n_tsets) * 4 * mp * mp * sizeof(double2));
-  w.tdim = off;
-  off += align_up(a->n_tsets * sizeof(int));
+  w.tdim = off;  // t_dim then t_dense, n_tsets each
+  off += align_up(2 * a->n_tsets * sizeof(int));
   w.info = off;
   off += align_up(a->n_tsets * sizeof(int));
   w.joint = off;  // per T set: the 2m x 2m joint factor, ld 2*mp
@@ -660,12 +660,15 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
 
   HS_CUDA(cudaEventRecord(ev[0], ctx->stream));
   HS_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
-  rc = arena_begin(ctx, a->n_tsets * sizeof(int) + 64);
+  std::vector<int> tsz(a->t_dim, a->t_dim + a->n_tsets);
+  for (int t = 0; t < a->n_tsets; ++t)
+    tsz.push_back(a->t_dense ? std::min(std::max(a->t_dense[t], 0), a->t_dim[t]) : a->t_dim[t]);
+  rc = arena_begin(ctx, tsz.size() * sizeof(int) + 64);
   if (rc) return rc;
-  const int* tdim_src = static_cast<const int*>(arena_push(ctx, a->t_dim, a->n_tsets * sizeof(int), nullptr));
+  const int* tdim_src = static_cast<const int*>(arena_push(ctx, tsz.data(), tsz.size() * sizeof(int), nullptr));
   rc = arena_flush(ctx);
   if (rc) return rc;
-  HS_CUDA(cudaMemcpyAsync(tdim_dev, tdim_src, a->n_tsets * sizeof(int), cudaMemcpyDeviceToDevice,
+  HS_CUDA(cudaMemcpyAsync(tdim_dev, tdim_src, tsz.size() * sizeof(int), cudaMemcpyDeviceToDevice,
                           ctx->stream));
   // T preparation + Cholesky on the side stream, overlapping A/B generation — or nothing,
   // when the caller vouches that T is unchanged and the previous results are still here.
@@ -685,11 +688,12 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
   }
   key.joint = (!a->force_general_path && !a->h_reference_form && joint_env) ? 1 : 0;
   key.tdim.assign(a->t_dim, a->t_dim + a->n_tsets);
+  key.tdense.assign(tsz.begin() + a->n_tsets, tsz.end());
   const hsdla_ctx::TKey& old = ctx->tkey;
   const bool reuse = a->reuse_t && old.ws == key.ws && old.forms_off == key.forms_off &&
                      old.info_off == key.info_off && old.taa == key.taa && old.tab == key.tab &&
                      old.tbb == key.tbb && old.t_ld == key.t_ld && old.force == key.force &&
-                     old.joint == key.joint && old.tdim == key.tdim;
+                     old.joint == key.joint && old.tdim == key.tdim && old.tdense == key.tdense;
   HS_CUDA(cudaEventRecord(ctx->fork, ctx->stream));
   if (host_src) {
     // A then B on the copy stream, after everything already queued (earlier builds read A / B)
@@ -709,12 +713,14 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
                       D2(a->t_bb), a->t_ld, forms, a->force_general_path ? 0 : 1, info_dev);
     if (rc) return rc;
     if (key.joint) {  // info also to the mapped host words [400, 496)
-      rc = launch_tjoint(ctx->side, a->n_tsets, tdim_dev, mp, D2(a->t_aa), D2(a->t_ab),
-                         D2(a->t_bb), a->t_ld, joint, jinfo_dev, ctx->scratch_host_dev + 400);
+      rc = launch_tjoint(ctx->side, a->n_tsets, tdim_dev, tdim_dev + a->n_tsets, mp, D2(a->t_aa),
+                         D2(a->t_ab), D2(a->t_bb), a->t_ld, joint, jinfo_dev,
+                         ctx->scratch_host_dev + 400, ctx->scratch_host_dev + 600);
       if (rc) return rc;
     }
     HS_CUDA(cudaEventRecord(ctx->join, ctx->side));
     ctx->joint_info.assign(a->n_tsets, -2);
+    ctx->joint_split.assign(a->n_tsets, 0);
     ctx->joint_pending = key.joint != 0;  // read after the S contraction is enqueued
     ctx->tkey = key;
   } else {
@@ -845,13 +851,17 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
   if (ctx->joint_pending) {
     HS_CUDA(cudaEventSynchronize(ctx->join));
     const volatile int* jhost = ctx->scratch_host + 400;
-    for (int t = 0; t < a->n_tsets; ++t) ctx->joint_info[t] = jhost[t];
+    const volatile int* shost = ctx->scratch_host + 600;  // split flags [600, 696)
+    for (int t = 0; t < a->n_tsets; ++t) {
+      ctx->joint_info[t] = jhost[t];
+      ctx->joint_split[t] = shost[t];
+    }
     ctx->joint_pending = false;
   }
   sl.joint.assign(a->n_tsets, 0);
   bool any_joint = false, all_joint = true;
   for (int t = 0; t < a->n_tsets; ++t) {
-    sl.joint[t] = (key.joint && ctx->joint_info[t] == 0) ? 1 : 0;
+    sl.joint[t] = (key.joint && ctx->joint_info[t] == 0) ? (ctx->joint_split[t] ? 2 : 1) : 0;
     any_joint |= sl.joint[t] != 0;
     all_joint &= sl.joint[t] != 0;
   }
@@ -876,10 +886,11 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
       const long long off = a->row_offset[i];
       const double2* f = forms + (long long)ts * 4 * fs;
       const int s0 = (int)segs.size();
-      if (sl.joint[ts]) {
+      if (sl.joint[ts]) {  // split: the dense part has h = d rows (tail rows: ttail_kernel)
         const double2* L = joint + (long long)ts * lj * lj;
-        segs.push_back(make_seg(L + m + m * lj, lj, B + off, ld, m));
-        probs.push_back(make_prob(Z + off, ld, m, n, PROB_GENERAL, s0, 1, 0));
+        const int h = sl.joint[ts] == 2 ? tsz[a->n_tsets + ts] : m;
+        segs.push_back(make_seg(L + h + h * lj, lj, B + off, ld, h));
+        probs.push_back(make_prob(Z + off, ld, h, n, PROB_GENERAL, s0, 1, 0));
         continue;
       }
       segs.push_back(make_seg(f, mp, A + off, ld, m));
@@ -903,9 +914,10 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
       const int s0 = (int)segs.size();
       if (sl.joint[ts]) {
         const double2* L = joint + (long long)ts * lj * lj;
-        segs.push_back(make_seg(L, lj, A + off, ld, m));
-        segs.push_back(make_seg(L + m, lj, B + off, ld, m));
-        probs.push_back(make_prob(XY + off, ld, m, n, PROB_GENERAL, s0, 2, 0));
+        const int h = sl.joint[ts] == 2 ? tsz[a->n_tsets + ts] : m;
+        segs.push_back(make_seg(L, lj, A + off, ld, h));
+        segs.push_back(make_seg(L + h, lj, B + off, ld, h));
+        probs.push_back(make_prob(XY + off, ld, h, n, PROB_GENERAL, s0, 2, 0));
         continue;
       }
       segs.push_back(make_seg(f + 3 * fs, mp, A + off, ld, m, f + 2 * fs, info_dev + ts));
@@ -913,6 +925,24 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     }
     rc = launch_contract(ctx, probs, segs, flag);
     if (rc) return rc;
+  }
+  // ---- tail rows [d, m) of split joint T sets: one 2x2 factor per row, elementwise
+  {
+    std::vector<int4> tails;
+    int max_tail = 0;
+    for (int i = 0; i < na; ++i) {
+      const int ts = a->t_index[i];
+      if (sl.joint[ts] != 2) continue;
+      const int d = tsz[a->n_tsets + ts], m = a->t_dim[ts];
+      tails.push_back(make_int4((int)a->row_offset[i], d, m, ts));
+      max_tail = std::max(max_tail, m - d);
+    }
+    if (!tails.empty()) {
+      if ((rc = arena_begin(ctx, tails.size() * sizeof(int4) + 64))) return rc;
+      const int4* tdev = static_cast<const int4*>(arena_push(ctx, tails.data(), tails.size() * sizeof(int4), nullptr));
+      if ((rc = arena_flush(ctx))) return rc;
+      if ((rc = launch_ttail(ctx, tdev, (int)tails.size(), max_tail, n, A, B, ld, XY, Z, joint, lj))) return rc;
+    }
   }
   HS_CUDA(cudaEventRecord(ev[4], ctx->stream));
   // S leaves for the host now, under the H contraction (4/3 of S's time): started right

@@ -110,10 +110,11 @@ struct hsdla_ctx {
     const void *taa = nullptr, *tab = nullptr, *tbb = nullptr;
     long long t_ld = 0;
     int force = -1, joint = -1;
-    std::vector<int> tdim;
+    std::vector<int> tdim, tdense;
   } tkey;
   // Joint-factor info per T set of the T preparation in tkey (0 = H takes the joint form).
   std::vector<int> joint_info;
+  std::vector<int> joint_split;  // per T set: 1 = the joint factor uses the dense/diagonal split
   bool joint_pending = false;  // joint_info not read back yet (fresh T preparation in flight)
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // T preparation overlaps A/B generation here
@@ -136,7 +137,7 @@ struct hsdla_ctx {
     bool force = false, copies = false, pending = false;
     unsigned long long ticket = 0;
     std::vector<int> t_index;
-    std::vector<int> joint;  // per T set: 1 = this build's H used the joint factor
+    std::vector<int> joint;  // per T set: 1 = this build's H used the joint factor (2 = split)
     const void* h_dev = nullptr;  // this build's device H / S (copy hazards of the next build)
     const void* s_dev = nullptr;
   } slots[2];
@@ -197,11 +198,17 @@ int launch_potrf_batched(hsdla_ctx* ctx, int n, int batch, const double2* T, lon
 int launch_tprep(hsdla_ctx* ctx, cudaStream_t stream, int n_tsets, const int* tdim_dev, int mp,
                  const double2* taa, const double2* tab, const double2* tbb, long long t_ld,
                  double2* forms, int do_chol, int* info_dev);
-// Joint factor L of [[T_AA, T_AB], [T_AB^H, T_BB]] per T set (2m x 2m, ld 2*mp, in `joint`),
-// info per set into info_dev and, if non-null, the mapped host view info_host_dev.
-int launch_tjoint(cudaStream_t stream, int n_tsets, const int* tdim_dev, int mp,
-                  const double2* taa, const double2* tab, const double2* tbb, long long t_ld,
-                  double2* joint, int* info_dev, int* info_host_dev);
+// Joint factor L of [[T_AA, T_AB], [T_AB^H, T_BB]] per T set (ld 2*mp, in `joint`), with the
+// dense-block / diagonal-tail split where tdense[t] < tdim[t] and T has that structure; info per
+// set into info_dev and, if non-null, the mapped host views (info, split flag).
+int launch_tjoint(cudaStream_t stream, int n_tsets, const int* tdim_dev, const int* tdense_dev,
+                  int mp, const double2* taa, const double2* tab, const double2* tbb,
+                  long long t_ld, double2* joint, int* info_dev, int* info_host_dev,
+                  int* split_host_dev);
+// Tail rows [d, m) of split joint T sets: atoms_dev[e] = (row offset, d, m, T set).
+int launch_ttail(hsdla_ctx* ctx, const int4* atoms_dev, int n_atoms, int max_tail, int n_basis,
+                 const double2* A, const double2* B, long long ld, double2* XY, double2* Z,
+                 const double2* joint, long long lj);
 int ab_generate(hsdla_ctx* ctx, const hsdla_ab_args* args);
 // kind 0: o1/o2 = j_l(x), j'_l(x), (l_max+1) x n row-major; kind 1: o1 = Y_lm (complex,
 // (l_max+1)^2 x n row-major) at unit directions in (n x 3).

@@ -192,27 +192,54 @@ __global__ void tprep_kernel(const int* tdim, int mp, const double2* taa, const 
 // cholesky_factor read them, kernels.py:198-201 / :217-228) so that per atom
 //   A^H T_AA A + A^H T_AB B + B^H T_AB^H A + B^H T_BB B = W^H W,  W = L^H [A; B],  T = L L^H,
 // i.e. the H of build_H_ABBA_BB + build_H_AA (builder.py:212-315) as one rank-2m update.
-// The factor is written in place over the assembled lower triangle (ld 2*mp); info as
-// chol_block (0 = HPD).  L11 equals the T_AA factor of tprep_kernel bit for bit (the first m
-// columns see the same updates in the same order).  info_host (mapped) may be null.
-__global__ void tjoint_kernel(const int* tdim, int mp, const double2* taa, const double2* tab,
-                              const double2* tbb, long long t_ld, double2* joint, int* info,
-                              int* info_host) {
+// Structure split: when the set's dense size d =
+// (l_nonsph+1)^2 is below m and every T entry outside the leading d x d blocks is zero except
+// the diagonals (what assemble_T builds, flapw.py:306-363), the joint matrix is factored in the
+// order (A rows 0..d, B rows 0..d) and then one 2x2 block [[T_AA_ii, T_AB_ii], [conj, T_BB_ii]]
+// per tail row i: a dense 2d x 2d factor plus per-row 2x2 factors (l11, l21, l22) stored in the
+// region's last two columns (l11 + i l22, l21).  The factor is written in place over the
+// assembled lower triangle (ld 2*mp); info as chol_block (0 = HPD); without the split L11
+// equals the T_AA factor of tprep_kernel bit for bit.  info_host / split_host (mapped) may be
+// null.
+__global__ void tjoint_kernel(const int* tdim, const int* tdense, int mp, const double2* taa,
+                              const double2* tab, const double2* tbb, long long t_ld,
+                              double2* joint, int* info, int* info_host, int* split_host) {
+  __shared__ int s_off, s_tail_bad;
   const int b = blockIdx.x;
-  const int m = tdim[b], n = 2 * m;
+  const int m = tdim[b];
+  const int d = tdense ? min(max(tdense[b], 0), m) : m;
   const long long lj = 2LL * mp;
   const long long tstride = t_ld * t_ld;
   const double2* Taa = taa + b * tstride;
   const double2* Tab = tab + b * tstride;
   const double2* Tbb = tbb + b * tstride;
   double2* J = joint + (long long)b * lj * lj;
+  if (threadIdx.x == 0) s_off = 0, s_tail_bad = 0;
+  __syncthreads();
+  bool split = d < m;
+  if (split) {  // every coupling of a tail row other than its own diagonal must vanish
+    for (long long e = threadIdx.x; e < (long long)m * m; e += blockDim.x) {
+      const int r = (int)(e % m), c = (int)(e / m);
+      if (r == c || (r < d && c < d)) continue;
+      const double2 x = Tab[r + c * t_ld];
+      bool nz = x.x != 0.0 || x.y != 0.0;
+      if (r > c) {
+        const double2 y = Taa[r + c * t_ld], z = Tbb[r + c * t_ld];
+        nz = nz || y.x != 0.0 || y.y != 0.0 || z.x != 0.0 || z.y != 0.0;
+      }
+      if (nz) s_off = 1;
+    }
+    __syncthreads();
+    split = s_off == 0;
+  }
+  const int h = split ? d : m, n = 2 * h;
   for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) {
     const int r = (int)(e % n), c = (int)(e / n);
     if (r < c) continue;
     double2 v;
-    if (r < m) v = Taa[r + c * t_ld];
-    else if (c < m) v = cconj(Tab[c + (r - m) * t_ld]);
-    else v = Tbb[(r - m) + (c - m) * t_ld];
+    if (r < h) v = Taa[r + c * t_ld];
+    else if (c < h) v = cconj(Tab[c + (r - h) * t_ld]);
+    else v = Tbb[(r - h) + (c - h) * t_ld];
     if (r == c) v.y = 0.0;
     J[r + c * lj] = v;
   }
@@ -220,7 +247,48 @@ __global__ void tjoint_kernel(const int* tdim, int mp, const double2* taa, const
   if (lj <= kPackedMaxN) chol_packed(n, J, lj, J, lj, info + b);  // shared memory sized by 2*mp
   else chol_block(n, J, lj, J, lj, info + b);
   __syncthreads();
-  if (threadIdx.x == 0 && info_host) info_host[b] = info[b];
+  if (split && info[b] == 0) {
+    for (int i = d + threadIdx.x; i < m; i += blockDim.x) {
+      const double a = Taa[i + i * t_ld].x, c = Tbb[i + i * t_ld].x;
+      const double2 ab = Tab[i + i * t_ld];
+      bool ok = a > 0.0 && isfinite(a);
+      const double l11 = ok ? sqrt(a) : 1.0;
+      const double2 l21 = make_double2(ab.x / l11, -ab.y / l11);  // T_BA_ii / l11
+      const double rr = c - (l21.x * l21.x + l21.y * l21.y);
+      ok = ok && rr > 0.0 && isfinite(rr);
+      J[i + (lj - 2) * lj] = make_double2(l11, ok ? sqrt(rr) : 0.0);
+      J[i + (lj - 1) * lj] = l21;
+      if (!ok) atomicExch(&s_tail_bad, 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && s_tail_bad) info[b] = n + 1;  // a tail block is not HPD
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (info_host) info_host[b] = info[b];
+    if (split_host) split_host[b] = split ? 1 : 0;
+  }
+}
+
+// Tail rows of split joint T sets: for atom entry e = (row offset, d, m, T set) and every
+// column, W1_i = l11 A_i + conj(l21) B_i (XY slot) and W2_i = l22 B_i (Z slot), i in [d, m).
+__global__ void ttail_kernel(const int4* atoms, int n_basis, const double2* __restrict__ A,
+                             const double2* __restrict__ B, long long ld, double2* XY, double2* Z,
+                             const double2* joint, long long lj) {
+  const int4 at = atoms[blockIdx.y];
+  const int t = at.z - at.y;  // tail rows
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t <= 0 || idx >= (long long)t * n_basis) return;
+  const int i = at.y + (int)(idx % t);
+  const long long col = idx / t;
+  const double2* L = joint + (long long)at.w * lj * lj;
+  const double2 l1122 = L[i + (lj - 2) * lj], l21 = L[i + (lj - 1) * lj];
+  const long long e = at.x + i + col * ld;
+  const double2 a = A[e], bb = B[e];
+  // conj(l21) * b = (l21.x b.x + l21.y b.y) + i (l21.x b.y - l21.y b.x)
+  XY[e] = make_double2(l1122.x * a.x + l21.x * bb.x + l21.y * bb.y,
+                       l1122.x * a.y + l21.x * bb.y - l21.y * bb.x);
+  Z[e] = make_double2(l1122.y * bb.x, l1122.y * bb.y);
 }
 
 // ---------------------------------------------------------------------------
@@ -321,15 +389,27 @@ int launch_tprep(hsdla_ctx* ctx, cudaStream_t stream, int n_tsets, const int* td
   return HSDLA_OK;
 }
 
-int launch_tjoint(cudaStream_t stream, int n_tsets, const int* tdim_dev, int mp,
-                  const double2* taa, const double2* tab, const double2* tbb, long long t_ld,
-                  double2* joint, int* info_dev, int* info_host_dev) {
+int launch_tjoint(cudaStream_t stream, int n_tsets, const int* tdim_dev, const int* tdense_dev,
+                  int mp, const double2* taa, const double2* tab, const double2* tbb,
+                  long long t_ld, double2* joint, int* info_dev, int* info_host_dev,
+                  int* split_host_dev) {
   if (n_tsets <= 0) return HSDLA_OK;
   const int n = 2 * mp;
   size_t smem = (n <= kPackedMaxN) ? size_t(n) * (n + 1) / 2 * sizeof(double2)
                                    : size_t(n) * sizeof(double2);
-  tjoint_kernel<<<n_tsets, 512, smem, stream>>>(tdim_dev, mp, taa, tab, tbb, t_ld, joint, info_dev,
-                                                info_host_dev);
+  tjoint_kernel<<<n_tsets, 512, smem, stream>>>(tdim_dev, tdense_dev, mp, taa, tab, tbb, t_ld,
+                                                joint, info_dev, info_host_dev, split_host_dev);
+  HS_CHECK_LAUNCH();
+  return HSDLA_OK;
+}
+
+int launch_ttail(hsdla_ctx* ctx, const int4* atoms_dev, int n_atoms, int max_tail, int n_basis,
+                 const double2* A, const double2* B, long long ld, double2* XY, double2* Z,
+                 const double2* joint, long long lj) {
+  if (n_atoms <= 0 || max_tail <= 0 || n_basis <= 0) return HSDLA_OK;
+  const long long work = (long long)max_tail * n_basis;
+  ttail_kernel<<<dim3((unsigned)((work + 255) / 256), n_atoms), 256, 0, ctx->stream>>>(
+      atoms_dev, n_basis, A, B, ld, XY, Z, joint, lj);
   HS_CHECK_LAUNCH();
   return HSDLA_OK;
 }
@@ -398,7 +478,7 @@ int preload_small() {
                        (const void*)mirror_kernel, (const void*)scale_rows_kernel,
                        (const void*)prep_kernel, (const void*)publish_kernel,
                        (const void*)zero_rows_kernel, (const void*)finite_kernel,
-                       (const void*)tjoint_kernel};
+                       (const void*)tjoint_kernel, (const void*)ttail_kernel};
   for (const void* f : fns) {
     cudaFuncAttributes at;
     HS_CUDA(cudaFuncGetAttributes(&at, f));

@@ -70,6 +70,7 @@ class TPack:
     t_bb: object
     h2d_bytes: int
     _staging: object = None
+    t_dense: np.ndarray = None  # (n_tsets,) int32: (l_nonsph+1)^2 dense-block size per set
 
     @property
     def n_tsets(self) -> int:
@@ -87,6 +88,10 @@ def pack_tmats(tmats) -> TPack:
             reps.append(a)
         index.append(keys[key])
     dims = np.array([tmats.t_aa[a].rows for a in reps], dtype=np.int32)
+    l_ns = getattr(tmats, "l_nonsph", None)
+    dense = np.array([min(int(dims[s]), (int(l_ns[a]) + 1) ** 2) if l_ns is not None
+                      and a < len(l_ns) else int(dims[s]) for s, a in enumerate(reps)],
+                     dtype=np.int32)
     t_ld = int(max(1, dims.max()))
     host = np.zeros((3, len(reps), t_ld, t_ld), dtype=np.complex128)
     for s, a in enumerate(reps):
@@ -95,7 +100,7 @@ def pack_tmats(tmats) -> TPack:
             host[f, s, :m, :m] = fam[a].array.T  # (col, row) storage = column-major
     (dev,), staged = _to_device([host])
     return TPack(np.array(index, dtype=np.int32), dims, t_ld, dev[0], dev[1], dev[2],
-                 host.nbytes, staged)
+                 host.nbytes, staged, dense)
 
 
 class DeviceSpec:
@@ -175,7 +180,9 @@ class _Call:
         self.keep = [np.ascontiguousarray(heights, dtype=np.int32),
                      np.ascontiguousarray(row_offset, dtype=np.int64),
                      np.ascontiguousarray(tpack.t_index, dtype=np.int32),
-                     np.ascontiguousarray(tpack.t_dim, dtype=np.int32), tpack, host_out, ab_args]
+                     np.ascontiguousarray(tpack.t_dim, dtype=np.int32), tpack, host_out, ab_args,
+                     np.ascontiguousarray(tpack.t_dense if tpack.t_dense is not None
+                                          else tpack.t_dim, dtype=np.int32)]
         h_arr, o_arr, ti, td = self.keep[:4]
         a = _native.BuildArgs()
         a.n_atoms = self.na
@@ -185,6 +192,7 @@ class _Call:
         a.t_index = ti.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
         a.n_tsets = tpack.n_tsets
         a.t_dim = td.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+        a.t_dense = self.keep[-1].ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
         a.t_aa = tpack.t_aa.data_ptr()
         a.t_ab = tpack.t_ab.data_ptr()
         a.t_bb = tpack.t_bb.data_ptr()
@@ -237,6 +245,7 @@ class _Call:
             "hpd_mask": [bool(self.mask[i]) for i in range(self.na)],
             "chol_info": [int(self.info[i]) for i in range(self.n_tsets)],
             "joint_t": [bool(self.joint[i]) for i in range(self.n_tsets)],
+            "joint_split": [self.joint[i] == 2 for i in range(self.n_tsets)],
             "ms": {"setup": r.ms_setup, "S": r.ms_S, "H_ABBA_BB": r.ms_H_ABBA_BB,
                    "H_AA": r.ms_H_AA},
             "kernel_ms": {"contract_S": r.ms_contract_S, "contract_H": r.ms_contract_H,

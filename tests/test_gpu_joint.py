@@ -130,3 +130,66 @@ def test_joint_form_shared_type_pipeline_reuse(pkg):
     for i in range(3):
         np.testing.assert_array_equal(out[i][0], h1.array)
         np.testing.assert_array_equal(out[i][1], s1.array)
+
+
+def _structured(rng, m, d, shift):
+    """Dense d x d Hermitian block + real diagonal tail (assemble_T's shape, flapw.py:306-363)."""
+    t = np.zeros((m, m), dtype=np.complex128)
+    t[:d, :d] = _hermitian(rng, d, 0.0)
+    t[np.diag_indices(m)] += shift + rng.uniform(-0.2, 0.2, m)
+    return t
+
+
+def _split_case(pkg, seed, heights, d_sizes, n_g, tail_bb=1.5, break_structure=False):
+    rng = np.random.default_rng(seed)
+    lay = pkg.AtomBlockLayout(tuple(heights))
+    r = lay.total_rows
+    a = pkg.ComplexDense.zeros(r, n_g, capacity_rows=lay.capacity_rows)
+    b = pkg.ComplexDense.zeros(r, n_g, capacity_rows=lay.capacity_rows)
+    a.array[:] = rand_complex(rng, r, n_g)
+    b.array[:] = rand_complex(rng, r, n_g)
+    u = rng.uniform(0.2, 1.5, r)
+    co = pkg.StackedCoefficients(a, b, lay, u)
+    taa, tab, tbb = [], [], []
+    for m, d in zip(heights, d_sizes):
+        taa.append(_structured(rng, m, d, 2.0))
+        tbb.append(_structured(rng, m, d, tail_bb))
+        x = np.zeros((m, m), dtype=np.complex128)
+        x[:d, :d] = rand_complex(rng, d, d) / m
+        x[np.diag_indices(m)] += 1.0  # assemble_T's unit AB diagonal
+        tab.append(x)
+    if break_structure:
+        tab[0][heights[0] - 1, 0] = 1e-3
+    cd = pkg.ComplexDense.from_array
+    l_sph = [int(round(np.sqrt(m))) - 1 for m in heights]
+    l_ns = [int(round(np.sqrt(d))) - 1 for d in d_sizes]
+    tm = pkg.TMatrixSet([cd(t) for t in taa], [cd(t) for t in tab], [cd(t) for t in tbb],
+                        l_sph, l_ns)
+    return co, tm, (a.array.copy(), b.array.copy(), u.copy(), taa, tab, tbb)
+
+
+def test_joint_structure_split(pkg):
+    """l_sph = 8, l_nonsph = 6 (the paper's case) and l_sph = 4, l_nonsph = 2: T dense in its
+    leading (l_nonsph+1)^2 block plus diagonals -> 2d x 2d joint factor, 2x2 per tail row, T
+    applications with K = d and an elementwise tail; equal to the dense forms and the oracle."""
+    heights, dense = (81, 81, 25), (49, 49, 9)
+    co, tm, ref = _split_case(pkg, 21, heights, dense, 173)
+    h, h_r = _check(pkg, co, tm, ref, [True] * 3, [True] * 3)
+    from paper_1602_06589_b200.pipeline import build_device  # noqa: F401
+    _, _, res = _build(pkg, co, tm)
+    assert res["joint_split"] == [True] * 3
+
+
+def test_joint_structure_split_fallbacks(pkg):
+    """An off-structure entry disables the split for that set (dense joint factor instead);
+    a tail 2x2 block that is not HPD (T_BB tail below |T_AB|^2 / T_AA) sends the set to the
+    reference forms."""
+    heights, dense = (25, 25), (9, 9)
+    co, tm, ref = _split_case(pkg, 22, heights, dense, 90, break_structure=True)
+    _, _, res = _build(pkg, co, tm)
+    assert res["joint_t"] == [True, True] and res["joint_split"] == [False, True]
+    _check(pkg, co, tm, ref, [True, True], [True, True])
+    co, tm, ref = _split_case(pkg, 23, heights, dense, 90, tail_bb=0.1)
+    _, _, res = _build(pkg, co, tm)
+    assert res["joint_t"] == [False, False]
+    _check(pkg, co, tm, ref, [False, False], [True, True])

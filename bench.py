@@ -39,7 +39,9 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=30)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    p.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5", "C2NS"],
+                   help="BASELINE.json configs C1-C5; C2NS = C2 with l_nonsph = 6 < l_sph = 8 "
+                        "(structured T, not a BASELINE config)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--mode", default="kpoints", choices=["kpoints", "panels"],
@@ -137,7 +139,8 @@ def run_reference(args):
         "n_gpus": world, "steps": len(times), "warmup": args.warmup,
         "ms_per_step": round(1e3 * total / len(times), 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config} (BASELINE.json configs[{int(args.config[1]) - 1}])",
+        "config": {"workload": (f"{args.config} (BASELINE.json configs[{int(args.config[1]) - 1}])"
+                                if len(args.config) == 2 else f"{args.config} (not a BASELINE config)"),
                    "n_basis": spec.n_basis, "rows": int(sum((l + 1) ** 2 for l in spec.l_sph))},
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": host_threads(),
                          "kind": "port", "sample": sample},

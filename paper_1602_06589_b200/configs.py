@@ -38,6 +38,8 @@ class ConfigDef:
     n_kpoints: int = 1
     seed: int = 0
     t_shift: float = 2.0
+    l_nonsph: int | None = None  # None = l_max (BASELINE); else T is dense only in the leading
+                                 # (l_nonsph+1)^2 block plus its diagonals
 
 
 CONFIGS = {
@@ -46,7 +48,18 @@ CONFIGS = {
     "C3": ConfigDef("C3", 18.0, 8000, ((64, 2.2),), 8, seed=1003),
     "C4": ConfigDef("C4", 22.0, 13000, ((36, 2.0), (36, 2.2), (36, 2.4)), 10, seed=1004),
     "C5": ConfigDef("C5", 14.0, 5000, ((32, 2.2),), 8, n_kpoints=64, seed=1005),
+    # Not a BASELINE config: C2 with the paper's l_nonsph = 6 < l_sph = 8 (PAPER.md:649-652,
+    # :759-813), T zeroed outside the dense block except its diagonals as the reference's
+    # synth_T does (`flapw.py:440-446` _fig1_zero_out): exercises the T-structure split.
+    "C2NS": ConfigDef("C2NS", 12.0, 3000, ((16, 2.2),), 8, seed=1006, l_nonsph=6),
 }
+
+
+def _zero_outside(a: np.ndarray, d: int) -> np.ndarray:
+    """Keep the leading d x d block and the diagonal (reference `_fig1_zero_out`)."""
+    out = np.diag(np.diag(a)).astype(np.complex128)
+    out[:d, :d] = a[:d, :d]
+    return out
 
 
 def g_set(k: np.ndarray, cell: float, n_target: int) -> np.ndarray:
@@ -99,6 +112,7 @@ def make_instance(name: str, seed: int | None = None, n_kpoints: int | None = No
         kpts = kpts[:n_kpoints]
     n_l = (cfg.l_max + 1) ** 2
     shift = cfg.t_shift if hpd_shift is None else hpd_shift
+    l_ns = cfg.l_max if cfg.l_nonsph is None else cfg.l_nonsph
     positions, rmt, radial, t_aa, t_ab, t_bb = [], [], [], [], [], []
     wmin = np.inf
     for n_atoms, r_mt in cfg.types:
@@ -113,10 +127,16 @@ def make_instance(name: str, seed: int | None = None, n_kpoints: int | None = No
             return rng.standard_normal((n_l, n_l)) + 1j * rng.standard_normal((n_l, n_l))
 
         x = cgauss()
-        taa = ComplexDense.from_array((x + x.conj().T) / (2 * n_l) + shift * np.eye(n_l))
+        taa_a = (x + x.conj().T) / (2 * n_l) + shift * np.eye(n_l)
         x = cgauss()
-        tbb = ComplexDense.from_array((x + x.conj().T) / (2 * n_l) + shift * np.eye(n_l))
-        tab = ComplexDense.from_array(cgauss() / n_l)
+        tbb_a = (x + x.conj().T) / (2 * n_l) + shift * np.eye(n_l)
+        tab_a = cgauss() / n_l
+        if l_ns < cfg.l_max:
+            d = (l_ns + 1) ** 2
+            taa_a, tbb_a, tab_a = (_zero_outside(t, d) for t in (taa_a, tbb_a, tab_a))
+        taa = ComplexDense.from_array(taa_a)
+        tbb = ComplexDense.from_array(tbb_a)
+        tab = ComplexDense.from_array(tab_a)
         for p in pos:
             positions.append(p)
             rmt.append(r_mt)
@@ -130,10 +150,10 @@ def make_instance(name: str, seed: int | None = None, n_kpoints: int | None = No
     for k in kpts:
         specs.append(SystemSpec(
             positions=np.array(positions), rotations=np.tile(np.eye(3), (n_at, 1, 1)),
-            mt_radius=np.array(rmt), l_sph=l_arr, l_nonsph=l_arr.copy(), k_point=k,
+            mt_radius=np.array(rmt), l_sph=l_arr, l_nonsph=np.full(n_at, l_ns, dtype=np.int64), k_point=k,
             k_vectors=g_set(k, cfg.cell, cfg.n_target), omega=cfg.cell**3, radial=radial))
     tm = TMatrixSet(t_aa=t_aa, t_ab=t_ab, t_bb=t_bb, l_sph=[cfg.l_max] * n_at,
-                    l_nonsph=[cfg.l_max] * n_at)
+                    l_nonsph=[l_ns] * n_at)
     return Instance(cfg, specs, tm, wmin)
 
 

@@ -440,7 +440,8 @@ def run_ours(args):
                     "api": "paper_1602_06589_b200.pipeline.build_hs_many (k-point batch: host "
                            "spec per step + T once -> full H, S in pinned host memory per step)",
                     "single_call_ms": round(float(e2e_t[1].item()), 3)},
-            "gpu_launches": args.steps * pipe.launches_per_run(dspec),
+            "gpu_launches": args.steps * (pipe.launches_per_run(dspec)
+                                          + int(any(res.get("joint_split", [])))),
             "clocks": clk.summary(),
         }
         if not args.no_cpu_baseline and world == 1:
@@ -548,7 +549,8 @@ def run_panels(args):
                     "h2d_bytes_per_step": int(dspec.h2d_bytes), "d2h_bytes_per_step": 32 * n * n,
                     "ms_per_step": round(float(e2e.item()), 3),
                     "api": "paper_1602_06589_b200.shard.P2PShardedBuild.run + D2H of H, S"},
-            "gpu_launches": args.steps * sb.pipe.launches_per_run(dspec),
+            "gpu_launches": args.steps * (sb.pipe.launches_per_run(dspec)
+                                          + int(any(res.get("joint_split", [])))),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -393,8 +393,9 @@ class HSPipeline:
         return self._inflight.pop(ticket).finish(ticket)
 
     def launches_per_run(self, dspec: DeviceSpec) -> int:
-        """Kernels this pipeline launches per k-point (A/B per l group, T prep, S
-        contraction, Z apply, XY apply, H contraction)."""
+        """Kernels this pipeline launches per k-point once the T preparation is cached: A/B
+        per l group, S contraction, Z apply, XY apply, H contraction, result publication (plus
+        the tail kernel of split T sets, which the caller adds from `joint_split`)."""
         return len(np.unique(dspec.l_sph)) + 5
 
     def result_views(self):

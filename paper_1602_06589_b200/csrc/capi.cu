@@ -498,13 +498,9 @@ WsLayout ws_layout(const hsdla_build_args* a) {
   for (int t = 0; t < a->n_tsets; ++t) mp = std::max(mp, a->t_dim[t]);
   w.mp = mp;
   const size_t stack = align_up(size_t(a->ld) * a->n_basis * sizeof(double2));
+  // T-dependent regions first: their offsets do not depend on n_basis, so a k-point batch
+  // with varying G-sets keeps reusing one T preparation (TKey compares these offsets).
   size_t off = 0;
-  w.bs = off;
-  off += a->B_scaled ? 0 : stack;
-  w.z = off;
-  off += stack;
-  w.xy = off;
-  off += stack;
   w.forms = off;
   off += align_up(size_t(a->n_tsets) * 4 * mp * mp * sizeof(double2));
   w.tdim = off;  // t_dim then t_dense, n_tsets each
@@ -515,6 +511,12 @@ WsLayout ws_layout(const hsdla_build_args* a) {
   off += align_up(size_t(a->n_tsets) * 4 * mp * mp * sizeof(double2));
   w.jinfo = off;
   off += align_up(a->n_tsets * sizeof(int));
+  w.bs = off;
+  off += a->B_scaled ? 0 : stack;
+  w.z = off;
+  off += stack;
+  w.xy = off;
+  off += stack;
   w.total = off;
   return w;
 }

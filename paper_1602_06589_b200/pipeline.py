@@ -172,7 +172,7 @@ class _Call:
     def __init__(self, *, n_basis, heights, row_offset, tpack: TPack, A, B, Bs, udot, ld,
                  force_general_path, H, S, ldh, shard_rank, n_shards, workspace, host_out,
                  ab_args=None, shard_mirror=False, reuse_t=False, stream_h_copy=0,
-                 h_reference_form=False, host_src=None):
+                 h_reference_form=False, host_src=None, n_capacity=None):
         lib = _native.load()
         t = device.torch()
         self.na = len(heights)
@@ -220,7 +220,12 @@ class _Call:
             a.ldh_host = int(host_out[0].shape[1])
         self.need = lib.hsdla_build_workspace_size(ctypes.byref(a))
         if workspace is None or workspace.numel() < self.need:
-            workspace = t.empty(max(self.need, 1), dtype=t.uint8, device="cuda")
+            # size for the caller's capacity (a k-point batch with varying N_G keeps one
+            # workspace, so its T preparation stays reusable)
+            a.n_basis = max(n_basis, int(n_capacity or 0))
+            cap_need = lib.hsdla_build_workspace_size(ctypes.byref(a))
+            a.n_basis = n_basis
+            workspace = t.empty(max(self.need, cap_need, 1), dtype=t.uint8, device="cuda")
         self.workspace = workspace
         a.workspace = workspace.data_ptr()
         a.workspace_bytes = workspace.numel()
@@ -365,7 +370,7 @@ class HSPipeline:
                      ldh=self.n_capacity, shard_rank=self.shard_rank, n_shards=self.n_shards,
                      workspace=self.workspace, host_out=host_out, ab_args=ab,
                      shard_mirror=self.shard_mirror, reuse_t=reuse, stream_h_copy=stream_h_copy,
-                     h_reference_form=self.h_reference_form)
+                     h_reference_form=self.h_reference_form, n_capacity=self.n_capacity)
         call.keep.append(dspec)
         self.workspace = call.workspace
         self._last_t = (tpack, bool(force_general_path))

@@ -98,9 +98,23 @@ def pack_tmats(tmats) -> TPack:
         m = int(dims[s])
         for f, fam in enumerate((tmats.t_aa, tmats.t_ab, tmats.t_bb)):
             host[f, s, :m, :m] = fam[a].array.T  # (col, row) storage = column-major
+    index = np.array(index, dtype=np.int32)
+    # Content cache: the same T values (any objects) on the same device reuse the uploaded pack,
+    # so repeated single calls keep the pipeline's cached T preparation (reuse_t); a T changed
+    # in place compares unequal and is uploaded afresh.
+    dev_id = device.torch().cuda.current_device()
+    hit = _TPACK_CACHE.get(dev_id)
+    if (hit is not None and hit[0].shape == host.shape and np.array_equal(hit[1], index)
+            and np.array_equal(hit[2], dense) and np.array_equal(hit[3].t_dim, dims)
+            and np.array_equal(hit[0], host)):
+        return hit[3]
     (dev,), staged = _to_device([host])
-    return TPack(np.array(index, dtype=np.int32), dims, t_ld, dev[0], dev[1], dev[2],
-                 host.nbytes, staged, dense)
+    pack = TPack(index, dims, t_ld, dev[0], dev[1], dev[2], host.nbytes, staged, dense)
+    _TPACK_CACHE[dev_id] = (host, index.copy(), dense, pack)
+    return pack
+
+
+_TPACK_CACHE: dict = {}  # device -> (packed host T, t_index, t_dense, TPack) of the last pack
 
 
 class DeviceSpec:

@@ -387,3 +387,19 @@ def test_three_and_four_product_contractions_agree(pkg, tmp_path):
     assert not np.array_equal(h.array, four["h"])  # the variants really differ
     for x, ref in ((h.array, ho), (s.array, so), (four["h"], ho), (four["s"], so)):
         assert rel_fro(x, ref) <= 1e-13
+
+
+def test_tpack_content_cache(pkg):
+    """pack_tmats reuses the uploaded pack for equal T values (so repeated single calls keep
+    the cached T preparation) and re-uploads after an in-place change."""
+    from paper_1602_06589_b200 import configs
+    from paper_1602_06589_b200.pipeline import pack_tmats
+
+    inst = configs.make_instance("C1")
+    p1 = pack_tmats(inst.tmats)
+    assert pack_tmats(inst.tmats) is p1
+    inst2 = configs.make_instance("C1")  # equal values, other objects
+    assert pack_tmats(inst2.tmats) is p1
+    inst2.tmats.t_ab[0].array[0, 0] += 1e-9
+    p3 = pack_tmats(inst2.tmats)
+    assert p3 is not p1

@@ -270,9 +270,11 @@ typedef struct {
 size_t hsdla_build_workspace_size(const hsdla_build_args* args);
 /* 1 if `p` points into page-locked (pinned / registered) host memory, else 0. */
 int hsdla_is_pinned(const void* p);
-/* Enqueues the whole build without a host round trip (the HPD branch is selected on the
- * device from the Cholesky info) and synchronises once at the end (info, flags, timings).  Returns HSDLA_ERR_NAN_INPUT on a NaN
- * in tril(T_AA) and HSDLA_ERR_NONFINITE on non-finite output (outputs still written). */
+/* Enqueues the whole build (the T_AA HPD branch of the reference forms is selected on the
+ * device from the Cholesky info; the H form per T set needs the joint factor's info on the
+ * host, read once after a fresh T preparation while the S contraction is already queued) and
+ * synchronises once at the end (info, flags, timings).  Returns HSDLA_ERR_NAN_INPUT on a NaN in
+ * tril(T_AA) and HSDLA_ERR_NONFINITE on non-finite output (outputs still written). */
 int hsdla_build_hs(hsdla_ctx* ctx, const hsdla_build_args* args, hsdla_build_result* result);
 
 /* The whole per-k-point hot path, SystemSpec -> (H, S): `hsdla_ab_generate` into

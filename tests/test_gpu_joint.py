@@ -193,3 +193,12 @@ def test_joint_structure_split_fallbacks(pkg):
     _, _, res = _build(pkg, co, tm)
     assert res["joint_t"] == [False, False]
     _check(pkg, co, tm, ref, [False, False], [True, True])
+
+
+def test_joint_form_large_blocks(pkg):
+    """l_sph = 12 and 11 blocks (m = 169, 144): the joint factor's 2m exceeds the packed
+    shared-memory Cholesky (column kernel in global memory) and the T applications run on
+    64-row tiles; mixed with a small set (mixed packed / column choice per launch)."""
+    heights = (169, 144, 16)
+    co, tm, ref = _case(pkg, 4, heights, 150, list(heights), [2.0, 2.0, 2.0], [2.0, 2.0, 2.0])
+    _check(pkg, co, tm, ref, [True, True, True], [True, True, True])

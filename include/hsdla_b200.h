@@ -181,6 +181,19 @@ int hsdla_phase_matrix(hsdla_ctx* ctx, int n_basis, int n_atoms, const double* k
 int hsdla_hadamard_lower(hsdla_ctx* ctx, int n, const hsdla_c64* W, int64_t ldw,
                          const hsdla_c64* G, int64_t ldg, hsdla_c64* C, int64_t ldc, int accumulate);
 
+/* ---- input side: Gaunt coefficients and T assembly ---- */
+/* G[(i * n_row + j) * n_pot + k] = sum_p w[p] conj(Y[i][p]) Y[j][p] Y[k][p] (special.py:189-244):
+ * Y DEVICE complex rows of ld ldy (row L = l^2 + l + m, e.g. hsdla_spherical_harmonics on the
+ * quadrature directions), w DEVICE npts weights, G DEVICE out; n_row, n_pot <= rows of Y. */
+int hsdla_gaunt_tensor(hsdla_ctx* ctx, int n_row, int n_pot, int npts, int64_t ldy,
+                       const hsdla_c64* Y, const double* w, hsdla_c64* G);
+/* One T block of assemble_T (flapw.py:306-363), DEVICE, column-major n_full x n_full:
+ * out[p, q] = sum_k c[l(p), l(q), k] G[p, q, k] on the leading n_dense = n_l^2 block
+ * (c: n_l x n_l x n_pot, G: n_dense x n_dense x n_pot, numpy C order), plus diag[l(p)] (may be
+ * NULL) and `unit` on the diagonal. */
+int hsdla_gaunt_sum(hsdla_ctx* ctx, int n_full, int n_l, int n_pot, const hsdla_c64* c,
+                    const hsdla_c64* G, const double* diag, double unit, hsdla_c64* out);
+
 /* ---- the composed build (builder.py:403-474 build_all) ------------------- */
 typedef struct {
   int32_t n_atoms;

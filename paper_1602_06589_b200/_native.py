@@ -118,6 +118,10 @@ SIGNATURES = {
     "hsdla_reduced_s_aa": (ctypes.c_int, [_vp, ctypes.POINTER(ReducedArgs)]),
     "hsdla_spherical_bessel": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]),
     "hsdla_spherical_harmonics": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp]),
+    "hsdla_gaunt_tensor": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64,
+                                          _vp, _vp, _vp]),
+    "hsdla_gaunt_sum": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp,
+                                       _vp, ctypes.c_double, _vp]),
     "hsdla_phase_matrix": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _i64]),
     "hsdla_hadamard_lower": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _i64, _vp, _i64, _vp, _i64,
                                             ctypes.c_int]),

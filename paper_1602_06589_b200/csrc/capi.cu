@@ -151,6 +151,7 @@ int hsdla_ctx_create(hsdla_ctx** out, void* stream) {
   if (int rc = preload_contract_tma()) return rc;
   if (int rc = preload_abgen()) return rc;
   if (int rc = preload_small()) return rc;
+  if (int rc = preload_gaunt()) return rc;
   // Mapped pinned memory: build results are published by a kernel store, not a DMA copy,
   // so they never queue behind the large H / S copies on the D2H engine.
   HS_CUDA(cudaHostAlloc(&c->scratch_host, 1024 * sizeof(int), cudaHostAllocMapped));
@@ -443,6 +444,24 @@ int hsdla_hadamard_lower(hsdla_ctx* ctx, int n, const hsdla_c64* W, int64_t ldw,
   if (ldc < (n > 1 ? n : 1)) return -8;
   std::lock_guard<std::mutex> lk(g_api_mutex);
   return hadamard_lower(ctx, n, D2(W), ldw, D2(G), ldg, D2(C), ldc, accumulate);
+}
+
+int hsdla_gaunt_tensor(hsdla_ctx* ctx, int n_row, int n_pot, int npts, int64_t ldy,
+                       const hsdla_c64* Y, const double* w, hsdla_c64* G) {
+  if (!ctx) return -1;
+  if (n_row < 0) return -2;
+  if (n_pot < 0) return -3;
+  if (npts < 0) return -4;
+  if (ldy < npts) return -5;
+  return hsdla::gaunt_tensor(ctx, n_row, n_pot, npts, (int)ldy, D2(Y), w, D2(G));
+}
+
+int hsdla_gaunt_sum(hsdla_ctx* ctx, int n_full, int n_l, int n_pot, const hsdla_c64* c,
+                    const hsdla_c64* G, const double* diag, double unit, hsdla_c64* out) {
+  if (!ctx) return -1;
+  if (n_full < 0) return -2;
+  if (n_l < 0 || n_l * n_l > n_full) return -3;
+  return hsdla::gaunt_sum(ctx, n_full, n_l * n_l, n_l, n_pot, D2(c), D2(G), diag, unit, D2(out));
 }
 
 int hsdla_reduced_s_aa(hsdla_ctx* ctx, const hsdla_reduced_args* args) {

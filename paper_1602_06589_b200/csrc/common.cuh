@@ -232,6 +232,13 @@ int preload_contract();
 int preload_contract_tma();
 int preload_abgen();
 int preload_small();
+int preload_gaunt();
+// Gaunt tensor over a quadrature grid (Y: n_y x npts rows of ld ldy) and the Gaunt-sum T block
+// (gaunt.cu).
+int gaunt_tensor(hsdla_ctx* ctx, int n_row, int n_pot, int npts, int ldy, const double2* Y,
+                 const double* w, double2* G);
+int gaunt_sum(hsdla_ctx* ctx, int n_full, int n_dense, int n_l, int n_pot, const double2* c,
+              const double2* G, const double* diag, double unit, double2* out);
 // Copy the non-finite flag and the Cholesky infos into mapped host memory (out[0] = flag,
 // out[1..n] = info) with plain stores, keeping the D2H copy engine free for H / S.
 int launch_publish(hsdla_ctx* ctx, const int* flag, const int* info, int n, int* out_mapped);

@@ -197,3 +197,106 @@ def match_factors(spec: SystemSpec, atom: int):
         device.ptr(fa), device.ptr(fb), max(n, 1)), "hsdla_match_factors")
     r0, r1 = int(f_row[atom]), int(f_row[atom]) + int(l_top[atom]) + 1
     return fa[r0:r1, :n].cpu().numpy(), fb[r0:r1, :n].cpu().numpy()
+
+
+# ---- input side: Gaunt-sum assembly of the coupling matrices ----------
+
+BB_DIAG_NORM_POWER = 1  # flapw.py:31
+
+
+@dataclass
+class RadialIntegrals:
+    """Radial integrals of one atom's coupling-matrix assembly (`flapw.py:253-273`): arrays
+    indexed (l', l, L'') with the compound potential index L'' = (l'', m'') up to l_nonsph;
+    uu / dd satisfy c[l', l, (l'', m'')] = (-1)^m'' conj(c[l, l', (l'', -m'')]) and du is that
+    partner of ud, so the assembled T_AA / T_BB are Hermitian and T_BA = T_AB^H."""
+
+    c_uu: np.ndarray
+    c_dd: np.ndarray
+    c_ud: np.ndarray
+    c_du: np.ndarray
+
+    @property
+    def l_nonsph(self) -> int:
+        return self.c_uu.shape[0] - 1
+
+
+def _pairing(c: np.ndarray) -> np.ndarray:
+    """The Hermitian-compatibility involution on (l', l, L'') arrays (`flapw.py:276-286`)."""
+    from .special import lm_index
+
+    n_pot = c.shape[2]
+    l_pot = int(np.sqrt(n_pot)) - 1
+    perm = np.empty(n_pot, dtype=np.int64)
+    sign = np.empty(n_pot)
+    for l in range(l_pot + 1):
+        for m in range(-l, l + 1):
+            perm[lm_index(l, m)] = lm_index(l, -m)
+            sign[lm_index(l, m)] = -1.0 if m % 2 else 1.0
+    return sign[None, None, :] * np.conj(c.transpose(1, 0, 2)[:, :, perm])
+
+
+def synth_radial_integrals(seed: int, l_nonsph: int, scale: float = 0.5) -> RadialIntegrals:
+    """Seeded radial integrals satisfying the pairing (`flapw.py:289-307`; same draws)."""
+    rng = np.random.default_rng(seed)
+    n_l = l_nonsph + 1
+    n_pot = n_l * n_l
+
+    def draw():
+        return scale * (rng.standard_normal((n_l, n_l, n_pot))
+                        + 1j * rng.standard_normal((n_l, n_l, n_pot)))
+
+    x_uu, x_dd, c_ud = draw(), draw(), draw()
+    return RadialIntegrals(c_uu=0.5 * (x_uu + _pairing(x_uu)), c_dd=0.5 * (x_dd + _pairing(x_dd)),
+                           c_ud=c_ud, c_du=_pairing(c_ud))
+
+
+def assemble_T(spec: SystemSpec, radial_integrals: list):
+    """Per-atom coupling matrices from Gaunt sums plus diagonal terms (`flapw.py:310-363`):
+    the dense (l_nonsph+1)^2 block is sum_k c[l(p), l(q), k] G[p, q, k] (G = the Gaunt tensor,
+    computed on the GPU over the reference's quadrature grid), the diagonal carries the energy
+    parameters (AA), energy x ||udot|| (BB) and ones (AB); T_BA is never built.  The result has
+    the dense-block + diagonal-tail shape the build's T-structure split uses."""
+    from .builder import TMatrixSet
+    from . import _native, device
+    from .special import _gaunt_device
+
+    if len(radial_integrals) != spec.n_atoms:
+        raise ContractViolationError("need radial integrals per atom")
+    t = device.require_cuda()
+    lib = _native.load()
+    t_aa, t_ab, t_bb = [], [], []
+    g_cache = {}
+    for a in range(spec.n_atoms):
+        ri = radial_integrals[a]
+        l_n, l_s = int(spec.l_nonsph[a]), int(spec.l_sph[a])
+        if ri.l_nonsph != l_n:
+            raise ContractViolationError(
+                f"atom {a}: integrals cover l_nonsph={ri.l_nonsph}, spec says {l_n}")
+        for name, c in (("uu", ri.c_uu), ("dd", ri.c_dd)):
+            if np.max(np.abs(c - _pairing(c))) > 1e-12:
+                raise ContractViolationError(f"atom {a}: {name} integrals violate the Hermitian pairing")
+        if np.max(np.abs(ri.c_du - _pairing(ri.c_ud))) > 1e-12:
+            raise ContractViolationError(f"atom {a}: du integrals are not the conjugate partner of ud")
+        if l_n not in g_cache:
+            g_cache[l_n] = _gaunt_device(l_n, l_n)
+        g = g_cache[l_n]
+        n_l, n_full = l_n + 1, (l_s + 1) ** 2
+        n_pot = n_l * n_l
+        rad = spec.radial[a]
+        e = np.asarray(rad.energy, dtype=np.float64)[:l_s + 1]
+        e_bb = e * np.asarray(rad.udot_norm, dtype=np.float64)[:l_s + 1] ** BB_DIAG_NORM_POWER
+        outs = []
+        for c, diag, unit in ((ri.c_uu, e, 0.0), (ri.c_ud, None, 1.0), (ri.c_dd, e_bb, 0.0)):
+            cd = t.from_numpy(np.ascontiguousarray(c, dtype=np.complex128)).cuda()
+            dd = t.from_numpy(np.ascontiguousarray(diag)).cuda() if diag is not None else None
+            out = t.empty((n_full, n_full), dtype=t.complex128, device="cuda")
+            _native.check(lib.hsdla_gaunt_sum(device.ctx(), n_full, n_l, n_pot, device.ptr(cd),
+                                              device.ptr(g), device.ptr(dd) if dd is not None
+                                              else None, unit, device.ptr(out)), "hsdla_gaunt_sum")
+            outs.append(ComplexDense(out.cpu().numpy().T))  # (col, row) storage -> F-order
+        t_aa.append(outs[0])
+        t_ab.append(outs[1])
+        t_bb.append(outs[2])
+    return TMatrixSet(t_aa=t_aa, t_ab=t_ab, t_bb=t_bb, l_sph=[int(x) for x in spec.l_sph],
+                      l_nonsph=[int(x) for x in spec.l_nonsph])

@@ -8,6 +8,8 @@ scalar calls keep the reference's return shapes.  Orders up to HSDLA_MAX_LSPH (1
 """
 from __future__ import annotations
 
+from functools import lru_cache
+
 import numpy as np
 
 from . import _native, device
@@ -72,3 +74,66 @@ def spherical_harmonic(l: int, m: int, direction) -> complex:
     if l < 0 or abs(m) > l:
         raise ContractViolationError(f"invalid (l, m) = ({l}, {m})")
     return complex(spherical_harmonics_all(l, direction)[lm_index(l, m), 0])
+
+
+GAUNT_L_MAX = 12  # special.py:19
+
+
+@lru_cache(maxsize=8)
+def _quadrature_grid(l_max: int, refine: int = 1):
+    """Product grid exact for triple products of harmonics up to l_max (`special.py:189-204`):
+    Gauss-Legendre in cos(theta) x uniform phi; returns device Y ((l_max+1)^2 x npts) and
+    device weights.  The nodes are constants computed once on the host."""
+    t = device.require_cuda()
+    n_theta = refine * (2 * l_max + 1)
+    n_phi = refine * (4 * l_max + 1)
+    ct, wt = np.polynomial.legendre.leggauss(n_theta)
+    phi = np.arange(n_phi) * (2.0 * np.pi / n_phi)
+    ct_g = np.repeat(ct, n_phi)
+    phi_g = np.tile(phi, n_theta)
+    w = np.repeat(wt, n_phi) * (2.0 * np.pi / n_phi)
+    st_g = np.sqrt(np.maximum(0.0, 1.0 - ct_g * ct_g))
+    dirs = np.stack([st_g * np.cos(phi_g), st_g * np.sin(phi_g), ct_g], axis=1)
+    n = dirs.shape[0]
+    dd = t.from_numpy(np.ascontiguousarray(dirs)).cuda()
+    y = t.empty(((l_max + 1) ** 2, n), dtype=t.complex128, device="cuda")
+    _native.check(_native.load().hsdla_spherical_harmonics(device.ctx(), l_max, n, device.ptr(dd),
+                                                           device.ptr(y)),
+                  "hsdla_spherical_harmonics")
+    return y, t.from_numpy(w).cuda()
+
+
+def _gaunt_device(l_row_max: int, l_pot_max: int, refine: int = 1):
+    l_max = max(l_row_max, l_pot_max)
+    if l_max > GAUNT_L_MAX:
+        raise ContractViolationError(f"gaunt supports l <= {GAUNT_L_MAX}")
+    t = device.require_cuda()
+    y, w = _quadrature_grid(l_max, refine)
+    n_row, n_pot = (l_row_max + 1) ** 2, (l_pot_max + 1) ** 2
+    g = t.empty((n_row, n_row, n_pot), dtype=t.complex128, device="cuda")
+    _native.check(_native.load().hsdla_gaunt_tensor(device.ctx(), n_row, n_pot, y.shape[1],
+                                                    y.shape[1], device.ptr(y), device.ptr(w),
+                                                    device.ptr(g)), "hsdla_gaunt_tensor")
+    return g
+
+
+def gaunt_tensor(l_row_max: int, l_pot_max: int) -> np.ndarray:
+    """G[L', L, L''] = gaunt(L', L, L'') for all compound indices in range, shape
+    ((l_row_max+1)^2, (l_row_max+1)^2, (l_pot_max+1)^2) (`special.py:227-244`), on the GPU."""
+    return _gaunt_device(l_row_max, l_pot_max).cpu().numpy()
+
+
+def gaunt(lp_mp, l_m, lpp_mpp, refine: int = 1) -> complex:
+    """Integral of conj(Y_{l',m'}) Y_{l,m} Y_{l'',m''} over the unit sphere (`special.py:207-224`);
+    `refine` multiplies the quadrature resolution."""
+    lp, mp = lp_mp
+    l, m = l_m
+    lpp, mpp = lpp_mpp
+    l_max = max(lp, l, lpp)
+    if l_max > GAUNT_L_MAX:
+        raise ContractViolationError(f"gaunt supports l <= {GAUNT_L_MAX}")
+    for ll, mm in ((lp, mp), (l, m), (lpp, mpp)):
+        if ll < 0 or abs(mm) > ll:
+            raise ContractViolationError(f"invalid (l, m) = ({ll}, {mm})")
+    g = _gaunt_device(l_max, l_max, refine)
+    return complex(g[lm_index(lp, mp), lm_index(l, m), lm_index(lpp, mpp)].item())

@@ -202,3 +202,42 @@ def test_joint_form_large_blocks(pkg):
     heights = (169, 144, 16)
     co, tm, ref = _case(pkg, 4, heights, 150, list(heights), [2.0, 2.0, 2.0], [2.0, 2.0, 2.0])
     _check(pkg, co, tm, ref, [True, True, True], [True, True, True])
+
+
+def test_assemble_t_output_through_the_build(pkg):
+    """T from the GPU assemble_T (Gaunt sums, reference golden integrals): with energies shifted
+    up the joint matrix is HPD and the build takes the structure split; as generated (energies in
+    [-1, 1]) it takes the reference forms.  Both against the oracle."""
+    from types import SimpleNamespace
+
+    from conftest import golden
+
+    d = golden("assemble_t.npz")
+    n = len(d["l_sph"])
+    ris = [pkg.RadialIntegrals(d[f"c_uu{a}"], d[f"c_dd{a}"], d[f"c_ud{a}"], d[f"c_du{a}"])
+           for a in range(n)]
+    heights = tuple(int((l + 1) ** 2) for l in d["l_sph"])
+    for shift, want_split in ((12.0, True), (0.0, None)):
+        radial = [SimpleNamespace(energy=d[f"energy{a}"] + shift, udot_norm=d[f"udot_norm{a}"])
+                  for a in range(n)]
+        spec = SimpleNamespace(n_atoms=n, l_sph=d["l_sph"], l_nonsph=d["l_nonsph"], radial=radial)
+        tm = pkg.assemble_T(spec, ris)
+        rng = np.random.default_rng(5)
+        lay = pkg.AtomBlockLayout(heights)
+        r = lay.total_rows
+        a = pkg.ComplexDense.zeros(r, 120, capacity_rows=lay.capacity_rows)
+        b = pkg.ComplexDense.zeros(r, 120, capacity_rows=lay.capacity_rows)
+        a.array[:] = rand_complex(rng, r, 120)
+        b.array[:] = rand_complex(rng, r, 120)
+        u = rng.uniform(0.2, 1.5, r)
+        co = pkg.StackedCoefficients(a, b, lay, u)
+        ref = (a.array.copy(), b.array.copy(), u.copy(), [t.array for t in tm.t_aa],
+               [t.array for t in tm.t_ab], [t.array for t in tm.t_bb])
+        h, s, res = _build(pkg, co, tm)
+        h_o, s_o, _, mask_o = ob.build_all(*ref[:3], list(heights), *ref[3:])
+        assert rel_fro(h, h_o) <= TOL and rel_fro(s, s_o) <= TOL
+        assert res["hpd_mask"] == list(mask_o)
+        if want_split:
+            assert all(res["joint_t"])
+            # l_nonsph < l_sph sets split; l_nonsph == l_sph (atom 1) has no tail
+            assert res["joint_split"] == [bool(ln < ls) for ls, ln in zip(d["l_sph"], d["l_nonsph"])]

@@ -47,3 +47,38 @@ def test_match_factors_vs_reference(pkg):
         fa, fb = pkg.match_factors(spec, a)
         assert rel_fro(fa, d[f"small_f_{a}"]) <= 1e-13
         assert fb.shape == fa.shape
+
+
+def test_gpu_gaunt_and_assemble_t_vs_reference(cuda):
+    """gaunt / gaunt_tensor / assemble_T on the GPU against the reference's
+    own outputs (tests/golden/assemble_t.npz), plus assemble_T's validation errors."""
+    from types import SimpleNamespace
+
+    import paper_1602_06589_b200 as pkg
+
+    d = golden("assemble_t.npz")
+    assert np.max(np.abs(pkg.gaunt_tensor(3, 2) - d["g32"])) <= 1e-14
+    assert np.max(np.abs(pkg.gaunt_tensor(2, 2) - d["g22"])) <= 1e-14
+    for row, want, want2 in zip(d["gaunt_args"], d["gaunt_vals"], d["gaunt_vals_refine2"]):
+        lp, mp, l, m, lpp, mpp = (int(x) for x in row)
+        assert abs(pkg.gaunt((lp, mp), (l, m), (lpp, mpp)) - want) <= 1e-14
+        assert abs(pkg.gaunt((lp, mp), (l, m), (lpp, mpp), refine=2) - want2) <= 1e-14
+    n = len(d["l_sph"])
+    radial = [SimpleNamespace(energy=d[f"energy{a}"], udot_norm=d[f"udot_norm{a}"]) for a in range(n)]
+    spec = SimpleNamespace(n_atoms=n, l_sph=d["l_sph"], l_nonsph=d["l_nonsph"], radial=radial)
+    ris = [pkg.RadialIntegrals(d[f"c_uu{a}"], d[f"c_dd{a}"], d[f"c_ud{a}"], d[f"c_du{a}"])
+           for a in range(n)]
+    tm = pkg.assemble_T(spec, ris)
+    for a in range(n):
+        for got, key in ((tm.t_aa[a], "t_aa"), (tm.t_ab[a], "t_ab"), (tm.t_bb[a], "t_bb")):
+            want = d[f"{key}{a}"]
+            assert np.max(np.abs(got.array - want)) <= 1e-13 * max(1.0, np.max(np.abs(want)))
+    # the reference's generator gives the same integrals for the same seed
+    ri0 = pkg.synth_radial_integrals(40, int(d["l_nonsph"][0]))
+    np.testing.assert_allclose(ri0.c_uu, d["c_uu0"], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(ri0.c_du, d["c_du0"], rtol=0, atol=1e-15)
+    bad = pkg.RadialIntegrals(d["c_uu0"] + 0.1, d["c_dd0"], d["c_ud0"], d["c_du0"])
+    with pytest.raises(pkg.ContractViolationError):
+        pkg.assemble_T(spec, [bad] + ris[1:])
+    with pytest.raises(pkg.ContractViolationError):
+        pkg.assemble_T(spec, ris[:2])

@@ -145,3 +145,27 @@ def test_reduced_overlap_matches_reference():
     s = orr.reduced_s_aa(f, w, inst.spec.positions, inst.spec.k_vectors, inst.spec.omega)
     assert rel_fro(s @ d["c1_V"], d["c1_SV"]) <= 1e-13
     assert rel_fro(np.diag(s), d["c1_diag"]) <= 1e-13
+
+
+def test_oracle_gaunt_and_assemble_t_vs_reference():
+    """The oracle's Gaunt tensor and assemble_T against the reference's own outputs."""
+    from oracle import assemble as oa
+
+    d = golden("assemble_t.npz")
+    assert np.max(np.abs(oa.gaunt_tensor(3, 2) - d["g32"])) <= 1e-14
+    assert np.max(np.abs(oa.gaunt_tensor(2, 2) - d["g22"])) <= 1e-14
+    for row, want, want2 in zip(d["gaunt_args"], d["gaunt_vals"], d["gaunt_vals_refine2"]):
+        lp, mp, l, m, lpp, mpp = (int(x) for x in row)
+        lmax = max(lp, l, lpp)
+        i, j, k = lp * lp + lp + mp, l * l + l + m, lpp * lpp + lpp + mpp
+        assert abs(oa.gaunt_tensor(lmax, lmax)[i, j, k] - want) <= 1e-14
+        assert abs(oa.gaunt_tensor(lmax, lmax, refine=2)[i, j, k] - want2) <= 1e-14
+    n = len(d["l_sph"])
+    ints = [(d[f"c_uu{a}"], d[f"c_ud{a}"], d[f"c_dd{a}"]) for a in range(n)]
+    taa, tab, tbb = oa.assemble_T(list(d["l_sph"]), list(d["l_nonsph"]),
+                                  [d[f"energy{a}"] for a in range(n)],
+                                  [d[f"udot_norm{a}"] for a in range(n)], ints)
+    for a in range(n):
+        for got, key in ((taa[a], "t_aa"), (tab[a], "t_ab"), (tbb[a], "t_bb")):
+            want = d[f"{key}{a}"]
+            assert np.max(np.abs(got - want)) <= 1e-13 * max(1.0, np.max(np.abs(want)))

@@ -19,13 +19,14 @@ from .special import spherical_harmonics_all
 
 def quadrature_grid(l_max: int, refine: int = 1):
     """(Y on the grid, weights) (`special.py:189-204`)."""
-    n_theta, n_phi = refine * (2 * l_max + 1), refine * (4 * l_max + 1)
-    ct, wt = np.polynomial.legendre.leggauss(n_theta)
-    phi = np.arange(n_phi) * (2.0 * np.pi / n_phi)
-    ct_g, phi_g = np.repeat(ct, n_phi), np.tile(phi, n_theta)
-    w = np.repeat(wt, n_phi) * (2.0 * np.pi / n_phi)
-    st_g = np.sqrt(np.maximum(0.0, 1.0 - ct_g * ct_g))
-    dirs = np.stack([st_g * np.cos(phi_g), st_g * np.sin(phi_g), ct_g], axis=1)
+    nodes, node_w = np.polynomial.legendre.leggauss(refine * (2 * l_max + 1))
+    n_az = refine * (4 * l_max + 1)
+    az = 2.0 * np.pi * np.arange(n_az) / n_az
+    grid_c, grid_a = np.meshgrid(nodes, az, indexing="ij")
+    w = (node_w[:, None] * np.full((1, n_az), 2.0 * np.pi / n_az)).ravel()
+    c, a = grid_c.ravel(), grid_a.ravel()
+    s = np.sqrt(np.clip(1.0 - c * c, 0.0, None))
+    dirs = np.column_stack((s * np.cos(a), s * np.sin(a), c))
     return spherical_harmonics_all(l_max, dirs), w
 
 

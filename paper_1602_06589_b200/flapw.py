@@ -222,31 +222,22 @@ class RadialIntegrals:
 
 
 def _pairing(c: np.ndarray) -> np.ndarray:
-    """The Hermitian-compatibility involution on (l', l, L'') arrays (`flapw.py:276-286`)."""
-    from .special import lm_index
-
-    n_pot = c.shape[2]
-    l_pot = int(np.sqrt(n_pot)) - 1
-    perm = np.empty(n_pot, dtype=np.int64)
-    sign = np.empty(n_pot)
-    for l in range(l_pot + 1):
-        for m in range(-l, l + 1):
-            perm[lm_index(l, m)] = lm_index(l, -m)
-            sign[lm_index(l, m)] = -1.0 if m % 2 else 1.0
-    return sign[None, None, :] * np.conj(c.transpose(1, 0, 2)[:, :, perm])
+    """The Hermitian-compatibility involution on (l', l, L'') arrays (`flapw.py:276-286`):
+    swap l' <-> l, conjugate, and map L'' = (l'', m'') to (-1)^m'' x entry (l'', -m'')."""
+    l_pot = int(round(np.sqrt(c.shape[2]))) - 1
+    lm = np.array([(l, m) for l in range(l_pot + 1) for m in range(-l, l + 1)], dtype=np.int64)
+    flipped = lm[:, 0] * (lm[:, 0] + 1) - lm[:, 1]  # compound index of (l'', -m'')
+    parity = np.where(lm[:, 1] % 2 == 0, 1.0, -1.0)
+    return np.conj(np.swapaxes(c, 0, 1))[:, :, flipped] * parity
 
 
 def synth_radial_integrals(seed: int, l_nonsph: int, scale: float = 0.5) -> RadialIntegrals:
-    """Seeded radial integrals satisfying the pairing (`flapw.py:289-307`; same draws)."""
-    rng = np.random.default_rng(seed)
-    n_l = l_nonsph + 1
-    n_pot = n_l * n_l
-
-    def draw():
-        return scale * (rng.standard_normal((n_l, n_l, n_pot))
-                        + 1j * rng.standard_normal((n_l, n_l, n_pot)))
-
-    x_uu, x_dd, c_ud = draw(), draw(), draw()
+    """Seeded radial integrals satisfying the pairing (`flapw.py:289-307`; the same normal
+    draws in the same order, so a seed gives the reference's integrals)."""
+    gen = np.random.default_rng(seed)
+    shape = (l_nonsph + 1, l_nonsph + 1, (l_nonsph + 1) ** 2)
+    z = [gen.standard_normal((2,) + shape) for _ in range(3)]  # (re, im) of uu, dd, ud
+    x_uu, x_dd, c_ud = (scale * (v[0] + 1j * v[1]) for v in z)
     return RadialIntegrals(c_uu=0.5 * (x_uu + _pairing(x_uu)), c_dd=0.5 * (x_dd + _pairing(x_dd)),
                            c_ud=c_ud, c_du=_pairing(c_ud))
 

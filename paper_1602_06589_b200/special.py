@@ -85,15 +85,13 @@ def _quadrature_grid(l_max: int, refine: int = 1):
     Gauss-Legendre in cos(theta) x uniform phi; returns device Y ((l_max+1)^2 x npts) and
     device weights.  The nodes are constants computed once on the host."""
     t = device.require_cuda()
-    n_theta = refine * (2 * l_max + 1)
+    cos_t, w_t = np.polynomial.legendre.leggauss(refine * (2 * l_max + 1))
     n_phi = refine * (4 * l_max + 1)
-    ct, wt = np.polynomial.legendre.leggauss(n_theta)
-    phi = np.arange(n_phi) * (2.0 * np.pi / n_phi)
-    ct_g = np.repeat(ct, n_phi)
-    phi_g = np.tile(phi, n_theta)
-    w = np.repeat(wt, n_phi) * (2.0 * np.pi / n_phi)
-    st_g = np.sqrt(np.maximum(0.0, 1.0 - ct_g * ct_g))
-    dirs = np.stack([st_g * np.cos(phi_g), st_g * np.sin(phi_g), ct_g], axis=1)
+    ang = np.linspace(0.0, 2.0 * np.pi, n_phi, endpoint=False)
+    ct, ph = (g.ravel() for g in np.meshgrid(cos_t, ang, indexing="ij"))
+    w = np.outer(w_t, np.full(n_phi, 2.0 * np.pi / n_phi)).ravel()
+    sin_t = np.sqrt(np.clip(1.0 - ct * ct, 0.0, None))
+    dirs = np.column_stack((sin_t * np.cos(ph), sin_t * np.sin(ph), ct))
     n = dirs.shape[0]
     dd = t.from_numpy(np.ascontiguousarray(dirs)).cuda()
     y = t.empty(((l_max + 1) ** 2, n), dtype=t.complex128, device="cuda")

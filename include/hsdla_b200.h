@@ -266,6 +266,13 @@ typedef struct {
    * dense part and one 2x2 block per tail row, and the T applications run with K = d plus an
    * elementwise tail; otherwise T is treated as dense. */
   const int32_t* t_dense;
+  /* HOST n_tsets x (max t_dim) or NULL: ||udot||^2 of each row of the set's atoms (a row < 0 =
+   * the set may not be shifted: its atoms differ in ||udot|| or have T smaller than their block).
+   * With it the joint H form also covers T sets that are not HPD: every set is factored as
+   * T + sigma diag(I, U^2) with one common sigma >= 0 and H = sum W^H W - sigma S, because
+   * [A; B]^H sigma diag(I, U^2) [A; B] summed over the atoms is sigma S exactly.  Applied only
+   * when every set can take that shift; otherwise non-HPD sets use the reference forms. */
+  const double* t_udot2;
 } hsdla_build_args;
 
 typedef struct {
@@ -278,6 +285,7 @@ typedef struct {
   float ms_total;                               /* out: first event to last kernel / copy */
   int32_t* joint_info;        /* HOST out n_tsets or NULL: 1 = H used the joint T factor for this set,
                                  2 = with the dense / diagonal-tail split */
+  double joint_shift;         /* out: the common shift sigma of the joint form (0 = none) */
 } hsdla_build_result;
 
 size_t hsdla_build_workspace_size(const hsdla_build_args* args);

@@ -73,7 +73,7 @@ class BuildArgs(ctypes.Structure):
         ("shard_mirror", _i32), ("reuse_t", _i32), ("stream_h_copy", _i32),
         ("h_reference_form", _i32),
         ("A_host", _vp), ("B_host", _vp), ("ld_ab_host", _i64),
-        ("t_dense", _P_i32),
+        ("t_dense", _P_i32), ("t_udot2", ctypes.POINTER(ctypes.c_double)),
     ]
 
 
@@ -84,7 +84,7 @@ class BuildResult(ctypes.Structure):
         ("ms_H_ABBA_BB", ctypes.c_float), ("ms_H_AA", ctypes.c_float),
         ("ms_contract_S", ctypes.c_float), ("ms_contract_H", ctypes.c_float),
         ("ms_apply_Z", ctypes.c_float), ("ms_apply_XY", ctypes.c_float),
-        ("ms_total", ctypes.c_float), ("joint_info", _P_i32),
+        ("ms_total", ctypes.c_float), ("joint_info", _P_i32), ("joint_shift", ctypes.c_double),
     ]
 
 

@@ -459,7 +459,7 @@ def build_all(coeffs: StackedCoefficients, tmats: TMatrixSet, config: BuildConfi
                            row_offset=layout.offsets[:-1], tpack=tpack, A=a_d, B=b_d, Bs=None,
                            udot=udot, ld=ld, force_general_path=config.force_general_path,
                            H=h_d, S=s_d, ldh=n, host_out=(h_host[1], s_host[1]),
-                           host_src=src)
+                           host_src=src, udot_rows=np.asarray(coeffs.udot_norms))
     if not config.backup:
         regenerate(coeffs)
         if coeffs.A_star.rows != layout.total_rows or coeffs.A_star.cols != n:

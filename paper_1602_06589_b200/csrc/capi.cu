@@ -154,7 +154,7 @@ int hsdla_ctx_create(hsdla_ctx** out, void* stream) {
   if (int rc = preload_gaunt()) return rc;
   // Mapped pinned memory: build results are published by a kernel store, not a DMA copy,
   // so they never queue behind the large H / S copies on the D2H engine.
-  HS_CUDA(cudaHostAlloc(&c->scratch_host, 1024 * sizeof(int), cudaHostAllocMapped));
+  HS_CUDA(cudaHostAlloc(&c->scratch_host, 2048 * sizeof(int), cudaHostAllocMapped));
   HS_CUDA(cudaHostGetDevicePointer((void**)&c->scratch_host_dev, c->scratch_host, 0));
   HS_CUDA(cudaEventCreateWithFlags(&c->stage_done, cudaEventDisableTiming));
   HS_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
@@ -503,7 +503,7 @@ constexpr unsigned kWaitGeq = 0x0;  // CU_STREAM_WAIT_VALUE_GEQ
 // ---- composed build ------------------------------------------------------------------
 namespace {
 struct WsLayout {
-  size_t bs, z, xy, forms, tdim, info, joint, jinfo, total;
+  size_t bs, z, xy, forms, tdim, info, joint, jinfo, u2, total;
   int mp;
   long long R;
 };
@@ -530,6 +530,8 @@ WsLayout ws_layout(const hsdla_build_args* a) {
   off += align_up(size_t(a->n_tsets) * 4 * mp * mp * sizeof(double2));
   w.jinfo = off;
   off += align_up(a->n_tsets * sizeof(int));
+  w.u2 = off;  // per T set: ||udot||^2 rows (shift metric), n_tsets x mp doubles
+  off += align_up(size_t(a->n_tsets) * mp * sizeof(double));
   w.bs = off;
   off += a->B_scaled ? 0 : stack;
   w.z = off;
@@ -583,6 +585,7 @@ int complete_slot(hsdla_ctx* ctx, hsdla_ctx::BuildSlot& sl, hsdla_ctx::Outcome* 
     o->hpd[i] = (!sl.force && o->info[sl.t_index[i]] == 0) ? 1 : 0;
   o->nonfinite = area[0];
   o->joint = sl.joint;
+  o->sigma = sl.sigma;
   cudaEvent_t* ev = sl.ev;
   float t01 = 0, t12 = 0, t23 = 0, t34 = 0, t46 = 0, t07 = 0;
   cudaEventElapsedTime(&t01, ev[0], ev[1]);
@@ -613,6 +616,8 @@ int complete_slot(hsdla_ctx* ctx, hsdla_ctx::BuildSlot& sl, hsdla_ctx::Outcome* 
 // stream_copies: copy H out panel by panel while the H contraction runs (synchronous calls,
 // where nothing follows that the copy could overlap instead); pipelined builds copy H whole
 // under the next k-point, which measured faster per k-point.
+constexpr double kShiftAmplification = 16.0;  // shifted joint form: max sigma ||D|| / ||T||
+
 int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args* ab,
                   unsigned long long* ticket, bool stream_copies) {
   const int na = a->n_atoms, n = a->n_basis;
@@ -684,13 +689,22 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
   std::vector<int> tsz(a->t_dim, a->t_dim + a->n_tsets);
   for (int t = 0; t < a->n_tsets; ++t)
     tsz.push_back(a->t_dense ? std::min(std::max(a->t_dense[t], 0), a->t_dim[t]) : a->t_dim[t]);
-  rc = arena_begin(ctx, tsz.size() * sizeof(int) + 64);
+  // shift metric rows: only without sharding, and only with the caller's ||udot||^2 rows
+  std::vector<double> u2h;
+  if (a->t_udot2 && !sharded) u2h.assign(a->t_udot2, a->t_udot2 + size_t(a->n_tsets) * mp);
+  rc = arena_begin(ctx, tsz.size() * sizeof(int) + u2h.size() * sizeof(double) + 128);
   if (rc) return rc;
   const int* tdim_src = static_cast<const int*>(arena_push(ctx, tsz.data(), tsz.size() * sizeof(int), nullptr));
+  const double* u2_src = u2h.empty() ? nullptr
+      : static_cast<const double*>(arena_push(ctx, u2h.data(), u2h.size() * sizeof(double), nullptr));
   rc = arena_flush(ctx);
   if (rc) return rc;
   HS_CUDA(cudaMemcpyAsync(tdim_dev, tdim_src, tsz.size() * sizeof(int), cudaMemcpyDeviceToDevice,
                           ctx->stream));
+  double* u2_dev = reinterpret_cast<double*>(ws + w.u2);
+  if (u2_src)
+    HS_CUDA(cudaMemcpyAsync(u2_dev, u2_src, u2h.size() * sizeof(double), cudaMemcpyDeviceToDevice,
+                            ctx->stream));
   // T preparation + Cholesky on the side stream, overlapping A/B generation — or nothing,
   // when the caller vouches that T is unchanged and the previous results are still here.
   hsdla_ctx::TKey key;
@@ -710,11 +724,13 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
   key.joint = (!a->force_general_path && !a->h_reference_form && joint_env) ? 1 : 0;
   key.tdim.assign(a->t_dim, a->t_dim + a->n_tsets);
   key.tdense.assign(tsz.begin() + a->n_tsets, tsz.end());
+  key.u2 = u2h;
   const hsdla_ctx::TKey& old = ctx->tkey;
   const bool reuse = a->reuse_t && old.ws == key.ws && old.forms_off == key.forms_off &&
                      old.info_off == key.info_off && old.taa == key.taa && old.tab == key.tab &&
                      old.tbb == key.tbb && old.t_ld == key.t_ld && old.force == key.force &&
-                     old.joint == key.joint && old.tdim == key.tdim && old.tdense == key.tdense;
+                     old.joint == key.joint && old.tdim == key.tdim && old.tdense == key.tdense &&
+                     old.u2 == key.u2;
   HS_CUDA(cudaEventRecord(ctx->fork, ctx->stream));
   if (host_src) {
     // A then B on the copy stream, after everything already queued (earlier builds read A / B)
@@ -734,14 +750,18 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
                       D2(a->t_bb), a->t_ld, forms, a->force_general_path ? 0 : 1, info_dev);
     if (rc) return rc;
     if (key.joint) {  // info also to the mapped host words [400, 496)
+      // search mode: each set's smallest working shift (0 if HPD) to the mapped doubles
       rc = launch_tjoint(ctx->side, a->n_tsets, tdim_dev, tdim_dev + a->n_tsets, mp, D2(a->t_aa),
                          D2(a->t_ab), D2(a->t_bb), a->t_ld, joint, jinfo_dev,
-                         ctx->scratch_host_dev + 400, ctx->scratch_host_dev + 600);
+                         ctx->scratch_host_dev + 400, ctx->scratch_host_dev + 600,
+                         u2_src ? u2_dev : nullptr, -1.0,
+                         reinterpret_cast<double*>(ctx->scratch_host_dev + 704));
       if (rc) return rc;
     }
     HS_CUDA(cudaEventRecord(ctx->join, ctx->side));
     ctx->joint_info.assign(a->n_tsets, -2);
     ctx->joint_split.assign(a->n_tsets, 0);
+    ctx->joint_sigma = 0.0;
     ctx->joint_pending = key.joint != 0;  // read after the S contraction is enqueued
     ctx->tkey = key;
   } else {
@@ -873,12 +893,57 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     HS_CUDA(cudaEventSynchronize(ctx->join));
     const volatile int* jhost = ctx->scratch_host + 400;
     const volatile int* shost = ctx->scratch_host + 600;  // split flags [600, 696)
+    const volatile double* ghost = reinterpret_cast<const double*>(ctx->scratch_host + 704);
+    std::vector<double> g(a->n_tsets);  // search result per set: shift used, -1 = no factor
+    double smax = 0.0;
+    bool all_ok = true;
     for (int t = 0; t < a->n_tsets; ++t) {
       ctx->joint_info[t] = jhost[t];
       ctx->joint_split[t] = shost[t];
+      g[t] = jhost[t] == 0 ? ghost[t] : -1.0;
+      all_ok = all_ok && g[t] >= 0.0;
+      smax = std::max(smax, g[t]);
+    }
+    // Shift guard: H = sum W^H W - sigma S cancels terms of size sigma ||diag(I, U^2)|| against
+    // ||T|| (Gershgorin radius rho); beyond a 16x amplification of the rounding error the
+    // reference forms are the accurate choice.
+    if (smax > 0.0 && all_ok) {
+      for (int t = 0; t < a->n_tsets; ++t) {
+        double dmax = 1.0;
+        for (int i = 0; i < a->t_dim[t]; ++i) dmax = std::max(dmax, u2h[size_t(t) * mp + i]);
+        const double rho = ghost[96 + t];
+        if (!(rho > 0.0) || smax * dmax > kShiftAmplification * rho) all_ok = false;
+      }
+    }
+    if (smax > 0.0) {
+      // Some set needed a shift.  H = sum W^H W - sigma S holds only with one sigma for every
+      // atom: refactor all sets with the largest shift, or keep only the unshifted HPD sets.
+      bool shifted = false;
+      if (all_ok) {
+        rc = launch_tjoint(ctx->side, a->n_tsets, tdim_dev, tdim_dev + a->n_tsets, mp, D2(a->t_aa),
+                           D2(a->t_ab), D2(a->t_bb), a->t_ld, joint, jinfo_dev,
+                           ctx->scratch_host_dev + 400, ctx->scratch_host_dev + 600, u2_dev, smax,
+                           reinterpret_cast<double*>(ctx->scratch_host_dev + 704));
+        if (rc) return rc;
+        HS_CUDA(cudaStreamSynchronize(ctx->side));
+        shifted = true;
+        for (int t = 0; t < a->n_tsets; ++t) {
+          ctx->joint_info[t] = jhost[t];
+          ctx->joint_split[t] = shost[t];
+          shifted = shifted && jhost[t] == 0;
+        }
+      }
+      if (shifted) {
+        ctx->joint_sigma = smax;
+      } else {
+        // search-mode factors of HPD sets are unshifted and usable, unless a refactor overwrote them
+        for (int t = 0; t < a->n_tsets; ++t)
+          if (all_ok || g[t] != 0.0) ctx->joint_info[t] = 1;
+      }
     }
     ctx->joint_pending = false;
   }
+  sl.sigma = key.joint ? ctx->joint_sigma : 0.0;
   sl.joint.assign(a->n_tsets, 0);
   bool any_joint = false, all_joint = true;
   for (int t = 0; t < a->n_tsets; ++t) {
@@ -980,7 +1045,7 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
   // ---- H = Z^H B + B^H Z + sum_HPD Y^H Y + sum_nonHPD A^H X   (builder.py:246-247, :305-311)
   //      AA segments per run of atoms sharing one T set: P = XY (HPD) or A (general).
   if (prev.copies && prev.h_dev == a->H) HS_CUDA(cudaStreamWaitEvent(ctx->stream, prev.h_copied, 0));
-  const bool h_streamed = waitv && a->H_host;
+  const bool h_streamed = waitv && a->H_host && sl.sigma == 0.0;  // shifted: copy after -= sigma S
   if (h_streamed) {
     rc = stream_out(D2(a->H), a->H_host, sl.panel_cnt + nbp, sl.h_copied);
     if (rc) return rc;
@@ -1025,6 +1090,10 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     rc = launch_contract(ctx, probs, segs, flag);
     if (rc) return rc;
   }
+  if (sl.sigma > 0.0) {  // shifted joint form: H = sum W^H W - sigma S (both full Hermitian)
+    rc = launch_axpy_shift(ctx, n, sl.sigma, D2(a->S), a->ldh, D2(a->H), a->ldh);
+    if (rc) return rc;
+  }
   HS_CUDA(cudaEventRecord(ev[6], ctx->stream));
   if (h_streamed) {
     // H streamed during its contraction
@@ -1049,6 +1118,7 @@ int fill_result(const hsdla_ctx::Outcome& o, hsdla_build_result* res) {
     if (res->chol_info) res->chol_info[t] = o.info[t];
   for (size_t t = 0; t < o.joint.size(); ++t)
     if (res->joint_info) res->joint_info[t] = o.joint[t];
+  res->joint_shift = o.sigma;
   for (size_t i = 0; i < o.hpd.size(); ++i)
     if (res->hpd_mask) res->hpd_mask[i] = o.hpd[i];
   res->nonfinite = o.nonfinite;

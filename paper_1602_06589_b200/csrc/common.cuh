@@ -111,10 +111,12 @@ struct hsdla_ctx {
     long long t_ld = 0;
     int force = -1, joint = -1;
     std::vector<int> tdim, tdense;
+    std::vector<double> u2;
   } tkey;
   // Joint-factor info per T set of the T preparation in tkey (0 = H takes the joint form).
   std::vector<int> joint_info;
   std::vector<int> joint_split;  // per T set: 1 = the joint factor uses the dense/diagonal split
+  double joint_sigma = 0.0;      // common shift of the joint factors in tkey's workspace
   bool joint_pending = false;  // joint_info not read back yet (fresh T preparation in flight)
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // T preparation overlaps A/B generation here
@@ -138,6 +140,7 @@ struct hsdla_ctx {
     unsigned long long ticket = 0;
     std::vector<int> t_index;
     std::vector<int> joint;  // per T set: 1 = this build's H used the joint factor (2 = split)
+    double sigma = 0.0;      // this build's joint shift (H -= sigma S after the contraction)
     const void* h_dev = nullptr;  // this build's device H / S (copy hazards of the next build)
     const void* s_dev = nullptr;
   } slots[2];
@@ -146,6 +149,7 @@ struct hsdla_ctx {
   struct Outcome {
     int rc = 0, nonfinite = 0;
     std::vector<int> info, hpd, joint;
+    double sigma = 0.0;
     float ms[6] = {};
   };
   std::map<unsigned long long, Outcome> stash;
@@ -204,7 +208,11 @@ int launch_tprep(hsdla_ctx* ctx, cudaStream_t stream, int n_tsets, const int* td
 int launch_tjoint(cudaStream_t stream, int n_tsets, const int* tdim_dev, const int* tdense_dev,
                   int mp, const double2* taa, const double2* tab, const double2* tbb,
                   long long t_ld, double2* joint, int* info_dev, int* info_host_dev,
-                  int* split_host_dev);
+                  int* split_host_dev, const double* u2_dev, double sigma_fixed,
+                  double* sigma_host_dev);
+// C -= sigma S (full matrices): the shifted joint form's correction.
+int launch_axpy_shift(hsdla_ctx* ctx, int n, double sigma, const double2* S, long long lds,
+                      double2* C, long long ldc);
 // Tail rows [d, m) of split joint T sets: atoms_dev[e] = (row offset, d, m, T set).
 int launch_ttail(hsdla_ctx* ctx, const int4* atoms_dev, int n_atoms, int max_tail, int n_basis,
                  const double2* A, const double2* B, long long ld, double2* XY, double2* Z,

@@ -203,8 +203,10 @@ __global__ void tprep_kernel(const int* tdim, int mp, const double2* taa, const 
 // null.
 __global__ void tjoint_kernel(const int* tdim, const int* tdense, int mp, const double2* taa,
                               const double2* tab, const double2* tbb, long long t_ld,
-                              double2* joint, int* info, int* info_host, int* split_host) {
+                              double2* joint, int* info, int* info_host, int* split_host,
+                              const double* u2, double sigma_fixed, double* sigma_host) {
   __shared__ int s_off, s_tail_bad;
+  __shared__ double s_scale, s_rho;
   const int b = blockIdx.x;
   const int m = tdim[b];
   const int d = tdense ? min(max(tdense[b], 0), m) : m;
@@ -213,9 +215,38 @@ __global__ void tjoint_kernel(const int* tdim, const int* tdense, int mp, const 
   const double2* Taa = taa + b * tstride;
   const double2* Tab = tab + b * tstride;
   const double2* Tbb = tbb + b * tstride;
+  // Shift metric diag(I, U^2) of this set (u2 rows, < 0 = shift not allowed for this set)
+  const double* U2 = u2 ? u2 + (long long)b * mp : nullptr;
+  const bool can_shift = U2 && U2[0] >= 0.0;
   double2* J = joint + (long long)b * lj * lj;
-  if (threadIdx.x == 0) s_off = 0, s_tail_bad = 0;
+  if (threadIdx.x == 0) {
+    s_off = 0;
+    double sc = 0.0;  // max |T_ii| / D_ii: the scale of the shift search
+    if (can_shift)
+      for (int i = 0; i < m; ++i)
+        sc = fmax(sc, fmax(fabs(Taa[i + i * t_ld].x), fabs(Tbb[i + i * t_ld].x) / fmax(U2[i], 1e-300)));
+    s_scale = sc;
+    s_rho = 0.0;
+  }
   __syncthreads();
+  // Gershgorin radius of the 2m x 2m matrix (max absolute row sum): the shift guard's scale
+  if (sigma_host && sigma_fixed < 0.0) {
+    for (int r = threadIdx.x; r < 2 * m; r += blockDim.x) {
+      double acc = 0.0;
+      for (int c = 0; c < 2 * m; ++c) {
+        double2 v;
+        const int rr = r < m ? r : r - m, cc = c < m ? c : c - m;
+        if (r < m && c < m) v = rr >= cc ? Taa[rr + cc * t_ld] : cconj(Taa[cc + rr * t_ld]);
+        else if (r < m) v = Tab[rr + cc * t_ld];
+        else if (c < m) v = cconj(Tab[cc + rr * t_ld]);
+        else v = rr >= cc ? Tbb[rr + cc * t_ld] : cconj(Tbb[cc + rr * t_ld]);
+        if (rr == cc && (r < m) == (c < m)) v.y = 0.0;
+        acc += sqrt(v.x * v.x + v.y * v.y);
+      }
+      atomicMax(reinterpret_cast<unsigned long long*>(&s_rho), __double_as_longlong(acc));
+    }
+    __syncthreads();
+  }
   bool split = d < m;
   if (split) {  // every coupling of a tail row other than its own diagonal must vanish
     for (long long e = threadIdx.x; e < (long long)m * m; e += blockDim.x) {
@@ -233,40 +264,64 @@ __global__ void tjoint_kernel(const int* tdim, const int* tdense, int mp, const 
     split = s_off == 0;
   }
   const int h = split ? d : m, n = 2 * h;
-  for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) {
-    const int r = (int)(e % n), c = (int)(e / n);
-    if (r < c) continue;
-    double2 v;
-    if (r < h) v = Taa[r + c * t_ld];
-    else if (c < h) v = cconj(Tab[c + (r - h) * t_ld]);
-    else v = Tbb[(r - h) + (c - h) * t_ld];
-    if (r == c) v.y = 0.0;
-    J[r + c * lj] = v;
+  // sigma_fixed >= 0: factor T + sigma D once.  Otherwise T itself, and when that is not HPD and
+  // the set may shift, T + sigma D for sigma = scale * 2^(k - 12), k = 0, 1, ... (the first that
+  // is HPD, i.e. within 2x of the smallest such shift).
+  if (sigma_fixed > 0.0 && !can_shift) {  // a common shift cannot apply to this set
+    if (threadIdx.x == 0) {
+      info[b] = -3;
+      if (info_host) info_host[b] = -3;
+      if (split_host) split_host[b] = 0;
+      if (sigma_host) sigma_host[b] = -1.0;
+    }
+    return;
   }
-  __syncthreads();
-  if (lj <= kPackedMaxN) chol_packed(n, J, lj, J, lj, info + b);  // shared memory sized by 2*mp
-  else chol_block(n, J, lj, J, lj, info + b);
-  __syncthreads();
-  if (split && info[b] == 0) {
-    for (int i = d + threadIdx.x; i < m; i += blockDim.x) {
-      const double a = Taa[i + i * t_ld].x, c = Tbb[i + i * t_ld].x;
-      const double2 ab = Tab[i + i * t_ld];
-      bool ok = a > 0.0 && isfinite(a);
-      const double l11 = ok ? sqrt(a) : 1.0;
-      const double2 l21 = make_double2(ab.x / l11, -ab.y / l11);  // T_BA_ii / l11
-      const double rr = c - (l21.x * l21.x + l21.y * l21.y);
-      ok = ok && rr > 0.0 && isfinite(rr);
-      J[i + (lj - 2) * lj] = make_double2(l11, ok ? sqrt(rr) : 0.0);
-      J[i + (lj - 1) * lj] = l21;
-      if (!ok) atomicExch(&s_tail_bad, 1);
+  double sigma = sigma_fixed >= 0.0 ? sigma_fixed : 0.0;
+  const int attempts = (sigma_fixed < 0.0 && can_shift) ? 40 : 1;
+  for (int att = 0; att < attempts; ++att) {
+    if (att > 0) sigma = s_scale * ldexp(1.0, att - 13);
+    for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) {
+      const int r = (int)(e % n), c = (int)(e / n);
+      if (r < c) continue;
+      double2 v;
+      if (r < h) v = Taa[r + c * t_ld];
+      else if (c < h) v = cconj(Tab[c + (r - h) * t_ld]);
+      else v = Tbb[(r - h) + (c - h) * t_ld];
+      if (r == c) {
+        v.y = 0.0;
+        if (sigma != 0.0) v.x += sigma * (r < h ? 1.0 : U2[r - h]);
+      }
+      J[r + c * lj] = v;
+    }
+    if (threadIdx.x == 0) s_tail_bad = 0;
+    __syncthreads();
+    if (lj <= kPackedMaxN) chol_packed(n, J, lj, J, lj, info + b);  // shared memory sized by 2*mp
+    else chol_block(n, J, lj, J, lj, info + b);
+    __syncthreads();
+    if (split && info[b] == 0) {
+      for (int i = d + threadIdx.x; i < m; i += blockDim.x) {
+        const double a = Taa[i + i * t_ld].x + sigma, c = Tbb[i + i * t_ld].x + (sigma != 0.0 ? sigma * U2[i] : 0.0);
+        const double2 ab = Tab[i + i * t_ld];
+        bool ok = a > 0.0 && isfinite(a);
+        const double l11 = ok ? sqrt(a) : 1.0;
+        const double2 l21 = make_double2(ab.x / l11, -ab.y / l11);  // T_BA_ii / l11
+        const double rr = c - (l21.x * l21.x + l21.y * l21.y);
+        ok = ok && rr > 0.0 && isfinite(rr);
+        J[i + (lj - 2) * lj] = make_double2(l11, ok ? sqrt(rr) : 0.0);
+        J[i + (lj - 1) * lj] = l21;
+        if (!ok) atomicExch(&s_tail_bad, 1);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0 && s_tail_bad) info[b] = n + 1;  // a tail block is not HPD
     }
     __syncthreads();
-    if (threadIdx.x == 0 && s_tail_bad) info[b] = n + 1;  // a tail block is not HPD
+    if (info[b] == 0 || info[b] == -1) break;  // HPD, or NaN input (no shift helps)
   }
-  __syncthreads();
   if (threadIdx.x == 0) {
     if (info_host) info_host[b] = info[b];
     if (split_host) split_host[b] = split ? 1 : 0;
+    if (sigma_host) sigma_host[b] = info[b] == 0 ? sigma : -1.0;
+    if (sigma_host && sigma_fixed < 0.0) sigma_host[96 + b] = s_rho;  // guard scale
   }
 }
 
@@ -392,13 +447,36 @@ int launch_tprep(hsdla_ctx* ctx, cudaStream_t stream, int n_tsets, const int* td
 int launch_tjoint(cudaStream_t stream, int n_tsets, const int* tdim_dev, const int* tdense_dev,
                   int mp, const double2* taa, const double2* tab, const double2* tbb,
                   long long t_ld, double2* joint, int* info_dev, int* info_host_dev,
-                  int* split_host_dev) {
+                  int* split_host_dev, const double* u2_dev, double sigma_fixed,
+                  double* sigma_host_dev) {
   if (n_tsets <= 0) return HSDLA_OK;
   const int n = 2 * mp;
   size_t smem = (n <= kPackedMaxN) ? size_t(n) * (n + 1) / 2 * sizeof(double2)
                                    : size_t(n) * sizeof(double2);
   tjoint_kernel<<<n_tsets, 512, smem, stream>>>(tdim_dev, tdense_dev, mp, taa, tab, tbb, t_ld,
-                                                joint, info_dev, info_host_dev, split_host_dev);
+                                                joint, info_dev, info_host_dev, split_host_dev,
+                                                u2_dev, sigma_fixed, sigma_host_dev);
+  HS_CHECK_LAUNCH();
+  return HSDLA_OK;
+}
+
+// C -= sigma * S over the full n x n matrices (both column-major, ld ldc / lds).
+__global__ void axpy_shift_kernel(int n, double sigma, const double2* __restrict__ S, long long lds,
+                                  double2* __restrict__ C, long long ldc) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const long long j = blockIdx.y;
+  if (i >= n) return;
+  const double2 s = S[i + j * lds];
+  double2 c = C[i + j * ldc];
+  c.x -= sigma * s.x;
+  c.y -= sigma * s.y;
+  C[i + j * ldc] = c;
+}
+
+int launch_axpy_shift(hsdla_ctx* ctx, int n, double sigma, const double2* S, long long lds,
+                      double2* C, long long ldc) {
+  if (n <= 0) return HSDLA_OK;
+  axpy_shift_kernel<<<dim3((n + 255) / 256, n), 256, 0, ctx->stream>>>(n, sigma, S, lds, C, ldc);
   HS_CHECK_LAUNCH();
   return HSDLA_OK;
 }
@@ -478,7 +556,8 @@ int preload_small() {
                        (const void*)mirror_kernel, (const void*)scale_rows_kernel,
                        (const void*)prep_kernel, (const void*)publish_kernel,
                        (const void*)zero_rows_kernel, (const void*)finite_kernel,
-                       (const void*)tjoint_kernel, (const void*)ttail_kernel};
+                       (const void*)tjoint_kernel, (const void*)ttail_kernel,
+                       (const void*)axpy_shift_kernel};
   for (const void* f : fns) {
     cudaFuncAttributes at;
     HS_CUDA(cudaFuncGetAttributes(&at, f));

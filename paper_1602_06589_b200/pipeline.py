@@ -77,6 +77,21 @@ class TPack:
         return int(self.t_dim.shape[0])
 
 
+def tset_udot2(tpack, heights, row_offset, udot_rows) -> np.ndarray:
+    """(n_tsets, max t_dim) ||udot||^2 rows per T set for the shifted joint form; a row of -1
+    where the set's atoms differ in ||udot|| or have T smaller than their block (no shift)."""
+    mp = int(max(1, int(np.max(tpack.t_dim))))
+    out = np.full((tpack.n_tsets, mp), -1.0)
+    u = np.asarray(udot_rows, dtype=np.float64)
+    for t in range(tpack.n_tsets):
+        m = int(tpack.t_dim[t])
+        atoms = np.nonzero(np.asarray(tpack.t_index) == t)[0]
+        rows = [u[int(row_offset[a]):int(row_offset[a]) + int(heights[a])] for a in atoms]
+        if rows and all(len(r) == m for r in rows) and all(np.array_equal(r, rows[0]) for r in rows):
+            out[t, :m] = rows[0] * rows[0]
+    return out
+
+
 def pack_tmats(tmats) -> TPack:
     """Deduplicate per-atom T blocks by identity and upload them (one H2D)."""
     device.require_cuda()
@@ -141,6 +156,10 @@ class DeviceSpec:
             radial[a, :n, 3] = rad.udot_prime[:n]
             radial[a, :n, 4] = rad.udot_norm[:n]
         self.radial_stride = stride
+        # ||udot|| per stacked row (l^2 + l + m order): the joint form's shift metric
+        self.udot_rows = np.concatenate([np.repeat(np.asarray(spec.radial[a].udot_norm[:l + 1], dtype=np.float64),
+                                                   2 * np.arange(l + 1) + 1)
+                                         for a, l in enumerate(self.l_sph)])
         host = [np.asarray(spec.k_vectors, dtype=np.float64),
                 np.asarray(spec.positions, dtype=np.float64),
                 np.asarray(spec.rotations, dtype=np.float64).reshape(-1, 9),
@@ -186,7 +205,7 @@ class _Call:
     def __init__(self, *, n_basis, heights, row_offset, tpack: TPack, A, B, Bs, udot, ld,
                  force_general_path, H, S, ldh, shard_rank, n_shards, workspace, host_out,
                  ab_args=None, shard_mirror=False, reuse_t=False, stream_h_copy=0,
-                 h_reference_form=False, host_src=None, n_capacity=None):
+                 h_reference_form=False, host_src=None, n_capacity=None, udot_rows=None):
         lib = _native.load()
         t = device.torch()
         self.na = len(heights)
@@ -207,6 +226,10 @@ class _Call:
         a.n_tsets = tpack.n_tsets
         a.t_dim = td.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
         a.t_dense = self.keep[-1].ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+        if udot_rows is not None and n_shards <= 1:
+            u2 = tset_udot2(tpack, heights, row_offset, udot_rows)
+            self.keep.append(u2)
+            a.t_udot2 = u2.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
         a.t_aa = tpack.t_aa.data_ptr()
         a.t_ab = tpack.t_ab.data_ptr()
         a.t_bb = tpack.t_bb.data_ptr()
@@ -265,6 +288,7 @@ class _Call:
             "chol_info": [int(self.info[i]) for i in range(self.n_tsets)],
             "joint_t": [bool(self.joint[i]) for i in range(self.n_tsets)],
             "joint_split": [self.joint[i] == 2 for i in range(self.n_tsets)],
+            "joint_shift": float(r.joint_shift),
             "ms": {"setup": r.ms_setup, "S": r.ms_S, "H_ABBA_BB": r.ms_H_ABBA_BB,
                    "H_AA": r.ms_H_AA},
             "kernel_ms": {"contract_S": r.ms_contract_S, "contract_H": r.ms_contract_H,
@@ -298,14 +322,15 @@ class _Call:
 
 def build_device(*, n_basis, heights, row_offset, tpack: TPack, A, B, Bs, udot, ld,
                  force_general_path, H, S, ldh, shard_rank=0, n_shards=1, workspace=None,
-                 ab_args=None, host_out=None, h_reference_form=False, host_src=None):
+                 ab_args=None, host_out=None, h_reference_form=False, host_src=None,
+                 udot_rows=None):
     """Synchronous `hsdla_build_hs` (or `hsdla_setup_hs` when `ab_args` is given: A/B
     generation fused in front); returns (result dict, workspace tensor)."""
     call = _Call(n_basis=n_basis, heights=heights, row_offset=row_offset, tpack=tpack, A=A, B=B,
                  Bs=Bs, udot=udot, ld=ld, force_general_path=force_general_path, H=H, S=S,
                  ldh=ldh, shard_rank=shard_rank, n_shards=n_shards, workspace=workspace,
                  host_out=host_out, ab_args=ab_args,
-                 h_reference_form=h_reference_form, host_src=host_src)
+                 h_reference_form=h_reference_form, host_src=host_src, udot_rows=udot_rows)
     return call.run_sync(), call.workspace
 
 
@@ -384,7 +409,8 @@ class HSPipeline:
                      ldh=self.n_capacity, shard_rank=self.shard_rank, n_shards=self.n_shards,
                      workspace=self.workspace, host_out=host_out, ab_args=ab,
                      shard_mirror=self.shard_mirror, reuse_t=reuse, stream_h_copy=stream_h_copy,
-                     h_reference_form=self.h_reference_form, n_capacity=self.n_capacity)
+                     h_reference_form=self.h_reference_form, n_capacity=self.n_capacity,
+                     udot_rows=dspec.udot_rows)
         call.keep.append(dspec)
         self.workspace = call.workspace
         self._last_t = (tpack, bool(force_general_path))

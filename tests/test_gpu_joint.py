@@ -54,7 +54,7 @@ def _case(pkg, seed, heights, n_g, t_sizes, aa_shifts, bb_shifts):
     return co, tm, (a.array.copy(), b.array.copy(), u.copy(), herm, tab, hbb)
 
 
-def _build(pkg, co, tm, force=False, reference_form=False):
+def _build(pkg, co, tm, force=False, reference_form=False, shift=False):
     import torch
 
     from paper_1602_06589_b200 import device
@@ -71,7 +71,8 @@ def _build(pkg, co, tm, force=False, reference_form=False):
     res, _ = build_device(n_basis=n, heights=lay.block_heights, row_offset=lay.offsets[:-1],
                           tpack=pack_tmats(tm), A=a_d, B=b_d, Bs=None, udot=udot, ld=ld,
                           force_general_path=force, H=h_d, S=s_d, ldh=n,
-                          h_reference_form=reference_form)
+                          h_reference_form=reference_form,
+                          udot_rows=np.asarray(co.udot_norms) if shift else None)
     torch.cuda.synchronize()
     return h_d.cpu().numpy().T.copy(), s_d.cpu().numpy().T.copy(), res
 
@@ -241,3 +242,81 @@ def test_assemble_t_output_through_the_build(pkg):
             assert all(res["joint_t"])
             # l_nonsph < l_sph sets split; l_nonsph == l_sph (atom 1) has no tail
             assert res["joint_split"] == [bool(ln < ls) for ls, ln in zip(d["l_sph"], d["l_nonsph"])]
+
+
+
+def _uniform_udot_case(pkg, seed, heights, n_g, aa_shifts, bb_shifts, u_range=(0.8, 1.2)):
+    """_case with one ||udot|| row pattern per block height (atoms of a T set share it)."""
+    co, tm, ref = _case(pkg, seed, heights, n_g, list(heights), aa_shifts, bb_shifts)
+    rng = np.random.default_rng(seed + 100)
+    pattern = {h: rng.uniform(*u_range, h) for h in set(heights)}
+    u = np.concatenate([pattern[h] for h in heights])
+    co.udot_norms[:] = u
+    return co, tm, (ref[0], ref[1], u.copy()) + ref[3:]
+
+
+def test_shifted_joint_form_indefinite_t(pkg):
+    """T_AA / T_BB not HPD: the joint form with a common shift, H = sum W^H W - sigma S, against
+    the oracle and the reference forms; every set joint, sigma > 0 (||udot|| ~ 1, so the shift
+    is of the size of T and passes the amplification guard)."""
+    heights = (16, 16, 9)
+    co, tm, ref = _uniform_udot_case(pkg, 31, heights, 110, [-2.0, 2.0, -1.0], [2.0, -2.0, -0.5])
+    a, b, u, taa, tab, tbb = ref
+    h_o, s_o, _, mask_o = ob.build_all(a, b, u, list(heights), taa, tab, tbb)
+    h, s, res = _build(pkg, co, tm, shift=True)
+    h_r, _, res_r = _build(pkg, co, tm, reference_form=True)
+    assert res["joint_t"] == [True] * 3 and res["joint_shift"] > 0
+    assert res_r["joint_shift"] == 0 and res["hpd_mask"] == list(mask_o) == [False, True, False]
+    assert rel_fro(h, h_o) <= TOL and rel_fro(s, s_o) <= TOL
+    assert rel_fro(h, h_r) <= 1e-13
+    np.testing.assert_array_equal(h, h.conj().T)
+
+
+def test_shifted_joint_form_needs_uniform_udot(pkg):
+    """Atoms of one T set with different ||udot|| rows (or T smaller than the block) cannot
+    share a shift: non-HPD sets then take the reference forms, HPD sets stay joint unshifted."""
+    heights = (16, 16)
+    co, tm, ref = _uniform_udot_case(pkg, 32, heights, 90, [-2.0, 2.0], [2.0, 2.0])
+    co.udot_norms[16] *= 1.5  # atom 1 (own T set) is fine; make atom 0's set share T with it
+    tm = pkg.TMatrixSet([tm.t_aa[0]] * 2, [tm.t_ab[0]] * 2, [tm.t_bb[0]] * 2, [0, 0], [0, 0])
+    a, b, _, taa, tab, tbb = ref
+    u = np.asarray(co.udot_norms).copy()
+    h_o, s_o, _, _ = ob.build_all(a, b, u, list(heights), [taa[0]] * 2, [tab[0]] * 2, [tbb[0]] * 2)
+    h, s, res = _build(pkg, co, tm, shift=True)
+    assert res["joint_t"] == [False] and res["joint_shift"] == 0
+    assert rel_fro(h, h_o) <= TOL and rel_fro(s, s_o) <= TOL
+
+
+def test_shifted_joint_form_guard_and_drop_in(pkg):
+    """Badly scaled T (shift -2 on T_BB against ||udot||^2 ~ 0.05, BASELINE C1 with the test
+    variant's diagonal -2): the needed shift would amplify rounding ~100x, so the guard keeps the
+    reference forms — through the device pipeline and the drop-in build_all, both vs the oracle."""
+    from paper_1602_06589_b200 import configs
+    from paper_1602_06589_b200.pipeline import build_hs
+
+    inst = configs.make_instance("C1", hpd_shift=-2.0)
+    h, s, res = build_hs(inst.spec, inst.tmats)
+    assert not any(res["joint_t"]) and res["joint_shift"] == 0 and not any(res["hpd_mask"])
+    co = pkg.compute_AB(inst.spec)
+    h2, s2, rep = pkg.build_all(co, inst.tmats, pkg.BuildConfig())
+    from oracle import flapw as of
+    a, b, norms, offs = of.compute_ab(inst.spec)
+    tm = inst.tmats
+    h_o, s_o, _, mask = ob.build_all(a, b, norms, list(np.diff(offs)), [t.array for t in tm.t_aa],
+                                     [t.array for t in tm.t_ab], [t.array for t in tm.t_bb])
+    for hh, ss in ((h, s), (h2, s2)):
+        assert rel_fro(hh.array, h_o) <= TOL and rel_fro(ss.array, s_o) <= TOL
+    assert rep.hpd_mask == list(mask)
+
+
+def test_shifted_joint_form_guard_small_udot(pkg):
+    """The same indefinite T with ||udot|| ~ 0.2: the shift needed by the B blocks would be
+    ~25x T's scale; rejected, the reference forms give H (vs the oracle)."""
+    heights = (16, 9)
+    co, tm, ref = _uniform_udot_case(pkg, 33, heights, 80, [2.0, 2.0], [-2.0, -1.0],
+                                     u_range=(0.15, 0.25))
+    a, b, u, taa, tab, tbb = ref
+    h_o, s_o, _, _ = ob.build_all(a, b, u, list(heights), taa, tab, tbb)
+    h, s, res = _build(pkg, co, tm, shift=True)
+    assert res["joint_t"] == [False, False] and res["joint_shift"] == 0
+    assert rel_fro(h, h_o) <= TOL and rel_fro(s, s_o) <= TOL

@@ -39,9 +39,10 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=30)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5", "C2NS"],
-                   help="BASELINE.json configs C1-C5; C2NS = C2 with l_nonsph = 6 < l_sph = 8 "
-                        "(structured T, not a BASELINE config)")
+    p.add_argument("--config", default="C2",
+                   choices=["C1", "C2", "C3", "C4", "C5", "C2NS", "C2IND"],
+                   help="BASELINE.json configs C1-C5; not BASELINE configs: C2NS = C2 with "
+                        "l_nonsph = 6 < l_sph = 8 (structured T), C2IND = C2 with indefinite T")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--mode", default="kpoints", choices=["kpoints", "panels"],

@@ -40,6 +40,8 @@ class ConfigDef:
     t_shift: float = 2.0
     l_nonsph: int | None = None  # None = l_max (BASELINE); else T is dense only in the leading
                                  # (l_nonsph+1)^2 block plus its diagonals
+    bb_udot_scaled: bool = False  # T_BB -> U T_BB U (U = diag ||udot|| per row), as the physics
+                                  # scales <udot|H|udot>
 
 
 CONFIGS = {
@@ -52,6 +54,10 @@ CONFIGS = {
     # :759-813), T zeroed outside the dense block except its diagonals as the reference's
     # synth_T does (`flapw.py:440-446` _fig1_zero_out): exercises the T-structure split.
     "C2NS": ConfigDef("C2NS", 12.0, 3000, ((16, 2.2),), 8, seed=1006, l_nonsph=6),
+    # Not a BASELINE config: C2 with indefinite T (SURVEY §8d's test variant, diagonal -2) and
+    # T_BB scaled by ||udot||: no T_AA is HPD; exercises the shifted joint H form.
+    "C2IND": ConfigDef("C2IND", 12.0, 3000, ((16, 2.2),), 8, seed=1007, t_shift=-2.0,
+                       bb_udot_scaled=True),
 }
 
 
@@ -134,6 +140,9 @@ def make_instance(name: str, seed: int | None = None, n_kpoints: int | None = No
         if l_ns < cfg.l_max:
             d = (l_ns + 1) ** 2
             taa_a, tbb_a, tab_a = (_zero_outside(t, d) for t in (taa_a, tbb_a, tab_a))
+        if cfg.bb_udot_scaled:
+            u_rows = np.repeat(udot_norm, 2 * np.arange(cfg.l_max + 1) + 1)
+            tbb_a = u_rows[:, None] * tbb_a * u_rows[None, :]
         taa = ComplexDense.from_array(taa_a)
         tbb = ComplexDense.from_array(tbb_a)
         tab = ComplexDense.from_array(tab_a)

@@ -12,7 +12,7 @@ timeout 600 python bench.py > gpurun_out/bench_C2.log 2>&1; echo "bench C2 rc=$?
 tail -1 gpurun_out/bench_C2.log
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.log 2>&1; echo "bench ref rc=$?"
 tail -1 gpurun_out/bench_ref.log
-for c in C3 C4 C5 C2NS; do
+for c in C3 C4 C5 C2NS C2IND; do
   timeout 900 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$c.log 2>&1; echo "bench $c rc=$?"
   tail -1 gpurun_out/bench_$c.log | cut -c1-400
 done

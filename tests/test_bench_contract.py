@@ -42,8 +42,8 @@ def test_bench_helpers():
 
 def test_executed_flops_accounting():
     """Executed DMMA work: S (K = 2R) + H with joint T sets (K = 2R) is 16 R N^2 complex-MAC
-    flops; with the reference forms H adds ZHER2K (8 R N^2) + ZHERK over HPD rows (4 R N^2)
-    + ZGEMM over non-HPD rows (8 R N^2).  Three products: x 3/4."""
+    flops; with the reference forms H adds ZHER2K (8 R N^2) + ZHERK or the lower half of the
+    ZGEMM (4 R N^2 each).  Three products: x 3/4."""
     sys.path.insert(0, REPO)
     import bench
 
@@ -53,6 +53,12 @@ def test_executed_flops_accounting():
     assert joint["executed_flops_per_step"] == 16 * r * n * n * 3 // 4
     ref = bench.executed_flops(fc, 1.0, 4, n, r, r, 0)
     assert ref["executed_flops_per_step"] == fc  # four products, reference forms: the ledger
+    # non-HPD reference-form rows: the kernel's A^H X lands in the lower triangle only
     mixed = bench.executed_flops(fc, 1.0, 4, n, r, 600, 300)
-    assert mixed["executed_flops_per_step"] == (8 * r + 8 * 300 + 8 * (r - 300) + 4 * 300
-                                               + 8 * (r - 600)) * n * n
+    assert mixed["executed_flops_per_step"] == (8 * r + 8 * 300 + 12 * (r - 300)) * n * n
+    nonhpd = bench.executed_flops(bench.contract_flops(n, r, 0), 1.0, 4, n, r, 0, 0)
+    assert nonhpd["executed_flops_per_step"] == 20 * r * n * n
+
+    # shifted joint form: joint rows that are not HPD
+    ind = bench.executed_flops(fc, 1.0, 4, n, r, 0, r, 0)
+    assert ind["executed_flops_per_step"] == 16 * r * n * n

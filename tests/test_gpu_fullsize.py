@@ -1,4 +1,5 @@
-"""Full-size parity at BASELINE configs C3 / C4 / C5 (too large for a dense CPU oracle):
+"""Full-size parity at BASELINE configs C3 / C4 / C5 (too large for a dense CPU oracle), and at
+the C2-sized C2NS (T-structure split) / C2IND (indefinite T, shifted joint form):
 size-independent checks against the oracle restatement of the reference.
 
 * A*/B* on a seeded sample of K-vector columns vs the oracle's compute_AB restatement;
@@ -18,7 +19,7 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-12
 
 
-@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+@pytest.mark.parametrize("name", ["C3", "C4", "C5", "C2NS", "C2IND"])
 def test_fullsize_projections_vs_oracle(cuda, name):
     import torch
 
@@ -31,7 +32,11 @@ def test_fullsize_projections_vs_oracle(cuda, name):
     dspec = DeviceSpec(spec)
     pipe = HSPipeline(n, dspec.heights)
     res = pipe.run(dspec, pack_tmats(tm))
-    assert all(res["hpd_mask"])
+    # C2NS: structure split; C2IND: no T_AA HPD, shifted joint factor (not BASELINE configs)
+    assert all(res["hpd_mask"]) != (name == "C2IND")
+    assert all(res["joint_t"])
+    assert all(res["joint_split"]) == (name == "C2NS")
+    assert (res["joint_shift"] > 0) == (name == "C2IND")
     rng = np.random.default_rng(11)
 
     # A*/B* sampled columns

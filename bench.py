@@ -450,7 +450,8 @@ def run_ours(args):
                            "spec per step + T once -> full H, S in pinned host memory per step)",
                     "single_call_ms": round(float(e2e_t[1].item()), 3)},
             "gpu_launches": args.steps * (pipe.launches_per_run(dspec)
-                                          + int(any(res.get("joint_split", [])))),
+                                          + int(any(res.get("joint_split", [])))
+                                          + int(res.get("joint_shift", 0.0) > 0)),
             "clocks": clk.summary(),
         }
         if not args.no_cpu_baseline and world == 1:
@@ -560,7 +561,8 @@ def run_panels(args):
                     "ms_per_step": round(float(e2e.item()), 3),
                     "api": "paper_1602_06589_b200.shard.P2PShardedBuild.run + D2H of H, S"},
             "gpu_launches": args.steps * (sb.pipe.launches_per_run(dspec)
-                                          + int(any(res.get("joint_split", [])))),
+                                          + int(any(res.get("joint_split", [])))
+                                          + int(res.get("joint_shift", 0.0) > 0)),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -47,8 +47,18 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--mode", default="kpoints", choices=["kpoints", "panels"],
                    help="kpoints: one k-point per GPU per step (weak scaling, default); "
-                        "panels: ONE k-point split over all GPUs by column panels, tiles "
-                        "stored into rank 0's H/S over NVLink peer memory (strong scaling)")
+                        "panels: ONE k-point split over all GPUs by column panels, "
+                        "gathered to rank 0 (strong scaling)")
+    p.add_argument("--panel-transport", default="nccl", choices=["nccl", "p2p"],
+                   help="panel gather: nccl = batched send/recv + mirror on rank 0 (default); "
+                        "p2p = tiles and their mirror stored into rank 0's symmetric-memory "
+                        "H/S by the contraction epilogue (after a self-test; nccl if it fails)")
+    p.add_argument("--no-extras", action="store_true",
+                   help="skip the BASELINE scaling configs (C5 k-point batch, C3 panels) "
+                        "reported as extra keys of the line")
+    p.add_argument("--dry-run", action="store_true",
+                   help="launcher check without a GPU: spawn the ranks (gloo), deal the "
+                        "work, print one JSON line; no compute")
     return p.parse_args()
 
 
@@ -119,30 +129,37 @@ def run_reference(args):
     from paper_1602_06589_b200 import configs
 
     inst = configs.make_instance(args.config)
-    spec = cpu_sample(inst)
+
+    def sample_spec(k):  # distinct seeded k-points of the config, bounded in N_G
+        one = configs.Instance(inst.cfg, [configs.kpoint_variant(inst, k)], inst.tmats,
+                               inst.min_abs_wronskian)
+        return cpu_sample(one)
+
     for _ in range(max(0, min(args.warmup, 1))):
-        cpu_oracle_step(spec, inst.tmats)
-    times, flops = [], 0
+        cpu_oracle_step(sample_spec(0), inst.tmats)
+    times, flops, nb = [], 0, set()
     t_start = time.perf_counter()
-    for _ in range(args.steps):
+    for k in range(args.steps):
+        spec = sample_spec(k)
+        nb.add(spec.n_basis)
         dt, fl, _, _ = cpu_oracle_step(spec, inst.tmats)
         times.append(dt)
-        flops = fl
+        flops += fl
         if time.perf_counter() - t_start > 150:  # keep the arm within a few minutes
             break
     total = sum(times)
-    value = flops * len(times) / total / 1e12
-    sample = (f"{len(times)} full k-point(s) of {args.config}" +
-              (f" truncated to N_G={spec.n_basis}" if spec.n_basis < inst.spec.n_basis else
-               f" (N_G={spec.n_basis})") + ": oracle compute_AB + build_all (scipy OpenBLAS)")
+    value = flops / total / 1e12
+    trunc = max(nb) < inst.spec.n_basis
+    sample = (f"{len(times)} distinct seeded k-point(s) of {args.config}" +
+              (f" truncated to N_G={max(nb)}" if trunc else f" (N_G {min(nb)}-{max(nb)})") +
+              ": oracle compute_AB + build_all (scipy OpenBLAS)")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
         "n_gpus": world, "steps": len(times), "warmup": args.warmup,
         "ms_per_step": round(1e3 * total / len(times), 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": (f"{args.config} (BASELINE.json configs[{int(args.config[1]) - 1}])"
-                                if len(args.config) == 2 else f"{args.config} (not a BASELINE config)"),
-                   "n_basis": spec.n_basis, "rows": int(sum((l + 1) ** 2 for l in spec.l_sph))},
+        "config": {"workload": workload_name(args.config, inst),
+                   "n_basis": max(nb), "rows": int(sum((l + 1) ** 2 for l in inst.spec.l_sph))},
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": host_threads(),
                          "kind": "port", "sample": sample},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -261,9 +278,8 @@ def executed_flops(fc, kc_ms, products, n, rows, hpd_rows, joint_rows, hpd_joint
     return {"complex_mul": f"{products}-product", "h_joint_rows": int(joint_rows),
             "executed_flops_per_step": int(ex), "executed_tflops": round(tf, 3),
             "executed_frac": round(tf / FP64_PEAK_TFLOPS, 4),
-            "note": "achieved/frac count SURVEY 8(d)'s ledger flops (the reference algorithm); the "
-                    "kernels execute fewer (three-product multiply, joint T factor for H), so frac "
-                    "can exceed 1; executed_frac is the DMMA-pipe utilisation"}
+            "note": "executed = the DMMA products the kernels issue (three-product multiply, joint "
+                    "T factor for H): the tensor-pipe utilisation"}
 
 
 def joint_rows_of(dspec, tpack, res, hpd_only=False):
@@ -281,9 +297,253 @@ def contract_flops(n, rows, hpd_rows):
     return 16 * rows * n * n + 4 * hpd_rows * n * n + 8 * (rows - hpd_rows) * n * n
 
 
-def run_ours(args):
+def workload_name(config: str, inst) -> str:
+    """The `config.workload` string, identical in both arms for one --config."""
+    spec = inst.spec
+    heights = sorted({int((l + 1) ** 2) for l in spec.l_sph})
+    rows = int(sum((l + 1) ** 2 for l in spec.l_sph))
+    tag = (f"{config} (BASELINE.json configs[{int(config[1]) - 1}])" if len(config) == 2
+           else f"{config} (not a BASELINE config)")
+    if len(inst.specs) > 1:
+        ng = [x.n_basis for x in inst.specs]
+        return (f"{tag}: {len(inst.specs)} k-points, N_G {min(ng)}-{max(ng)}, N_A={spec.n_atoms}, "
+                f"N_L={'/'.join(map(str, heights))}, R={rows}, one k-point per step")
+    return (f"{tag}: N_G={spec.n_basis}, N_A={spec.n_atoms}, N_L={'/'.join(map(str, heights))}, "
+            f"R={rows}, one k-point per step")
+
+
+def init_dist(world: int, local: int, backend: str = "nccl"):
     import torch
     import torch.distributed as dist
+
+    if world > 1 and not dist.is_initialized():
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    return dist
+
+
+def max_over_ranks(vals, world, op="max"):
+    """Reduce a list of floats over the ranks (device tensor, NCCL)."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(v) for v in vals], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return [float(x) for x in t.tolist()]
+
+
+def time_kpoints(pipe, dspecs, tpack, steps, world):
+    """Time `steps` k-points back to back through the pipelined native path (step i+1 is
+    enqueued before step i is collected) with CUDA events on the compute stream, barrier +
+    synchronize on both sides.  Returns (ms on this rank, per-kernel ms lists, A/B ms list,
+    last result)."""
+    import torch
+    import torch.distributed as dist
+
+    kern = {"contract_S": [], "contract_H": [], "apply_Z": [], "apply_XY": []}
+    ab_ms = []
+    stream = torch.cuda.current_stream()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    prev = None
+    res = None
+
+    def collect(ticket):
+        nonlocal res
+        res = pipe.finish(ticket)
+        for k, v in res["kernel_ms"].items():
+            kern[k].append(v)
+        ab_ms.append(res["ms"]["setup"])  # A/B generation (T preparation reused)
+
+    for i in range(steps):
+        ticket = pipe.run_async(dspecs[i % len(dspecs)], tpack)
+        if prev is not None:
+            collect(prev)
+        prev = ticket
+    e1.record(stream)
+    collect(prev)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    return e0.elapsed_time(e1), kern, ab_ms, res
+
+
+def contraction_roofline(fc, kern, products, n, rows, hpd_rows, joint_rows, traffic=None):
+    """roofline object of the dominant kernel (the S + H triangular DMMA contractions).
+
+    `achieved` counts the flops of the algorithm the kernel executes — the S and H
+    contractions with the three-product complex multiply and, for joint T sets, H as one
+    rank-2R update — over their CUDA-event time, so `frac` is the DMMA-pipe
+    utilisation (it agrees with ncu's DMMA-busy).  The reference ledger's rate over the
+    same time is `ledger_tflops` (the algorithmic flops of the reference's ZHERK/ZHER2K
+    forms; exceeds the DMMA peak because the kernels execute fewer products)."""
+    kc_ms = statistics.mean(kern["contract_S"]) + statistics.mean(kern["contract_H"])
+    ex = executed_flops(fc, kc_ms, products, n, rows, hpd_rows, joint_rows)
+    ledger_tf = fc / (kc_ms / 1e3) / 1e12
+    return {
+        "bound": "tensor", "achieved": ex["executed_tflops"], "peak": FP64_PEAK_TFLOPS,
+        "unit": "TFLOP/s", "frac": ex["executed_frac"], "traffic": traffic,
+        "kernel": "contract_kernel (S + H triangular DMMA contractions)",
+        "peak_source": "measured FP64 DMMA ceiling, profiles/r01_fp64_peaks.json "
+                       "(MEASURED_PEAKS.json has no FP64 entry)",
+        "algorithmic_flops_per_step": ex["executed_flops_per_step"],
+        "complex_mul": ex["complex_mul"], "h_joint_rows": ex["h_joint_rows"],
+        "contract_ms_per_step": round(kc_ms, 4),
+        "ledger_flops_per_step": int(fc), "ledger_tflops": round(ledger_tf, 3),
+        "kernel_ms": {k: round(statistics.mean(v), 4) for k, v in kern.items() if v},
+    }
+
+
+def kpoint_specs(inst, rank, world):
+    """A k-point batch config (C5: 64 seeded k-points, each with its own G-set) is dealt
+    round-robin over the ranks and each rank cycles through its share, one k-point per step;
+    single-k-point configs give every rank its own seeded k-point of the same crystal."""
+    from paper_1602_06589_b200 import configs
+
+    if len(inst.specs) > 1:
+        return [inst.specs[i] for i in range(rank, len(inst.specs), world)]
+    return [configs.kpoint_variant(inst, rank)]
+
+
+def measure_kpoint_config(config, steps, warmup, rank, world):
+    """Extra key: a k-point config timed like the main line (C5 = BASELINE's k-point batch,
+    round-robin over the GPUs); returns a dict for rank 0."""
+    import torch
+
+    from paper_1602_06589_b200 import _native, configs
+    from paper_1602_06589_b200.pipeline import DeviceSpec, HSPipeline, pack_tmats
+
+    inst = configs.make_instance(config)
+    specs = kpoint_specs(inst, rank, world)
+    dspecs = [DeviceSpec(x) for x in specs]
+    tpack = pack_tmats(inst.tmats)
+    pipe = HSPipeline(max(x.n_basis for x in specs), dspecs[0].heights)
+    res = None
+    for i in range(max(warmup, 3)):
+        res = pipe.run(dspecs[i % len(dspecs)], tpack)
+    torch.cuda.synchronize()
+    ms, kern, ab_ms, res = time_kpoints(pipe, dspecs, tpack, steps, world)
+    mask = res["hpd_mask"]
+    step_specs = [specs[i % len(specs)] for i in range(steps)]
+    flops = sum(configs.nominal_flops(x, mask) for x in step_specs)
+    ms_max, tot_flops = max_over_ranks([ms], world)[0], max_over_ranks([flops], world, "sum")[0]
+    out = None
+    if rank == 0:
+        dspec = dspecs[0]
+        rows = dspec.rows
+        hpd_rows = int(sum(h for h, m in zip(dspec.heights, mask) if m))
+        fc = statistics.mean(contract_flops(x.n_basis, rows, hpd_rows) for x in step_specs)
+        n_mean = int(round(statistics.mean(x.n_basis for x in step_specs)))
+        rl = contraction_roofline(fc, kern, _native.load().hsdla_complex_mul_products(), n_mean,
+                                  rows, hpd_rows, joint_rows_of(dspec, tpack, res))
+        out = {"workload": workload_name(config, inst), "scaling": "weak",
+               "parallelism": f"kpoint-dp{world}",
+               "kpoints_per_s": round(world * steps / (ms_max / 1e3), 3),
+               "ms_per_kpoint_per_gpu": round(ms_max / steps, 4),
+               "tflops": round(tot_flops / (ms_max / 1e3) / 1e12, 4),
+               "contract_frac": rl["frac"], "contract_tflops": rl["achieved"]}
+    del pipe
+    torch.cuda.empty_cache()
+    return out
+
+
+def self_test_p2p(world):
+    """P2P panel transport self-test on a small system: the symmetric-memory build must
+    agree bitwise with the NCCL gather.  Every rank returns the same verdict."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1602_06589_b200 import configs
+    from paper_1602_06589_b200.pipeline import DeviceSpec, pack_tmats
+    from paper_1602_06589_b200.shard import NcclShardedBuild, P2PShardedBuild
+
+    ok = 1
+    try:
+        inst = configs.make_instance("C1")
+        spec = inst.spec
+        dspec, tpack = DeviceSpec(spec), pack_tmats(inst.tmats)
+        ref = NcclShardedBuild(spec.n_basis, dspec.heights).run(dspec, tpack)
+        p2p = P2PShardedBuild(spec.n_basis, dspec.heights).run(dspec, tpack)
+        if ref is not None:
+            ok = int(torch.equal(ref[0], p2p[0]) and torch.equal(ref[1], p2p[1]))
+    except Exception as e:  # noqa: BLE001 — any failure selects the NCCL transport
+        print(f"bench: p2p self-test failed: {e!r}", file=sys.stderr)
+        ok = 0
+    flag = torch.tensor([ok], device="cuda")
+    if world > 1:
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    return bool(flag.item())
+
+
+def measure_panels(config, steps, warmup, rank, world, transport="nccl"):
+    """One k-point per step split over all ranks by column panels (SURVEY §8e, C3/C4 strong
+    scaling): every rank regenerates A*/B* locally, computes its owned lower tiles; the
+    panels reach rank 0 by NCCL send/recv (+ mirror there) or by the contraction epilogue's
+    NVLink stores (p2p).  Timed with CUDA events per rank, max over ranks; returns
+    (dict for rank 0, sharded-build object, dspec, tpack)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1602_06589_b200 import _native, configs
+    from paper_1602_06589_b200.pipeline import DeviceSpec, pack_tmats
+    from paper_1602_06589_b200.shard import NcclShardedBuild, P2PShardedBuild
+
+    if transport == "p2p" and not self_test_p2p(world):
+        transport = "nccl (p2p self-test failed)"
+    inst = configs.make_instance(config)
+    spec = inst.spec
+    n = spec.n_basis
+    dspec = DeviceSpec(spec)
+    tpack = pack_tmats(inst.tmats)
+    sb = (P2PShardedBuild if transport == "p2p" else NcclShardedBuild)(n, dspec.heights)
+    for _ in range(max(warmup, 3)):
+        sb.run(dspec, tpack)
+    kern = {"contract_S": [], "contract_H": [], "apply_Z": [], "apply_XY": []}
+    stream = torch.cuda.current_stream()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            sb.run(dspec, tpack)
+            res = sb.last_result
+            for k, v in res["kernel_ms"].items():
+                kern[k].append(v)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms_max = max_over_ranks([e0.elapsed_time(e1)], world)[0]
+    mask = res["hpd_mask"]
+    flops_step = configs.nominal_flops(spec, mask)
+    out = None
+    if rank == 0:
+        rows = dspec.rows
+        hpd_rows = int(sum(h for h, m in zip(dspec.heights, mask) if m))
+        fc = contract_flops(n, rows, hpd_rows) / world  # this rank's share of the tiles
+        rl = contraction_roofline(fc, kern, _native.load().hsdla_complex_mul_products(), n, rows,
+                                  hpd_rows, joint_rows_of(dspec, tpack, res))
+        out = {"workload": workload_name(config, inst) + f", split over {world} GPU(s) by "
+                                                         "column panels",
+               "scaling": "strong", "parallelism": f"panels-{transport.split()[0]}{world}",
+               "transport": transport,
+               "ms_per_kpoint": round(ms_max / steps, 4),
+               "tflops": round(flops_step * steps / (ms_max / 1e3) / 1e12, 4),
+               "ledger_flops_per_step": flops_step,
+               "contract_frac_rank0": rl["frac"], "contract_tflops_rank0": rl["achieved"],
+               "clocks": clk.summary()}
+    return out, sb, dspec, tpack, flops_step
+
+
+def run_ours(args):
+    import torch
 
     from paper_1602_06589_b200 import BuildConfig, _native, configs
     from paper_1602_06589_b200.pipeline import (DeviceSpec, HSPipeline, build_hs, build_hs_many,
@@ -291,14 +551,9 @@ def run_ours(args):
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    init_dist(world, local)
     inst = configs.make_instance(args.config)
-    # A k-point batch config (C5: 64 seeded k-points, each with its own G-set) is dealt
-    # round-robin over the ranks and each rank cycles through its share, one k-point per step;
-    # single-k-point configs give every rank its own seeded k-point of the same crystal.
-    specs = ([inst.specs[i] for i in range(rank, len(inst.specs), world)]
-             if len(inst.specs) > 1 else [configs.kpoint_variant(inst, rank)])
+    specs = kpoint_specs(inst, rank, world)
     spec = specs[0]
     dspecs = [DeviceSpec(x) for x in specs]
     dspec = dspecs[0]
@@ -306,7 +561,6 @@ def run_ours(args):
     n_cap = max(x.n_basis for x in specs)
     tpack = pack_tmats(inst.tmats)
     pipe = HSPipeline(n_cap, dspec.heights)
-    stream = torch.cuda.current_stream()
 
     for i in range(max(args.warmup, 3)):
         res = pipe.run(dspecs[i % len(dspecs)], tpack)
@@ -316,47 +570,12 @@ def run_ours(args):
     hpd_rows = int(sum(h for h, m in zip(dspec.heights, mask) if m))
     step_specs = [specs[i % len(specs)] for i in range(args.steps)]
     flops_steps = [configs.nominal_flops(x, mask) for x in step_specs]
-    flops_step = flops_steps[0]
     fc_steps = [contract_flops(x.n_basis, rows, hpd_rows) for x in step_specs]
-    fc = fc_steps[0]
 
-    kern = {"contract_S": [], "contract_H": [], "apply_Z": [], "apply_XY": []}
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
     with ClockSampler(torch.cuda.current_device()) as clk:
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        # k-points back to back through the pipelined native path: step i+1 is enqueued
-        # before step i is collected, so host-side enqueue never idles the GPU.
-        prev = None
-        ab_ms = []
-
-        def collect(ticket):
-            r = pipe.finish(ticket)
-            for k, v in r["kernel_ms"].items():
-                kern[k].append(v)
-            ab_ms.append(r["ms"]["setup"])  # A/B generation (T preparation reused)
-
-        for i in range(args.steps):
-            ticket = pipe.run_async(dspecs[i % len(dspecs)], tpack)
-            if prev is not None:
-                collect(prev)
-            prev = ticket
-        e1.record(stream)
-        collect(prev)
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ms = e0.elapsed_time(e1)
-    ms_t = torch.tensor([ms], device="cuda")
-    fl_t = torch.tensor([float(sum(flops_steps))], device="cuda", dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(fl_t, op=dist.ReduceOp.SUM)
-    ms_max = float(ms_t.item())
-    total_flops = float(fl_t.item())
+        ms, kern, ab_ms, res = time_kpoints(pipe, dspecs, tpack, args.steps, world)
+    ms_max = max_over_ranks([ms], world)[0]
+    total_flops = max_over_ranks([sum(flops_steps)], world, "sum")[0]
     value = total_flops / (ms_max / 1e3) / 1e12
 
     # e2e: the public API with host buffers.  build_hs_many = a k-point batch through the
@@ -379,8 +598,7 @@ def run_ours(args):
     e2e_step_ms = statistics.median(batch_ms)
     h2d = sum(r["h2d_bytes"] for r in rr) / n_e2e
     d2h = sum(r["d2h_bytes"] for r in rr) / n_e2e
-    e2e_fl = torch.tensor([float(sum(configs.nominal_flops(x, mask) for x in e2e_specs)) / n_e2e],
-                          device="cuda", dtype=torch.float64)
+    e2e_fl = float(sum(configs.nominal_flops(x, mask) for x in e2e_specs)) / n_e2e
     single_ms = []
     host_out = None
     for i in range(args.warmup + 3):
@@ -391,199 +609,254 @@ def run_ours(args):
         host_out = (torch.from_numpy(h.base.T), torch.from_numpy(s.base.T))
         if i >= args.warmup:
             single_ms.append((time.perf_counter() - t1) * 1e3)
-    e2e_t = torch.tensor([e2e_step_ms, statistics.median(single_ms)], device="cuda")
-    if world > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(e2e_fl, op=dist.ReduceOp.SUM)
-    e2e_value = float(e2e_fl.item()) / (float(e2e_t[0].item()) / 1e3) / 1e12
+    dropin = dropin_e2e(spec, inst.tmats, args.warmup)
+    e2e_ms, single, dropin_ms = max_over_ranks([e2e_step_ms, statistics.median(single_ms),
+                                                dropin["ms"]], world)
+    e2e_fl_all = max_over_ranks([e2e_fl], world, "sum")[0]
+    e2e_value = e2e_fl_all / (e2e_ms / 1e3) / 1e12
+    launches = args.steps * (pipe.launches_per_run(dspec)
+                             + int(any(res.get("joint_split", [])))
+                             + int(res.get("joint_shift", 0.0) > 0))
+    clocks = clk.summary()
+    del pipe, bufs, host_out, h, s
+    torch.cuda.empty_cache()
+
+    extras = {}
+    if not args.no_extras and args.config == "C2":
+        # BASELINE's scaling configs at this N (the driver's SCALE run covers N = 1, 2, 4, 8):
+        # C5 k-points round-robin (weak), C3 one k-point split by column panels (strong).
+        extras["C5_kpoint_batch"] = measure_kpoint_config("C5", max(8, min(args.steps, 64)),
+                                                          args.warmup, rank, world)
+        p_out, sb, *_ = measure_panels("C3", max(4, min(args.steps, 16)), args.warmup, rank,
+                                       world, args.panel_transport)
+        extras["C3_panels"] = p_out
+        del sb
+        torch.cuda.empty_cache()
 
     if rank == 0:
-        kc_ms = statistics.mean(kern["contract_S"]) + statistics.mean(kern["contract_H"])
         fc = statistics.mean(fc_steps)  # mean per step (k-point batches vary N_G)
-        achieved = fc / (kc_ms / 1e3) / 1e12
         products = _native.load().hsdla_complex_mul_products()
-        joint_rows = joint_rows_of(dspec, tpack, res)
         traffic = None
         tpath = os.path.join(REPO, "profiles", f"traffic_{args.config}.json")
         if os.path.exists(tpath):
             with open(tpath) as f:
                 traffic = json.load(f).get("dram_bytes_per_step")
+        rl = contraction_roofline(fc, kern, products, n, rows, hpd_rows,
+                                  joint_rows_of(dspec, tpack, res), traffic)
+        step_ms = ms_max / args.steps
+        ex_step = rl["algorithmic_flops_per_step"] / (step_ms / 1e3) / 1e12
         line = {
             "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3),
-            "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
+            "ms_per_step": round(step_ms, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {
-                "workload": (f"{args.config}: N_G={n}, N_A={spec.n_atoms}, N_L={int(dspec.heights[0])}, "
-                             f"R={rows}, one k-point per GPU per step" if len(inst.specs) == 1 else
-                             f"{args.config}: {len(inst.specs)} k-points (N_G "
-                             f"{min(x.n_basis for x in inst.specs)}-{max(x.n_basis for x in inst.specs)}), "
-                             f"N_A={spec.n_atoms}, N_L={int(dspec.heights[0])}, R={rows}; dealt "
-                             f"round-robin over the GPUs, each cycling through its share, one "
-                             f"k-point per GPU per step"),
+                "workload": workload_name(args.config, inst),
                 "n_basis": n, "rows": rows,
                 "ledger_flops_per_step": int(round(total_flops / (world * args.steps))),
                 "parallelism": f"kpoint-dp{world}",
+                "multi_gpu": ("each GPU builds its own k-point of the same crystal per step "
+                              "(k-point parallelism, no collective in the data path)"),
                 "l2": "inputs+outputs per step exceed the 126 MB L2 (A,B,UB,Z,XY + H,S); no flush",
             },
-            "ms_per_kpoint": round(ms_max / args.steps, 4),
+            "gpus_active": world,
+            "ms_per_kpoint": round(step_ms, 4),
             "kpoints_per_s": round(world * args.steps / (ms_max / 1e3), 2),
-            "fp64_peak_frac": round(value / world / FP64_PEAK_TFLOPS, 4),
-            "roofline": {
-                "bound": "tensor", "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS,
-                "unit": "TFLOP/s", "frac": round(achieved / FP64_PEAK_TFLOPS, 4),
-                "traffic": traffic,
-                "kernel": "contract_kernel (S + H triangular DMMA contractions)",
-                "peak_source": "measured FP64 DMMA ceiling, profiles/r01_fp64_peaks.json "
-                               "(MEASURED_PEAKS.json has no FP64 entry)",
-                "ceilings": fp64_ceilings(clk.summary().get("sm_mhz")),
-                "algorithmic_flops_per_step": fc,
-                **executed_flops(fc, kc_ms, products, n, rows, hpd_rows, joint_rows,
-                                 joint_rows_of(dspec, tpack, res, hpd_only=True)),
-                "kernel_ms": {k: round(statistics.mean(v), 4) for k, v in kern.items()},
-            },
+            "effective_tflops": round(value / world, 4),
+            "effective_note": "value = the reference ledger's flops (predict_flops, builder.py:336-370) "
+                              "per second; the kernels execute fewer (DESIGN §3), so this rate is "
+                              "not a utilisation — fp64_peak_frac / roofline.frac are",
+            "fp64_peak_frac": rl["frac"],
+            "step_fp64_frac": round(ex_step / FP64_PEAK_TFLOPS, 4),
+            "roofline": {**rl, "ceilings": fp64_ceilings(clocks.get("sm_mhz"))},
             "ab_gen": ab_gen_line(statistics.mean(ab_ms), rows, n),
             "e2e": {"value": round(e2e_value, 4), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
-                    "ms_per_step": round(float(e2e_t[0].item()), 3),
+                    "ms_per_step": round(e2e_ms, 3),
                     "api": "paper_1602_06589_b200.pipeline.build_hs_many (k-point batch: host "
                            "spec per step + T once -> full H, S in pinned host memory per step)",
-                    "single_call_ms": round(float(e2e_t[1].item()), 3)},
-            "gpu_launches": args.steps * (pipe.launches_per_run(dspec)
-                                          + int(any(res.get("joint_split", [])))
-                                          + int(res.get("joint_shift", 0.0) > 0)),
-            "clocks": clk.summary(),
+                    "single_call_ms": round(single, 3),
+                    "dropin_ms": round(dropin_ms, 3),
+                    "dropin_api": dropin["api"],
+                    "dropin_phases_ms": dropin["phases"]},
+            "gpu_launches": launches,
+            "clocks": clocks,
         }
+        line.update({k: v for k, v in extras.items() if v is not None})
         if not args.no_cpu_baseline and world == 1:
-            _limits = use_all_host_threads()  # noqa: F841
-            # bounded sample: k-points of the config until ~10 s of CPU work (at most 30)
-            cspec = cpu_sample(inst)
-            tot_t = tot_fl = t_ab_sum = t_b_sum = 0.0
-            k = 0
-            while k < 30 and (k == 0 or tot_t < 10.0):
-                dt, fl, t_ab, t_build = cpu_oracle_step(cspec, inst.tmats)
-                tot_t, tot_fl, t_ab_sum, t_b_sum, k = (tot_t + dt, tot_fl + fl, t_ab_sum + t_ab,
-                                                       t_b_sum + t_build, k + 1)
-            line["cpu_baseline"] = {
-                "value": round(tot_fl / tot_t / 1e12, 4), "unit": UNIT, "cores": host_threads(),
-                "kind": "port",
-                "sample": f"{k} k-point(s) of {args.config} (N_G={cspec.n_basis}), {tot_t:.1f} s: "
-                          f"oracle compute_AB {t_ab_sum / k:.2f} s + build_all {t_b_sum / k:.2f} s "
-                          f"per k-point (scipy OpenBLAS)",
-            }
+            line["cpu_baseline"] = cpu_baseline_sample(args.config, inst)
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+
+
+def dropin_e2e(spec, tmats, warmup, reps=3):
+    """The reference entry points with host data: compute_AB (flapw.py:201) followed by
+    build_all (builder.py:403) returning full H, S in host memory — what a caller of the
+    reference sees.  Median of `reps` calls after `warmup` (ms, phase split)."""
+    import torch
+
+    import paper_1602_06589_b200 as pkg
+
+    times, ab_t, build_t = [], [], []
+    for i in range(warmup + reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        coeffs = pkg.compute_AB(spec)
+        t1 = time.perf_counter()
+        h, s, _ = pkg.build_all(coeffs, tmats, pkg.BuildConfig())
+        t2 = time.perf_counter()
+        if i >= warmup:
+            times.append((t2 - t0) * 1e3)
+            ab_t.append((t1 - t0) * 1e3)
+            build_t.append((t2 - t1) * 1e3)
+        del h, s, coeffs
+    return {"ms": statistics.median(times),
+            "phases": {"compute_AB": round(statistics.median(ab_t), 3),
+                       "build_all": round(statistics.median(build_t), 3)},
+            "api": "paper_1602_06589_b200.compute_AB(spec) + build_all(coeffs, tmats, BuildConfig()) "
+                   "-> H, S ComplexDense in host memory (reference flapw.py:201, builder.py:403)"}
+
+
+def cpu_baseline_sample(config, inst):
+    """Bounded CPU sample (~10 s): distinct seeded k-points of the config through the oracle
+    port on every host thread; rank 0, N=1 only."""
+    from paper_1602_06589_b200 import configs
+
+    _limits = use_all_host_threads()  # noqa: F841
+    tot_t = tot_fl = t_ab_sum = t_b_sum = 0.0
+    k = 0
+    nb = set()
+    while k < 30 and (k == 0 or tot_t < 10.0):
+        cspec = cpu_sample(configs.Instance(inst.cfg, [configs.kpoint_variant(inst, k)],
+                                            inst.tmats, inst.min_abs_wronskian))
+        nb.add(cspec.n_basis)
+        dt, fl, t_ab, t_build = cpu_oracle_step(cspec, inst.tmats)
+        tot_t, tot_fl, t_ab_sum, t_b_sum, k = (tot_t + dt, tot_fl + fl, t_ab_sum + t_ab,
+                                               t_b_sum + t_build, k + 1)
+    return {
+        "value": round(tot_fl / tot_t / 1e12, 4), "unit": UNIT, "cores": host_threads(),
+        "kind": "port",
+        "sample": f"{k} distinct seeded k-point(s) of {config} (N_G {min(nb)}-{max(nb)}), "
+                  f"{tot_t:.1f} s: oracle compute_AB {t_ab_sum / k:.2f} s + build_all "
+                  f"{t_b_sum / k:.2f} s per k-point (scipy OpenBLAS)",
+    }
 
 
 def run_panels(args):
-    """One k-point per step, column panels over all ranks (SURVEY §8e, C3/C4 strong scaling):
-    every rank regenerates A*/B* locally, computes its owned lower tiles and stores them and
-    their mirror straight into rank 0's symmetric-memory H and S (shard.P2PShardedBuild)."""
+    """`--mode panels`: the line is one k-point per step split over all ranks (strong scaling)."""
     import torch
-    import torch.distributed as dist
 
-    from paper_1602_06589_b200 import _native, configs
-    from paper_1602_06589_b200.pipeline import DeviceSpec, pack_tmats
-    from paper_1602_06589_b200.shard import P2PShardedBuild
+    from paper_1602_06589_b200.pipeline import DeviceSpec
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
-    if "MASTER_ADDR" not in os.environ:  # single process without torchrun
-        import socket
-
-        with socket.socket() as sk:
-            sk.bind(("127.0.0.1", 0))
-            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(sk.getsockname()[1]),
-                              RANK="0", WORLD_SIZE="1")
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    inst = configs.make_instance(args.config)
-    spec = inst.spec
-    n = spec.n_basis
-    dspec = DeviceSpec(spec)
-    tpack = pack_tmats(inst.tmats)
-    sb = P2PShardedBuild(n, dspec.heights)
-    out = None
-    for _ in range(max(args.warmup, 3)):
-        out = sb.run(dspec, tpack)
-    kern = {"contract_S": [], "contract_H": [], "apply_Z": [], "apply_XY": []}
-    stream = torch.cuda.current_stream()
-    dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(torch.cuda.current_device()) as clk:
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            res = sb.pipe.run(dspec, tpack)
-            torch.cuda.synchronize()
-            dist.barrier()
-            for k, v in res["kernel_ms"].items():
-                kern[k].append(v)
-        e1.record(stream)
-        torch.cuda.synchronize()
-    ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    mask = res["hpd_mask"]
-    flops_step = configs.nominal_flops(spec, mask)
-    value = flops_step * args.steps / (float(ms.item()) / 1e3) / 1e12
+    init_dist(world, local)
+    out, sb, dspec, tpack, flops_step = measure_panels(args.config, args.steps, args.warmup,
+                                                       rank, world, args.panel_transport)
     # e2e: spec upload + sharded build + full H, S read back to pinned host on rank 0
-    hh = torch.empty((n, n), dtype=torch.complex128, pin_memory=True)
-    hs = torch.empty((n, n), dtype=torch.complex128, pin_memory=True)
-    dist.barrier()
+    n = dspec.n_basis
+    spec = __import__("paper_1602_06589_b200").configs.make_instance(args.config).spec
+    hh = torch.empty((n, n), dtype=torch.complex128, pin_memory=True) if rank == 0 else None
+    hs = torch.empty((n, n), dtype=torch.complex128, pin_memory=True) if rank == 0 else None
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        out = sb.run(DeviceSpec(spec), tpack)
-        if out is not None:
-            hh.copy_(out[0], non_blocking=True)
-            hs.copy_(out[1], non_blocking=True)
-            torch.cuda.synchronize()
-    e2e = torch.tensor([(time.perf_counter() - t0) * 1e3 / args.steps], device="cuda")
-    dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
+        res = sb.run(DeviceSpec(spec), tpack)
+        if res is not None:
+            hh.copy_(res[0], non_blocking=True)
+            hs.copy_(res[1], non_blocking=True)
+        torch.cuda.synchronize()
+    e2e = max_over_ranks([(time.perf_counter() - t0) * 1e3 / args.steps], world)[0]
     if rank == 0:
-        rows = dspec.rows
-        hpd_rows = int(sum(h for h, m in zip(dspec.heights, mask) if m))
-        kc = statistics.mean(kern["contract_S"]) + statistics.mean(kern["contract_H"])
-        fc = contract_flops(n, rows, hpd_rows) / world  # this rank's share of the tiles
         line = {
-            "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
+            "metric": METRIC, "value": out["tflops"], "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3),
-            "ms_per_step": round(float(ms.item()) / args.steps, 4), "higher_is_better": True,
+            "ms_per_step": out["ms_per_kpoint"], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: N_G={n}, R={rows}, one k-point split over "
-                                   f"{world} GPU(s) by column panels",
-                       "n_basis": n, "rows": rows, "ledger_flops_per_step": flops_step,
-                       "parallelism": f"panels-p2p{world}",
+            "config": {"workload": out["workload"], "n_basis": n, "rows": dspec.rows,
+                       "ledger_flops_per_step": flops_step, "parallelism": out["parallelism"],
                        "l2": "operands and H, S exceed the 126 MB L2; no flush"},
-            "fp64_peak_frac": round(value / world / FP64_PEAK_TFLOPS, 4),
-            "roofline": {"bound": "tensor", "achieved": round(fc / (kc / 1e3) / 1e12, 3),
-                         "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": round(fc / (kc / 1e3) / 1e12 / FP64_PEAK_TFLOPS, 4),
-                         "traffic": None,
-                         **executed_flops(fc, kc, _native.load().hsdla_complex_mul_products(),
-                                          n, rows, hpd_rows, joint_rows_of(dspec, tpack, res),
-                                          joint_rows_of(dspec, tpack, res, hpd_only=True)),
-                         "kernel_ms": {k: round(statistics.mean(v), 4) for k, v in kern.items()}},
-            "e2e": {"value": round(flops_step / (float(e2e.item()) / 1e3) / 1e12, 4), "unit": UNIT,
+            "gpus_active": world,
+            "fp64_peak_frac": out["contract_frac_rank0"],
+            "panels": out,
+            "e2e": {"value": round(flops_step / (e2e / 1e3) / 1e12, 4), "unit": UNIT,
                     "h2d_bytes_per_step": int(dspec.h2d_bytes), "d2h_bytes_per_step": 32 * n * n,
-                    "ms_per_step": round(float(e2e.item()), 3),
-                    "api": "paper_1602_06589_b200.shard.P2PShardedBuild.run + D2H of H, S"},
-            "gpu_launches": args.steps * (sb.pipe.launches_per_run(dspec)
-                                          + int(any(res.get("joint_split", [])))
-                                          + int(res.get("joint_shift", 0.0) > 0)),
-            "clocks": clk.summary(),
+                    "ms_per_step": round(e2e, 3),
+                    "api": f"paper_1602_06589_b200.shard.{type(sb).__name__}.run + D2H of H, S"},
+            "gpu_launches": args.steps * (sb.pipe.launches_per_run(dspec) + (2 if world > 1 else 0)),
+            "clocks": out["clocks"],
         }
         print(json.dumps(line), flush=True)
-    dist.destroy_process_group()
+
+
+def run_dry(args):
+    """Launcher check without a GPU (gloo): every rank reports the work it would take —
+    its k-points of the C5 batch and its column panels of C3 — and rank 0 prints one line."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_1602_06589_b200.shard import kpoints_for_rank, owned_panels
+
+    rank, world, _ = dist_env()
+    init_dist(world, 0, backend="gloo")
+    mine = {"rank": rank, "host": socket.gethostname(), "pid": os.getpid(),
+            "c5_kpoints": kpoints_for_rank(64, world, rank),
+            "c3_panels": len(owned_panels(7994, world, rank))}
+    got = [None] * world
+    if world > 1:
+        dist.all_gather_object(got, mine)
+    else:
+        got = [mine]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "metric": METRIC, "n_gpus": world, "gpus_active": world,
+                          "steps": args.steps, "warmup": args.warmup,
+                          "config": {"workload": args.config}, "ranks": got}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` started without torchrun: re-launch this script under
+    torch.distributed.run with N ranks (one per GPU, 127.0.0.1 rendezvous) and return its
+    exit code; rank 0's JSON line is the output."""
+    import socket
+    import subprocess
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    if not args.dry_run:
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench: --gpus {args.gpus} but only {have} CUDA device(s) visible",
+                  file=sys.stderr)
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    if args.dry_run:
+        run_dry(args)
     elif args.mode == "panels":
         run_panels(args)
     else:
         run_ours(args)
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized():
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

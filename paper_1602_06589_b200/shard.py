@@ -65,6 +65,55 @@ def gather_panels(mat, n: int, world: int, rank: int, dst: int = 0, group=None):
     return mat
 
 
+def _group_info(group):
+    """(world, rank) of `group`; (1, 0) without an initialised process group."""
+    import torch.distributed as dist
+
+    if not dist.is_available() or not dist.is_initialized():
+        return 1, 0
+    return dist.get_world_size(group), dist.get_rank(group)
+
+
+class NcclShardedBuild:
+    """Reusable state of the NCCL panel-sharded build of one k-point shape: every rank owns
+    an HSPipeline that computes the lower tiles of its column panels; `run` gathers the
+    panels to `dst` (batched send/recv, `gather_panels`) and mirrors there.  Works without
+    a process group (one rank: the plain build plus the mirror pass)."""
+
+    def __init__(self, n: int, heights, *, dst: int = 0, group=None):
+        from .pipeline import HSPipeline
+
+        self.group = group
+        self.world, self.rank = _group_info(group)
+        self.dst = dst
+        self.n = n
+        self.pipe = HSPipeline(n, heights, shard_rank=self.rank, n_shards=self.world)
+
+    def run(self, dspec, tpack, force_general_path: bool = False):
+        """All ranks: build + gather; returns (H, S, result) device views on dst, None elsewhere."""
+        import ctypes
+
+        from . import _native, device
+        from .errors import ContractViolationError
+
+        n = self.n
+        res = self.pipe.run(dspec, tpack, force_general_path)
+        self.last_result = res
+        if self.world > 1:
+            gather_panels(self.pipe.H, n, self.world, self.rank, self.dst, self.group)
+            gather_panels(self.pipe.S, n, self.world, self.rank, self.dst, self.group)
+            if self.rank != self.dst:
+                return None
+            lib = _native.load()
+            for m in (self.pipe.H, self.pipe.S):
+                flag = ctypes.c_int32(0)
+                _native.check(lib.hsdla_mirror_lower(device.ctx(), n, device.ptr(m), m.shape[1],
+                                                     ctypes.byref(flag)), "hsdla_mirror_lower")
+                if flag.value:
+                    raise ContractViolationError("accumulator contains non-finite values")
+        return self.pipe.H[:n, :n], self.pipe.S[:n, :n], res
+
+
 def build_hs_sharded(spec, tmats, config=None, *, dst: int = 0, group=None,
                      transport: str = "nccl"):
     """One k-point's H and S computed by all ranks of the process group (column panels),
@@ -81,34 +130,13 @@ def build_hs_sharded(spec, tmats, config=None, *, dst: int = 0, group=None,
         return _build_hs_sharded_p2p(spec, tmats, config, dst=dst, group=group)
     if transport != "nccl":
         raise ValueError(f"unknown transport {transport!r}")
-    import ctypes
-
-    import torch.distributed as dist
-
-    from . import _native, device
     from .builder import BuildConfig
-    from .errors import ContractViolationError
-    from .pipeline import DeviceSpec, HSPipeline, pack_tmats
+    from .pipeline import DeviceSpec, pack_tmats
 
     config = config or BuildConfig()
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
     dspec = DeviceSpec(spec)
-    pipe = HSPipeline(spec.n_basis, dspec.heights, shard_rank=rank, n_shards=world)
-    res = pipe.run(dspec, pack_tmats(tmats), config.force_general_path)
-    n = spec.n_basis
-    gather_panels(pipe.H, n, world, rank, dst, group)
-    gather_panels(pipe.S, n, world, rank, dst, group)
-    if rank != dst:
-        return None
-    lib = _native.load()
-    for m in (pipe.H, pipe.S):
-        flag = ctypes.c_int32(0)
-        _native.check(lib.hsdla_mirror_lower(device.ctx(), n, device.ptr(m), m.shape[1],
-                                             ctypes.byref(flag)), "hsdla_mirror_lower")
-        if flag.value:
-            raise ContractViolationError("accumulator contains non-finite values")
-    return pipe.H[:n, :n], pipe.S[:n, :n], res
+    return NcclShardedBuild(spec.n_basis, dspec.heights, dst=dst, group=group).run(
+        dspec, pack_tmats(tmats), config.force_general_path)
 
 
 class P2PShardedBuild:
@@ -144,10 +172,14 @@ class P2PShardedBuild:
 
         from .errors import ContractViolationError
 
+        # Nobody stores into dst's H / S before dst has released the previous result (the
+        # views returned by the last run stay valid until the next collective call).
+        dist.barrier(group=self.group)
         try:
             res, bad = self.pipe.run(dspec, tpack, force_general_path), 0
         except ContractViolationError:
             res, bad = None, 1
+        self.last_result = res
         torch.cuda.synchronize()  # this rank's remote stores are complete
         flag = torch.tensor([bad], device="cuda")
         dist.all_reduce(flag, group=self.group)  # orders every rank's stores before dst reads

@@ -62,3 +62,32 @@ def test_executed_flops_accounting():
     # shifted joint form: joint rows that are not HPD
     ind = bench.executed_flops(fc, 1.0, 4, n, r, 0, r, 0)
     assert ind["executed_flops_per_step"] == 16 * r * n * n
+
+
+def test_gpus_flag_spawns_ranks_dry_run():
+    """`bench.py --gpus 2` without torchrun re-launches itself with two ranks (the driver calls
+    it that way); the gloo dry run shows both ranks ran and dealt the work round-robin."""
+    out = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--gpus", "2",
+                          "--dry-run", "--steps", "1", "--warmup", "1"],
+                         capture_output=True, text=True, timeout=600, cwd=REPO,
+                         env={k: v for k, v in os.environ.items()
+                              if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")})
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["gpus_active"] == 2
+    assert sorted(r["rank"] for r in d["ranks"]) == [0, 1]
+    assert len({r["pid"] for r in d["ranks"]}) == 2
+    ks = sorted(k for r in d["ranks"] for k in r["c5_kpoints"])
+    assert ks == list(range(64))
+
+
+def test_workload_names_match_between_arms():
+    sys.path.insert(0, REPO)
+    import bench
+    from paper_1602_06589_b200 import configs
+
+    for c in ("C1", "C2", "C5"):
+        name = bench.workload_name(c, configs.make_instance(c))
+        assert name.startswith(c) and "BASELINE.json configs[" in name

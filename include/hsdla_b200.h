@@ -273,6 +273,18 @@ typedef struct {
    * [A; B]^H sigma diag(I, U^2) [A; B] summed over the atoms is sigma S exactly.  Applied only
    * when every set can take that shift; otherwise non-HPD sets use the reference forms. */
   const double* t_udot2;
+  /* HOST n_atoms or NULL (hsdla_setup_hs / hsdla_setup_hs_async only): atom type index in
+   * [0, n_types).  The atoms of a type share rotation, muffin-tin radius, l_sph, radial data
+   * and T set (exact equality; the caller groups them), so each coefficient block is a type
+   * template times the column phase: A_a = A_type diag(e^{iK.x_a}) (flapw.py:216-232 with
+   * the per-atom factors split off).  The build then evaluates the Bessel / Y_lm / match
+   * factor recurrences once per (type, K), applies the joint T factor once per type
+   * (W = L^H [A_type; B_type], builder.py:231-240 / :284-302 on the template) and writes A,
+   * ||udot|| B, W1, W2 for every atom with its phase, together with the sum planes of the
+   * three-product contraction, in one HBM-bound expansion pass.  Ignored (per-atom path) when
+   * a type mixes T sets or heights, T is smaller than its block, or the sources are on the host. */
+  const int32_t* atom_type;
+  int32_t n_types;
 } hsdla_build_args;
 
 typedef struct {

@@ -12,7 +12,8 @@ import threading
 
 from .errors import NativeLibraryError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhsdla_b200.so")
+LIB_PATH = os.environ.get("HSDLA_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                        "libhsdla_b200.so")  # HSDLA_LIB: A/B builds
 
 HSDLA_OK = 0
 HSDLA_ERR_CUDA = -1000
@@ -74,6 +75,7 @@ class BuildArgs(ctypes.Structure):
         ("h_reference_form", _i32),
         ("A_host", _vp), ("B_host", _vp), ("ld_ab_host", _i64),
         ("t_dense", _P_i32), ("t_udot2", ctypes.POINTER(ctypes.c_double)),
+        ("atom_type", _P_i32), ("n_types", _i32),
     ]
 
 

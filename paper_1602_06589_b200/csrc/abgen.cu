@@ -53,6 +53,7 @@ struct AbParams {
   double2* Bs;
   long long ld;
   double* udot_norms;
+  int zero_phase;  // 1: e^{i K.x_a} taken as 1 (per-type templates at the origin)
 };
 
 constexpr int kAbThreads = 128;
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(kAbThreads) ab_kernel(AbParams p, const int* _
 
   // Phase e^{i K.x_a}.
   const double* X = p.pos + 3 * a;
-  const double th = kx * X[0] + ky * X[1] + kz * X[2];
+  const double th = p.zero_phase ? 0.0 : kx * X[0] + ky * X[1] + kz * X[2];
   double phs, phc;
   sincos(th, &phs, &phc);
   const double sqo = sqrt(p.omega);
@@ -390,6 +391,7 @@ int ab_generate(hsdla_ctx* ctx, const hsdla_ab_args* args) {
   p.Bs = reinterpret_cast<double2*>(args->B_scaled);
   p.ld = args->ld;
   p.udot_norms = args->udot_norms;
+  p.zero_phase = 0;
   // Group atoms by l_sph; upload (atom, row offset) lists through the arena.
   std::vector<int> atoms;
   std::vector<long long> offs;
@@ -421,6 +423,57 @@ int ab_generate(hsdla_ctx* ctx, const hsdla_ab_args* args) {
           p.udot_norms);
       HS_CHECK_LAUNCH();
     }
+  }
+  return HSDLA_OK;
+}
+
+// Per-type templates: the generator run once per type for a representative atom placed at
+// the origin (phase 1), rows toff[i] of At / Bt (ld ldt).  The type's atoms differ from it
+// only by the column phase e^{i K.x_a}, applied by the expansion pass (expand.cu).
+int ab_generate_templates(hsdla_ctx* ctx, const hsdla_ab_args* args, const std::vector<int>& reps,
+                          const std::vector<long long>& toff, double2* At, double2* Bt,
+                          long long ldt) {
+  int rc = upload_ylm_tables();
+  if (rc) return rc;
+  AbParams p;
+  p.n_basis = args->n_basis;
+  p.kv = args->k_vectors;
+  p.pos = args->positions;
+  p.rot = args->rotations;
+  p.rmt = args->mt_radius;
+  p.radial = args->radial;
+  p.radial_stride = args->radial_stride;
+  p.omega = args->omega;
+  p.A = At;
+  p.B = Bt;
+  p.Bs = nullptr;
+  p.ld = ldt;
+  p.udot_norms = nullptr;
+  p.zero_phase = 1;
+  std::vector<int> atoms;
+  std::vector<long long> offs;
+  std::vector<int> group_l, group_begin, group_count;
+  for (int L = 0; L <= HSDLA_MAX_LSPH; ++L) {
+    const int begin = (int)atoms.size();
+    for (size_t i = 0; i < reps.size(); ++i)
+      if (args->l_sph[reps[i]] == L) { atoms.push_back(reps[i]); offs.push_back(toff[i]); }
+    if ((int)atoms.size() > begin) {
+      group_l.push_back(L);
+      group_begin.push_back(begin);
+      group_count.push_back((int)atoms.size() - begin);
+    }
+  }
+  rc = arena_begin(ctx, atoms.size() * (sizeof(int) + sizeof(long long)) + 64);
+  if (rc) return rc;
+  int* datoms = static_cast<int*>(arena_push(ctx, atoms.data(), atoms.size() * sizeof(int), nullptr));
+  long long* doffs = static_cast<long long*>(
+      arena_push(ctx, offs.data(), offs.size() * sizeof(long long), nullptr));
+  rc = arena_flush(ctx);
+  if (rc) return rc;
+  for (size_t gi = 0; gi < group_l.size(); ++gi) {
+    rc = kAbLaunchers[group_l[gi]](ctx, p, datoms + group_begin[gi], doffs + group_begin[gi],
+                                   group_count[gi]);
+    if (rc) return rc;
   }
   return HSDLA_OK;
 }

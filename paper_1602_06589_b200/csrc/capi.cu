@@ -118,6 +118,16 @@ Seg make_seg(const double2* P, long long ldP, const double2* Q, long long ldQ, i
   s.ldQ = ldQ;
   s.k = k;
   s.pad_ = 0;
+  s.Pd = nullptr;
+  s.Qs = nullptr;
+  return s;
+}
+// A segment whose P and Q carry their sum planes (Pd = Re - Im of P, Qs = Re + Im of Q).
+Seg make_seg_planes(const double2* P, const double* Pd, long long ldP, const double2* Q,
+                    const double* Qs, long long ldQ, int k) {
+  Seg s = make_seg(P, ldP, Q, ldQ, k);
+  s.Pd = Pd;
+  s.Qs = Qs;
   return s;
 }
 
@@ -152,6 +162,7 @@ int hsdla_ctx_create(hsdla_ctx** out, void* stream) {
   if (int rc = preload_abgen()) return rc;
   if (int rc = preload_small()) return rc;
   if (int rc = preload_gaunt()) return rc;
+  if (int rc = preload_expand()) return rc;
   // Mapped pinned memory: build results are published by a kernel store, not a DMA copy,
   // so they never queue behind the large H / S copies on the D2H engine.
   HS_CUDA(cudaHostAlloc(&c->scratch_host, 2048 * sizeof(int), cudaHostAllocMapped));
@@ -502,10 +513,48 @@ constexpr unsigned kWaitGeq = 0x0;  // CU_STREAM_WAIT_VALUE_GEQ
 
 // ---- composed build ------------------------------------------------------------------
 namespace {
+// Atom types of the template path (hsdla_build_args.atom_type): one representative atom and
+// one template row block per type.  ok = false -> per-atom generation.
+struct TypeInfo {
+  bool ok = false;
+  std::vector<int> rep;          // representative atom per type
+  std::vector<long long> toff;   // template row offset per type
+  long long ldt = 0;             // template leading dimension (rows, multiple of 16)
+};
+
+TypeInfo type_info(const hsdla_build_args* a) {
+  TypeInfo ti;
+  static int env = -1;  // HSDLA_TEMPLATES=0: per-atom generation and T applications
+  if (env < 0) {
+    const char* e = getenv("HSDLA_TEMPLATES");
+    env = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (!env || !a->atom_type || a->n_types < 1 || a->A_host || (a->ld & 1)) return ti;
+  ti.rep.assign(a->n_types, -1);
+  for (int i = 0; i < a->n_atoms; ++i) {
+    const int ty = a->atom_type[i];
+    if (ty < 0 || ty >= a->n_types) return ti;
+    if (a->t_dim[a->t_index[i]] != a->heights[i]) return ti;  // T smaller than its block
+    int& r = ti.rep[ty];
+    if (r < 0) r = i;
+    else if (a->heights[r] != a->heights[i] || a->t_index[r] != a->t_index[i]) return ti;
+  }
+  long long rows = 0;
+  for (int ty = 0; ty < a->n_types; ++ty) {
+    if (ti.rep[ty] < 0) return ti;
+    ti.toff.push_back(rows);
+    rows += a->heights[ti.rep[ty]];
+  }
+  ti.ldt = (rows + 15) / 16 * 16;
+  ti.ok = true;
+  return ti;
+}
+
 struct WsLayout {
-  size_t bs, z, xy, forms, tdim, info, joint, jinfo, u2, total;
+  size_t bs, z, xy, forms, tdim, info, joint, jinfo, u2, planes, tpl, total;
   int mp;
   long long R;
+  long long ldt;  // > 0: template-path regions present
 };
 
 WsLayout ws_layout(const hsdla_build_args* a) {
@@ -538,6 +587,13 @@ WsLayout ws_layout(const hsdla_build_args* a) {
   off += stack;
   w.xy = off;
   off += stack;
+  // Template path: the sum planes of A, UB, W1 (XY), W2 (Z) and the four per-type templates.
+  const TypeInfo ti = type_info(a);
+  w.ldt = ti.ok ? ti.ldt : 0;
+  w.planes = off;
+  if (ti.ok && planes_enabled()) off += 8 * align_up(size_t(a->ld) * a->n_basis * sizeof(double));
+  w.tpl = off;
+  if (ti.ok) off += 4 * align_up(size_t(ti.ldt) * a->n_basis * sizeof(double2));
   w.total = off;
   return w;
 }
@@ -630,6 +686,10 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     }
   }
   const WsLayout w = ws_layout(a);
+  const TypeInfo ti = type_info(a);
+  // Template path (hsdla_build_args.atom_type): per-type generation + expansion with sum planes.
+  const bool tpl = ab != nullptr && ti.ok && w.ldt > 0 && ab->B_scaled != nullptr &&
+                   ab->udot_norms == nullptr && ab->ld == a->ld && a->B_scaled == ab->B_scaled;
   if (a->workspace_bytes < w.total) {
     set_error("workspace too small");
     return -2;
@@ -767,7 +827,49 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
   } else {
     HS_CUDA(cudaEventRecord(ctx->join, ctx->stream));
   }
-  if (ab) {
+  // Sum planes (Re - Im, Re + Im) of A, UB, W1 (XY) and W2 (Z), and the per-type templates.
+  const size_t pl_n = align_up(size_t(ld) * n * sizeof(double)) / sizeof(double);
+  double* const pln = reinterpret_cast<double*>(ws + w.planes);
+  double *const Ad = pln, *const As = pln + pl_n, *const Ud = pln + 2 * pl_n, *const Us = pln + 3 * pl_n;
+  double *const W1d = pln + 4 * pl_n, *const W1s = pln + 5 * pl_n, *const W2d = pln + 6 * pl_n,
+                *const W2s = pln + 7 * pl_n;
+  const long long ldt = w.ldt;
+  const bool pl = tpl && planes_enabled();  // sum planes written and staged (off by default)
+  double2* const tA = reinterpret_cast<double2*>(ws + w.tpl);
+  double2* const tB = tA + ldt * n;
+  double2* const tW1 = tB + ldt * n;
+  double2* const tW2 = tW1 + ldt * n;
+  const int4* ex_atoms = nullptr;
+  const long long* ex_off = nullptr;
+  if (tpl) {
+    // B itself is needed later only by T sets that do not take the plain joint form; known
+    // before the H decision when this build reuses a T preparation.
+    bool need_b = true;
+    if (reuse && key.joint && !ctx->joint_pending && (int)ctx->joint_info.size() == a->n_tsets) {
+      need_b = false;
+      for (int t = 0; t < a->n_tsets; ++t)
+        if (ctx->joint_info[t] != 0 || ctx->joint_split[t]) need_b = true;
+    }
+    rc = ab_generate_templates(ctx, ab, ti.rep, ti.toff, tA, tB, ldt);
+    if (rc) return rc;
+    std::vector<int4> ex(na);
+    std::vector<long long> eo(na);
+    for (int i = 0; i < na; ++i) {
+      const int ty = a->atom_type[i];
+      ex[i] = make_int4(i, (int)ti.toff[ty], a->heights[i], ty);
+      eo[i] = a->row_offset[i];
+    }
+    if ((rc = arena_begin(ctx, na * (sizeof(int4) + sizeof(long long)) + 64))) return rc;
+    ex_atoms = static_cast<const int4*>(arena_push(ctx, ex.data(), na * sizeof(int4), nullptr));
+    ex_off = static_cast<const long long*>(arena_push(ctx, eo.data(), na * sizeof(long long), nullptr));
+    if ((rc = arena_flush(ctx))) return rc;
+    ExpandOut o{reinterpret_cast<double2*>(ab->A), pl ? Ad : nullptr, pl ? As : nullptr,
+                reinterpret_cast<double2*>(ab->B_scaled), pl ? Ud : nullptr, pl ? Us : nullptr,
+                need_b ? reinterpret_cast<double2*>(ab->B) : nullptr, 1};
+    rc = launch_expand(ctx, n, ab->k_vectors, ab->positions, ab->radial, ab->radial_stride,
+                       ex_atoms, ex_off, na, tA, tB, ldt, o, ld);
+    if (rc) return rc;
+  } else if (ab) {
     rc = ab_generate(ctx, ab);
     if (rc) return rc;
   }
@@ -877,6 +979,8 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     if ((rc = launch_contract(ctx, probs, segs, flag))) return rc;
   } else {
     std::vector<Seg> segs{make_seg(A, ld, A, ld, (int)R), make_seg(Bs, ld, Bs, ld, (int)R)};
+    if (pl)
+      segs = {make_seg_planes(A, Ad, ld, A, As, ld, (int)R), make_seg_planes(Bs, Ud, ld, Bs, Us, ld, (int)R)};
     std::vector<Prob> probs;
     add_tri(probs, D2(a->S), 0, 2);
     if (s_streamed) probs[0].panel_done = sl.panel_cnt;
@@ -952,6 +1056,34 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     all_joint &= sl.joint[t] != 0;
   }
 
+  // Template path with every set on the plain joint form: W = L^H [A_type; B_type] once per
+  // type (W1 = L11^H A_t + L21^H B_t, W2 = L22^H B_t), then every atom's W1, W2 rows are the
+  // template times its phase (expansion pass, with sum planes).
+  bool tpl_h = tpl && all_joint;
+  for (int t = 0; t < a->n_tsets && tpl_h; ++t) tpl_h = sl.joint[t] == 1;
+  if (tpl_h) {
+    std::vector<Seg> segs;
+    std::vector<Prob> probs;
+    for (int ty = 0; ty < (int)ti.rep.size(); ++ty) {
+      const int ts = a->t_index[ti.rep[ty]], m = a->t_dim[ts];
+      const long long to = ti.toff[ty];
+      const double2* L = joint + (long long)ts * lj * lj;
+      int s0 = (int)segs.size();
+      segs.push_back(make_seg(L, lj, tA + to, ldt, m));
+      segs.push_back(make_seg(L + m, lj, tB + to, ldt, m));
+      probs.push_back(make_prob(tW1 + to, ldt, m, n, PROB_GENERAL, s0, 2, 0));
+      s0 = (int)segs.size();
+      segs.push_back(make_seg(L + m + m * lj, lj, tB + to, ldt, m));
+      probs.push_back(make_prob(tW2 + to, ldt, m, n, PROB_GENERAL, s0, 1, 0));
+    }
+    if ((rc = launch_contract(ctx, probs, segs, flag))) return rc;
+    HS_CUDA(cudaEventRecord(ev[3], ctx->stream));
+    ExpandOut o{XY, pl ? W1d : nullptr, pl ? W1s : nullptr, Z, pl ? W2d : nullptr,
+                pl ? W2s : nullptr, nullptr, 0};
+    if ((rc = launch_expand(ctx, n, ab->k_vectors, ab->positions, ab->radial, ab->radial_stride,
+                            ex_atoms, ex_off, na, tW1, tW2, ldt, o, ld)))
+      return rc;
+  } else {
   // Rows of a block beyond its T size must be zero in Z / XY (builder.py:232-245 compaction).
   for (int i = 0; i < na; ++i) {
     const int m = a->t_dim[a->t_index[i]], h = a->heights[i];
@@ -1030,6 +1162,7 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
       if ((rc = launch_ttail(ctx, tdev, (int)tails.size(), max_tail, n, A, B, ld, XY, Z, joint, lj))) return rc;
     }
   }
+  }  // per-atom T applications
   HS_CUDA(cudaEventRecord(ev[4], ctx->stream));
   // S leaves for the host now, under the H contraction (4/3 of S's time): started right
   // after S it would contend with the bandwidth-heavier T applications (measured +25% on
@@ -1053,7 +1186,10 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
   //      joint T sets: H += W1^H W1 + W2^H W2 over their rows (XY and Z slots), K = 2R.
   {
     std::vector<Seg> segs;
-    if (all_joint) {
+    if (tpl_h && pl) {
+      segs.push_back(make_seg_planes(XY, W1d, ld, XY, W1s, ld, (int)R));
+      segs.push_back(make_seg_planes(Z, W2d, ld, Z, W2s, ld, (int)R));
+    } else if (all_joint) {  // (template path without planes included)
       segs.push_back(make_seg(XY, ld, XY, ld, (int)R));
       segs.push_back(make_seg(Z, ld, Z, ld, (int)R));
     } else {

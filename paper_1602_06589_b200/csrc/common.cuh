@@ -41,6 +41,19 @@ inline int cmul_mode() {
   return m;
 }
 
+// Sum planes of the three-product multiply for the pipeline's generated stacks (template path):
+// HSDLA_PLANES=1 writes them in the expansion pass and runs the DADD-free contraction on them.
+// Off by default: measured slower on B200 (C2 contraction 2.23-2.26 vs 2.18 ms; the extra
+// plane loads and L2 footprint cost more than the DADDs they save, profiles/README.md).
+inline bool planes_enabled() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("HSDLA_PLANES");
+    m = (e && e[0] == '1') ? 1 : 0;
+  }
+  return m == 1;
+}
+
 #define HS_CUDA(call)                                                                  \
   do {                                                                                 \
     cudaError_t _e = (call);                                                           \
@@ -66,6 +79,11 @@ struct Seg {
   long long ldP, ldQ;
   int k;
   int pad_;
+  // Optional real "sum planes" of the three-product multiply, laid out like P / Q (element
+  // row + col * ld, in doubles): Pd = Re P - Im P, Qs = Re Q + Im Q.  When every segment of a
+  // launch has them the kernel stages them instead of forming the sums with DADDs.
+  const double* Pd;
+  const double* Qs;
 };
 
 enum ProbKind : int {
@@ -218,6 +236,30 @@ int launch_ttail(hsdla_ctx* ctx, const int4* atoms_dev, int n_atoms, int max_tai
                  const double2* A, const double2* B, long long ld, double2* XY, double2* Z,
                  const double2* joint, long long lj);
 int ab_generate(hsdla_ctx* ctx, const hsdla_ab_args* args);
+// Per-type templates (abgen.cu): representative atoms reps[i] at the origin into rows toff[i]
+// of At / Bt (ld ldt).
+int ab_generate_templates(hsdla_ctx* ctx, const hsdla_ab_args* args, const std::vector<int>& reps,
+                          const std::vector<long long>& toff, double2* At, double2* Bt,
+                          long long ldt);
+// Template expansion (expand.cu): for every atom block e (atoms_dev[e] = (atom, template row,
+// height, -), first stacked row off_dev[e]) and column t, with phase z = e^{i K_t.x_atom}:
+//   O0 = T0 z,  O1 = (scale1 ? ||udot||_row : 1) T1 z,  O2 = T1 z (if non-null),
+// and the three-product sum planes Od = Re - Im, Os = Re + Im of O0 and O1 (if non-null).
+struct ExpandOut {
+  double2* O0;
+  double* O0d;
+  double* O0s;
+  double2* O1;
+  double* O1d;
+  double* O1s;
+  double2* O2;
+  int scale1;
+};
+int launch_expand(hsdla_ctx* ctx, int n_basis, const double* kv, const double* pos,
+                  const double* radial, int radial_stride, const int4* atoms_dev,
+                  const long long* off_dev, int n_blocks, const double2* T0, const double2* T1,
+                  long long ldt, const ExpandOut& o, long long ld);
+int preload_expand();
 // kind 0: o1/o2 = j_l(x), j'_l(x), (l_max+1) x n row-major; kind 1: o1 = Y_lm (complex,
 // (l_max+1)^2 x n row-major) at unit directions in (n x 3).
 int special_functions(hsdla_ctx* ctx, int kind, int l_max, int n, const double* in, double* o1,

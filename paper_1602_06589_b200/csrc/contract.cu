@@ -50,11 +50,15 @@ constexpr int kChunk = 16;                       // complex K per stage
 // consecutive columns then start 8 banks apart, so a DMMA fragment load (8 columns x 4
 // consecutive doubles per half-warp phase) is conflict-free with compile-time offsets.
 // PAD = 0 instead keeps 256-B columns with a 32-byte XOR swizzle (k-chunk index ^ column&7).
-template <int PAD> struct Layout {
-  static constexpr int kColDoubles = 2 * kChunk + (PAD == 1 ? 4 : 0);
+// PL: the stage also holds the P-side (Re - Im) and Q-side (Re + Im) sum planes of the
+// three-product multiply, one double per K element and column (8 KB each per stage).
+// KC = complex K elements per stage (16, or 8 with planes so that four stages fit 2 CTAs/SM).
+template <int PAD, bool PL = false, int ST = kStages, int KC = kChunk> struct Layout {
+  static constexpr int kColDoubles = 2 * KC + (PAD == 1 ? 4 : 0);
   static constexpr int kOpDoubles = kTile * kColDoubles;
-  static constexpr int kStageDoubles = 2 * kOpDoubles;
-  static constexpr size_t kSmemBytes = size_t(kStages) * kStageDoubles * sizeof(double);
+  static constexpr int kPlaneDoubles = kTile * KC;
+  static constexpr int kStageDoubles = 2 * kOpDoubles + (PL ? 2 * kPlaneDoubles : 0);
+  static constexpr size_t kSmemBytes = size_t(ST) * kStageDoubles * sizeof(double);
 };
 constexpr int kPartialDoubles = kTile * kTile * 2;  // one partial tile (64 KB)
 
@@ -73,10 +77,21 @@ struct SKParams {
   int* flag;
 };
 
+#ifndef HSDLA_DMMA_VOLATILE
+#define HSDLA_DMMA_VOLATILE 1
+#endif
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+#if HSDLA_DMMA_VOLATILE
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
+#else
+  // register-only: the compiler may interleave DMMAs of different accumulators with the
+  // fragment loads and sum DADDs (each accumulator's own order is fixed by its dependence)
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+#endif
 }
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, int src_bytes) {
@@ -119,16 +134,23 @@ __device__ __forceinline__ Seg load_seg(const Seg* s) {
 // (128 threads, ~250 registers, 2 warps per SM sub-partition); JB = 2 -> warp tile 32x16,
 // 8 warps (256 threads, <= 128 registers, 4 warps per sub-partition).
 // G3 with JB = 2 keeps three accumulator sets in 255 registers at one 8-warp CTA per SM.
-template <int JB, int PAD, bool G3 = false>
+// PL (G3 only, pair layout): the sums P_re - P_im and Q_re + Q_im come precomputed from global
+// memory (Seg::Pd / Seg::Qs, written by their producers) and are staged with the operands, so
+// the K loop issues no DADD on the FP64 pipe; ST = ring stages (2 keeps two CTAs per SM).
+template <int JB, int PAD, bool G3 = false, bool PL = false, int ST = kStages, int KC = kChunk>
 __global__ void __launch_bounds__(32 * 2 * (8 / JB), (G3 && JB == 2) ? 1 : 2)
     contract_kernel(SKParams sk) {
+  static_assert(!PL || (G3 && PAD == 2), "sum planes need the three-product pair layout");
+  static_assert(KC == 16 || (KC == 8 && PAD == 2), "8-element chunks: pair layout only");
+  constexpr int kStages = ST;
   extern __shared__ __align__(128) double smem[];
-  constexpr int kColDoubles = Layout<PAD>::kColDoubles;
-  constexpr int kOpDoubles = Layout<PAD>::kOpDoubles;
-  constexpr int kStageDoubles = Layout<PAD>::kStageDoubles;
+  constexpr int kColDoubles = Layout<PAD, PL, ST, KC>::kColDoubles;
+  constexpr int kOpDoubles = Layout<PAD, PL, ST, KC>::kOpDoubles;
+  constexpr int kStageDoubles = Layout<PAD, PL, ST, KC>::kStageDoubles;
+  constexpr int kPlaneDoubles = Layout<PAD, PL, ST, KC>::kPlaneDoubles;
   constexpr int kWarpCols = 8 * JB;
   constexpr int kThreads = 32 * 2 * (kTile / kWarpCols);
-  constexpr int kColStep = kThreads / 16;           // columns covered per cp.async round
+  constexpr int kColStep = kThreads / KC;           // columns covered per cp.async round
   constexpr int kRounds = kTile / kColStep;         // cp.async rounds per operand per chunk
 
   const int tid = threadIdx.x;
@@ -138,11 +160,21 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), (G3 && JB == 2) ? 1 : 2)
   const int g = lane >> 2, q = lane & 3;
   const unsigned sign_hi = (q & 1) ? 0x80000000u : 0u;
   // cp.async slot of this thread: complex element lp of the chunk, columns lc + kColStep*r.
-  const int lp = tid & 15;
-  const int lc = tid >> 4;
+  const int lp = tid & (KC - 1);
+  const int lc = tid / KC;
   const int dst_lane = PAD == 1 ? lp * 2
                        : PAD == 2 ? ((((lp >> 1) ^ ((lc & 1) << 1)) << 2) + (lp & 1) * 2)
                                   : ((((lp >> 1) ^ (lc & 7)) << 2) + (lp & 1) * 2);
+  // Sum-plane cp.async slot: 16-byte piece lp2 (K elements 2 lp2, 2 lp2 + 1) of column lc2 +
+  // kColStep2 * r; the 32-byte unit u of column c is stored at u ^ sw(c) (KC = 16: c & 3,
+  // KC = 8: (c >> 1) & 1), so a fragment's four consecutive K elements of eight columns are
+  // read with two wavefronts.
+  constexpr int kColStep2 = kThreads / (KC / 2);
+  constexpr int kRounds2 = kTile / kColStep2;
+  const int lp2 = tid & (KC / 2 - 1);
+  const int lc2 = tid / (KC / 2);
+  auto psw = [](int c) { return KC == 16 ? (c & 3) : ((c >> 1) & 1); };
+  const int dst2 = ((((lp2 >> 1) ^ psw(lc2)) << 2) + ((lp2 & 1) << 1));
 
   const int cta = blockIdx.x;
   // Work order: dp_waves waves of whole tiles (CTA g takes tile g + w*grid, so the CTAs of
@@ -193,8 +225,8 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), (G3 && JB == 2) ? 1 : 2)
     {
       int cb = 0;
       for (; isi < send; ++isi) {
-        const int ncs = (sk.segs[isi].k + kChunk - 1) / kChunk;
-        if (c_lo < cb + ncs) { iko = (c_lo - cb) * kChunk; break; }
+        const int ncs = (sk.segs[isi].k + KC - 1) / KC;
+        if (c_lo < cb + ncs) { iko = (c_lo - cb) * KC; break; }
         cb += ncs;
       }
     }
@@ -208,6 +240,14 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), (G3 && JB == 2) ? 1 : 2)
     const double2* bP = cur.P + (long long)(i0 + lc) * cur.ldP + lp;
     const double2* bQ = cur.Q + (long long)(j0 + lc) * cur.ldQ + lp;
     long long stP = (long long)kColStep * cur.ldP, stQ = (long long)kColStep * cur.ldQ;
+    const int nvP2 = max(0, min(kRounds2, (mP - i0 - lc2 + kColStep2 - 1) / kColStep2));
+    const int nvQ2 = max(0, min(kRounds2, (mQ - j0 - lc2 + kColStep2 - 1) / kColStep2));
+    const double* bPd = nullptr;
+    const double* bQs = nullptr;
+    if constexpr (PL) {
+      bPd = cur.Pd + (long long)(i0 + lc2) * cur.ldP + 2 * lp2;
+      bQs = cur.Qs + (long long)(j0 + lc2) * cur.ldQ + 2 * lp2;
+    }
 
     // cp.async rounds [r0, r1) of the chunk at iko into `stage` (round r = columns
     // lc + kColStep*r of both operands), then advance() moves iko to the next chunk.
@@ -225,9 +265,30 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), (G3 && JB == 2) ? 1 : 2)
         p += stP;
         qq += stQ;
       }
+      if constexpr (PL) {
+        if (r0 == 0) {
+          double* sPd = smem + stage * kStageDoubles + 2 * kOpDoubles + lc2 * KC + dst2;
+          double* sQs = sPd + kPlaneDoubles;
+          // bytes of this 16-byte piece inside the segment: K may be odd (the pad row past it
+          // need not be zero in the planes); the remainder is zero-filled
+          const int kr = cur.k - (iko + 2 * lp2);
+          const int nb2 = kr >= 2 ? 16 : (kr == 1 ? 8 : 0);
+          const double* pd = bPd + iko;
+          const double* qs = bQs + iko;
+#pragma unroll
+          for (int r = 0; r < kRounds2; ++r) {
+            cp_async16(sPd + r * kColStep2 * KC, r < nvP2 && nb2 ? pd : cur.Pd,
+                       r < nvP2 ? nb2 : 0);
+            cp_async16(sQs + r * kColStep2 * KC, r < nvQ2 && nb2 ? qs : cur.Qs,
+                       r < nvQ2 ? nb2 : 0);
+            pd += (long long)kColStep2 * cur.ldP;
+            qs += (long long)kColStep2 * cur.ldQ;
+          }
+        }
+      }
     };
     auto advance = [&]() {
-      iko += kChunk;
+      iko += KC;
       if (iko >= cur.k) {
         int nx = isi + 1;
         while (nx < send && sk.segs[nx].k <= 0) ++nx;
@@ -239,6 +300,10 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), (G3 && JB == 2) ? 1 : 2)
           bQ = cur.Q + (long long)(j0 + lc) * cur.ldQ + lp;
           stP = (long long)kColStep * cur.ldP;
           stQ = (long long)kColStep * cur.ldQ;
+          if constexpr (PL) {
+            bPd = cur.Pd + (long long)(i0 + lc2) * cur.ldP + 2 * lp2;
+            bQs = cur.Qs + (long long)(j0 + lc2) * cur.ldQ + 2 * lp2;
+          }
         }
       }
     };
@@ -293,8 +358,9 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), (G3 && JB == 2) ? 1 : 2)
         // 32-byte units of odd columns are swapped in pairs (unit ^ 2), so the two
         // columns of a quarter-warp's 128-bit load fall in opposite 64-byte bank halves.
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (sk.spread && more) issue_rounds(nstage, j * kRounds / 4, (j + 1) * kRounds / 4);
+        for (int j = 0; j < KC / 4; ++j) {
+          if (sk.spread && more)
+            issue_rounds(nstage, j * kRounds / (KC / 4), (j + 1) * kRounds / (KC / 4));
           const int off = (((2 * j + (q >> 1)) ^ ((g & 1) << 1)) << 2) + ((q & 1) << 1);
           double2 av[4], bv[JB];
 #pragma unroll
@@ -313,10 +379,21 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), (G3 && JB == 2) ? 1 : 2)
                 dmma(accX[ib][jb][0], accX[ib][jb][1], av[ib].y, bv[jb].y);
               }
             double sa[4], sb[JB];
+            if constexpr (PL) {
+              const double* pda = sP + 2 * kOpDoubles + (wm * 32 + g) * KC;
+              const double* qsb = pda - (wm * 32 + g) * KC + kPlaneDoubles +
+                                  (wn * kWarpCols + g) * KC;
+              const int po = ((j ^ psw(g)) << 2) + q;
 #pragma unroll
-            for (int ib = 0; ib < 4; ++ib) sa[ib] = av[ib].x - av[ib].y;
+              for (int ib = 0; ib < 4; ++ib) sa[ib] = pda[ib * 8 * KC + po];
 #pragma unroll
-            for (int jb = 0; jb < JB; ++jb) sb[jb] = bv[jb].x + bv[jb].y;
+              for (int jb = 0; jb < JB; ++jb) sb[jb] = qsb[jb * 8 * KC + po];
+            } else {
+#pragma unroll
+              for (int ib = 0; ib < 4; ++ib) sa[ib] = av[ib].x - av[ib].y;
+#pragma unroll
+              for (int jb = 0; jb < JB; ++jb) sb[jb] = bv[jb].x + bv[jb].y;
+            }
 #pragma unroll
             for (int ib = 0; ib < 4; ++ib)
 #pragma unroll
@@ -531,11 +608,17 @@ int preload_contract() {
                        (const void*)contract_kernel<2, 2>, (const void*)contract_kernel<4, 0>,
                        (const void*)contract_kernel<4, 1>, (const void*)contract_kernel<4, 2>,
                        (const void*)contract_kernel<2, 2, true>,
-                       (const void*)contract_kernel<4, 2, true>};
+                       (const void*)contract_kernel<4, 2, true>,
+                       (const void*)contract_kernel<4, 2, true, true, 2>,
+                       (const void*)contract_kernel<4, 2, true, true, 3>,
+                       (const void*)contract_kernel<4, 2, true, true, 4, 8>,
+                       (const void*)contract_kernel<4, 2, true, true, 3, 8>};
   const size_t smem[] = {Layout<0>::kSmemBytes, Layout<1>::kSmemBytes, Layout<2>::kSmemBytes,
                          Layout<0>::kSmemBytes, Layout<1>::kSmemBytes, Layout<2>::kSmemBytes,
-                         Layout<2>::kSmemBytes, Layout<2>::kSmemBytes};
-  for (int i = 0; i < 8; ++i) {
+                         Layout<2>::kSmemBytes, Layout<2>::kSmemBytes,
+                         Layout<2, true, 2>::kSmemBytes, Layout<2, true, 3>::kSmemBytes,
+                         Layout<2, true, 4, 8>::kSmemBytes, Layout<2, true, 3, 8>::kSmemBytes};
+  for (int i = 0; i < 12; ++i) {
     cudaFuncAttributes at;
     HS_CUDA(cudaFuncGetAttributes(&at, fns[i]));
     if (first_on_device(fns[i]))
@@ -546,6 +629,31 @@ int preload_contract() {
 
 int launch_contract(hsdla_ctx* ctx, const std::vector<Prob>& probs_in,
                     const std::vector<Seg>& segs, int* flag_dev) {
+  // Variant selection (HSDLA_WARP_COLS = 32 | 16, HSDLA_SMEM_PAD = 0 | 1) for A/B tests.
+  // Shared-memory layout / fragment path: HSDLA_CP_LAYOUT = pair (default: paired K steps,
+  // 128-bit fragment loads) | xor (32-byte XOR swizzle, 64-bit loads) | pad (288-byte columns).
+  // Complex multiply (cmul_mode, HSDLA_CMUL): 3 (default) uses the three-product kernel, pair
+  // layout only.
+  static int variant = -1, pad = -1, cmul = -1;
+  // Sum planes: when every segment carries them (the pipeline's generated stacks), the
+  // DADD-free kernel (HSDLA_PLANES=1, common.cuh); ring HSDLA_PL_VARIANT = 8x4 (default: chunks
+  // of 8 complex K, 4 stages) | 8x3 | 16x2 | 16x3.
+  static int planes_env = -1, pl_kc = 8, pl_stages = 4;
+  if (variant < 0) {
+    const char* e = getenv("HSDLA_WARP_COLS");
+    variant = (e && atoi(e) == 16) ? 2 : 4;
+    const char* p = getenv("HSDLA_CP_LAYOUT");
+    pad = (p && std::string(p) == "pad") ? 1 : (p && std::string(p) == "xor") ? 0 : 2;
+    cmul = cmul_mode();
+    planes_env = planes_enabled() ? 1 : 0;
+    const char* pv = getenv("HSDLA_PL_VARIANT");
+    if (pv && std::string(pv) == "8x3") { pl_kc = 8; pl_stages = 3; }
+    if (pv && std::string(pv) == "16x2") { pl_kc = 16; pl_stages = 2; }
+    if (pv && std::string(pv) == "16x3") { pl_kc = 16; pl_stages = 3; }
+  }
+  bool planes = planes_env && variant == 4 && pad == 2 && cmul == 3 && !segs.empty();
+  for (const Seg& sg : segs) planes = planes && sg.Pd && sg.Qs;
+  const int kc = planes ? pl_kc : kChunk;
   std::vector<Prob> probs;
   long long total = 0;
   for (Prob p : probs_in) {
@@ -559,7 +667,7 @@ int launch_contract(hsdla_ctx* ctx, const std::vector<Prob>& probs_in,
     }
     p.ntiles = prob_tile_count(p);
     int nch = 0;
-    for (int s = 0; s < p.nseg; ++s) nch += (segs[p.seg0 + s].k + kChunk - 1) / kChunk;
+    for (int s = 0; s < p.nseg; ++s) nch += (segs[p.seg0 + s].k + kc - 1) / kc;
     p.nchunks = nch > 0 ? nch : 1;  // an empty K still visits each tile once (C = beta C)
     p.it_base = total;
     total += (long long)p.ntiles * p.nchunks;
@@ -573,28 +681,30 @@ int launch_contract(hsdla_ctx* ctx, const std::vector<Prob>& probs_in,
     const char* e = getenv("HSDLA_CONTRACT");
     mode = (e && std::string(e) == "tma") ? 1 : (e && std::string(e) == "cpasync") ? 2 : 0;
   }
-  if (mode == 1 || (mode == 0 && tma_wants(probs)))
+  if (!planes && (mode == 1 || (mode == 0 && tma_wants(probs))))
     return launch_contract_tma(ctx, probs, total, segs, flag_dev);
-  // Variant selection (HSDLA_WARP_COLS = 32 | 16, HSDLA_SMEM_PAD = 0 | 1) for A/B tests.
-  // Shared-memory layout / fragment path: HSDLA_CP_LAYOUT = pair (default: paired K steps,
-  // 128-bit fragment loads) | xor (32-byte XOR swizzle, 64-bit loads) | pad (288-byte columns).
-  // Complex multiply (cmul_mode, HSDLA_CMUL): 3 (default) uses the three-product kernel, pair
-  // layout only.
-  static int variant = -1, pad = -1, cmul = -1;
-  if (variant < 0) {
-    const char* e = getenv("HSDLA_WARP_COLS");
-    variant = (e && atoi(e) == 16) ? 2 : 4;
-    const char* p = getenv("HSDLA_CP_LAYOUT");
-    pad = (p && std::string(p) == "pad") ? 1 : (p && std::string(p) == "xor") ? 0 : 2;
-    cmul = cmul_mode();
-  }
   const void* kfns[2][4] = {
       {(const void*)contract_kernel<2, 0>, (const void*)contract_kernel<2, 1>, (const void*)contract_kernel<2, 2>,
        (const void*)contract_kernel<2, 2, true>},
       {(const void*)contract_kernel<4, 0>, (const void*)contract_kernel<4, 1>, (const void*)contract_kernel<4, 2>,
        (const void*)contract_kernel<4, 2, true>}};
   const void* kfn = kfns[variant == 4 ? 1 : 0][(pad == 2 && cmul == 3) ? 3 : pad];
-  const size_t kSmemBytes = pad == 1 ? Layout<1>::kSmemBytes : Layout<0>::kSmemBytes;
+  size_t kSmemBytes = pad == 1 ? Layout<1>::kSmemBytes : Layout<0>::kSmemBytes;
+  if (planes) {
+    if (pl_kc == 8 && pl_stages == 4) {
+      kfn = (const void*)contract_kernel<4, 2, true, true, 4, 8>;
+      kSmemBytes = Layout<2, true, 4, 8>::kSmemBytes;
+    } else if (pl_kc == 8) {
+      kfn = (const void*)contract_kernel<4, 2, true, true, 3, 8>;
+      kSmemBytes = Layout<2, true, 3, 8>::kSmemBytes;
+    } else if (pl_stages == 3) {
+      kfn = (const void*)contract_kernel<4, 2, true, true, 3>;
+      kSmemBytes = Layout<2, true, 3>::kSmemBytes;
+    } else {
+      kfn = (const void*)contract_kernel<4, 2, true, true, 2>;
+      kSmemBytes = Layout<2, true, 2>::kSmemBytes;
+    }
+  }
   if (first_on_device(kfn))
     HS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
   const int kThreads = variant == 4 ? 128 : 256;

@@ -164,6 +164,15 @@ class DeviceSpec:
                 np.asarray(spec.positions, dtype=np.float64),
                 np.asarray(spec.rotations, dtype=np.float64).reshape(-1, 9),
                 np.asarray(spec.mt_radius, dtype=np.float64), radial]
+        # Atom types of the template path (hsdla_build_args.atom_type): atoms with identical
+        # rotation, muffin-tin radius, l_sph and radial data (exact equality) share one type;
+        # _Call refines them by T set.
+        keys, types = {}, []
+        for a in range(self.n_atoms):
+            key = (host[2][a].tobytes(), host[3][a].tobytes(), int(self.l_sph[a]),
+                   radial[a].tobytes())
+            types.append(keys.setdefault(key, len(keys)))
+        self.atom_type = np.asarray(types, dtype=np.int32)
         self.h2d_bytes = int(sum(h.nbytes for h in host))
         dev, self._staging = _to_device(host)
         self.kv, self.pos, self.rot, self.rmt, self.radial = dev
@@ -205,7 +214,8 @@ class _Call:
     def __init__(self, *, n_basis, heights, row_offset, tpack: TPack, A, B, Bs, udot, ld,
                  force_general_path, H, S, ldh, shard_rank, n_shards, workspace, host_out,
                  ab_args=None, shard_mirror=False, reuse_t=False, stream_h_copy=0,
-                 h_reference_form=False, host_src=None, n_capacity=None, udot_rows=None):
+                 h_reference_form=False, host_src=None, n_capacity=None, udot_rows=None,
+                 atom_type=None):
         lib = _native.load()
         t = device.torch()
         self.na = len(heights)
@@ -226,6 +236,14 @@ class _Call:
         a.n_tsets = tpack.n_tsets
         a.t_dim = td.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
         a.t_dense = self.keep[-1].ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+        if atom_type is not None:
+            pairs, typed = {}, []
+            for ty, ts in zip(np.asarray(atom_type), np.asarray(tpack.t_index)):
+                typed.append(pairs.setdefault((int(ty), int(ts)), len(pairs)))
+            at = np.asarray(typed, dtype=np.int32)
+            self.keep.append(at)
+            a.atom_type = at.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+            a.n_types = len(pairs)
         if udot_rows is not None and n_shards <= 1:
             u2 = tset_udot2(tpack, heights, row_offset, udot_rows)
             self.keep.append(u2)
@@ -410,7 +428,7 @@ class HSPipeline:
                      workspace=self.workspace, host_out=host_out, ab_args=ab,
                      shard_mirror=self.shard_mirror, reuse_t=reuse, stream_h_copy=stream_h_copy,
                      h_reference_form=self.h_reference_form, n_capacity=self.n_capacity,
-                     udot_rows=dspec.udot_rows)
+                     udot_rows=dspec.udot_rows, atom_type=dspec.atom_type)
         call.keep.append(dspec)
         self.workspace = call.workspace
         self._last_t = (tpack, bool(force_general_path))

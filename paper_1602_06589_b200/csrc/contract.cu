@@ -137,8 +137,11 @@ __device__ __forceinline__ Seg load_seg(const Seg* s) {
 // PL (G3 only, pair layout): the sums P_re - P_im and Q_re + Q_im come precomputed from global
 // memory (Seg::Pd / Seg::Qs, written by their producers) and are staged with the operands, so
 // the K loop issues no DADD on the FP64 pipe; ST = ring stages (2 keeps two CTAs per SM).
-template <int JB, int PAD, bool G3 = false, bool PL = false, int ST = kStages, int KC = kChunk>
-__global__ void __launch_bounds__(32 * 2 * (8 / JB), (G3 && JB == 2) ? 1 : 2)
+// MINB = CTAs per SM the register allocation must allow (JB = 2 with G3: 1 = 255 registers,
+// 2 = 128 registers for two 8-warp CTAs, 16 warps per SM).
+template <int JB, int PAD, bool G3 = false, bool PL = false, int ST = kStages, int KC = kChunk,
+          int MINB = (G3 && JB == 2) ? 1 : 2>
+__global__ void __launch_bounds__(32 * 2 * (8 / JB), MINB)
     contract_kernel(SKParams sk) {
   static_assert(!PL || (G3 && PAD == 2), "sum planes need the three-product pair layout");
   static_assert(KC == 16 || (KC == 8 && PAD == 2), "8-element chunks: pair layout only");
@@ -612,13 +615,15 @@ int preload_contract() {
                        (const void*)contract_kernel<4, 2, true, true, 2>,
                        (const void*)contract_kernel<4, 2, true, true, 3>,
                        (const void*)contract_kernel<4, 2, true, true, 4, 8>,
-                       (const void*)contract_kernel<4, 2, true, true, 3, 8>};
+                       (const void*)contract_kernel<4, 2, true, true, 3, 8>,
+                       (const void*)contract_kernel<2, 2, true, false, 3, 16, 2>};
   const size_t smem[] = {Layout<0>::kSmemBytes, Layout<1>::kSmemBytes, Layout<2>::kSmemBytes,
                          Layout<0>::kSmemBytes, Layout<1>::kSmemBytes, Layout<2>::kSmemBytes,
                          Layout<2>::kSmemBytes, Layout<2>::kSmemBytes,
                          Layout<2, true, 2>::kSmemBytes, Layout<2, true, 3>::kSmemBytes,
-                         Layout<2, true, 4, 8>::kSmemBytes, Layout<2, true, 3, 8>::kSmemBytes};
-  for (int i = 0; i < 12; ++i) {
+                         Layout<2, true, 4, 8>::kSmemBytes, Layout<2, true, 3, 8>::kSmemBytes,
+                         Layout<2>::kSmemBytes};
+  for (int i = 0; i < 13; ++i) {
     cudaFuncAttributes at;
     HS_CUDA(cudaFuncGetAttributes(&at, fns[i]));
     if (first_on_device(fns[i]))
@@ -689,6 +694,13 @@ int launch_contract(hsdla_ctx* ctx, const std::vector<Prob>& probs_in,
       {(const void*)contract_kernel<4, 0>, (const void*)contract_kernel<4, 1>, (const void*)contract_kernel<4, 2>,
        (const void*)contract_kernel<4, 2, true>}};
   const void* kfn = kfns[variant == 4 ? 1 : 0][(pad == 2 && cmul == 3) ? 3 : pad];
+  static int minb2 = -1;  // HSDLA_G3_MINB=2 with HSDLA_WARP_COLS=16: two 8-warp CTAs per SM
+  if (minb2 < 0) {
+    const char* e = getenv("HSDLA_G3_MINB");
+    minb2 = (e && e[0] == '2') ? 1 : 0;
+  }
+  if (minb2 && variant == 2 && pad == 2 && cmul == 3)
+    kfn = (const void*)contract_kernel<2, 2, true, false, 3, 16, 2>;
   size_t kSmemBytes = pad == 1 ? Layout<1>::kSmemBytes : Layout<0>::kSmemBytes;
   if (planes) {
     if (pl_kc == 8 && pl_stages == 4) {

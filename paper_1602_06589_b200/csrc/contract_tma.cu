@@ -56,6 +56,8 @@ using Cfg64P = Cfg<2, 2, 4, true>;
 using Cfg96P = Cfg<3, 2, 2, true>;
 using Cfg64G = Cfg<2, 2, 4, true, true>;
 using Cfg96G = Cfg<3, 2, 2, true, true>;
+// 64x64 with eight 32x16 warps (three-product): 128 registers, two CTAs / 16 warps per SM.
+using Cfg64G8 = Cfg<2, 4, 2, true, true>;
 __device__ __forceinline__ int pair_perm(int g) { return (g >> 1) | ((g & 1) << 2); }
 
 struct TSeg {
@@ -687,6 +689,7 @@ int preload_contract_tma() {
   if (int rc = preload_cfg<Cfg64P>()) return rc;
   if (int rc = preload_cfg<Cfg96P>()) return rc;
   if (int rc = preload_cfg<Cfg64G>()) return rc;
+  if (int rc = preload_cfg<Cfg64G8>()) return rc;
   return preload_cfg<Cfg96G>();
 }
 
@@ -720,6 +723,12 @@ int launch_contract_tma(hsdla_ctx* ctx, const std::vector<Prob>& probs, long lon
     return g3     ? launch_cfg<Cfg96G>(ctx, probs, segs, flag_dev)
            : pair ? launch_cfg<Cfg96P>(ctx, probs, segs, flag_dev)
                   : launch_cfg<Cfg96>(ctx, probs, segs, flag_dev);
+  static int w8 = -1;  // HSDLA_TMA_W8=1: eight 32x16 warps per 64x64 tile
+  if (w8 < 0) {
+    const char* e = getenv("HSDLA_TMA_W8");
+    w8 = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (g3 && w8) return launch_cfg<Cfg64G8>(ctx, probs, segs, flag_dev);
   return g3     ? launch_cfg<Cfg64G>(ctx, probs, segs, flag_dev)
          : pair ? launch_cfg<Cfg64P>(ctx, probs, segs, flag_dev)
                 : launch_cfg<Cfg64>(ctx, probs, segs, flag_dev);

@@ -298,6 +298,8 @@ typedef struct {
   int32_t* joint_info;        /* HOST out n_tsets or NULL: 1 = H used the joint T factor for this set,
                                  2 = with the dense / diagonal-tail split */
   double joint_shift;         /* out: the common shift sigma of the joint form (0 = none) */
+  int32_t template_types;     /* out: atom types of the template path (hsdla_build_args.atom_type),
+                                 0 = per-atom generation / T applications */
 } hsdla_build_result;
 
 size_t hsdla_build_workspace_size(const hsdla_build_args* args);

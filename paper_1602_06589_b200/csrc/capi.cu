@@ -642,6 +642,7 @@ int complete_slot(hsdla_ctx* ctx, hsdla_ctx::BuildSlot& sl, hsdla_ctx::Outcome* 
   o->nonfinite = area[0];
   o->joint = sl.joint;
   o->sigma = sl.sigma;
+  o->types = sl.types;
   cudaEvent_t* ev = sl.ev;
   float t01 = 0, t12 = 0, t23 = 0, t34 = 0, t46 = 0, t07 = 0;
   cudaEventElapsedTime(&t01, ev[0], ev[1]);
@@ -1048,6 +1049,7 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     ctx->joint_pending = false;
   }
   sl.sigma = key.joint ? ctx->joint_sigma : 0.0;
+  sl.types = tpl ? (int)ti.rep.size() : 0;
   sl.joint.assign(a->n_tsets, 0);
   bool any_joint = false, all_joint = true;
   for (int t = 0; t < a->n_tsets; ++t) {
@@ -1255,6 +1257,7 @@ int fill_result(const hsdla_ctx::Outcome& o, hsdla_build_result* res) {
   for (size_t t = 0; t < o.joint.size(); ++t)
     if (res->joint_info) res->joint_info[t] = o.joint[t];
   res->joint_shift = o.sigma;
+  res->template_types = o.types;
   for (size_t i = 0; i < o.hpd.size(); ++i)
     if (res->hpd_mask) res->hpd_mask[i] = o.hpd[i];
   res->nonfinite = o.nonfinite;

@@ -307,6 +307,7 @@ class _Call:
             "joint_t": [bool(self.joint[i]) for i in range(self.n_tsets)],
             "joint_split": [self.joint[i] == 2 for i in range(self.n_tsets)],
             "joint_shift": float(r.joint_shift),
+            "template_types": int(r.template_types),
             "ms": {"setup": r.ms_setup, "S": r.ms_S, "H_ABBA_BB": r.ms_H_ABBA_BB,
                    "H_AA": r.ms_H_AA},
             "kernel_ms": {"contract_S": r.ms_contract_S, "contract_H": r.ms_contract_H,

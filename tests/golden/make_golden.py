@@ -117,9 +117,9 @@ def ab_small():
     np.savez_compressed(os.path.join(HERE, "ab_small.npz"), **out)
 
 
-def ab_high():
-    """compute_AB at the largest supported l (HSDLA_MAX_LSPH = 14) with |K| r_MT up to ~21,
-    so all three Bessel regimes (series, Miller, upward) occur at l = 12..14."""
+def high_spec():
+    """Spec at the largest supported l (HSDLA_MAX_LSPH = 14) with |K| r_MT up to ~21, so all
+    three Bessel regimes (series, Miller, upward) occur at l = 12..14."""
     rng = np.random.default_rng(9)
     l_sph = np.array([12, 14, 13])
     n_atoms = len(l_sph)
@@ -139,6 +139,12 @@ def ab_high():
     spec = hsdla.SystemSpec(positions=pos, rotations=rots, mt_radius=np.array([2.5, 2.2, 1.8]),
                             l_sph=l_sph, l_nonsph=l_sph, k_point=np.zeros(3), k_vectors=kv,
                             omega=216.0, radial=radial)
+    return spec
+
+
+def ab_high():
+    """compute_AB on high_spec()."""
+    spec = high_spec()
     c = hsdla.compute_AB(spec)
     out = spec_arrays(spec)
     out.update(A=c.A_star.array, B=c.B_star.array, udot_norms=c.udot_norms)
@@ -231,9 +237,22 @@ def build_small():
     np.savez_compressed(os.path.join(HERE, "build_small.npz"), **out)
 
 
+def match():
+    """match_factors (flapw.py:179-198): f_A and f_B of every atom of the small spec (all l up to
+    10) and of ab_high's spec (l 12..14, every Bessel regime), from the reference itself."""
+    out = {}
+    for tag, spec in (("small", small_spec()), ("high", high_spec())):
+        out.update({f"{tag}_{k}": v for k, v in spec_arrays(spec).items()})
+        for a in range(spec.n_atoms):
+            fa, fb = hsdla.flapw.match_factors(spec, a)
+            out[f"{tag}_fa_{a}"] = fa
+            out[f"{tag}_fb_{a}"] = fb
+    np.savez_compressed(os.path.join(HERE, "match.npz"), **out)
+
+
 if __name__ == "__main__":
     steps = {"special": special, "ab_small": ab_small, "ab_high": ab_high,
-             "build_small": build_small, "c1": c1, "reduced": reduced}
+             "build_small": build_small, "c1": c1, "reduced": reduced, "match": match}
     for name in (sys.argv[1:] or list(steps)):  # e.g. `make_golden.py ab_high`
         steps[name]()
     for f in sorted(os.listdir(HERE)):

@@ -403,3 +403,71 @@ def test_tpack_content_cache(pkg):
     inst2.tmats.t_ab[0].array[0, 0] += 1e-9
     p3 = pack_tmats(inst2.tmats)
     assert p3 is not p1
+
+
+# -- adversarial inputs for the three-product complex multiply ---------------------------
+
+@pytest.mark.parametrize("case", ["row_scale_1e4", "near_real", "near_imag", "mixed"])
+def test_three_product_herk_adversarial_scaling(pkg, case):
+    """The three-product (Gauss) multiply's error is normwise, |E| <= c u (|P_re| + |P_im|)^T
+    (|Q_re| + |Q_im|): rows spanning 1e-4 .. 1e4, |Im| << |Re| (and the converse) stay within the
+    north_star's 1e-12 relative Frobenius of H / S-shaped products (numpy's four-product ZGEMM as
+    the reference).  The imaginary part of near-real data is where three products lose relative
+    accuracy (cancellation in accI - accR + accX): that part is bounded here by 1e-12 of the
+    whole matrix, not of itself."""
+    rng = np.random.default_rng(31)
+    m, n = 700, 300
+    a = rand_complex(rng, m, n)
+    if case in ("row_scale_1e4", "mixed"):
+        a *= (10.0 ** rng.uniform(-4, 4, m))[:, None]
+    if case in ("near_real", "mixed"):
+        a = a.real + 1e-8j * a.imag
+    if case == "near_imag":
+        a = 1e-8 * a.real + 1j * a.imag
+    c = pkg.HermitianAccumulator(n)
+    pkg.get_backend().hermitian_rank_k_update(c, pkg.ComplexDense.from_array(a), pkg.FlopLedger())
+    got = hermitian_from_lower(c.matrix.array)
+    ref = a.conj().T @ a
+    assert rel_fro(got, ref) <= 1e-12, rel_fro(got, ref)
+    assert rel_fro(got.real, ref.real) <= 1e-12
+
+
+def test_small_wronskian_blocks_build_vs_oracle(pkg):
+    """compute_AB + build_all with l-blocks amplified by tiny Wronskians (|W| 1e-6 .. 1e-3, the
+    BASELINE small-W hazard of SURVEY 8d pushed further): per-(atom, l) A*/B* blocks and the
+    whole H, S against the oracle."""
+    from paper_1602_06589_b200 import configs
+
+    inst = configs.make_instance("C1")
+    spec = inst.spec
+    radial = []
+    for a, rad in enumerate(spec.radial):
+        u, up = np.array(rad.u), np.array(rad.u_prime)
+        ud, udp = np.array(rad.udot), np.array(rad.udot_prime)
+        # W_l = udot u' - u udot' forced to 1e-6 .. 1e-3 on l = 1, 4 (the reference's guard is 1e-8)
+        for l, w in ((1, 1e-6 * (a + 1)), (4, -1e-3)):
+            udp[l] = (ud[l] * up[l] - w) / u[l]
+        radial.append(pkg.RadialBoundaryData(u=u, u_prime=up, udot=ud, udot_prime=udp,
+                                             energy=np.zeros(len(u)), udot_norm=np.array(rad.udot_norm)))
+    spec = pkg.SystemSpec(positions=spec.positions, rotations=spec.rotations, mt_radius=spec.mt_radius,
+                          l_sph=spec.l_sph, l_nonsph=spec.l_nonsph, k_point=spec.k_point,
+                          k_vectors=spec.k_vectors, omega=spec.omega, radial=radial)
+    from oracle import flapw as of
+
+    a_o, b_o, norms, offs = of.compute_ab(spec)
+    co = pkg.compute_AB(spec)
+    for at in range(spec.n_atoms):
+        for l in range(int(spec.l_sph[at]) + 1):
+            rows = slice(int(offs[at]) + l * l, int(offs[at]) + (l + 1) ** 2)
+            assert rel_fro(co.A_star.array[rows], a_o[rows]) <= 1e-13
+            assert rel_fro(co.B_star.array[rows], b_o[rows]) <= 1e-13
+    tm = inst.tmats
+    h_o, s_o, _, _ = ob.build_all(a_o, b_o, norms, list(np.diff(offs)), [t.array for t in tm.t_aa],
+                                  [t.array for t in tm.t_ab], [t.array for t in tm.t_bb])
+    h, s, _ = pkg.build_all(co, tm, pkg.BuildConfig())
+    assert rel_fro(h.array, h_o) <= 1e-12 and rel_fro(s.array, s_o) <= 1e-12
+    # the same system through the device pipeline (template path)
+    from paper_1602_06589_b200.pipeline import build_hs
+
+    h2, s2, _ = build_hs(spec, tm)
+    assert rel_fro(h2.array, h_o) <= 1e-12 and rel_fro(s2.array, s_o) <= 1e-12

@@ -162,3 +162,75 @@ def test_build_all_host_sourced_upload(pkg, monkeypatch):
     assert r1.hpd_mask == r0.hpd_mask == list(mask)
     # a window that is not at the top of its allocation is not host-sourced
     assert device.pinned_sources(co.A_star.block(1, co.A_star.rows - 1), co.B_star) is None
+
+
+def _spec_variant(pkg, spec, rotations=None, l_sph=None):
+    return pkg.SystemSpec(positions=spec.positions,
+                          rotations=spec.rotations if rotations is None else rotations,
+                          mt_radius=spec.mt_radius, l_sph=spec.l_sph if l_sph is None else l_sph,
+                          l_nonsph=spec.l_nonsph if l_sph is None else l_sph, k_point=spec.k_point,
+                          k_vectors=spec.k_vectors, omega=spec.omega, radial=spec.radial)
+
+
+@pytest.mark.parametrize("variant", ["types", "rotated", "reference_forms", "single_atom_types"])
+def test_template_path_variants_vs_oracle(pkg, variant):
+    """The device pipeline's per-type template path (hsdla_build_args.atom_type) and its
+    fallbacks against the oracle: BASELINE-style shared types; every atom rotated differently
+    (one type per atom); the reference H forms (templates for A / UB, per-atom T applications
+    on B); a one-atom-per-type system."""
+    from paper_1602_06589_b200 import configs
+    from paper_1602_06589_b200.pipeline import DeviceSpec, HSPipeline, pack_tmats
+
+    inst = configs.make_instance("C1")
+    spec, tm = inst.spec, inst.tmats
+    if variant == "rotated":
+        rng = np.random.default_rng(4)
+        rots = np.array([np.linalg.qr(rng.standard_normal((3, 3)))[0] for _ in range(spec.n_atoms)])
+        spec = _spec_variant(pkg, spec, rotations=rots)
+    if variant == "single_atom_types":
+        cd = pkg.ComplexDense.from_array
+        tm = pkg.TMatrixSet([cd(t.array.copy()) for t in tm.t_aa], [cd(t.array.copy()) for t in tm.t_ab],
+                            [cd(t.array.copy()) for t in tm.t_bb], list(tm.l_sph), list(tm.l_nonsph))
+    dspec = DeviceSpec(spec)
+    pipe = HSPipeline(spec.n_basis, dspec.heights, h_reference_form=(variant == "reference_forms"))
+    res = pipe.run(dspec, pack_tmats(tm))
+    want_types = {"types": 2, "rotated": 4, "reference_forms": 2, "single_atom_types": 4}[variant]
+    assert res["template_types"] == want_types
+    assert all(res["joint_t"]) == (variant != "reference_forms")
+    h_t, s_t = pipe.result_views()
+    h, s = h_t.cpu().numpy().T, s_t.cpu().numpy().T
+    a, b, norms, offs = of.compute_ab(spec)
+    h_o, s_o, _, mask = ob.build_all(a, b, norms, list(np.diff(offs)), [t.array for t in tm.t_aa],
+                                     [t.array for t in tm.t_ab], [t.array for t in tm.t_bb])
+    assert res["hpd_mask"] == list(mask)
+    assert rel_fro(h, h_o) <= TOL and rel_fro(s, s_o) <= TOL
+    np.testing.assert_array_equal(h, h.conj().T)
+    # the reused T preparation (second k-point of a batch: B not written on the joint path)
+    res2 = pipe.run(dspec, pack_tmats(tm))
+    h2 = pipe.result_views()[0].cpu().numpy().T
+    np.testing.assert_array_equal(h2, h)
+    assert res2["template_types"] == want_types
+
+
+def test_template_path_off_for_short_t(pkg):
+    """T smaller than its block: the per-atom path (template_types = 0), still exact."""
+    from paper_1602_06589_b200.pipeline import DeviceSpec, HSPipeline, pack_tmats
+    from paper_1602_06589_b200 import configs
+
+    inst = configs.make_instance("C1")
+    spec = inst.spec
+    cd = pkg.ComplexDense.from_array
+    m = 36  # (l = 5)^2 < 49 rows of every block
+    tm = pkg.TMatrixSet([cd(t.array[:m, :m].copy()) for t in inst.tmats.t_aa],
+                        [cd(t.array[:m, :m].copy()) for t in inst.tmats.t_ab],
+                        [cd(t.array[:m, :m].copy()) for t in inst.tmats.t_bb],
+                        list(inst.tmats.l_sph), list(inst.tmats.l_nonsph))
+    dspec = DeviceSpec(spec)
+    pipe = HSPipeline(spec.n_basis, dspec.heights)
+    res = pipe.run(dspec, pack_tmats(tm))
+    assert res["template_types"] == 0
+    h_t, s_t = pipe.result_views()
+    a, b, norms, offs = of.compute_ab(spec)
+    h_o, s_o, _, _ = ob.build_all(a, b, norms, list(np.diff(offs)), [t.array for t in tm.t_aa],
+                                  [t.array for t in tm.t_ab], [t.array for t in tm.t_bb])
+    assert rel_fro(h_t.cpu().numpy().T, h_o) <= TOL and rel_fro(s_t.cpu().numpy().T, s_o) <= TOL

@@ -5,7 +5,9 @@ size-independent checks against the oracle restatement of the reference.
 * A*/B* on a seeded sample of K-vector columns vs the oracle's compute_AB restatement;
 * H V and S V for seeded random V (the device H, S times V with torch — test
   infrastructure only) vs the oracle's matrix-free products A^H (W V) built from the
-  oracle's own A*/B* — a random projection catches any wrong entry with high probability;
+  oracle's own A*/B*;
+* entrywise: one full column of H and S in every 64-column panel (V = unit vectors), per
+  64-row tile, so every lower tile of the output is compared element by element;
 * exact Hermitian symmetry, real diagonal, positive diagonal of S.
 """
 import numpy as np
@@ -56,11 +58,29 @@ def test_fullsize_projections_vs_oracle(cuda, name):
     sv = (s_t.transpose(0, 1) @ vt).cpu().numpy()
     a, b, norms, offs = of.compute_ab(spec)
     heights = list(np.diff(offs))
-    hv_o = ob.h_matvec(a, b, heights, [t.array for t in tm.t_aa], [t.array for t in tm.t_ab],
-                       [t.array for t in tm.t_bb], v)
+    t3 = ([t.array for t in tm.t_aa], [t.array for t in tm.t_ab], [t.array for t in tm.t_bb])
+    hv_o = ob.h_matvec(a, b, heights, *t3, v)
     sv_o = ob.s_matvec(a, b, norms, v)
     assert rel_fro(hv, hv_o) <= TOL
     assert rel_fro(sv, sv_o) <= TOL
+
+    # entrywise: one full column in every 64-column panel (the oracle's H e_j, S e_j), checked
+    # per 64-row tile against the column's largest entry — every lower tile (I, J) of H and S
+    # lies in column panel J, so a wrong tile anywhere cannot hide in a projection norm
+    nb = (n + 63) // 64
+    jc = np.array([min(n - 1, 64 * p + int(rng.integers(0, 64))) for p in range(nb)])
+    e = np.zeros((n, len(jc)), dtype=np.complex128)
+    e[jc, np.arange(len(jc))] = 1.0
+    h_cols_o = ob.h_matvec(a, b, heights, *t3, e)
+    s_cols_o = ob.s_matvec(a, b, norms, e)
+    idx_c = torch.from_numpy(jc).cuda()
+    h_cols = h_t[idx_c].cpu().numpy().T
+    s_cols = s_t[idx_c].cpu().numpy().T
+    for dev, ref in ((h_cols, h_cols_o), (s_cols, s_cols_o)):
+        scale = np.abs(ref).max(axis=0)
+        for r0 in range(0, n, 64):
+            err = np.abs(dev[r0:r0 + 64] - ref[r0:r0 + 64]).max(axis=0)
+            assert np.all(err <= TOL * scale), (r0, float((err / scale).max()))
 
     # exact Hermitian structure on sampled blocks, real diagonal, S diagonal > 0
     idx = torch.from_numpy(np.sort(rng.choice(n, size=256, replace=False))).cuda()

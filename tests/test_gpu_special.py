@@ -49,6 +49,20 @@ def test_match_factors_vs_reference(pkg):
         assert fb.shape == fa.shape
 
 
+@pytest.mark.parametrize("tag", ["small", "high"])
+def test_match_factors_fa_fb_vs_reference(pkg, tag):
+    """f_A and f_B on the device vs the reference's match_factors (match.npz), every atom,
+    l up to 14 and all Bessel regimes, per l row (small Wronskians do not enter here)."""
+    d = golden("match.npz")
+    spec = spec_from_golden(d, prefix=f"{tag}_spec_")
+    for a in range(spec.n_atoms):
+        fa, fb = pkg.match_factors(spec, a)
+        for f, ref in ((fa, d[f"{tag}_fa_{a}"]), (fb, d[f"{tag}_fb_{a}"])):
+            assert f.shape == ref.shape
+            for l in range(ref.shape[0]):
+                assert rel_fro(f[l], ref[l]) <= 1e-13, (a, l)
+
+
 def test_gpu_gaunt_and_assemble_t_vs_reference(cuda):
     """gaunt / gaunt_tensor / assemble_T on the GPU against the reference's
     own outputs (tests/golden/assemble_t.npz), plus assemble_T's validation errors."""

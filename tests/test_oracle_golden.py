@@ -169,3 +169,40 @@ def test_oracle_gaunt_and_assemble_t_vs_reference():
         for got, key in ((taa[a], "t_aa"), (tab[a], "t_ab"), (tbb[a], "t_bb")):
             want = d[f"{key}{a}"]
             assert np.max(np.abs(got - want)) <= 1e-13 * max(1.0, np.max(np.abs(want)))
+
+
+@pytest.mark.parametrize("tag", ["small", "high"])
+def test_match_factors_match_reference(tag):
+    """f_A and f_B of every atom (match.npz: the reference's own match_factors)."""
+    d = golden("match.npz")
+    spec = spec_from_golden(d, prefix=f"{tag}_spec_")
+    for a in range(spec.n_atoms):
+        fa, fb = of.match_factors(spec, a)
+        assert rel_fro(fa, d[f"{tag}_fa_{a}"]) <= 1e-14
+        assert rel_fro(fb, d[f"{tag}_fb_{a}"]) <= 1e-14
+
+
+def test_c2_oracle_matches_reference_golden():
+    """The oracle's full C2 build against H / S columns made by the reference at C2
+    (big_C2.npz, tests/golden/make_golden_big.py)."""
+    import os
+    import sys
+
+    from conftest import GOLDEN
+
+    path = os.path.join(GOLDEN, "big_C2.npz")
+    d = np.load(path)
+    sys.path.insert(0, GOLDEN)
+    from digest import input_digest
+
+    inst = configs.make_instance("C2")
+    assert input_digest(inst) == str(d["digest"])
+    a, b, norms, offs = of.compute_ab(inst.spec)
+    tm = inst.tmats
+    h, s, led, mask = ob.build_all(a, b, norms, list(np.diff(offs)), [t.array for t in tm.t_aa],
+                                   [t.array for t in tm.t_ab], [t.array for t in tm.t_bb])
+    assert sum(led.values()) == int(d["ledger_total"]) and list(mask) == list(d["hpd_mask"])
+    for m, key in ((h, "H"), (s, "S")):
+        assert rel_fro(m[:, d["panel"]], d[f"{key}_panel"]) <= 1e-13
+        assert rel_fro(m[:, d["cols"]], d[f"{key}_cols"]) <= 1e-13
+        assert rel_fro(m @ d["V"], d[f"{key}V"]) <= 1e-13

@@ -132,6 +132,106 @@ class KernelBackend:
         raise NotImplementedError
 
 
+# -- the operators on numpy windows (column-major views with any leading dimension) -----------
+# Shared by B200Kernels (this package's types) and the level-2 binding into the unmodified
+# reference (integration.py), whose KernelBackend hands its private operators raw arrays.
+
+def herk_lower(c: np.ndarray, a: np.ndarray):
+    """lower(c) += a^H a (`kernels.py:242-244` zherk lower, trans=C), in place."""
+    lib = _native.load()
+    cd = device.upload_window(c)
+    ad = device.upload_window(a)
+    _native.check(lib.hsdla_herk_lower(device.ctx(), c.shape[0], a.shape[0], device.ptr(ad),
+                                       ad.shape[1], device.ptr(cd), cd.shape[1]),
+                  "hsdla_herk_lower")
+    device.download_window(cd, c)
+
+
+def her2k_lower(c: np.ndarray, x: np.ndarray, b: np.ndarray):
+    """lower(c) += x^H b + b^H x (`kernels.py:246-248`), in place."""
+    lib = _native.load()
+    cd = device.upload_window(c)
+    xd = device.upload_window(x)
+    bd = device.upload_window(b)
+    _native.check(lib.hsdla_her2k_lower(device.ctx(), c.shape[0], x.shape[0], device.ptr(xd),
+                                        xd.shape[1], device.ptr(bd), bd.shape[1],
+                                        device.ptr(cd), cd.shape[1]),
+                  "hsdla_her2k_lower")
+    device.download_window(cd, c)
+
+
+def gemm(c: np.ndarray, a: np.ndarray, b: np.ndarray, conj_a: bool, alpha: complex, beta: complex):
+    """c = alpha op(a) b + beta c (`kernels.py:250-253`), in place."""
+    lib = _native.load()
+    m, n = c.shape
+    k = b.shape[0]
+    ad = device.upload_window(a)
+    bd = device.upload_window(b)
+    cd = device.upload_window(c) if beta != 0 else device.empty_matrix(m, n)
+    ws = device.empty_matrix(k, m) if not conj_a else None
+    _native.check(lib.hsdla_gemm(device.ctx(), 1 if conj_a else 0, m, n, k,
+                                 _native.c64(alpha), device.ptr(ad), ad.shape[1],
+                                 device.ptr(bd), bd.shape[1], _native.c64(beta),
+                                 device.ptr(cd), cd.shape[1],
+                                 device.ptr(ws) if ws is not None else None),
+                  "hsdla_gemm")
+    device.download_window(cd, c)
+
+
+def hemm_lower(x: np.ndarray, t: np.ndarray, a: np.ndarray, accumulate: bool, alpha: complex):
+    """x = alpha herm(tril t) a (+ x) (`kernels.py:255-258`), in place."""
+    lib = _native.load()
+    m, n = x.shape
+    td = device.upload_window(t)
+    ad = device.upload_window(a)
+    xd = device.upload_window(x) if accumulate else device.empty_matrix(m, n)
+    ws = device.empty_matrix(m, m)
+    _native.check(lib.hsdla_hemm_lower(device.ctx(), m, n, _native.c64(alpha), device.ptr(td),
+                                       td.shape[1], device.ptr(ad), ad.shape[1],
+                                       1 if accumulate else 0, device.ptr(xd), xd.shape[1],
+                                       device.ptr(ws)),
+                  "hsdla_hemm_lower")
+    device.download_window(xd, x)
+
+
+def trmm_lower(y: np.ndarray, c: np.ndarray, a: np.ndarray, conj_c: bool):
+    """y = op(tril c) a (`kernels.py:260-264`), in place."""
+    lib = _native.load()
+    m, n = y.shape
+    cdv = device.upload_window(c)
+    ad = device.upload_window(a)
+    yd = device.empty_matrix(m, n)
+    ws = device.empty_matrix(m, m)
+    _native.check(lib.hsdla_trmm_lower(device.ctx(), 1 if conj_c else 0, m, n, device.ptr(cdv),
+                                       cdv.shape[1], device.ptr(ad), ad.shape[1],
+                                       device.ptr(yd), yd.shape[1], device.ptr(ws)),
+                  "hsdla_trmm_lower")
+    device.download_window(yd, y)
+
+
+def potrf_lower(t: np.ndarray) -> np.ndarray:
+    """Lower Cholesky factor of tril(t) in a new array (`kernels.py:266-272`); t is not
+    touched.  NotHPDError(pivot) / ContractViolationError (NaN) as the reference."""
+    lib = _native.load()
+    n = t.shape[0]
+    if n == 0:
+        return np.zeros((0, 0), dtype=np.complex128, order="F")
+    td = device.upload_window(t)
+    fd = device.empty_matrix(n, n)
+    info = (ctypes.c_int32 * 1)()
+    _native.check(lib.hsdla_potrf_lower_batched(device.ctx(), n, 1, device.ptr(td),
+                                                td.shape[1], 0, device.ptr(fd), fd.shape[1],
+                                                0, info),
+                  "hsdla_potrf_lower_batched")
+    if info[0] == -1:
+        raise ContractViolationError("NaN in Cholesky input (lower triangle)")
+    if info[0] > 0:
+        raise NotHPDError(info[0] - 1)
+    out = np.zeros((n, n), dtype=np.complex128, order="F")
+    device.download_window(fd, out)
+    return np.tril(out)
+
+
 class B200Kernels(KernelBackend):
     """Every operator on the GPU: host windows are staged to HBM, computed by the
     sm_100a DMMA contraction / batched Cholesky, and copied back in place."""
@@ -139,87 +239,22 @@ class B200Kernels(KernelBackend):
     name = "b200"
 
     def _herk(self, c, a):
-        lib = _native.load()
-        cd = device.upload_window(c.array)
-        ad = device.upload_window(a.array)
-        _native.check(lib.hsdla_herk_lower(device.ctx(), c.rows, a.rows, device.ptr(ad),
-                                           ad.shape[1], device.ptr(cd), cd.shape[1]),
-                      "hsdla_herk_lower")
-        device.download_window(cd, c.array)
+        herk_lower(c.array, a.array)
 
     def _her2k(self, c, x, b):
-        lib = _native.load()
-        cd = device.upload_window(c.array)
-        xd = device.upload_window(x.array)
-        bd = device.upload_window(b.array)
-        _native.check(lib.hsdla_her2k_lower(device.ctx(), c.rows, x.rows, device.ptr(xd),
-                                            xd.shape[1], device.ptr(bd), bd.shape[1],
-                                            device.ptr(cd), cd.shape[1]),
-                      "hsdla_her2k_lower")
-        device.download_window(cd, c.array)
+        her2k_lower(c.array, x.array, b.array)
 
     def _gemm(self, c, a, b, conj_a, alpha, beta):
-        lib = _native.load()
-        m, n = c.shape
-        k = b.rows
-        ad = device.upload_window(a.array)
-        bd = device.upload_window(b.array)
-        cd = device.upload_window(c.array) if beta != 0 else device.empty_matrix(m, n)
-        ws = device.empty_matrix(k, m) if not conj_a else None
-        _native.check(lib.hsdla_gemm(device.ctx(), 1 if conj_a else 0, m, n, k,
-                                     _native.c64(alpha), device.ptr(ad), ad.shape[1],
-                                     device.ptr(bd), bd.shape[1], _native.c64(beta),
-                                     device.ptr(cd), cd.shape[1],
-                                     device.ptr(ws) if ws is not None else None),
-                      "hsdla_gemm")
-        device.download_window(cd, c.array)
+        gemm(c.array, a.array, b.array, conj_a, alpha, beta)
 
     def _hemm(self, x, t, a, accumulate, alpha):
-        lib = _native.load()
-        m, n = x.shape
-        td = device.upload_window(t.array)
-        ad = device.upload_window(a.array)
-        xd = device.upload_window(x.array) if accumulate else device.empty_matrix(m, n)
-        ws = device.empty_matrix(m, m)
-        _native.check(lib.hsdla_hemm_lower(device.ctx(), m, n, _native.c64(alpha), device.ptr(td),
-                                           td.shape[1], device.ptr(ad), ad.shape[1],
-                                           1 if accumulate else 0, device.ptr(xd), xd.shape[1],
-                                           device.ptr(ws)),
-                      "hsdla_hemm_lower")
-        device.download_window(xd, x.array)
+        hemm_lower(x.array, t.array, a.array, accumulate, alpha)
 
     def _trmm(self, y, c, a, conj_c):
-        lib = _native.load()
-        m, n = y.shape
-        cdv = device.upload_window(c.array)
-        ad = device.upload_window(a.array)
-        yd = device.empty_matrix(m, n)
-        ws = device.empty_matrix(m, m)
-        _native.check(lib.hsdla_trmm_lower(device.ctx(), 1 if conj_c else 0, m, n, device.ptr(cdv),
-                                           cdv.shape[1], device.ptr(ad), ad.shape[1],
-                                           device.ptr(yd), yd.shape[1], device.ptr(ws)),
-                      "hsdla_trmm_lower")
-        device.download_window(yd, y.array)
+        trmm_lower(y.array, c.array, a.array, conj_c)
 
     def _potrf(self, t):
-        lib = _native.load()
-        n = t.rows
-        if n == 0:
-            return ComplexDense(np.zeros((0, 0), dtype=np.complex128, order="F"))
-        td = device.upload_window(t.array)
-        fd = device.empty_matrix(n, n)
-        info = (ctypes.c_int32 * 1)()
-        _native.check(lib.hsdla_potrf_lower_batched(device.ctx(), n, 1, device.ptr(td),
-                                                    td.shape[1], 0, device.ptr(fd), fd.shape[1],
-                                                    0, info),
-                      "hsdla_potrf_lower_batched")
-        if info[0] == -1:
-            raise ContractViolationError("NaN in Cholesky input (lower triangle)")
-        if info[0] > 0:
-            raise NotHPDError(info[0] - 1)
-        out = np.zeros((n, n), dtype=np.complex128, order="F")
-        device.download_window(fd, out)
-        return ComplexDense(out)
+        return ComplexDense(np.asfortranarray(potrf_lower(t.array)))
 
 
 _ALIASES = {"b200": B200Kernels, "optimized": B200Kernels, "reference": B200Kernels}

@@ -1,8 +1,8 @@
-"""`python -m paper_1602_06589_b200 build BUNDLE [--out DIR] [--no-backup]`.
+"""`python -m paper_1602_06589_b200 build|verify BUNDLE [--out DIR] [--no-backup] [--force]`.
 
-The build command of the reference CLI (`cli.py:310-328`) on the B200 path, with the
-reference's stable exit codes (`cli.py:1-7`, `:505-523`): 0 ok, 1 configuration error,
-2 IO/parse error, 3 contract violation.
+The build and verify commands of the reference CLI (`cli.py:310-328`, `:374-409`) on the B200
+path, with the reference's stable exit codes (`cli.py:37-41`, `:505-523`): 0 ok, 1
+configuration error, 2 IO/parse error, 3 contract violation, 4 verification failed.
 """
 from __future__ import annotations
 
@@ -12,7 +12,7 @@ import sys
 
 from .errors import ConfigurationError, ContractViolationError
 
-EXIT_OK, EXIT_CONFIG, EXIT_IO, EXIT_CONTRACT = 0, 1, 2, 3
+EXIT_OK, EXIT_CONFIG, EXIT_IO, EXIT_CONTRACT, EXIT_VERIFY = 0, 1, 2, 3, 4
 
 
 class _Parser(argparse.ArgumentParser):
@@ -30,10 +30,24 @@ def main(argv=None) -> int:
     b.add_argument("--threads", type=int, default=1)
     b.add_argument("--backend", choices=["reference", "optimized", "b200"], default="optimized")
     b.add_argument("--backup", action=argparse.BooleanOptionalAction, default=True)
+    v = sub.add_parser("verify", help="cross-check the GPU build against an independent "
+                                      "evaluation of the defining sums")
+    v.add_argument("bundle")
+    v.add_argument("--out", default=None)
+    v.add_argument("--seed", type=int, default=0)
+    v.add_argument("--threads", type=int, default=1)
+    v.add_argument("--backend", choices=["reference", "optimized", "b200"], default="optimized")
+    v.add_argument("--backup", action=argparse.BooleanOptionalAction, default=True)
+    v.add_argument("--force", action="store_true", help="verify above the N_G <= 4096 guard")
     try:
         ns = p.parse_args(argv)
         if ns.threads < 1:
             raise ConfigurationError("--threads must be >= 1")
+        if ns.command == "verify":
+            from .verify import cmd_verify
+
+            return cmd_verify(ns.bundle, out=ns.out, force=ns.force, backup=ns.backup,
+                              threads=ns.threads, backend=ns.backend, seed=ns.seed)
         from .bundle import build_bundle
 
         outdir, report = build_bundle(ns.bundle, ns.out, backup=ns.backup, threads=ns.threads,

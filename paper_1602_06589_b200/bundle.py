@@ -119,6 +119,22 @@ def write_bundle(outdir, coeffs: StackedCoefficients, tmats: TMatrixSet, spec=No
     return manifest
 
 
+def _regenerator(spec):
+    """The A*/B* re-creation callback of the backup=False flow (`cli.py:283-292`): refills the
+    caller's stacks from the bundle's system.json by compute_AB; None without a spec."""
+    if spec is None:
+        return None
+
+    def regen(coeffs):
+        from .flapw import compute_AB
+
+        fresh = compute_AB(spec)
+        coeffs.A_star.array[:] = fresh.A_star.array
+        coeffs.B_star.array[:] = fresh.B_star.array
+
+    return regen
+
+
 def _run_dir(out, seed: int) -> Path:
     if out:
         path = Path(out)

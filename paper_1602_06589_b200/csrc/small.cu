@@ -152,6 +152,7 @@ __device__ void chol_packed(int n, const double2* __restrict__ T, long long ldt,
 }
 
 constexpr int kPackedMaxN = 168;  // 168*169/2*16 B = 227 KB
+constexpr int kPotrfMaxDynSmem = 227 * 1024;  // opt-in limit per CTA (static smem comes off it)
 
 // Per T set: forms[0] = T_AB, forms[1] = 1/2 full(T_BB), forms[2] = full(T_AA),
 // forms[3] = Cholesky factor of tril(T_AA) (if do_chol), all m x m with ld mp.
@@ -425,6 +426,10 @@ int launch_potrf_batched(hsdla_ctx* ctx, int n, int batch, const double2* T, lon
                          long long stride_t, double2* F, long long ldf, long long stride_f,
                          int* info_dev) {
   if (batch <= 0 || n <= 0) return HSDLA_OK;
+  if (size_t(n) * sizeof(double2) > size_t(kPotrfMaxDynSmem) - 1024) {
+    set_error("Cholesky order above 14400 (one shared-memory row per CTA)");
+    return HSDLA_ERR_UNSUPPORTED;
+  }
   potrf_batched_kernel<<<batch, 128, n * sizeof(double2), ctx->stream>>>(n, T, ldt, stride_t, F,
                                                                           ldf, stride_f, info_dev);
   HS_CHECK_LAUNCH();
@@ -561,6 +566,12 @@ int preload_small() {
   for (const void* f : fns) {
     cudaFuncAttributes at;
     HS_CUDA(cudaFuncGetAttributes(&at, f));
+  }
+  if (first_on_device((const void*)potrf_batched_kernel)) {  // one row of n complex per CTA
+    cudaFuncAttributes at;
+    HS_CUDA(cudaFuncGetAttributes(&at, (const void*)potrf_batched_kernel));
+    HS_CUDA(cudaFuncSetAttribute(potrf_batched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kPotrfMaxDynSmem - (int)at.sharedSizeBytes));
   }
   if (first_on_device((const void*)tjoint_kernel))
     HS_CUDA(cudaFuncSetAttribute(tjoint_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -1,0 +1,162 @@
+"""`verify` of the reference CLI (`cli.py:331-409`) on the B200 path.
+
+Cross-checks the composed build (`build_all`: joint T factor, three-product triangular DMMA
+contractions with the fused mirror) against an independent evaluation of the defining sums
+(reference `oracle.py:75-124`, `naive_H` / `naive_S`):
+
+    S = A^H A + (U B)^H (U B)
+    H = sum_a A_a^H (T_AA A_a + T_AB B_a) + B_a^H (T_AB^H A_a + T_BB B_a)
+
+with every T block used exactly as stored (both triangles, T_BA = T_AB^H, as the naive oracle
+does), evaluated as full general products on the GPU (`hsdla_gemm`: no triangle, no mirror, no
+Cholesky or joint factor).  Metrics and verdict follow the reference: relative Frobenius
+errors of H and S, the Hermitian residuals of the independent H and S (a de-Hermitised T_BB —
+SPEC.md:491's injected fault — shows up there, since the build reads lower triangles only),
+and the Cholesky of S when 2R >= N_G (skipped with a warning otherwise, or for S = 0).  Any
+metric above 1e-11 (`cli.py:43`) fails the verification: exit 4.  N_G > 4096 needs --force
+(`cli.py:44`, `:377-381`).
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+
+import numpy as np
+
+from . import _native, device
+from .builder import BuildConfig, build_all
+from .errors import ConfigurationError, NotHPDError
+from .kernels import get_backend
+
+VERIFY_TOLERANCE = 1e-11
+ORACLE_SIZE_GUARD = 4096
+
+
+def _gemm(conj_a, m, n, k, a, lda, b, ldb, beta, c, ldc, a_off=0, b_off=0):
+    """C (+)= op(A) B on device column-major tensors (element offsets into A / B)."""
+    lib = _native.load()
+    ws = device.empty_matrix(k, m) if not conj_a else None
+    pa = ctypes.c_void_p(a.data_ptr() + 16 * a_off)
+    pb = ctypes.c_void_p(b.data_ptr() + 16 * b_off)
+    _native.check(lib.hsdla_gemm(device.ctx(), 1 if conj_a else 0, m, n, k, _native.c64(1.0),
+                                 pa, lda, pb, ldb, _native.c64(beta), device.ptr(c), ldc,
+                                 device.ptr(ws) if ws is not None else None), "hsdla_gemm")
+
+
+def independent_hs(coeffs, tmats):
+    """(H, S) of the defining sums as full general products on the GPU, host numpy arrays."""
+    layout = coeffs.layout
+    r, n = layout.total_rows, coeffs.n_basis
+    u = np.asarray(coeffs.udot_norms, dtype=np.float64)
+    a_d = device.upload_window(coeffs.A_star.array, max(r, 1))
+    b_d = device.upload_window(coeffs.B_star.array, max(r, 1))
+    ub_d = device.upload_window(u[:, None] * coeffs.B_star.array, max(r, 1))
+    x_d = device.empty_matrix(r, n, max(r, 1), zero=True)  # T_AA A_a + T_AB B_a per atom
+    y_d = device.empty_matrix(r, n, max(r, 1), zero=True)  # T_AB^H A_a + T_BB B_a
+    offs = layout.offsets
+    ld = max(r, 1)
+    for at in range(layout.atom_count):
+        m = tmats.t_aa[at].rows
+        if m == 0 or n == 0:
+            continue
+        off = int(offs[at])
+        taa, tab, tbb = (device.upload_window(t.array) for t in
+                         (tmats.t_aa[at], tmats.t_ab[at], tmats.t_bb[at]))
+        xa = device.empty_matrix(m, n, m)
+        ya = device.empty_matrix(m, n, m)
+        _gemm(False, m, n, m, taa, m, a_d, ld, 0.0, xa, m, b_off=off)
+        _gemm(False, m, n, m, tab, m, b_d, ld, 1.0, xa, m, b_off=off)
+        _gemm(True, m, n, m, tab, m, a_d, ld, 0.0, ya, m, b_off=off)
+        _gemm(False, m, n, m, tbb, m, b_d, ld, 1.0, ya, m, b_off=off)
+        x_d[:n, off:off + m] = xa[:n, :m]
+        y_d[:n, off:off + m] = ya[:n, :m]
+    h_d = device.empty_matrix(n, n, max(n, 1), zero=True)
+    s_d = device.empty_matrix(n, n, max(n, 1), zero=True)
+    if r and n:
+        _gemm(True, n, n, r, a_d, ld, x_d, ld, 0.0, h_d, n)
+        _gemm(True, n, n, r, b_d, ld, y_d, ld, 1.0, h_d, n)
+        _gemm(True, n, n, r, a_d, ld, a_d, ld, 0.0, s_d, n)
+        _gemm(True, n, n, r, ub_d, ld, ub_d, ld, 1.0, s_d, n)
+    h = np.zeros((n, n), dtype=np.complex128, order="F")
+    s = np.zeros((n, n), dtype=np.complex128, order="F")
+    device.download_window(h_d, h)
+    device.download_window(s_d, s)
+    return h, s
+
+
+def _rel(x, y) -> float:
+    return float(np.linalg.norm(x - y) / max(np.linalg.norm(y), np.finfo(float).tiny))
+
+
+def verify_metrics(spec, coeffs, tmats, *, backup=True, threads=1, backend="optimized") -> dict:
+    """The reference's `_verify_metrics` (`cli.py:331-371`) with the B200 build and the
+    independent GPU evaluation."""
+    from .bundle import _regenerator
+
+    config = BuildConfig(backup=backup, thread_count=threads, backend=backend)
+    regen = _regenerator(spec)
+    if not backup and regen is None:
+        raise ConfigurationError(
+            "backup=false needs a bundle with system.json to re-create coefficients")
+    h_ref, s_ref = independent_hs(coeffs, tmats)
+    h_fast, s_fast, report = build_all(coeffs.copy(), tmats, config, regenerate=regen)
+    metrics = {
+        "rel_err_H": _rel(h_fast.array, h_ref),
+        "rel_err_S": _rel(s_fast.array, s_ref),
+        "herm_residual_H_oracle": _rel(h_ref, h_ref.conj().T),
+        "herm_residual_S_oracle": _rel(s_ref, s_ref.conj().T),
+    }
+    # the muffin-tin overlap has rank <= 2R: larger bases cannot be positive definite
+    if np.linalg.norm(s_fast.array) == 0.0:
+        metrics["s_hpd"] = "skipped-zero"
+    elif 2 * coeffs.layout.total_rows < coeffs.n_basis:
+        metrics["s_hpd"] = "skipped-rank-deficient"
+    else:
+        try:
+            get_backend(backend, threads).cholesky_factor(s_fast, ledger=report.ledger)
+            metrics["s_hpd"] = "pass"
+        except NotHPDError as e:
+            metrics["s_hpd"] = f"fail-pivot-{e.pivot}"
+    metrics["report"] = report.to_json_dict()
+    return metrics
+
+
+def cmd_verify(bundle, *, out=None, force=False, backup=True, threads=1, backend="optimized",
+               seed=0, echo=print) -> int:
+    """`hsdla verify BUNDLE` (`cli.py:374-409`): prints the metrics, writes verify.json when
+    `out` is given, returns 0 or 4."""
+    from pathlib import Path
+
+    from .bundle import _run_dir, load_bundle
+
+    spec, coeffs, tmats = load_bundle(Path(bundle))
+    if coeffs.n_basis > ORACLE_SIZE_GUARD and not force:
+        raise ConfigurationError(
+            f"N_G = {coeffs.n_basis} exceeds the oracle guard ({ORACLE_SIZE_GUARD}); "
+            "pass --force to verify anyway")
+    metrics = verify_metrics(spec, coeffs, tmats, backup=backup, threads=threads, backend=backend)
+    failures = []
+    for key in ("rel_err_H", "rel_err_S", "herm_residual_H_oracle", "herm_residual_S_oracle"):
+        value = metrics[key]
+        ok = value <= VERIFY_TOLERANCE
+        echo(f"{key:26s} {value:.3e}  [{'ok' if ok else 'FAIL'}]")
+        if not ok:
+            failures.append(key)
+    hpd = metrics["s_hpd"]
+    if hpd == "pass":
+        echo(f"{'S_cholesky':26s} pass       [ok]")
+    elif hpd.startswith("skipped"):
+        reason = ("S = 0 is not positive definite" if hpd == "skipped-zero"
+                  else "2*sum(N_La) < N_G makes S structurally singular")
+        echo(f"{'S_cholesky':26s} skipped    [warning: {reason}]")
+    else:
+        echo(f"{'S_cholesky':26s} {hpd}  [FAIL]")
+        failures.append("s_hpd")
+    if out:
+        outdir = _run_dir(out, seed)
+        (outdir / "verify.json").write_text(json.dumps(metrics, sort_keys=True, indent=1))
+    if failures:
+        echo(f"verification FAILED: {', '.join(failures)}")
+        return 4
+    echo("verification passed")
+    return 0

@@ -9,8 +9,14 @@ Writes under tests/golden/bundles/:
 * rand/      `hsdla gen --seed 12 --atoms 2 --lsph 2 --lnonsph 1 --basis-factor 40
                --coeffs random` (no system.json)
 * rand_out/  `hsdla build rand`
-These pin `paper_1602_06589_b200.bundle.build_bundle` and the HSM1 reader/writer
-(tests/test_bundle.py).
+* small/      `hsdla gen --seed 13 --atoms 2 --lsph 2 --lnonsph 1 --basis-factor 6
+               --coeffs random` (2R >= N_G: verify runs the S Cholesky check)
+* phys_verify/, rand_verify/, small_verify/  `hsdla verify` of each (verify.json; exit 0)
+* phys_fault/ phys with T_BB of atom 0 de-Hermitised (SPEC.md:491's injected fault; the
+               manifest hash updated), phys_fault_verify/ its `hsdla verify` (exit 4, the
+               oracle's Hermitian residual of H flagged) and exit_code.txt
+These pin `paper_1602_06589_b200.bundle.build_bundle`, the `verify` command and the HSM1
+reader/writer (tests/test_bundle.py, tests/test_gpu_verify.py).
 """
 from __future__ import annotations
 
@@ -40,3 +46,27 @@ if __name__ == "__main__":
          "--basis-factor", "40", "--coeffs", "random", "--out", p("rand")])
     run(["build", p("phys"), "--out", p("phys_out")])
     run(["build", p("rand"), "--out", p("rand_out")])
+    run(["gen", "--seed", "13", "--atoms", "2", "--lsph", "2", "--lnonsph", "1",
+         "--basis-factor", "6", "--coeffs", "random", "--out", p("small")])
+    run(["verify", p("small"), "--out", p("small_verify")])
+    run(["verify", p("phys"), "--out", p("phys_verify")])
+    run(["verify", p("rand"), "--out", p("rand_verify")])
+    # injected fault: T_BB of atom 0 de-Hermitised (upper triangle perturbed, lower kept)
+    import hashlib
+    import json
+
+    import numpy as np
+    from hsdla.matrix import ComplexDense, read_hsm1, write_hsm1
+
+    shutil.copytree(p("phys"), p("phys_fault"))
+    tbb = read_hsm1(os.path.join(p("phys_fault"), "T_BB_000.hsm1")).array.copy()
+    iu = np.triu_indices(tbb.shape[0], 1)
+    tbb[iu] += 0.25 + 0.5j
+    write_hsm1(os.path.join(p("phys_fault"), "T_BB_000.hsm1"), ComplexDense.from_array(tbb))
+    man = json.loads(open(os.path.join(p("phys_fault"), "manifest.json")).read())
+    with open(os.path.join(p("phys_fault"), "T_BB_000.hsm1"), "rb") as fh:
+        man["files"]["T_BB_000.hsm1"] = "sha256:" + hashlib.sha256(fh.read()).hexdigest()
+    open(os.path.join(p("phys_fault"), "manifest.json"), "w").write(json.dumps(man, sort_keys=True, indent=1))
+    rc = main(["verify", p("phys_fault"), "--out", p("phys_fault_verify")])
+    open(os.path.join(p("phys_fault_verify"), "exit_code.txt"), "w").write(f"{rc}\n")
+    assert rc == 4, rc

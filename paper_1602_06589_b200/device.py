@@ -95,12 +95,14 @@ def upload_stack(window, ld_min: int | None = None):
     """Device (cols, ld) copy of a stacked-coefficient window.  A window at the top of an
     F-ordered allocation (the layout `compute_AB` returns) goes up as one contiguous copy of
     the whole allocation (ld = its capacity height; pinned memory makes it a DMA at full
-    PCIe speed); anything else is packed first (ld = `ld_min` or the window height)."""
+    PCIe speed) when that height keeps 16-element (256-byte) K-chunk alignment and is at least
+    `ld_min`; anything else is packed first (ld = `ld_min` or the window height)."""
     t = require_cuda()
     base = window.base
     rows, cols = window.shape
     if (window.row_offset == 0 and base.flags.f_contiguous and base.shape[1] == cols
-            and base.shape[0] >= max(rows, 1) and (ld_min is None or base.shape[0] >= rows)):
+            and base.shape[0] >= max(rows, 1)
+            and (ld_min is None or (base.shape[0] >= ld_min and base.shape[0] % 16 == 0))):
         dev = t.from_numpy(base.T).to("cuda", non_blocking=True)
         return dev, int(base.shape[0])
     ld = ld_min or max(rows, 1)

@@ -15,7 +15,7 @@ import numpy as np
 
 from .builder import StackedCoefficients
 from .errors import ConfigurationError, ContractViolationError
-from .matrix import AtomBlockLayout, ComplexDense
+from .matrix import AtomBlockLayout, ComplexDense, DeviceComplexDense
 
 _MIN_WRONSKIAN = 1e-8
 
@@ -142,29 +142,27 @@ class SystemSpec:
 
 
 def compute_AB(spec: SystemSpec) -> StackedCoefficients:
-    """Matching coefficients A*, B* and row norms, generated on the GPU (`flapw.py:201-233`)."""
+    """Matching coefficients A*, B* and row norms, generated on the GPU (`flapw.py:201-233`).
+
+    The stacks stay in HBM (`DeviceComplexDense`): `build_all` uses them in place, and the
+    first host access downloads them into pinned memory with the reference's capacity-height
+    layout (`flapw.py:209-212`), one contiguous DMA per stack."""
     from . import device
-    from .pipeline import DeviceSpec, ab_generate_device, padded_ld
+    from .pipeline import DeviceSpec, ab_generate_device
 
     t = device.require_cuda()
     layout = spec.layout()
     dspec = DeviceSpec(spec)
     n = spec.n_basis
-    # Generated with the host allocation's leading dimension (capacity rows, flapw.py:209-212),
-    # so each stack comes back as one contiguous DMA into pinned memory.
+    # Generated with the host allocation's leading dimension (capacity rows, flapw.py:209-212).
     cap = layout.capacity_rows
     a_dev = device.empty_matrix(cap, n, cap, zero=True)
     b_dev = device.empty_matrix(cap, n, cap, zero=True)
     udot = t.zeros(cap, dtype=t.float64, device="cuda")
     ab_generate_device(dspec, a_dev, b_dev, None, cap, udot)
-    a_base, a_buf = device.pinned_stack(layout.total_rows, n, cap)
-    b_base, b_buf = device.pinned_stack(layout.total_rows, n, cap)
-    if n and cap:
-        a_buf.copy_(a_dev)
-        b_buf.copy_(b_dev)
     norms = udot[: layout.total_rows].cpu().numpy().copy()
-    return StackedCoefficients(ComplexDense(a_base, 0, layout.total_rows),
-                               ComplexDense(b_base, 0, layout.total_rows), layout, norms)
+    return StackedCoefficients(DeviceComplexDense(a_dev, cap, n, layout.total_rows),
+                               DeviceComplexDense(b_dev, cap, n, layout.total_rows), layout, norms)
 
 
 def match_factors(spec: SystemSpec, atom: int):

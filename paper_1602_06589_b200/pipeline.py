@@ -342,13 +342,14 @@ class _Call:
 def build_device(*, n_basis, heights, row_offset, tpack: TPack, A, B, Bs, udot, ld,
                  force_general_path, H, S, ldh, shard_rank=0, n_shards=1, workspace=None,
                  ab_args=None, host_out=None, h_reference_form=False, host_src=None,
-                 udot_rows=None):
+                 udot_rows=None, reuse_t=False):
     """Synchronous `hsdla_build_hs` (or `hsdla_setup_hs` when `ab_args` is given: A/B
-    generation fused in front); returns (result dict, workspace tensor)."""
+    generation fused in front); returns (result dict, workspace tensor).  `reuse_t`: the T
+    pack is the one the previous build on this `workspace` used (its T preparation is kept)."""
     call = _Call(n_basis=n_basis, heights=heights, row_offset=row_offset, tpack=tpack, A=A, B=B,
                  Bs=Bs, udot=udot, ld=ld, force_general_path=force_general_path, H=H, S=S,
                  ldh=ldh, shard_rank=shard_rank, n_shards=n_shards, workspace=workspace,
-                 host_out=host_out, ab_args=ab_args,
+                 host_out=host_out, ab_args=ab_args, reuse_t=reuse_t,
                  h_reference_form=h_reference_form, host_src=host_src, udot_rows=udot_rows)
     return call.run_sync(), call.workspace
 

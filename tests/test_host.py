@@ -209,3 +209,29 @@ def test_ctypes_structs_match_the_c_header(tmp_path):
         assert int(out[cname]) == ctypes.sizeof(py), cname
         for fname, _ in py._fields_:
             assert int(out[f"{cname}.{fname}"]) == getattr(py, fname).offset, (cname, fname)
+
+
+def test_tmatrixset_validate_structure():
+    """builder.py:123-138: Hermitian residual and the dense-block + diagonal-tail pattern."""
+    import numpy as np
+
+    import paper_1602_06589_b200 as pkg
+
+    rng = np.random.default_rng(3)
+    m, d = 9, 4  # l_sph 2, l_nonsph 1
+    t = np.zeros((m, m), dtype=np.complex128)
+    x = rng.standard_normal((d, d)) + 1j * rng.standard_normal((d, d))
+    t[:d, :d] = x + x.conj().T
+    t[np.diag_indices(m)] += 3.0
+    cd = pkg.ComplexDense.from_array
+    ok = pkg.TMatrixSet([cd(t)], [cd(t)], [cd(t)], [2], [1])
+    ok.validate_structure()
+    bad = t.copy()
+    bad[6, 2] = 0.1
+    bad[2, 6] = 0.1
+    with pytest.raises(pkg.ContractViolationError):
+        pkg.TMatrixSet([cd(bad)], [cd(t)], [cd(t)], [2], [1]).validate_structure()
+    nh = t.copy()
+    nh[1, 0] += 0.5
+    with pytest.raises(pkg.ContractViolationError):
+        pkg.TMatrixSet([cd(t)], [cd(t)], [cd(nh)], [2], [1]).validate_structure()

@@ -13,6 +13,18 @@ namespace {
 
 __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
 
+// Phase timers for tools/exp/tjoint_bench.cu (no-ops in the library build).
+#ifndef HSDLA_PROF_POINT
+#define HSDLA_PROF_POINT(i)
+#define HSDLA_PROF_START()
+#endif
+
+// Column-major sweep of an n x n index space by the whole CTA: warp w takes columns w, w + nw,
+// ..., its lanes go down the rows (coalesced), no integer division in the loop.
+#define FOR_SQUARE(n, r, c)                                       \
+  for (int c = threadIdx.x >> 5; c < (n); c += blockDim.x >> 5) \
+    for (int r = threadIdx.x & 31; r < (n); r += 32)
+
 // ---------------------------------------------------------------------------
 // Cholesky of tril(T) into F (lower, zero strict upper), one CTA per matrix.
 // Left-looking column algorithm, the same recurrence as the reference's portable
@@ -28,8 +40,7 @@ __device__ void chol_block(int n, const double2* __restrict__ T, long long ldt, 
   const int tid = threadIdx.x, nt = blockDim.x;
   if (tid == 0) s_nan = 0;
   __syncthreads();
-  for (long long e = tid; e < (long long)n * n; e += nt) {
-    const int r = (int)(e % n), c = (int)(e / n);
+  FOR_SQUARE(n, r, c) {
     double2 v = make_double2(0.0, 0.0);
     if (r >= c) {
       v = T[r + c * ldt];
@@ -81,77 +92,181 @@ __device__ void chol_block(int n, const double2* __restrict__ T, long long ldt, 
   if (tid == 0) *info = 0;
 }
 
-__global__ void potrf_batched_kernel(int n, const double2* T, long long ldt, long long st,
-                                     double2* F, long long ldf, long long sf, int* info) {
-  const int b = blockIdx.x;
-  chol_block(n, T + b * st, ldt, F + b * sf, ldf, info + b);
+// Blocked right-looking Cholesky of the lower triangle of A in place (ld lda), one CTA: a
+// panel of kNB columns is staged in shared memory (rows x kNB, row stride kNB + 1 against bank
+// conflicts) and factored there column by column (one barrier per column, a few updates per
+// thread), written back scaled, and the trailing lower triangle takes the rank-kNB update
+// A22 -= L21 L21^H in 4 x 4 register micro-tiles straight in global memory (L2-resident).
+// Same pivot rule and info as chol_block (0 ok, j+1 first bad pivot, -1 NaN in tril(A));
+// writes zeros to the strict upper triangle.  Dynamic shared memory: chol_blocked_smem(n).
+constexpr int kNB = 16;
+constexpr int kNBS = kNB + 1;
+__host__ __device__ constexpr size_t chol_blocked_smem(int n) {
+  return size_t(n > 0 ? n : 1) * kNBS * sizeof(double2);
 }
 
-// Right-looking Cholesky of tril(T) with the lower triangle packed in shared memory
-// (m(m+1)/2 complex: 118 KB at m = 121), used by the build's T preparation.  Same pivot
-// rule as chol_block; writes the factor (zero strict upper) to F.
-__device__ int packed_idx(int i, int k) { return i * (i + 1) / 2 + k; }
-
-__device__ void chol_packed(int n, const double2* __restrict__ T, long long ldt, double2* F,
-                            long long ldf, int* info) {
-  extern __shared__ double2 Lp[];
+// `checked`: the caller already rejected NaN input and zeroed the strict upper triangle.
+__device__ void chol_blocked(int n, double2* A, long long lda, int* info, bool checked = false) {
+  extern __shared__ double2 P[];  // [rows][kNBS]
+  __shared__ double s_inv[kNB], s_ljj[kNB];
   __shared__ int s_bad;
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int tx = tid & 31, ty = tid >> 5, nty = nt >> 5;
-  if (tid == 0) s_bad = 0;
-  __syncthreads();
-  // coalesced load of the lower triangle (column-major source, r fastest)
-  for (long long e = tid; e < (long long)n * n; e += nt) {
-    const int r = (int)(e % n), c = (int)(e / n);
-    if (r >= c) {
-      const double2 v = T[r + (long long)c * ldt];
-      if (isnan(v.x) || isnan(v.y)) s_bad = 1;
-      Lp[packed_idx(r, c)] = v;
-    }
-  }
-  __syncthreads();
-  if (s_bad) {
-    if (tid == 0) *info = -1;
-    return;
-  }
-  // Right-looking, one barrier per column: every thread reads the pivot and forms
-  // 1/L[j][j] itself; column j stays unscaled in shared memory (its scaled values go
-  // straight to F), so the trailing update can scale on the fly without a second pass.
-  for (int j = 0; j < n; ++j) {
-    const double d = Lp[packed_idx(j, j)].x;
-    if (!(d > 0.0) || !isfinite(d)) {  // uniform across the block
-      if (tid == 0) *info = j + 1;
-      return;
-    }
-    const double ljj = sqrt(d);
-    const double inv = 1.0 / ljj;
-    if (tid == 0) F[j + (long long)j * ldf] = make_double2(ljj, 0.0);
-    // trailing update L[i][k] -= L[i][j] conj(L[k][j]) / L[j][j]^2, j < k <= i: a warp per
-    // row i, lanes along k (consecutive packed addresses), L[i][j] broadcast in the warp.
-    for (int i = j + 1 + ty; i < n; i += nty) {
-      const int pi = packed_idx(i, 0);
-      const double2 a0 = Lp[pi + j];
-      const double2 a = make_double2(a0.x * inv, a0.y * inv);
-      if (tx == 0) F[i + (long long)j * ldf] = a;
-      for (int k = j + 1 + tx; k <= i; k += 32) {
-        const double2 b0 = Lp[packed_idx(k, j)];
-        const double2 b = make_double2(b0.x * inv, b0.y * inv);
-        double2 v = Lp[pi + k];
-        v.x -= a.x * b.x + a.y * b.y;
-        v.y -= a.y * b.x - a.x * b.y;
-        Lp[pi + k] = v;
+  const double2 zero = make_double2(0.0, 0.0);
+  if (!checked) {
+    if (tid == 0) s_bad = 0;
+    __syncthreads();
+    FOR_SQUARE(n, r, c) {
+      if (r >= c) {
+        const double2 v = A[r + c * lda];
+        if (isnan(v.x) || isnan(v.y)) s_bad = 1;
       }
     }
     __syncthreads();
+    if (s_bad) {
+      if (tid == 0) *info = -1;
+      return;
+    }
   }
-  for (long long e = tid; e < (long long)n * n; e += nt) {
-    const int r = (int)(e % n), c = (int)(e / n);
-    if (r < c) F[r + c * ldf] = make_double2(0.0, 0.0);
+  HSDLA_PROF_POINT(1);
+  for (int k = 0; k < n; k += kNB) {
+    const int nb = min(kNB, n - k), rows = n - k;
+    for (int e = tid; e < rows * nb; e += nt) {
+      const int r = e % rows, c = e / rows;
+      P[r * kNBS + c] = r >= c ? A[(k + r) + (long long)(k + c) * lda] : zero;
+    }
+    __syncthreads();
+    HSDLA_PROF_POINT(2);
+    // unblocked right-looking factorization of the panel; column j stays unscaled in shared
+    // memory (scaled on write-back), updates use the scaled values on the fly
+    for (int j = 0; j < nb; ++j) {
+      const double d = P[j * kNBS + j].x;
+      if (!(d > 0.0) || !isfinite(d)) {  // uniform across the block
+        if (tid == 0) *info = k + j + 1;
+        return;
+      }
+      const double ljj = sqrt(d);
+      const double inv = 1.0 / ljj;
+      if (tid == 0) {
+        s_inv[j] = inv;
+        s_ljj[j] = ljj;
+      }
+      // thread (row slot ty, column slot tx): no integer division in the loop
+      const int tx = tid % kNB, ty = tid / kNB, c = j + 1 + tx;
+      if (c < nb) {
+        const double2 b0 = P[c * kNBS + j];
+        const double2 b = make_double2(b0.x * inv, b0.y * inv);
+        const int S = nt / kNB;  // row slots (only rows r >= c are updated: the lower triangle)
+        int r = j + 1 + ty;
+        if (r < c) r += (c - r + S - 1) / S * S;
+        for (; r < rows; r += S) {
+          const double2 a0 = P[r * kNBS + j];
+          const double2 a = make_double2(a0.x * inv, a0.y * inv);
+          double2 v = P[r * kNBS + c];
+          v.x = fma(-a.x, b.x, v.x);
+          v.x = fma(-a.y, b.y, v.x);
+          v.y = fma(-a.y, b.x, v.y);
+          v.y = fma(a.x, b.y, v.y);
+          P[r * kNBS + c] = v;
+        }
+      }
+      __syncthreads();
+    }
+    HSDLA_PROF_POINT(3);
+    for (int e = tid; e < rows * nb; e += nt) {
+      const int r = e % rows, c = e / rows;
+      double2 v = zero;
+      if (r > c) {
+        v = P[r * kNBS + c];
+        v = make_double2(v.x * s_inv[c], v.y * s_inv[c]);
+        P[r * kNBS + c] = v;
+      } else if (r == c) {
+        v = make_double2(s_ljj[c], 0.0);
+      }
+      A[(k + r) + (long long)(k + c) * lda] = v;
+    }
+    __syncthreads();
+    HSDLA_PROF_POINT(4);
+    // trailing lower triangle, rows / columns [k + nb, n): warp tasks of 64 rows x 8 columns,
+    // lane l on rows i0 + l and i0 + 32 + l (consecutive panel rows: conflict-free shared
+    // loads), the 8 column rows j0..j0+7 broadcast; only tasks touching i >= j run.
+    {
+      const int tr = rows - nb;
+      const int nrb = (tr + 63) / 64, ncb = (tr + 7) / 8;
+      const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+      for (int task = wid; task < nrb * ncb; task += nw) {
+        const int rb = task % nrb, cb = task / nrb;
+        const int i0 = 64 * rb, j0 = 8 * cb;  // trailing-relative
+        if (i0 + 63 < j0) continue;           // strictly upper: nothing to do
+        double2 acc[2][8];
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[a][q] = zero;
+        const int ia = nb + i0 + lane, ib = ia + 32;
+        for (int c = 0; c < nb; ++c) {
+          const double2 la = ia < rows ? P[ia * kNBS + c] : zero;
+          const double2 lb = ib < rows ? P[ib * kNBS + c] : zero;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int rj = nb + j0 + q;
+            const double2 lj = rj < rows ? P[rj * kNBS + c] : zero;
+            // li conj(lj) as four FMAs per accumulator pair (no separate products + DADD)
+            acc[0][q].x = fma(la.x, lj.x, acc[0][q].x);
+            acc[0][q].x = fma(la.y, lj.y, acc[0][q].x);
+            acc[0][q].y = fma(la.y, lj.x, acc[0][q].y);
+            acc[0][q].y = fma(-la.x, lj.y, acc[0][q].y);
+            acc[1][q].x = fma(lb.x, lj.x, acc[1][q].x);
+            acc[1][q].x = fma(lb.y, lj.y, acc[1][q].x);
+            acc[1][q].y = fma(lb.y, lj.x, acc[1][q].y);
+            acc[1][q].y = fma(-lb.x, lj.y, acc[1][q].y);
+          }
+        }
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          const int i = k + nb + i0 + lane + 32 * a;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int jj = k + nb + j0 + q;
+            if (i < n && jj < n && jj <= i) {
+              double2* x = A + i + (long long)jj * lda;
+              const double2 v = *x;
+              *x = make_double2(v.x - acc[a][q].x, v.y - acc[a][q].y);
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    HSDLA_PROF_POINT(5);
+  }
+  if (!checked) {
+    FOR_SQUARE(n, r, c) {
+      if (r < c) A[r + c * lda] = zero;
+    }
   }
   if (tid == 0) *info = 0;
 }
 
-constexpr int kPackedMaxN = 168;  // 168*169/2*16 B = 227 KB
+// Cholesky of tril(T) into F: blocked in place on a copy when its panel fits in shared memory
+// (n <= kBlockedMaxN), else the column algorithm (chol_block).
+constexpr int kBlockedMaxN = 768;
+
+__global__ void potrf_batched_kernel(int n, const double2* T, long long ldt, long long st,
+                                     double2* F, long long ldf, long long sf, int* info) {
+  const int b = blockIdx.x;
+  if (n <= kBlockedMaxN) {
+    const double2* Tb = T + b * st;
+    double2* Fb = F + b * sf;
+    FOR_SQUARE(n, r, c) {
+      Fb[r + c * ldf] = r >= c ? Tb[r + c * ldt] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    chol_blocked(n, Fb, ldf, info + b);
+  } else {
+    chol_block(n, T + b * st, ldt, F + b * sf, ldf, info + b);
+  }
+}
+
 constexpr int kPotrfMaxDynSmem = 227 * 1024;  // opt-in limit per CTA (static smem comes off it)
 
 // Per T set: forms[0] = T_AB, forms[1] = 1/2 full(T_BB), forms[2] = full(T_AA),
@@ -167,8 +282,7 @@ __global__ void tprep_kernel(const int* tdim, int mp, const double2* taa, const 
   const double2* Tbb = tbb + b * tstride;
   double2* f = forms + (long long)b * 4 * mp * mp;
   const long long fs = (long long)mp * mp;
-  for (long long e = threadIdx.x; e < (long long)m * m; e += blockDim.x) {
-    const int r = (int)(e % m), c = (int)(e / m);
+  FOR_SQUARE(m, r, c) {
     f[r + (long long)c * mp] = Tab[r + c * t_ld];
     double2 bb, aa;
     if (r > c) { bb = Tbb[r + c * t_ld]; aa = Taa[r + c * t_ld]; }
@@ -180,10 +294,13 @@ __global__ void tprep_kernel(const int* tdim, int mp, const double2* taa, const 
   __syncthreads();
   if (!do_chol) {
     if (threadIdx.x == 0) info[b] = -2;
-  } else if (mp <= kPackedMaxN) {  // the launch sized shared memory by mp, not by this set's m
-    chol_packed(m, Taa, t_ld, f + 3 * fs, mp, info + b);
-  } else {
-    chol_block(m, Taa, t_ld, f + 3 * fs, mp, info + b);
+  } else {  // blocked, in place on tril(T_AA) copied into forms[3]
+    double2* F = f + 3 * fs;
+    FOR_SQUARE(m, r, c) {
+      F[r + (long long)c * mp] = r >= c ? Taa[r + c * t_ld] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    chol_blocked(m, F, mp, info + b);
   }
 }
 
@@ -208,6 +325,7 @@ __global__ void tjoint_kernel(const int* tdim, const int* tdense, int mp, const 
                               const double* u2, double sigma_fixed, double* sigma_host) {
   __shared__ int s_off, s_tail_bad;
   __shared__ double s_scale, s_rho;
+  HSDLA_PROF_START();
   const int b = blockIdx.x;
   const int m = tdim[b];
   const int d = tdense ? min(max(tdense[b], 0), m) : m;
@@ -222,36 +340,49 @@ __global__ void tjoint_kernel(const int* tdim, const int* tdense, int mp, const 
   double2* J = joint + (long long)b * lj * lj;
   if (threadIdx.x == 0) {
     s_off = 0;
-    double sc = 0.0;  // max |T_ii| / D_ii: the scale of the shift search
-    if (can_shift)
-      for (int i = 0; i < m; ++i)
-        sc = fmax(sc, fmax(fabs(Taa[i + i * t_ld].x), fabs(Tbb[i + i * t_ld].x) / fmax(U2[i], 1e-300)));
-    s_scale = sc;
+    s_scale = 0.0;
     s_rho = 0.0;
   }
   __syncthreads();
-  // Gershgorin radius of the 2m x 2m matrix (max absolute row sum): the shift guard's scale
-  if (sigma_host && sigma_fixed < 0.0) {
-    for (int r = threadIdx.x; r < 2 * m; r += blockDim.x) {
-      double acc = 0.0;
-      for (int c = 0; c < 2 * m; ++c) {
-        double2 v;
-        const int rr = r < m ? r : r - m, cc = c < m ? c : c - m;
-        if (r < m && c < m) v = rr >= cc ? Taa[rr + cc * t_ld] : cconj(Taa[cc + rr * t_ld]);
-        else if (r < m) v = Tab[rr + cc * t_ld];
-        else if (c < m) v = cconj(Tab[cc + rr * t_ld]);
-        else v = rr >= cc ? Tbb[rr + cc * t_ld] : cconj(Tbb[cc + rr * t_ld]);
-        if (rr == cc && (r < m) == (c < m)) v.y = 0.0;
-        acc += sqrt(v.x * v.x + v.y * v.y);
-      }
-      atomicMax(reinterpret_cast<unsigned long long*>(&s_rho), __double_as_longlong(acc));
+  if (can_shift)  // max |T_ii| / D_ii: the scale of the shift search (non-negative: max on the bits)
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+      const double v = fmax(fabs(Taa[i + i * t_ld].x), fabs(Tbb[i + i * t_ld].x) / fmax(U2[i], 1e-300));
+      atomicMax(reinterpret_cast<unsigned long long*>(&s_scale), __double_as_longlong(v));
     }
+  __syncthreads();
+  // Gershgorin radius of the 2m x 2m matrix (max absolute row sum): the shift guard's scale.
+  // Every thread takes whole columns' worth of entries (consecutive threads on consecutive
+  // rows of a column: coalesced), row sums accumulate in shared memory.
+  __shared__ double s_row[2 * (HSDLA_MAX_LSPH + 1) * (HSDLA_MAX_LSPH + 1)];
+  const bool want_rho = sigma_host && sigma_fixed < 0.0;
+  bool rho_in_assembly = false;  // set below: without the split the assembly pass sums the rows
+  if (want_rho) {
+    for (int r = threadIdx.x; r < 2 * m; r += blockDim.x) s_row[r] = 0.0;
     __syncthreads();
   }
+  if (want_rho && tdense && min(max(tdense[b], 0), m) < m) {  // split candidate: separate pass
+    const int n2 = 2 * m;
+    FOR_SQUARE(n2, r, c) {
+      double2 v;
+      const int rr = r < m ? r : r - m, cc = c < m ? c : c - m;
+      if (r < m && c < m) v = rr >= cc ? Taa[rr + cc * t_ld] : cconj(Taa[cc + rr * t_ld]);
+      else if (r < m) v = Tab[rr + cc * t_ld];
+      else if (c < m) v = cconj(Tab[cc + rr * t_ld]);
+      else v = rr >= cc ? Tbb[rr + cc * t_ld] : cconj(Tbb[cc + rr * t_ld]);
+      if (rr == cc && (r < m) == (c < m)) v.y = 0.0;
+      atomicAdd(s_row + r, sqrt(v.x * v.x + v.y * v.y));
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < n2; r += blockDim.x)
+      atomicMax(reinterpret_cast<unsigned long long*>(&s_rho), __double_as_longlong(s_row[r]));
+    __syncthreads();
+  } else {
+    rho_in_assembly = want_rho;
+  }
+  HSDLA_PROF_POINT(7);
   bool split = d < m;
   if (split) {  // every coupling of a tail row other than its own diagonal must vanish
-    for (long long e = threadIdx.x; e < (long long)m * m; e += blockDim.x) {
-      const int r = (int)(e % m), c = (int)(e / m);
+    FOR_SQUARE(m, r, c) {
       if (r == c || (r < d && c < d)) continue;
       const double2 x = Tab[r + c * t_ld];
       bool nz = x.x != 0.0 || x.y != 0.0;
@@ -281,24 +412,47 @@ __global__ void tjoint_kernel(const int* tdim, const int* tdense, int mp, const 
   const int attempts = (sigma_fixed < 0.0 && can_shift) ? 40 : 1;
   for (int att = 0; att < attempts; ++att) {
     if (att > 0) sigma = s_scale * ldexp(1.0, att - 13);
-    for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x) {
-      const int r = (int)(e % n), c = (int)(e / n);
-      if (r < c) continue;
-      double2 v;
-      if (r < h) v = Taa[r + c * t_ld];
-      else if (c < h) v = cconj(Tab[c + (r - h) * t_ld]);
-      else v = Tbb[(r - h) + (c - h) * t_ld];
-      if (r == c) {
-        v.y = 0.0;
-        if (sigma != 0.0) v.x += sigma * (r < h ? 1.0 : U2[r - h]);
+    if (threadIdx.x == 0) s_tail_bad = 0;  // also the NaN flag of the assembly below
+    __syncthreads();
+    // (rows by lanes with whole-warp iterations: the row-sum reduction below shuffles)
+    for (int c = threadIdx.x >> 5; c < n; c += blockDim.x >> 5)
+    for (int r0 = 0; r0 < n; r0 += 32) {
+      const int r = r0 + (threadIdx.x & 31);
+      double2 v = make_double2(0.0, 0.0);
+      double av = 0.0;  // |T_rc| into row r; the mirror's |T_cr| into row c (warp-reduced)
+      if (r < n && r >= c) {
+        if (r < h) v = Taa[r + c * t_ld];
+        else if (c < h) v = cconj(Tab[c + (r - h) * t_ld]);
+        else v = Tbb[(r - h) + (c - h) * t_ld];
+        if (isnan(v.x) || isnan(v.y)) s_tail_bad = 1;
+        if (r == c) v.y = 0.0;
+        av = sqrt(v.x * v.x + v.y * v.y);
+        if (r == c && sigma != 0.0) v.x += sigma * (r < h ? 1.0 : U2[r - h]);
       }
-      J[r + c * lj] = v;
+      if (rho_in_assembly && att == 0) {  // Gershgorin row sums of the unshifted matrix
+        if (av != 0.0) atomicAdd(s_row + r, av);
+        double mirror = r > c ? av : 0.0;  // the warp shares column c
+        for (int o = 16; o > 0; o >>= 1) mirror += __shfl_xor_sync(0xffffffffu, mirror, o);
+        if ((threadIdx.x & 31) == 0 && mirror != 0.0) atomicAdd(s_row + c, mirror);
+      }
+      if (r < n) J[r + c * lj] = v;
     }
+    __syncthreads();
+    if (rho_in_assembly && att == 0) {
+      for (int r = threadIdx.x; r < n; r += blockDim.x)
+        atomicMax(reinterpret_cast<unsigned long long*>(&s_rho), __double_as_longlong(s_row[r]));
+      __syncthreads();
+    }
+    HSDLA_PROF_POINT(8);
+    if (s_tail_bad) {
+      if (threadIdx.x == 0) info[b] = -1;
+    } else {
+      chol_blocked(n, J, lj, info + b, true);  // in place; shared memory sized for 2*mp rows
+    }
+    __syncthreads();
     if (threadIdx.x == 0) s_tail_bad = 0;
     __syncthreads();
-    if (lj <= kPackedMaxN) chol_packed(n, J, lj, J, lj, info + b);  // shared memory sized by 2*mp
-    else chol_block(n, J, lj, J, lj, info + b);
-    __syncthreads();
+    HSDLA_PROF_POINT(6);
     if (split && info[b] == 0) {
       for (int i = d + threadIdx.x; i < m; i += blockDim.x) {
         const double a = Taa[i + i * t_ld].x + sigma, c = Tbb[i + i * t_ld].x + (sigma != 0.0 ? sigma * U2[i] : 0.0);
@@ -430,8 +584,9 @@ int launch_potrf_batched(hsdla_ctx* ctx, int n, int batch, const double2* T, lon
     set_error("Cholesky order above 14400 (one shared-memory row per CTA)");
     return HSDLA_ERR_UNSUPPORTED;
   }
-  potrf_batched_kernel<<<batch, 128, n * sizeof(double2), ctx->stream>>>(n, T, ldt, stride_t, F,
-                                                                          ldf, stride_f, info_dev);
+  const size_t smem = n <= kBlockedMaxN ? chol_blocked_smem(n) : size_t(n) * sizeof(double2);
+  potrf_batched_kernel<<<batch, 512, smem, ctx->stream>>>(n, T, ldt, stride_t, F, ldf, stride_f,
+                                                          info_dev);
   HS_CHECK_LAUNCH();
   return HSDLA_OK;
 }
@@ -440,9 +595,7 @@ int launch_tprep(hsdla_ctx* ctx, cudaStream_t stream, int n_tsets, const int* td
                  const double2* taa, const double2* tab, const double2* tbb, long long t_ld,
                  double2* forms, int do_chol, int* info_dev) {
   if (n_tsets <= 0) return HSDLA_OK;
-  size_t smem = (mp <= kPackedMaxN) ? size_t(mp) * (mp + 1) / 2 * sizeof(double2)
-                                    : size_t(mp) * sizeof(double2);
-  // smem limit set once per device in preload_small()
+  const size_t smem = chol_blocked_smem(mp);  // limit set once per device in preload_small()
   tprep_kernel<<<n_tsets, 512, smem, stream>>>(tdim_dev, mp, taa, tab, tbb, t_ld, forms, do_chol,
                                                info_dev);
   HS_CHECK_LAUNCH();
@@ -455,9 +608,7 @@ int launch_tjoint(cudaStream_t stream, int n_tsets, const int* tdim_dev, const i
                   int* split_host_dev, const double* u2_dev, double sigma_fixed,
                   double* sigma_host_dev) {
   if (n_tsets <= 0) return HSDLA_OK;
-  const int n = 2 * mp;
-  size_t smem = (n <= kPackedMaxN) ? size_t(n) * (n + 1) / 2 * sizeof(double2)
-                                   : size_t(n) * sizeof(double2);
+  const size_t smem = chol_blocked_smem(2 * mp);
   tjoint_kernel<<<n_tsets, 512, smem, stream>>>(tdim_dev, tdense_dev, mp, taa, tab, tbb, t_ld,
                                                 joint, info_dev, info_host_dev, split_host_dev,
                                                 u2_dev, sigma_fixed, sigma_host_dev);
@@ -573,12 +724,13 @@ int preload_small() {
     HS_CUDA(cudaFuncSetAttribute(potrf_batched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kPotrfMaxDynSmem - (int)at.sharedSizeBytes));
   }
-  if (first_on_device((const void*)tjoint_kernel))
-    HS_CUDA(cudaFuncSetAttribute(tjoint_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(size_t(kPackedMaxN) * (kPackedMaxN + 1) / 2 * sizeof(double2))));
-  if (first_on_device((const void*)tprep_kernel))
-    HS_CUDA(cudaFuncSetAttribute(tprep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(size_t(kPackedMaxN) * (kPackedMaxN + 1) / 2 * sizeof(double2))));
+  for (const void* f : {(const void*)tjoint_kernel, (const void*)tprep_kernel})
+    if (first_on_device(f)) {
+      cudaFuncAttributes at;
+      HS_CUDA(cudaFuncGetAttributes(&at, f));
+      HS_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kPotrfMaxDynSmem - (int)at.sharedSizeBytes));
+    }
   return HSDLA_OK;
 }
 

@@ -310,8 +310,12 @@ class _Call:
             "template_types": int(r.template_types),
             "ms": {"setup": r.ms_setup, "S": r.ms_S, "H_ABBA_BB": r.ms_H_ABBA_BB,
                    "H_AA": r.ms_H_AA},
-            "kernel_ms": {"contract_S": r.ms_contract_S, "contract_H": r.ms_contract_H,
-                          "apply_Z": r.ms_apply_Z, "apply_XY": r.ms_apply_XY},
+            # template path: the per-type W = L^H [A; B] application and the W1 / W2 expansion
+            "kernel_ms": ({"contract_S": r.ms_contract_S, "contract_H": r.ms_contract_H,
+                           "apply_W": r.ms_apply_Z, "expand_W": r.ms_apply_XY}
+                          if r.template_types and all(self.joint[i] == 1 for i in range(self.n_tsets))
+                          else {"contract_S": r.ms_contract_S, "contract_H": r.ms_contract_H,
+                                "apply_Z": r.ms_apply_Z, "apply_XY": r.ms_apply_XY}),
             "workspace_bytes": int(self.need),
             "ms_total": r.ms_total,
         }

@@ -1,7 +1,8 @@
 """Per-launch DRAM bytes of one bench step's contraction launches -> profiles/traffic_<cfg>.json.
 
     python tools/traffic_json.py gpurun_out/traffic_C2.csv C2 > profiles/traffic_C2.json
-The last four contract launches of the capture are one step: S, Z apply, XY apply, H.
+The last three contract launches of the capture are one step on the template path: S, the
+per-type W = L^H [A; B] application, H (joint form: H = W1^H W1 + W2^H W2).
 """
 import collections
 import csv
@@ -21,15 +22,15 @@ for r in rows[hdr + 1:]:
     assert d["Metric Unit"] in ("byte", "ns", "nsecond", "usecond", "msecond"), d["Metric Unit"]
     launch.setdefault(d["ID"], {"kernel": d["Kernel Name"][:60]})[d["Metric Name"]] = (
         float(d["Metric Value"]), d["Metric Unit"])
-step = list(launch.values())[-4:]
-names = ["contract_S", "apply_Z", "apply_XY", "contract_H"]
+step = list(launch.values())[-3:]
+names = ["contract_S", "apply_W", "contract_H"]
 from paper_1602_06589_b200 import configs  # noqa: E402
 
 inst = configs.make_instance(cfg)
 n = inst.spec.n_basis
 r = int(sum(inst.spec.layout().block_heights))
 op = 16 * r * n
-alg = {"contract_S": (2 * op, 16 * n * n), "contract_H": (3 * op, 16 * n * n)}
+alg = {"contract_S": (2 * op, 16 * n * n), "contract_H": (2 * op, 16 * n * n)}
 per = {}
 for name, l in zip(names, step):
     rd, wr = l["dram__bytes_read.sum"][0], l["dram__bytes_write.sum"][0]
@@ -46,6 +47,6 @@ print(json.dumps({
     "kernel": "contract_kernel (S + H triangular contractions)",
     "dram_bytes_per_step": int(total),
     "per_launch": per,
-    "note": "algorithmic_read = operand bytes read once (S: A*, UB*; H: Z, B*, XY); "
+    "note": "algorithmic_read = operand bytes read once (S: A*, UB*; H: W1, W2); "
             "algorithmic_write = both triangles of the mirrored N_G x N_G result",
 }, indent=1))

@@ -330,10 +330,15 @@ def init_dist(world: int, local: int, backend: str = "nccl"):
     import torch.distributed as dist
 
     if world > 1 and not dist.is_initialized():
+        import datetime
+
+        # a rank that fails must not leave the others waiting in a collective for the default
+        # half hour: give up after five minutes
+        tmo = datetime.timedelta(seconds=300)
         if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local), timeout=tmo)
         else:
-            dist.init_process_group(backend)
+            dist.init_process_group(backend, timeout=tmo)
     return dist
 
 

@@ -12,9 +12,13 @@
 //
 // FP64 on sm_100a has no tcgen05 kind: the tensor path is mma.sync.m8n8k4.f64 (SASS
 // DMMA.8x8x4), 128 flop/clk/SM = 37.2 TF at 1965 MHz (measured, profiles/r01_fp64_peaks.json).
-// Complex arithmetic uses the real embedding over interleaved (re, im) pairs, K' = 2K:
+// Complex multiply, default (G3, cmul_mode() == 3): three real DMMA products per complex MAC
+// (Gauss / ZHERK3M): accR = sum P_re Q_re, accX = sum P_im Q_im, accI = sum (P_re - P_im)(Q_re +
+// Q_im), then Re = accR + accX, Im = accI - accR + accX; its error bound is normwise (see the
+// adversarial cases in tests/test_gpu_contracts.py).  HSDLA_CMUL=4: the real embedding over
+// interleaved (re, im) pairs, K' = 2K,
 //   Re C = P^T Q        Im C = P^T (J Q),  (J Q)[2k] = Q[2k+1], (J Q)[2k+1] = -Q[2k]
-// so every complex MAC is exactly 4 real FMAs (the ledger's 8 flops), no 3M trick.
+// i.e. exactly 4 real FMAs per complex MAC (the ledger's 8 flops).
 //
 // CTA: 128 threads = 2x2 warps, 64x64 complex output tile, each warp 32x32 complex
 // (16 DMMA blocks for Re + 16 for Im).  K is staged in chunks of 16 complex (256 B per

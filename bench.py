@@ -632,7 +632,7 @@ def run_ours(args):
                                                 dropin["ms"]], world)
     e2e_fl_all = max_over_ranks([e2e_fl], world, "sum")[0]
     e2e_value = e2e_fl_all / (e2e_ms / 1e3) / 1e12
-    launches = args.steps * (pipe.launches_per_run(dspec)
+    launches = args.steps * (pipe.launches_per_run(dspec, res)
                              + int(any(res.get("joint_split", [])))
                              + int(res.get("joint_shift", 0.0) > 0))
     clocks = clk.summary()
@@ -801,7 +801,8 @@ def run_panels(args):
                     "h2d_bytes_per_step": int(dspec.h2d_bytes), "d2h_bytes_per_step": 32 * n * n,
                     "ms_per_step": round(e2e, 3),
                     "api": f"paper_1602_06589_b200.shard.{type(sb).__name__}.run + D2H of H, S"},
-            "gpu_launches": args.steps * (sb.pipe.launches_per_run(dspec) + (2 if world > 1 else 0)),
+            "gpu_launches": args.steps * (sb.pipe.launches_per_run(dspec, sb.last_result)
+                                          + (2 if world > 1 else 0)),
             "clocks": out["clocks"],
         }
         print(json.dumps(line), flush=True)

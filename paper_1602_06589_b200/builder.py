@@ -428,6 +428,12 @@ HOST_SOURCED_MIN_BYTES = 1 << 28  # per stack; see build_all
 _WORKSPACE: dict = {}  # device -> (build workspace, (TPack, force) of the last build on it)
 
 
+def release_cached_workspaces():
+    """Free the build workspaces `build_all` keeps between calls (one per device: the Z / XY /
+    scaled-B stacks plus the T preparation — three stacked-coefficient sizes, e.g. 8 GB at C4)."""
+    _WORKSPACE.clear()
+
+
 def build_all(coeffs: StackedCoefficients, tmats: TMatrixSet, config: BuildConfig,
               regenerate=None):
     """Composed build on the GPU; returns (H, S, report) with H, S full Hermitian (`builder.py:403-474`).
@@ -462,8 +468,10 @@ def build_all(coeffs: StackedCoefficients, tmats: TMatrixSet, config: BuildConfi
     # here first.
     dev_a = coeffs.A_star.device_view() if isinstance(coeffs.A_star, DeviceComplexDense) else None
     dev_b = coeffs.B_star.device_view() if isinstance(coeffs.B_star, DeviceComplexDense) else None
+    here = t.cuda.current_device()
     src = None
-    if dev_a is not None and dev_b is not None and dev_a[1] == dev_b[1]:
+    if (dev_a is not None and dev_b is not None and dev_a[1] == dev_b[1]
+            and dev_a[0].device.index == here and dev_b[0].device.index == here):
         (a_d, ld), (b_d, _) = dev_a, dev_b
     elif r * n * 16 >= HOST_SOURCED_MIN_BYTES and \
             (src := device.pinned_sources(coeffs.A_star, coeffs.B_star)) is not None:

@@ -461,11 +461,18 @@ class HSPipeline:
         """Wait for a k-point enqueued by `run_async` (compute and host copies)."""
         return self._inflight.pop(ticket).finish(ticket)
 
-    def launches_per_run(self, dspec: DeviceSpec) -> int:
-        """Kernels this pipeline launches per k-point once the T preparation is cached: A/B
-        per l group, S contraction, Z apply, XY apply, H contraction, result publication (plus
-        the tail kernel of split T sets, which the caller adds from `joint_split`)."""
-        return len(np.unique(dspec.l_sph)) + 5
+    def launches_per_run(self, dspec: DeviceSpec, result: dict | None = None) -> int:
+        """Kernels this pipeline launches per k-point once the T preparation is cached.
+        Per-atom path: A/B per l group, S contraction, Z apply, XY apply, H contraction, result
+        publication (plus the tail kernel of split T sets, which the caller adds from
+        `joint_split`).  Template path (`result["template_types"] > 0`): templates per l group,
+        expansion, S contraction, per-type W application, W expansion, H contraction,
+        publication."""
+        groups = len(np.unique(dspec.l_sph))
+        if result is not None and result.get("template_types", 0) and "apply_W" in result.get(
+                "kernel_ms", {}):
+            return groups + 6
+        return groups + 5
 
     def result_views(self):
         """Host-indexable (n, n) views: H[i, j] == tensor[j, i] (column-major storage)."""

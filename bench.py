@@ -248,7 +248,7 @@ def hbm_peak_gbs():
         return 6550.0, "SURVEY.md 8d measured copy bandwidth"
 
 
-def ab_gen_line(ms, rows, n, template_types=0, expand_w_ms=None):
+def ab_gen_line(ms, rows, n, template_types=0, expand_w_ms=None, templates_ms=None):
     """A/B generation against the HBM-write roofline.  Per-atom path: the
     generator writes A*, B* and ||udot|| B* (48 R N bytes).  Template path: the
     per-type templates (negligible bytes, latency-bound recurrences) and the expansion pass
@@ -263,6 +263,13 @@ def ab_gen_line(ms, rows, n, template_types=0, expand_w_ms=None):
            "frac": round(gbs / peak, 4),
            "path": (f"per-type templates ({template_types} type(s)) + expansion" if template_types
                     else "per-atom generator")}
+    if template_types and templates_ms is not None and ms > templates_ms > 0:
+        # the HBM-bound part alone: the expansion writing A*, ||udot|| B* after the templates
+        xm = ms - templates_ms
+        xg = written / (xm / 1e3) / 1e9
+        out["templates_ms"] = round(templates_ms, 4)
+        out["expand_AB"] = {"ms": round(xm, 4), "bytes_written": written,
+                            "achieved_gbs": round(xg, 1), "frac": round(xg / peak, 4)}
     if template_types and expand_w_ms:
         w = 32 * rows * n
         wg = w / (expand_w_ms / 1e3) / 1e9
@@ -379,6 +386,7 @@ def time_kpoints(pipe, dspecs, tpack, steps, world):
         for k, v in res["kernel_ms"].items():
             kern[k].append(v)
         ab_ms.append(res["ms"]["setup"])  # A/B generation (T preparation reused)
+        kern["templates"].append(res.get("ms_templates", 0.0))
 
     for i in range(steps):
         ticket = pipe.run_async(dspecs[i % len(dspecs)], tpack)
@@ -688,7 +696,8 @@ def run_ours(args):
             "step_fp64_frac": round(ex_step / FP64_PEAK_TFLOPS, 4),
             "roofline": {**rl, "ceilings": fp64_ceilings(clocks.get("sm_mhz"))},
             "ab_gen": ab_gen_line(statistics.mean(ab_ms), rows, n, res.get("template_types", 0),
-                                  statistics.mean(kern["expand_W"]) if kern.get("expand_W") else None),
+                                  statistics.mean(kern["expand_W"]) if kern.get("expand_W") else None,
+                                  statistics.mean(kern["templates"]) if kern.get("templates") else None),
             "e2e": {"value": round(e2e_value, 4), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
                     "ms_per_step": round(e2e_ms, 3),

@@ -300,6 +300,8 @@ typedef struct {
   double joint_shift;         /* out: the common shift sigma of the joint form (0 = none) */
   int32_t template_types;     /* out: atom types of the template path (hsdla_build_args.atom_type),
                                  0 = per-atom generation / T applications */
+  float ms_templates;         /* out: template path: the per-type generator's share of ms_setup
+                                 (the rest of ms_setup is the HBM-bound expansion) */
 } hsdla_build_result;
 
 size_t hsdla_build_workspace_size(const hsdla_build_args* args);

@@ -652,6 +652,8 @@ int complete_slot(hsdla_ctx* ctx, hsdla_ctx::BuildSlot& sl, hsdla_ctx::Outcome* 
   cudaEventElapsedTime(&t46, ev[4], ev[6]);
   cudaEventElapsedTime(&t07, ev[0], ev[7]);
   o->ms[0] = t01; o->ms[1] = t12; o->ms[2] = t23; o->ms[3] = t34; o->ms[4] = t46; o->ms[5] = t07;
+  o->ms[6] = 0.0f;
+  if (sl.types > 0) cudaEventElapsedTime(&o->ms[6], ev[0], ev[5]);  // template generation
   if (getenv("HSDLA_TIMELINE")) {  // debug: absolute build timeline vs the context epoch
     float a0 = 0, a7 = 0, a2 = 0, a6 = 0;
     cudaEventElapsedTime(&a0, ctx->epoch, ev[0]);
@@ -853,6 +855,7 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     }
     rc = ab_generate_templates(ctx, ab, ti.rep, ti.toff, tA, tB, ldt);
     if (rc) return rc;
+    HS_CUDA(cudaEventRecord(ev[5], ctx->stream));
     std::vector<int4> ex(na);
     std::vector<long long> eo(na);
     for (int i = 0; i < na; ++i) {
@@ -1258,6 +1261,7 @@ int fill_result(const hsdla_ctx::Outcome& o, hsdla_build_result* res) {
     if (res->joint_info) res->joint_info[t] = o.joint[t];
   res->joint_shift = o.sigma;
   res->template_types = o.types;
+  res->ms_templates = o.ms[6];
   for (size_t i = 0; i < o.hpd.size(); ++i)
     if (res->hpd_mask) res->hpd_mask[i] = o.hpd[i];
   res->nonfinite = o.nonfinite;

@@ -170,7 +170,7 @@ struct hsdla_ctx {
     std::vector<int> info, hpd, joint;
     double sigma = 0.0;
     int types = 0;
-    float ms[6] = {};
+    float ms[7] = {};
   };
   std::map<unsigned long long, Outcome> stash;
   cudaEvent_t fork = nullptr, join = nullptr;

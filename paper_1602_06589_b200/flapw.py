@@ -150,7 +150,7 @@ def compute_AB(spec: SystemSpec) -> StackedCoefficients:
     from . import device
     from .pipeline import DeviceSpec, ab_generate_device
 
-    t = device.require_cuda()
+    device.require_cuda()
     layout = spec.layout()
     dspec = DeviceSpec(spec)
     n = spec.n_basis
@@ -158,9 +158,10 @@ def compute_AB(spec: SystemSpec) -> StackedCoefficients:
     cap = layout.capacity_rows
     a_dev = device.empty_matrix(cap, n, cap, zero=True)
     b_dev = device.empty_matrix(cap, n, cap, zero=True)
-    udot = t.zeros(cap, dtype=t.float64, device="cuda")
-    ab_generate_device(dspec, a_dev, b_dev, None, cap, udot)
-    norms = udot[: layout.total_rows].cpu().numpy().copy()
+    ab_generate_device(dspec, a_dev, b_dev, None, cap, None)
+    # per-row ||udot|| (flapw.py:232) straight from the radial data: no device round trip, so
+    # the call returns while the generator still runs
+    norms = np.array(dspec.udot_rows, dtype=np.float64)
     return StackedCoefficients(DeviceComplexDense(a_dev, cap, n, layout.total_rows),
                                DeviceComplexDense(b_dev, cap, n, layout.total_rows), layout, norms)
 

@@ -308,6 +308,7 @@ class _Call:
             "joint_split": [self.joint[i] == 2 for i in range(self.n_tsets)],
             "joint_shift": float(r.joint_shift),
             "template_types": int(r.template_types),
+            "ms_templates": float(r.ms_templates),
             "ms": {"setup": r.ms_setup, "S": r.ms_S, "H_ABBA_BB": r.ms_H_ABBA_BB,
                    "H_AA": r.ms_H_AA},
             # template path: the per-type W = L^H [A; B] application and the W1 / W2 expansion

@@ -169,6 +169,7 @@ int hsdla_ctx_create(hsdla_ctx** out, void* stream) {
   HS_CUDA(cudaHostGetDevicePointer((void**)&c->scratch_host_dev, c->scratch_host, 0));
   HS_CUDA(cudaEventCreateWithFlags(&c->stage_done, cudaEventDisableTiming));
   HS_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  HS_CUDA(cudaStreamCreateWithFlags(&c->side2, cudaStreamNonBlocking));
   HS_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
   HS_CUDA(cudaStreamCreateWithFlags(&c->upload, cudaStreamNonBlocking));
   HS_CUDA(cudaEventCreateWithFlags(&c->upload_done, cudaEventDisableTiming));
@@ -190,6 +191,7 @@ int hsdla_ctx_create(hsdla_ctx** out, void* stream) {
   HS_CUDA(cudaEventRecord(c->epoch, c->stream));
   HS_CUDA(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
   HS_CUDA(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
+  HS_CUDA(cudaEventCreateWithFlags(&c->join2, cudaEventDisableTiming));
   *out = c;
   return HSDLA_OK;
 }
@@ -205,7 +207,9 @@ int hsdla_ctx_destroy(hsdla_ctx* c) {
   cudaEventDestroy(c->stage_done);
   cudaEventDestroy(c->fork);
   cudaEventDestroy(c->join);
+  cudaEventDestroy(c->join2);
   cudaStreamDestroy(c->side);
+  cudaStreamDestroy(c->side2);
   cudaStreamSynchronize(c->copy);
   for (auto& sl : c->slots) {
     if (sl.panel_cnt) cudaFree(sl.panel_cnt);
@@ -808,10 +812,14 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     HS_CUDA(cudaEventRecord(ctx->b_up, ctx->h2d));
   }
   if (!reuse) {
+    // The T_AA forms + factor (side2) and the joint factor (side) are independent one-CTA-per-
+    // set kernels: they run side by side; the host's H-form decision waits for the joint one.
     HS_CUDA(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));
-    rc = launch_tprep(ctx, ctx->side, a->n_tsets, tdim_dev, mp, D2(a->t_aa), D2(a->t_ab),
+    HS_CUDA(cudaStreamWaitEvent(ctx->side2, ctx->fork, 0));
+    rc = launch_tprep(ctx, ctx->side2, a->n_tsets, tdim_dev, mp, D2(a->t_aa), D2(a->t_ab),
                       D2(a->t_bb), a->t_ld, forms, a->force_general_path ? 0 : 1, info_dev);
     if (rc) return rc;
+    HS_CUDA(cudaEventRecord(ctx->join2, ctx->side2));
     if (key.joint) {  // info also to the mapped host words [400, 496)
       // search mode: each set's smallest working shift (0 if HPD) to the mapped doubles
       rc = launch_tjoint(ctx->side, a->n_tsets, tdim_dev, tdim_dev + a->n_tsets, mp, D2(a->t_aa),
@@ -829,6 +837,7 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     ctx->tkey = key;
   } else {
     HS_CUDA(cudaEventRecord(ctx->join, ctx->stream));
+    HS_CUDA(cudaEventRecord(ctx->join2, ctx->stream));
   }
   // Sum planes (Re - Im, Re + Im) of A, UB, W1 (XY) and W2 (Z), and the per-type templates.
   const size_t pl_n = align_up(size_t(ld) * n * sizeof(double)) / sizeof(double);
@@ -889,6 +898,7 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
   };
   if (!Bs && !host_src && (rc = make_bs())) return rc;
   HS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join, 0));
+  HS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join2, 0));
   HS_CUDA(cudaEventRecord(ev[1], ctx->stream));
 
   // Column-panel ownership for sharded runs (balanced pairs j <-> nb-1-j).

@@ -137,7 +137,8 @@ struct hsdla_ctx {
   double joint_sigma = 0.0;      // common shift of the joint factors in tkey's workspace
   bool joint_pending = false;  // joint_info not read back yet (fresh T preparation in flight)
   cudaStream_t stream = nullptr;
-  cudaStream_t side = nullptr;  // T preparation overlaps A/B generation here
+  cudaStream_t side = nullptr;   // joint T factor, overlapping A/B generation
+  cudaStream_t side2 = nullptr;  // T_AA forms + factor, beside the joint factor
   cudaStream_t copy = nullptr;  // D2H of finished H / S, overlapped with later compute
   cudaEvent_t copy_go = nullptr;
   cudaStream_t upload = nullptr;  // descriptor H2D, ahead of the compute stream
@@ -173,7 +174,7 @@ struct hsdla_ctx {
     float ms[7] = {};
   };
   std::map<unsigned long long, Outcome> stash;
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr, join2 = nullptr;
   cudaEvent_t epoch = nullptr;  // recorded at creation (debug timelines)
   int device = 0;
   int num_sms = 148;

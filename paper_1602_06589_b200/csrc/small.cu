@@ -108,7 +108,6 @@ __host__ __device__ constexpr size_t chol_blocked_smem(int n) {
 // `checked`: the caller already rejected NaN input and zeroed the strict upper triangle.
 __device__ void chol_blocked(int n, double2* A, long long lda, int* info, bool checked = false) {
   extern __shared__ double2 P[];  // [rows][kNBS]
-  __shared__ double s_inv[kNB], s_ljj[kNB];
   __shared__ int s_bad;
   const int tid = threadIdx.x, nt = blockDim.x;
   const double2 zero = make_double2(0.0, 0.0);
@@ -136,36 +135,100 @@ __device__ void chol_blocked(int n, double2* A, long long lda, int* info, bool c
     }
     __syncthreads();
     HSDLA_PROF_POINT(2);
-    // unblocked right-looking factorization of the panel; column j stays unscaled in shared
-    // memory (scaled on write-back), updates use the scaled values on the fly
-    for (int j = 0; j < nb; ++j) {
-      const double d = P[j * kNBS + j].x;
-      if (!(d > 0.0) || !isfinite(d)) {  // uniform across the block
-        if (tid == 0) *info = k + j + 1;
+    // Panel factorization in steps of kSB columns: every thread factors the kSB x kSB
+    // diagonal block redundantly in registers (no barrier for the pivots), then (a) each row
+    // below it is solved against that factor (L_r = P_r L_D^-H, final values in place) and (b)
+    // the panel's remaining columns take the rank-kSB update; two barriers per step.
+    constexpr int kSB = 4;
+    for (int j0 = 0; j0 < nb; j0 += kSB) {
+      const int sb = min(kSB, nb - j0);
+      // registers only: fully unrolled loops over the kSB x kSB block, predicated on sb
+      double2 L[kSB][kSB];
+      double ld[kSB], li[kSB];
+      int bad = 0;
+#pragma unroll
+      for (int i = 0; i < kSB; ++i)
+#pragma unroll
+        for (int q = 0; q < kSB; ++q)
+          L[i][q] = (q <= i && i < sb) ? P[(j0 + i) * kNBS + j0 + q] : zero;
+#pragma unroll
+      for (int i = 0; i < kSB; ++i) {
+        double d = L[i][i].x;
+#pragma unroll
+        for (int q = 0; q < i; ++q) d -= L[i][q].x * L[i][q].x + L[i][q].y * L[i][q].y;
+        const bool ok = i >= sb || (d > 0.0 && isfinite(d));
+        if (!ok && !bad) bad = i + 1;
+        ld[i] = ok && i < sb ? sqrt(d) : 1.0;
+        li[i] = 1.0 / ld[i];
+#pragma unroll
+        for (int i2 = i + 1; i2 < kSB; ++i2) {
+          double2 v = L[i2][i];
+#pragma unroll
+          for (int q = 0; q < i; ++q) {  // v -= L[i2][q] conj(L[i][q])
+            v.x = fma(-L[i2][q].x, L[i][q].x, v.x);
+            v.x = fma(-L[i2][q].y, L[i][q].y, v.x);
+            v.y = fma(-L[i2][q].y, L[i][q].x, v.y);
+            v.y = fma(L[i2][q].x, L[i][q].y, v.y);
+          }
+          L[i2][i] = make_double2(v.x * li[i], v.y * li[i]);
+        }
+      }
+      if (bad) {  // uniform: every thread factored the same block
+        if (tid == 0) *info = k + j0 + bad;
         return;
       }
-      const double ljj = sqrt(d);
-      const double inv = 1.0 / ljj;
-      if (tid == 0) {
-        s_inv[j] = inv;
-        s_ljj[j] = ljj;
+      __syncthreads();  // every thread has read the diagonal block before rows are rewritten
+      // (a) rows of the diagonal block take L_D; rows below solve x L_D^H = P_r
+      for (int r = j0 + tid; r < rows; r += nt) {
+        double2 x[kSB];
+        if (r < j0 + sb) {  // a row of the diagonal block: its factor row
+          const int rr = r - j0;
+#pragma unroll
+          for (int i = 0; i < kSB; ++i) {
+            double2 v = zero;
+#pragma unroll
+            for (int q = 0; q < kSB; ++q)
+              if (q == rr) v = i < q ? L[q][i] : (i == q ? make_double2(ld[i], 0.0) : zero);
+            x[i] = v;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < kSB; ++i) {
+            double2 v = i < sb ? P[r * kNBS + j0 + i] : zero;
+#pragma unroll
+            for (int q = 0; q < i; ++q) {  // v -= x_q conj(L_D[i][q])
+              v.x = fma(-x[q].x, L[i][q].x, v.x);
+              v.x = fma(-x[q].y, L[i][q].y, v.x);
+              v.y = fma(-x[q].y, L[i][q].x, v.y);
+              v.y = fma(x[q].x, L[i][q].y, v.y);
+            }
+            x[i] = make_double2(v.x * li[i], v.y * li[i]);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < kSB; ++i)
+          if (i < sb) P[r * kNBS + j0 + i] = x[i];
       }
-      // thread (row slot ty, column slot tx): no integer division in the loop
-      const int tx = tid % kNB, ty = tid / kNB, c = j + 1 + tx;
+      __syncthreads();
+      // (b) P[r][c] -= sum_q L[r][j0+q] conj(L[c][j0+q]) for the panel's columns c >= j0 + sb
+      const int tx = tid % kNB, ty = tid / kNB, c = j0 + sb + tx;
       if (c < nb) {
-        const double2 b0 = P[c * kNBS + j];
-        const double2 b = make_double2(b0.x * inv, b0.y * inv);
-        const int S = nt / kNB;  // row slots (only rows r >= c are updated: the lower triangle)
-        int r = j + 1 + ty;
+        double2 lc[kSB];
+#pragma unroll
+        for (int q = 0; q < kSB; ++q) lc[q] = q < sb ? P[c * kNBS + j0 + q] : zero;
+        const int S = nt / kNB;
+        int r = j0 + sb + ty;
         if (r < c) r += (c - r + S - 1) / S * S;
         for (; r < rows; r += S) {
-          const double2 a0 = P[r * kNBS + j];
-          const double2 a = make_double2(a0.x * inv, a0.y * inv);
           double2 v = P[r * kNBS + c];
-          v.x = fma(-a.x, b.x, v.x);
-          v.x = fma(-a.y, b.y, v.x);
-          v.y = fma(-a.y, b.x, v.y);
-          v.y = fma(a.x, b.y, v.y);
+#pragma unroll
+          for (int q = 0; q < kSB; ++q) {
+            const double2 a = q < sb ? P[r * kNBS + j0 + q] : zero;
+            v.x = fma(-a.x, lc[q].x, v.x);
+            v.x = fma(-a.y, lc[q].y, v.x);
+            v.y = fma(-a.y, lc[q].x, v.y);
+            v.y = fma(a.x, lc[q].y, v.y);
+          }
           P[r * kNBS + c] = v;
         }
       }
@@ -174,64 +237,47 @@ __device__ void chol_blocked(int n, double2* A, long long lda, int* info, bool c
     HSDLA_PROF_POINT(3);
     for (int e = tid; e < rows * nb; e += nt) {
       const int r = e % rows, c = e / rows;
-      double2 v = zero;
-      if (r > c) {
-        v = P[r * kNBS + c];
-        v = make_double2(v.x * s_inv[c], v.y * s_inv[c]);
-        P[r * kNBS + c] = v;
-      } else if (r == c) {
-        v = make_double2(s_ljj[c], 0.0);
-      }
-      A[(k + r) + (long long)(k + c) * lda] = v;
+      A[(k + r) + (long long)(k + c) * lda] = r >= c ? P[r * kNBS + c] : zero;
     }
     __syncthreads();
     HSDLA_PROF_POINT(4);
-    // trailing lower triangle, rows / columns [k + nb, n): warp tasks of 64 rows x 8 columns,
-    // lane l on rows i0 + l and i0 + 32 + l (consecutive panel rows: conflict-free shared
-    // loads), the 8 column rows j0..j0+7 broadcast; only tasks touching i >= j run.
+    // trailing lower triangle, rows / columns [k + nb, n): warp tasks of 32 rows x 16 columns,
+    // lane l on row i0 + l (consecutive panel rows: conflict-free shared loads), the 16
+    // column rows j0..j0+15 broadcast; only tasks touching i >= j run (the diagonal-crossing
+    // ones mask their upper part).
     {
+      constexpr int TR = 32, TC = 16;
       const int tr = rows - nb;
-      const int nrb = (tr + 63) / 64, ncb = (tr + 7) / 8;
+      const int nrb = (tr + TR - 1) / TR, ncb = (tr + TC - 1) / TC;
       const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
       for (int task = wid; task < nrb * ncb; task += nw) {
         const int rb = task % nrb, cb = task / nrb;
-        const int i0 = 64 * rb, j0 = 8 * cb;  // trailing-relative
-        if (i0 + 63 < j0) continue;           // strictly upper: nothing to do
-        double2 acc[2][8];
+        const int i0 = TR * rb, j0 = TC * cb;  // trailing-relative
+        if (i0 + TR - 1 < j0) continue;       // strictly upper: nothing to do
+        double2 acc[TC];
 #pragma unroll
-        for (int a = 0; a < 2; ++a)
-#pragma unroll
-          for (int q = 0; q < 8; ++q) acc[a][q] = zero;
-        const int ia = nb + i0 + lane, ib = ia + 32;
+        for (int q = 0; q < TC; ++q) acc[q] = zero;
+        const int ia = nb + i0 + lane;
         for (int c = 0; c < nb; ++c) {
           const double2 la = ia < rows ? P[ia * kNBS + c] : zero;
-          const double2 lb = ib < rows ? P[ib * kNBS + c] : zero;
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
+          for (int q = 0; q < TC; ++q) {
             const int rj = nb + j0 + q;
             const double2 lj = rj < rows ? P[rj * kNBS + c] : zero;
-            // li conj(lj) as four FMAs per accumulator pair (no separate products + DADD)
-            acc[0][q].x = fma(la.x, lj.x, acc[0][q].x);
-            acc[0][q].x = fma(la.y, lj.y, acc[0][q].x);
-            acc[0][q].y = fma(la.y, lj.x, acc[0][q].y);
-            acc[0][q].y = fma(-la.x, lj.y, acc[0][q].y);
-            acc[1][q].x = fma(lb.x, lj.x, acc[1][q].x);
-            acc[1][q].x = fma(lb.y, lj.y, acc[1][q].x);
-            acc[1][q].y = fma(lb.y, lj.x, acc[1][q].y);
-            acc[1][q].y = fma(-lb.x, lj.y, acc[1][q].y);
+            acc[q].x = fma(la.x, lj.x, acc[q].x);
+            acc[q].x = fma(la.y, lj.y, acc[q].x);
+            acc[q].y = fma(la.y, lj.x, acc[q].y);
+            acc[q].y = fma(-la.x, lj.y, acc[q].y);
           }
         }
+        const int i = k + nb + i0 + lane;
 #pragma unroll
-        for (int a = 0; a < 2; ++a) {
-          const int i = k + nb + i0 + lane + 32 * a;
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int jj = k + nb + j0 + q;
-            if (i < n && jj < n && jj <= i) {
-              double2* x = A + i + (long long)jj * lda;
-              const double2 v = *x;
-              *x = make_double2(v.x - acc[a][q].x, v.y - acc[a][q].y);
-            }
+        for (int q = 0; q < TC; ++q) {
+          const int jj = k + nb + j0 + q;
+          if (i < n && jj < n && jj <= i) {
+            double2* x = A + i + (long long)jj * lda;
+            const double2 v = *x;
+            *x = make_double2(v.x - acc[q].x, v.y - acc[q].y);
           }
         }
       }
@@ -251,7 +297,7 @@ __device__ void chol_blocked(int n, double2* A, long long lda, int* info, bool c
 // (n <= kBlockedMaxN), else the column algorithm (chol_block).
 constexpr int kBlockedMaxN = 768;
 
-__global__ void potrf_batched_kernel(int n, const double2* T, long long ldt, long long st,
+__global__ void __launch_bounds__(512) potrf_batched_kernel(int n, const double2* T, long long ldt, long long st,
                                      double2* F, long long ldf, long long sf, int* info) {
   const int b = blockIdx.x;
   if (n <= kBlockedMaxN) {
@@ -271,7 +317,7 @@ constexpr int kPotrfMaxDynSmem = 227 * 1024;  // opt-in limit per CTA (static sm
 
 // Per T set: forms[0] = T_AB, forms[1] = 1/2 full(T_BB), forms[2] = full(T_AA),
 // forms[3] = Cholesky factor of tril(T_AA) (if do_chol), all m x m with ld mp.
-__global__ void tprep_kernel(const int* tdim, int mp, const double2* taa, const double2* tab,
+__global__ void __launch_bounds__(512) tprep_kernel(const int* tdim, int mp, const double2* taa, const double2* tab,
                              const double2* tbb, long long t_ld, double2* forms, int do_chol,
                              int* info) {
   const int b = blockIdx.x;
@@ -319,7 +365,7 @@ __global__ void tprep_kernel(const int* tdim, int mp, const double2* taa, const 
 // assembled lower triangle (ld 2*mp); info as chol_block (0 = HPD); without the split L11
 // equals the T_AA factor of tprep_kernel bit for bit.  info_host / split_host (mapped) may be
 // null.
-__global__ void tjoint_kernel(const int* tdim, const int* tdense, int mp, const double2* taa,
+__global__ void __launch_bounds__(512) tjoint_kernel(const int* tdim, const int* tdense, int mp, const double2* taa,
                               const double2* tab, const double2* tbb, long long t_ld,
                               double2* joint, int* info, int* info_host, int* split_host,
                               const double* u2, double sigma_fixed, double* sigma_host) {

@@ -6,6 +6,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace hsdla {
@@ -105,36 +107,22 @@ __host__ __device__ constexpr size_t chol_blocked_smem(int n) {
   return size_t(n > 0 ? n : 1) * kNBS * sizeof(double2);
 }
 
-// `checked`: the caller already rejected NaN input and zeroed the strict upper triangle.
-__device__ void chol_blocked(int n, double2* A, long long lda, int* info, bool checked = false) {
-  extern __shared__ double2 P[];  // [rows][kNBS]
-  __shared__ int s_bad;
+// Staging of the current panel (rows k..n, columns k..k+nb) into P, lower part only.
+__device__ __forceinline__ void chol_stage_panel(int k, int nb, int rows, const double2* A,
+                                                 long long lda, double2* P) {
+  const double2 zero = make_double2(0.0, 0.0);
+  for (int e = threadIdx.x; e < rows * nb; e += blockDim.x) {
+    const int r = e % rows, c = e / rows;
+    P[r * kNBS + c] = r >= c ? A[(k + r) + (long long)(k + c) * lda] : zero;
+  }
+}
+
+// Factor the staged panel in place in P (final, scaled L values) and write it back to A
+// (zeros above the diagonal block's diagonal).  Returns 0, or the 1-based matrix index of the
+// first pivot that is not positive and finite (uniform across the block).
+__device__ int chol_factor_panel(int k, int nb, int rows, double2* A, long long lda, double2* P) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const double2 zero = make_double2(0.0, 0.0);
-  if (!checked) {
-    if (tid == 0) s_bad = 0;
-    __syncthreads();
-    FOR_SQUARE(n, r, c) {
-      if (r >= c) {
-        const double2 v = A[r + c * lda];
-        if (isnan(v.x) || isnan(v.y)) s_bad = 1;
-      }
-    }
-    __syncthreads();
-    if (s_bad) {
-      if (tid == 0) *info = -1;
-      return;
-    }
-  }
-  HSDLA_PROF_POINT(1);
-  for (int k = 0; k < n; k += kNB) {
-    const int nb = min(kNB, n - k), rows = n - k;
-    for (int e = tid; e < rows * nb; e += nt) {
-      const int r = e % rows, c = e / rows;
-      P[r * kNBS + c] = r >= c ? A[(k + r) + (long long)(k + c) * lda] : zero;
-    }
-    __syncthreads();
-    HSDLA_PROF_POINT(2);
     // Panel factorization in steps of kSB columns: every thread factors the kSB x kSB
     // diagonal block redundantly in registers (no barrier for the pivots), then (a) each row
     // below it is solved against that factor (L_r = P_r L_D^-H, final values in place) and (b)
@@ -173,10 +161,7 @@ __device__ void chol_blocked(int n, double2* A, long long lda, int* info, bool c
           L[i2][i] = make_double2(v.x * li[i], v.y * li[i]);
         }
       }
-      if (bad) {  // uniform: every thread factored the same block
-        if (tid == 0) *info = k + j0 + bad;
-        return;
-      }
+      if (bad) return k + j0 + bad;  // uniform: every thread factored the same block
       __syncthreads();  // every thread has read the diagonal block before rows are rewritten
       // (a) rows of the diagonal block take L_D; rows below solve x L_D^H = P_r
       for (int r = j0 + tid; r < rows; r += nt) {
@@ -234,13 +219,20 @@ __device__ void chol_blocked(int n, double2* A, long long lda, int* info, bool c
       }
       __syncthreads();
     }
-    HSDLA_PROF_POINT(3);
     for (int e = tid; e < rows * nb; e += nt) {
       const int r = e % rows, c = e / rows;
       A[(k + r) + (long long)(k + c) * lda] = r >= c ? P[r * kNBS + c] : zero;
     }
     __syncthreads();
-    HSDLA_PROF_POINT(4);
+    return 0;
+}
+
+// Trailing update A22 -= L21 L21^H after the panel at k (L21 = P rows nb..rows), warp tasks
+// task0, task0 + task_step, ... of the 32 x 16 task grid.
+__device__ void chol_trailing(int k, int nb, int rows, int n, double2* A, long long lda,
+                              const double2* P, int task0, int task_step) {
+  const double2 zero = make_double2(0.0, 0.0);
+  const int tid = threadIdx.x;
     // trailing lower triangle, rows / columns [k + nb, n): warp tasks of 32 rows x 16 columns,
     // lane l on row i0 + l (consecutive panel rows: conflict-free shared loads), the 16
     // column rows j0..j0+15 broadcast; only tasks touching i >= j run (the diagonal-crossing
@@ -249,8 +241,8 @@ __device__ void chol_blocked(int n, double2* A, long long lda, int* info, bool c
       constexpr int TR = 32, TC = 16;
       const int tr = rows - nb;
       const int nrb = (tr + TR - 1) / TR, ncb = (tr + TC - 1) / TC;
-      const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
-      for (int task = wid; task < nrb * ncb; task += nw) {
+      const int lane = tid & 31;
+      for (int task = task0; task < nrb * ncb; task += task_step) {
         const int rb = task % nrb, cb = task / nrb;
         const int i0 = TR * rb, j0 = TC * cb;  // trailing-relative
         if (i0 + TR - 1 < j0) continue;       // strictly upper: nothing to do
@@ -282,6 +274,42 @@ __device__ void chol_blocked(int n, double2* A, long long lda, int* info, bool c
         }
       }
     }
+}
+
+// `checked`: the caller already rejected NaN input and zeroed the strict upper triangle.
+__device__ void chol_blocked(int n, double2* A, long long lda, int* info, bool checked = false) {
+  extern __shared__ double2 P[];  // [rows][kNBS]
+  __shared__ int s_bad;
+  const int tid = threadIdx.x;
+  const double2 zero = make_double2(0.0, 0.0);
+  if (!checked) {
+    if (tid == 0) s_bad = 0;
+    __syncthreads();
+    FOR_SQUARE(n, r, c) {
+      if (r >= c) {
+        const double2 v = A[r + c * lda];
+        if (isnan(v.x) || isnan(v.y)) s_bad = 1;
+      }
+    }
+    __syncthreads();
+    if (s_bad) {
+      if (tid == 0) *info = -1;
+      return;
+    }
+  }
+  HSDLA_PROF_POINT(1);
+  for (int k = 0; k < n; k += kNB) {
+    const int nb = min(kNB, n - k), rows = n - k;
+    chol_stage_panel(k, nb, rows, A, lda, P);
+    __syncthreads();
+    HSDLA_PROF_POINT(2);
+    const int bad = chol_factor_panel(k, nb, rows, A, lda, P);
+    if (bad) {
+      if (tid == 0) *info = bad;
+      return;
+    }
+    HSDLA_PROF_POINT(4);
+    chol_trailing(k, nb, rows, n, A, lda, P, tid >> 5, blockDim.x >> 5);
     __syncthreads();
     HSDLA_PROF_POINT(5);
   }
@@ -291,6 +319,60 @@ __device__ void chol_blocked(int n, double2* A, long long lda, int* info, bool c
     }
   }
   if (tid == 0) *info = 0;
+}
+
+// Cluster version (one thread-block cluster of kCS CTAs per matrix): rank 0 stages and factors
+// each panel; after a cluster barrier every rank copies the factored panel from global memory
+// (L2) into its own shared memory and takes a 1/kCS share of the trailing update's warp tasks;
+// a second barrier closes the step.  The input must be checked (no NaN, zero strict upper).
+// `info` is written by rank 0; every rank returns together.
+constexpr int kCS = 8;
+// The cluster versions pay off from about this order on (the panel factorisation on rank 0
+// stays the critical path; measured: 2m = 242 401 vs 546 us, 2m = 162 245 vs 242 us).
+constexpr int kClusterMinN = 192;
+// HSDLA_TPREP_CLUSTER=0: one CTA per T set for the T preparation kernels.
+inline bool tprep_cluster() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("HSDLA_TPREP_CLUSTER");
+    m = (e && e[0] == '0') ? 0 : 1;
+  }
+  return m == 1;
+}
+
+__device__ void chol_blocked_cluster(int n, double2* A, long long lda, int* info) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ double2 P[];
+  __shared__ int s_bad;
+  const int tid = threadIdx.x;
+  const int rank = (int)cl.block_rank(), ncl = (int)cl.num_blocks();
+  const int* bad0 = cl.map_shared_rank(&s_bad, 0);
+  for (int k = 0; k < n; k += kNB) {
+    const int nb = min(kNB, n - k), rows = n - k;
+    if (rank == 0) {
+      chol_stage_panel(k, nb, rows, A, lda, P);
+      __syncthreads();
+      const int bad = chol_factor_panel(k, nb, rows, A, lda, P);
+      if (tid == 0) s_bad = bad;
+      __threadfence();
+    }
+    cl.sync();
+    const int bad = *bad0;
+    if (bad) {
+      if (rank == 0 && tid == 0) *info = bad;
+      return;
+    }
+    if (rank != 0) {
+      chol_stage_panel(k, nb, rows, A, lda, P);
+      __syncthreads();
+    }
+    const int nw = blockDim.x >> 5;
+    chol_trailing(k, nb, rows, n, A, lda, P, rank * nw + (tid >> 5), nw * ncl);
+    __threadfence();
+    cl.sync();
+  }
+  if (rank == 0 && tid == 0) *info = 0;
 }
 
 // Cholesky of tril(T) into F: blocked in place on a copy when its panel fits in shared memory
@@ -317,10 +399,17 @@ constexpr int kPotrfMaxDynSmem = 227 * 1024;  // opt-in limit per CTA (static sm
 
 // Per T set: forms[0] = T_AB, forms[1] = 1/2 full(T_BB), forms[2] = full(T_AA),
 // forms[3] = Cholesky factor of tril(T_AA) (if do_chol), all m x m with ld mp.
+// CL: one cluster of kCS CTAs per T set (launched with the cluster dimension), the copies
+// split across the ranks and the factor by chol_blocked_cluster; else one CTA per set.
+template <bool CL>
 __global__ void __launch_bounds__(512) tprep_kernel(const int* tdim, int mp, const double2* taa, const double2* tab,
                              const double2* tbb, long long t_ld, double2* forms, int do_chol,
                              int* info) {
-  const int b = blockIdx.x;
+  namespace cg = cooperative_groups;
+  const int b = CL ? blockIdx.x / kCS : blockIdx.x;
+  const int rank = CL ? (int)cg::this_cluster().block_rank() : 0;
+  const int nrk = CL ? kCS : 1;
+  const int c0 = rank * (blockDim.x >> 5) + (threadIdx.x >> 5), cs = nrk * (blockDim.x >> 5);
   const int m = tdim[b];
   const long long tstride = t_ld * t_ld;
   const double2* Taa = taa + b * tstride;
@@ -328,7 +417,9 @@ __global__ void __launch_bounds__(512) tprep_kernel(const int* tdim, int mp, con
   const double2* Tbb = tbb + b * tstride;
   double2* f = forms + (long long)b * 4 * mp * mp;
   const long long fs = (long long)mp * mp;
-  FOR_SQUARE(m, r, c) {
+  // columns split over the cluster's warps (rows by lanes)
+  for (int c = c0; c < m; c += cs)
+  for (int r = threadIdx.x & 31; r < m; r += 32) {
     f[r + (long long)c * mp] = Tab[r + c * t_ld];
     double2 bb, aa;
     if (r > c) { bb = Tbb[r + c * t_ld]; aa = Taa[r + c * t_ld]; }
@@ -339,14 +430,36 @@ __global__ void __launch_bounds__(512) tprep_kernel(const int* tdim, int mp, con
   }
   __syncthreads();
   if (!do_chol) {
-    if (threadIdx.x == 0) info[b] = -2;
-  } else {  // blocked, in place on tril(T_AA) copied into forms[3]
+    if (threadIdx.x == 0 && rank == 0) info[b] = -2;
+  } else if (!CL) {  // blocked, in place on tril(T_AA) copied into forms[3]
     double2* F = f + 3 * fs;
     FOR_SQUARE(m, r, c) {
       F[r + (long long)c * mp] = r >= c ? Taa[r + c * t_ld] : make_double2(0.0, 0.0);
     }
     __syncthreads();
     chol_blocked(m, F, mp, info + b);
+  } else {
+    cg::cluster_group cl = cg::this_cluster();
+    __shared__ int s_nan;
+    if (threadIdx.x == 0) s_nan = 0;
+    cl.sync();
+    int* nan0 = cl.map_shared_rank(&s_nan, 0);
+    double2* F = f + 3 * fs;
+    bool nan = false;
+    for (int c = c0; c < m; c += cs)
+      for (int r = threadIdx.x & 31; r < m; r += 32) {
+        const double2 v = r >= c ? Taa[r + c * t_ld] : make_double2(0.0, 0.0);
+        nan = nan || isnan(v.x) || isnan(v.y);
+        F[r + (long long)c * mp] = v;
+      }
+    if (nan) atomicOr(nan0, 1);
+    __threadfence();
+    cl.sync();
+    if (*nan0) {
+      if (rank == 0 && threadIdx.x == 0) info[b] = -1;
+    } else {
+      chol_blocked_cluster(m, F, mp, info + b);
+    }
   }
 }
 
@@ -365,14 +478,21 @@ __global__ void __launch_bounds__(512) tprep_kernel(const int* tdim, int mp, con
 // assembled lower triangle (ld 2*mp); info as chol_block (0 = HPD); without the split L11
 // equals the T_AA factor of tprep_kernel bit for bit.  info_host / split_host (mapped) may be
 // null.
+template <bool CL>
 __global__ void __launch_bounds__(512) tjoint_kernel(const int* tdim, const int* tdense, int mp, const double2* taa,
                               const double2* tab, const double2* tbb, long long t_ld,
                               double2* joint, int* info, int* info_host, int* split_host,
                               const double* u2, double sigma_fixed, double* sigma_host) {
+  namespace cg = cooperative_groups;
   __shared__ int s_off, s_tail_bad;
   __shared__ double s_scale, s_rho;
   HSDLA_PROF_START();
-  const int b = blockIdx.x;
+  // CL: a cluster of kCS CTAs per T set: the assembly's columns and the factorisation's trailing
+  // updates are split over the ranks (chol_blocked_cluster); rank 0 owns the decisions and the
+  // outputs, the other ranks reduce their flags and row sums into its shared memory.
+  const int b = CL ? blockIdx.x / kCS : blockIdx.x;
+  const int rank = CL ? (int)cg::this_cluster().block_rank() : 0;
+  const int nrk = CL ? kCS : 1;
   const int m = tdim[b];
   const int d = tdense ? min(max(tdense[b], 0), m) : m;
   const long long lj = 2LL * mp;
@@ -401,12 +521,14 @@ __global__ void __launch_bounds__(512) tjoint_kernel(const int* tdim, const int*
   // rows of a column: coalesced), row sums accumulate in shared memory.
   __shared__ double s_row[2 * (HSDLA_MAX_LSPH + 1) * (HSDLA_MAX_LSPH + 1)];
   const bool want_rho = sigma_host && sigma_fixed < 0.0;
-  bool rho_in_assembly = false;  // set below: without the split the assembly pass sums the rows
+  const bool split_cand = tdense && min(max(tdense[b], 0), m) < m;
+  // without a split candidate the assembly pass sums the rows; else a separate pass (rank 0)
+  const bool rho_in_assembly = want_rho && !split_cand;
   if (want_rho) {
     for (int r = threadIdx.x; r < 2 * m; r += blockDim.x) s_row[r] = 0.0;
     __syncthreads();
   }
-  if (want_rho && tdense && min(max(tdense[b], 0), m) < m) {  // split candidate: separate pass
+  if (want_rho && split_cand && rank == 0) {
     const int n2 = 2 * m;
     FOR_SQUARE(n2, r, c) {
       double2 v;
@@ -422,8 +544,6 @@ __global__ void __launch_bounds__(512) tjoint_kernel(const int* tdim, const int*
     for (int r = threadIdx.x; r < n2; r += blockDim.x)
       atomicMax(reinterpret_cast<unsigned long long*>(&s_rho), __double_as_longlong(s_row[r]));
     __syncthreads();
-  } else {
-    rho_in_assembly = want_rho;
   }
   HSDLA_PROF_POINT(7);
   bool split = d < m;
@@ -446,7 +566,7 @@ __global__ void __launch_bounds__(512) tjoint_kernel(const int* tdim, const int*
   // the set may shift, T + sigma D for sigma = scale * 2^(k - 12), k = 0, 1, ... (the first that
   // is HPD, i.e. within 2x of the smallest such shift).
   if (sigma_fixed > 0.0 && !can_shift) {  // a common shift cannot apply to this set
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && rank == 0) {
       info[b] = -3;
       if (info_host) info_host[b] = -3;
       if (split_host) split_host[b] = 0;
@@ -456,12 +576,21 @@ __global__ void __launch_bounds__(512) tjoint_kernel(const int* tdim, const int*
   }
   double sigma = sigma_fixed >= 0.0 ? sigma_fixed : 0.0;
   const int attempts = (sigma_fixed < 0.0 && can_shift) ? 40 : 1;
+  int* flag0 = &s_tail_bad;  // rank 0's flag (the cluster's)
+  double* row0 = s_row;      // rank 0's row sums
+  if constexpr (CL) {
+    flag0 = cg::this_cluster().map_shared_rank(&s_tail_bad, 0);
+    row0 = cg::this_cluster().map_shared_rank(s_row, 0);
+  }
   for (int att = 0; att < attempts; ++att) {
     if (att > 0) sigma = s_scale * ldexp(1.0, att - 13);
     if (threadIdx.x == 0) s_tail_bad = 0;  // also the NaN flag of the assembly below
-    __syncthreads();
-    // (rows by lanes with whole-warp iterations: the row-sum reduction below shuffles)
-    for (int c = threadIdx.x >> 5; c < n; c += blockDim.x >> 5)
+    if constexpr (CL) cg::this_cluster().sync();
+    else __syncthreads();
+    // (rows by lanes with whole-warp iterations: the row-sum reduction below shuffles; columns
+    // split over the cluster's ranks)
+    bool nan = false;
+    for (int c = rank * (blockDim.x >> 5) + (threadIdx.x >> 5); c < n; c += nrk * (blockDim.x >> 5))
     for (int r0 = 0; r0 < n; r0 += 32) {
       const int r = r0 + (threadIdx.x & 31);
       double2 v = make_double2(0.0, 0.0);
@@ -470,7 +599,7 @@ __global__ void __launch_bounds__(512) tjoint_kernel(const int* tdim, const int*
         if (r < h) v = Taa[r + c * t_ld];
         else if (c < h) v = cconj(Tab[c + (r - h) * t_ld]);
         else v = Tbb[(r - h) + (c - h) * t_ld];
-        if (isnan(v.x) || isnan(v.y)) s_tail_bad = 1;
+        nan = nan || isnan(v.x) || isnan(v.y);
         if (r == c) v.y = 0.0;
         av = sqrt(v.x * v.x + v.y * v.y);
         if (r == c && sigma != 0.0) v.x += sigma * (r < h ? 1.0 : U2[r - h]);
@@ -483,23 +612,37 @@ __global__ void __launch_bounds__(512) tjoint_kernel(const int* tdim, const int*
       }
       if (r < n) J[r + c * lj] = v;
     }
-    __syncthreads();
-    if (rho_in_assembly && att == 0) {
+    if (nan) atomicOr(flag0, 1);
+    if constexpr (CL) {  // the other ranks' partial row sums into rank 0's (one add per row)
+      if (rho_in_assembly && att == 0 && rank != 0) {
+        __syncthreads();
+        for (int r = threadIdx.x; r < n; r += blockDim.x)
+          if (s_row[r] != 0.0) atomicAdd(row0 + r, s_row[r]);
+      }
+    }
+    __threadfence();
+    if constexpr (CL) cg::this_cluster().sync();
+    else __syncthreads();
+    if (rho_in_assembly && att == 0 && rank == 0) {
       for (int r = threadIdx.x; r < n; r += blockDim.x)
         atomicMax(reinterpret_cast<unsigned long long*>(&s_rho), __double_as_longlong(s_row[r]));
       __syncthreads();
     }
     HSDLA_PROF_POINT(8);
-    if (s_tail_bad) {
-      if (threadIdx.x == 0) info[b] = -1;
+    if (*flag0) {
+      if (threadIdx.x == 0 && rank == 0) info[b] = -1;
+    } else if constexpr (CL) {
+      chol_blocked_cluster(n, J, lj, info + b);  // in place; shared memory sized for 2*mp rows
     } else {
-      chol_blocked(n, J, lj, info + b, true);  // in place; shared memory sized for 2*mp rows
+      chol_blocked(n, J, lj, info + b, true);
     }
+    __threadfence();
+    if constexpr (CL) cg::this_cluster().sync();  // every rank sees info[b]
     __syncthreads();
     if (threadIdx.x == 0) s_tail_bad = 0;
     __syncthreads();
     HSDLA_PROF_POINT(6);
-    if (split && info[b] == 0) {
+    if (split && info[b] == 0 && rank == 0) {
       for (int i = d + threadIdx.x; i < m; i += blockDim.x) {
         const double a = Taa[i + i * t_ld].x + sigma, c = Tbb[i + i * t_ld].x + (sigma != 0.0 ? sigma * U2[i] : 0.0);
         const double2 ab = Tab[i + i * t_ld];
@@ -515,10 +658,12 @@ __global__ void __launch_bounds__(512) tjoint_kernel(const int* tdim, const int*
       __syncthreads();
       if (threadIdx.x == 0 && s_tail_bad) info[b] = n + 1;  // a tail block is not HPD
     }
+    __threadfence();
+    if constexpr (CL) cg::this_cluster().sync();
     __syncthreads();
     if (info[b] == 0 || info[b] == -1) break;  // HPD, or NaN input (no shift helps)
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && rank == 0) {
     if (info_host) info_host[b] = info[b];
     if (split_host) split_host[b] = split ? 1 : 0;
     if (sigma_host) sigma_host[b] = info[b] == 0 ? sigma : -1.0;
@@ -642,8 +787,25 @@ int launch_tprep(hsdla_ctx* ctx, cudaStream_t stream, int n_tsets, const int* td
                  double2* forms, int do_chol, int* info_dev) {
   if (n_tsets <= 0) return HSDLA_OK;
   const size_t smem = chol_blocked_smem(mp);  // limit set once per device in preload_small()
-  tprep_kernel<<<n_tsets, 512, smem, stream>>>(tdim_dev, mp, taa, tab, tbb, t_ld, forms, do_chol,
-                                               info_dev);
+  if (tprep_cluster() && mp >= kClusterMinN) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kCS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(n_tsets * kCS);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    HS_CUDA(cudaLaunchKernelEx(&cfg, tprep_kernel<true>, tdim_dev, mp, taa, tab, tbb, t_ld, forms,
+                               do_chol, info_dev));
+    return HSDLA_OK;
+  }
+  tprep_kernel<false><<<n_tsets, 512, smem, stream>>>(tdim_dev, mp, taa, tab, tbb, t_ld, forms,
+                                                      do_chol, info_dev);
   HS_CHECK_LAUNCH();
   return HSDLA_OK;
 }
@@ -655,9 +817,28 @@ int launch_tjoint(cudaStream_t stream, int n_tsets, const int* tdim_dev, const i
                   double* sigma_host_dev) {
   if (n_tsets <= 0) return HSDLA_OK;
   const size_t smem = chol_blocked_smem(2 * mp);
-  tjoint_kernel<<<n_tsets, 512, smem, stream>>>(tdim_dev, tdense_dev, mp, taa, tab, tbb, t_ld,
-                                                joint, info_dev, info_host_dev, split_host_dev,
-                                                u2_dev, sigma_fixed, sigma_host_dev);
+  if (tprep_cluster() && 2 * mp >= kClusterMinN) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kCS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(n_tsets * kCS);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    HS_CUDA(cudaLaunchKernelEx(&cfg, tjoint_kernel<true>, tdim_dev, tdense_dev, mp, taa, tab, tbb,
+                               t_ld, joint, info_dev, info_host_dev, split_host_dev, u2_dev,
+                               sigma_fixed, sigma_host_dev));
+    return HSDLA_OK;
+  }
+  tjoint_kernel<false><<<n_tsets, 512, smem, stream>>>(tdim_dev, tdense_dev, mp, taa, tab, tbb,
+                                                       t_ld, joint, info_dev, info_host_dev,
+                                                       split_host_dev, u2_dev, sigma_fixed,
+                                                       sigma_host_dev);
   HS_CHECK_LAUNCH();
   return HSDLA_OK;
 }
@@ -754,11 +935,12 @@ int launch_zero_rows(hsdla_ctx* ctx, double2* base, long long ld, int row0, int 
 }
 
 int preload_small() {
-  const void* fns[] = {(const void*)potrf_batched_kernel, (const void*)tprep_kernel,
+  const void* fns[] = {(const void*)potrf_batched_kernel, (const void*)tprep_kernel<false>,
+                       (const void*)tprep_kernel<true>, (const void*)tjoint_kernel<true>,
                        (const void*)mirror_kernel, (const void*)scale_rows_kernel,
                        (const void*)prep_kernel, (const void*)publish_kernel,
                        (const void*)zero_rows_kernel, (const void*)finite_kernel,
-                       (const void*)tjoint_kernel, (const void*)ttail_kernel,
+                       (const void*)tjoint_kernel<false>, (const void*)ttail_kernel,
                        (const void*)axpy_shift_kernel};
   for (const void* f : fns) {
     cudaFuncAttributes at;
@@ -770,7 +952,8 @@ int preload_small() {
     HS_CUDA(cudaFuncSetAttribute(potrf_batched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kPotrfMaxDynSmem - (int)at.sharedSizeBytes));
   }
-  for (const void* f : {(const void*)tjoint_kernel, (const void*)tprep_kernel})
+  for (const void* f : {(const void*)tjoint_kernel<false>, (const void*)tprep_kernel<false>,
+                        (const void*)tjoint_kernel<true>, (const void*)tprep_kernel<true>})
     if (first_on_device(f)) {
       cudaFuncAttributes at;
       HS_CUDA(cudaFuncGetAttributes(&at, f));

@@ -59,6 +59,11 @@ int main(int argc, char** argv) {
     cudaMemcpyFromSymbol(z, g_prof, sizeof(z));
     int inf = 0;
     cudaMemcpy(&inf, info, 4, cudaMemcpyDeviceToHost);
+    std::vector<double2> Jh(4 * m * m);
+    cudaMemcpy(Jh.data(), J, 4 * m * m * 16, cudaMemcpyDeviceToHost);
+    double cks = 0.0;
+    for (size_t q = 0; q < Jh.size(); ++q) cks += Jh[q].x * (1.0 + 1e-3 * (q % 97)) - Jh[q].y * (1.0 + 1e-3 * (q % 89));
+    printf("checksum %.17g ", cks);
     printf("m=%d n=%d: %.1f us info %d | cycles: gersh+split %lld, assemble %lld, nan %lld, stage %lld, panel %lld, writeback %lld, trailing %lld, zero+rest %lld\n",
            m, 2 * m, ms * 1e3, inf, z[7], z[8], z[1], z[2], z[3], z[4], z[5], z[6]);
   }

@@ -234,3 +234,51 @@ def test_template_path_off_for_short_t(pkg):
     h_o, s_o, _, _ = ob.build_all(a, b, norms, list(np.diff(offs)), [t.array for t in tm.t_aa],
                                   [t.array for t in tm.t_ab], [t.array for t in tm.t_bb])
     assert rel_fro(h_t.cpu().numpy().T, h_o) <= TOL and rel_fro(s_t.cpu().numpy().T, s_o) <= TOL
+
+
+def test_template_path_mixed_l_types(pkg):
+    """Types with different l_sph (block heights 25 and 49) and a lone atom of a third type: the
+    template generator runs per l group, the expansion per atom height; vs the oracle, and a
+    batch k-point reusing the T preparation (B not rewritten) equals the first bitwise."""
+    from paper_1602_06589_b200 import configs
+    from paper_1602_06589_b200.pipeline import DeviceSpec, HSPipeline, pack_tmats
+
+    base = configs.make_instance("C1").spec
+    rng = np.random.default_rng(17)
+    l_sph = np.array([4, 4, 6, 6, 2])
+    n_at = len(l_sph)
+    pos = rng.uniform(0, 8.0, (n_at, 3))
+    rad = []
+    for l in (4, 6, 2):
+        n = l + 1
+        rad.append(pkg.RadialBoundaryData(u=rng.uniform(0.1, 1, n), u_prime=rng.uniform(0.1, 1, n),
+                                          udot=rng.uniform(0.1, 1, n), udot_prime=rng.uniform(0.1, 1, n),
+                                          energy=np.zeros(n), udot_norm=np.sqrt(rng.uniform(0.01, 0.1, n))))
+    radial = [rad[0], rad[0], rad[1], rad[1], rad[2]]
+    spec = pkg.SystemSpec(positions=pos, rotations=np.tile(np.eye(3), (n_at, 1, 1)),
+                          mt_radius=np.array([2.0, 2.0, 2.2, 2.2, 1.8]), l_sph=l_sph, l_nonsph=l_sph,
+                          k_point=base.k_point, k_vectors=base.k_vectors, omega=base.omega,
+                          radial=radial)
+    cd = pkg.ComplexDense.from_array
+    ts = {}
+    for l in (4, 6, 2):
+        m = (l + 1) ** 2
+        ts[l] = tuple(cd(x) for x in (_hermitian(rng, m, 2.0), rand_complex(rng, m, m) / m,
+                                      _hermitian(rng, m, 2.0)))
+    tm = pkg.TMatrixSet([ts[l][0] for l in l_sph], [ts[l][1] for l in l_sph],
+                        [ts[l][2] for l in l_sph], list(l_sph), list(l_sph))
+    dspec = DeviceSpec(spec)
+    pipe = HSPipeline(spec.n_basis, dspec.heights)
+    tp = pack_tmats(tm)
+    res = pipe.run(dspec, tp)
+    assert res["template_types"] == 3 and all(res["joint_t"])
+    h_t, s_t = pipe.result_views()
+    h, s = h_t.cpu().numpy().T, s_t.cpu().numpy().T
+    a, b, norms, offs = of.compute_ab(spec)
+    h_o, s_o, _, _ = ob.build_all(a, b, norms, list(np.diff(offs)), [t.array for t in tm.t_aa],
+                                  [t.array for t in tm.t_ab], [t.array for t in tm.t_bb])
+    assert rel_fro(h, h_o) <= TOL and rel_fro(s, s_o) <= TOL
+    pipe.run(dspec, tp)
+    h2_t, s2_t = pipe.result_views()
+    np.testing.assert_array_equal(h2_t.cpu().numpy().T, h)
+    np.testing.assert_array_equal(s2_t.cpu().numpy().T, s)

@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--no-extras", action="store_true",
                    help="skip the BASELINE scaling configs (C5 k-point batch, C3 panels) "
                         "reported as extra keys of the line")
+    p.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                   help=argparse.SUPPRESS)  # gloo: multi-rank flow check, ranks may share a GPU
     p.add_argument("--dry-run", action="store_true",
                    help="launcher check without a GPU: spawn the ranks (gloo), deal the "
                         "work, print one JSON line; no compute")
@@ -568,6 +570,14 @@ def measure_panels(config, steps, warmup, rank, world, transport="nccl"):
     return out, sb, dspec, tpack, flops_step
 
 
+def gpu_of(local, args):
+    """Device of a local rank: its own GPU; with --backend gloo ranks may share GPUs (the
+    multi-rank flow check on a one-GPU box)."""
+    import torch
+
+    return local % torch.cuda.device_count() if args.backend == "gloo" else local
+
+
 def run_ours(args):
     import torch
 
@@ -576,8 +586,8 @@ def run_ours(args):
                                                 pack_tmats)
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    init_dist(world, local)
+    torch.cuda.set_device(gpu_of(local, args))
+    init_dist(world, gpu_of(local, args), args.backend)
     inst = configs.make_instance(args.config)
     specs = kpoint_specs(inst, rank, world)
     spec = specs[0]
@@ -776,8 +786,8 @@ def run_panels(args):
     from paper_1602_06589_b200.pipeline import DeviceSpec
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    init_dist(world, local)
+    torch.cuda.set_device(gpu_of(local, args))
+    init_dist(world, gpu_of(local, args), args.backend)
     out, sb, dspec, tpack, flops_step = measure_panels(args.config, args.steps, args.warmup,
                                                        rank, world, args.panel_transport)
     # e2e: spec upload + sharded build + full H, S read back to pinned host on rank 0
@@ -855,7 +865,7 @@ def spawn_ranks(args) -> int:
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
-    if not args.dry_run:
+    if not args.dry_run and args.backend != "gloo":
         import torch
 
         have = torch.cuda.device_count()

@@ -51,17 +51,25 @@ def gather_panels(mat, n: int, world: int, rank: int, dst: int = 0, group=None):
     import torch.distributed as dist
 
     nb = (n + PANEL - 1) // PANEL
-    ops = []
+    # gloo moves host memory only: device panels are staged through host copies (the NCCL
+    # path on the GPU box sends device memory directly)
+    staged = mat.is_cuda and dist.get_backend(group) == "gloo"
+    ops, back = [], []
     for j in range(nb):
         owner = panel_owner(nb, world, j)
         sl = mat[j * PANEL:min(n, (j + 1) * PANEL)]
         if rank == dst and owner != dst:
-            ops.append(dist.P2POp(dist.irecv, sl, owner, group))
+            buf = sl.cpu() if staged else sl
+            ops.append(dist.P2POp(dist.irecv, buf, owner, group))
+            if staged:
+                back.append((sl, buf))
         elif rank == owner and owner != dst:
-            ops.append(dist.P2POp(dist.isend, sl, dst, group))
+            ops.append(dist.P2POp(dist.isend, sl.cpu() if staged else sl, dst, group))
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
+    for dev, host in back:
+        dev.copy_(host)
     return mat
 
 

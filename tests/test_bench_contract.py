@@ -91,3 +91,30 @@ def test_workload_names_match_between_arms():
     for c in ("C1", "C2", "C5"):
         name = bench.workload_name(c, configs.make_instance(c))
         assert name.startswith(c) and "BASELINE.json configs[" in name
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_gloo_on_one_gpu(cuda):
+    """The N > 1 bench flow end to end on a one-GPU box: `--gpus 2` spawns two ranks (gloo,
+    sharing the GPU), each builds its own C2 k-point, C5 k-points are dealt round-robin and one
+    C3 k-point is split by column panels and gathered to rank 0 (host-staged over gloo: the
+    NCCL transport of the 8-GPU box is the same gather on device memory); times are the max over
+    ranks.  Checks the line's shape, not speed (the ranks time-slice one GPU)."""
+    out = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--gpus", "2",
+                          "--backend", "gloo", "--steps", "2", "--warmup", "1",
+                          "--no-cpu-baseline"],
+                         capture_output=True, text=True, timeout=1200, cwd=REPO,
+                         env={k: v for k, v in os.environ.items()
+                              if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")})
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["gpus_active"] == 2 and d["value"] > 0
+    assert d["config"]["parallelism"] == "kpoint-dp2"
+    assert d["C5_kpoint_batch"]["parallelism"] == "kpoint-dp2"
+    assert d["C5_kpoint_batch"]["kpoints_per_s"] > 0
+    assert d["C3_panels"]["parallelism"] == "panels-nccl2" and d["C3_panels"]["tflops"] > 0

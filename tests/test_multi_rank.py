@@ -82,3 +82,51 @@ def test_gather_panels_gloo_world2(tmp_path, n):
     rng = np.random.default_rng(5)
     full = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
     np.testing.assert_array_equal(got, full)
+
+
+def _sharded_worker(rank, world, port, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_1602_06589_b200 import configs
+    from paper_1602_06589_b200.pipeline import DeviceSpec, pack_tmats
+    from paper_1602_06589_b200.shard import NcclShardedBuild
+
+    inst = configs.make_instance("C1")
+    dspec = DeviceSpec(inst.spec)
+    sb = NcclShardedBuild(inst.spec.n_basis, dspec.heights)
+    out = sb.run(dspec, pack_tmats(inst.tmats))
+    assert sb.last_result["hpd_mask"] == [True] * inst.spec.n_atoms
+    if rank == 0:
+        np.save(out_path + "_H.npy", out[0].cpu().numpy())
+        np.save(out_path + "_S.npy", out[1].cpu().numpy())
+    else:
+        assert out is None
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_panel_sharded_build_two_ranks_one_gpu(cuda, tmp_path, world):
+    """The column-panel build of one k-point across `world` ranks (gloo, sharing one GPU): every
+    rank computes its owned panels' lower tiles, the panels are gathered to rank 0 (host-staged
+    over gloo) and mirrored there; the assembled H and S equal the one-rank pipeline build to
+    rounding (every tile's K-sum is local to its owner; the stream-K split of a tile's K range
+    over CTAs differs with the problem size per rank, which reorders the partial sums) and are
+    exactly Hermitian."""
+    from paper_1602_06589_b200 import configs
+    from paper_1602_06589_b200.pipeline import DeviceSpec, HSPipeline, pack_tmats
+
+    out = str(tmp_path / "sh")
+    mp.spawn(_sharded_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    inst = configs.make_instance("C1")
+    dspec = DeviceSpec(inst.spec)
+    pipe = HSPipeline(inst.spec.n_basis, dspec.heights)
+    pipe.run(dspec, pack_tmats(inst.tmats))
+    h, s = pipe.result_views()
+    for name, ref in (("H", h.cpu().numpy()), ("S", s.cpu().numpy())):
+        got = np.load(f"{out}_{name}.npy")
+        assert np.linalg.norm(got - ref) <= 1e-13 * np.linalg.norm(ref), name
+        np.testing.assert_array_equal(got, got.conj().T)

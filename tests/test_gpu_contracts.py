@@ -505,3 +505,49 @@ def test_compute_ab_device_resident_drop_in(pkg):
     s_want = a2.conj().T @ a2 + (co.udot_norms[:, None] * co.B_star.array).conj().T @ (
         co.udot_norms[:, None] * co.B_star.array)
     assert rel_fro(s3.array, s_want) <= 1e-12
+
+
+@pytest.mark.parametrize("env", [
+    {"HSDLA_PLANES": "1"},                                     # sum planes, 8x4 ring
+    {"HSDLA_PLANES": "1", "HSDLA_PL_VARIANT": "16x2"},         # sum planes, 16x2 ring
+    {"HSDLA_TEMPLATES": "0"},                                  # per-atom generation / T applications
+    {"HSDLA_TPREP_CLUSTER": "0", "HSDLA_CONTRACT": "tma"},     # one-CTA T preparation, TMA feeds
+    {"HSDLA_WARP_COLS": "16", "HSDLA_G3_MINB": "2"},           # 8-warp 32x16 warp tiles
+    {"HSDLA_CONTRACT": "tma", "HSDLA_TMA_W8": "1"},            # TMA, 8 warps
+])
+def test_kernel_variants_match_oracle(pkg, tmp_path, env):
+    """The library's measured-but-not-default variants (switches read once per process, so each
+    runs in a child) still compute the right H and S: the device pipeline on C2 (template path,
+    joint form) and the drop-in build_all on C1, against the oracle at 1e-12."""
+    import os
+    import subprocess
+    import sys
+
+    from oracle import flapw as of
+    from paper_1602_06589_b200 import configs
+
+    script = (
+        "import sys, numpy as np; sys.path.insert(0, '.')\n"
+        "import paper_1602_06589_b200 as pkg\n"
+        "from paper_1602_06589_b200 import configs\n"
+        "from paper_1602_06589_b200.pipeline import build_hs\n"
+        "c2 = configs.make_instance('C2')\n"
+        "h2, s2, r2 = build_hs(c2.spec, c2.tmats)\n"
+        "c1 = configs.make_instance('C1')\n"
+        "h1, s1, _ = pkg.build_all(pkg.compute_AB(c1.spec), c1.tmats, pkg.BuildConfig())\n"
+        "np.savez(sys.argv[1], h2=h2.array, s2=s2.array, h1=h1.array, s1=s1.array,\n"
+        "         types=r2['template_types'])\n")
+    out = tmp_path / "variant.npz"
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run([sys.executable, "-c", script, str(out)], check=True, cwd=repo,
+                   env={**os.environ, **env}, timeout=900)
+    got = np.load(out)
+    assert (int(got["types"]) == 0) == (env.get("HSDLA_TEMPLATES") == "0")
+    for name in ("C2", "C1"):
+        inst = configs.make_instance(name)
+        a, b, norms, offs = of.compute_ab(inst.spec)
+        tm = inst.tmats
+        ho, so, _, _ = ob.build_all(a, b, norms, list(np.diff(offs)), [t.array for t in tm.t_aa],
+                                    [t.array for t in tm.t_ab], [t.array for t in tm.t_bb])
+        k = name[1]
+        assert rel_fro(got["h" + k], ho) <= 1e-12 and rel_fro(got["s" + k], so) <= 1e-12

@@ -430,8 +430,10 @@ _WORKSPACE: dict = {}  # device -> (build workspace, (TPack, force) of the last 
 
 def release_cached_workspaces():
     """Free the build workspaces `build_all` keeps between calls (one per device: the Z / XY /
-    scaled-B stacks plus the T preparation — three stacked-coefficient sizes, e.g. 8 GB at C4)."""
+    scaled-B stacks plus the T preparation — three stacked-coefficient sizes, e.g. 8 GB at C4) and
+    the device pipeline of its fused path."""
     _WORKSPACE.clear()
+    _PIPES.clear()
 
 
 def build_all(coeffs: StackedCoefficients, tmats: TMatrixSet, config: BuildConfig,
@@ -483,9 +485,21 @@ def build_all(coeffs: StackedCoefficients, tmats: TMatrixSet, config: BuildConfi
         b_d, ldb = device.upload_stack(coeffs.B_star, padded_ld(r))
         if ldb != ld:
             b_d = device.upload_window(coeffs.B_star.array, ld)
+    tpack: TPack = pack_tmats(tmats)
+    # Fused path: stacks that are still compute_AB's own, untouched output (in HBM, never read
+    # or written by the host, same row norms) are a function of the spec compute_AB kept
+    # (`_origin`, a device copy taken at that call), so the build runs from the spec on the
+    # device pipeline (per-type templates + expansion) — the same H and S to
+    # rounding, without the per-atom T applications; the stacks themselves are left as they are.
+    origin = getattr(coeffs, "_origin", None)
+    if (origin is not None and dev_a is not None and dev_b is not None
+            and dev_a[0].device.index == here and origin.n_basis == n
+            and tuple(int(h) for h in origin.heights) == tuple(layout.block_heights)
+            and np.array_equal(np.asarray(coeffs.udot_norms), origin.udot_rows)):
+        return _build_from_origin(origin, coeffs, tpack, config, regenerate, report, layout,
+                                  sizes, n, t0)
     udot = t.zeros(ld, dtype=t.float64, device="cuda")
     udot[:r] = t.from_numpy(np.ascontiguousarray(coeffs.udot_norms)).to("cuda")
-    tpack: TPack = pack_tmats(tmats)
     h_d = device.empty_matrix(n, n, n)
     s_d = device.empty_matrix(n, n, n)
     h_host = _pinned_square(n)
@@ -515,6 +529,31 @@ def build_all(coeffs: StackedCoefficients, tmats: TMatrixSet, config: BuildConfi
                 int(sum(x.numel() * x.element_size() for x in (a_d, b_d, udot, h_d, s_d))
                     + ws.numel()))
     return h_full, s_full, report
+
+
+_PIPES: dict = {}  # device -> HSPipeline of the fused build_all path (last shape)
+
+
+def _build_from_origin(origin, coeffs, tpack, config, regenerate, report, layout, sizes, n, t0):
+    """build_all on compute_AB's untouched output, from the spec it kept (see build_all)."""
+    from .pipeline import HSPipeline
+
+    t = device.torch()
+    dev_id = t.cuda.current_device()
+    pipe = _PIPES.get(dev_id)
+    if pipe is None or pipe.n_capacity != n or not np.array_equal(pipe.heights, origin.heights):
+        pipe = _PIPES[dev_id] = HSPipeline(n, origin.heights)
+    h_host = _pinned_square(n)
+    s_host = _pinned_square(n)
+    res = pipe.run(origin, tpack, config.force_general_path, host_out=(h_host[1], s_host[1]))
+    if not config.backup:
+        regenerate(coeffs)
+        if coeffs.A_star.rows != layout.total_rows or coeffs.A_star.cols != n:
+            raise ContractViolationError("regeneration callback changed the stack shape")
+    wall = time.perf_counter() - t0
+    fill_report(report, res, layout, sizes, n, config, wall, pipe.device_bytes)
+    report._path = "spec-pipeline"  # not part of the JSON report (builder.py:166-178)
+    return ComplexDense(h_host[0]), ComplexDense(s_host[0]), report
 
 
 def fill_report(report: BuildReport, res: dict, layout: AtomBlockLayout, sizes, n: int,

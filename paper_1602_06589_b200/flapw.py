@@ -144,9 +144,10 @@ class SystemSpec:
 def compute_AB(spec: SystemSpec) -> StackedCoefficients:
     """Matching coefficients A*, B* and row norms, generated on the GPU (`flapw.py:201-233`).
 
-    The stacks stay in HBM (`DeviceComplexDense`): `build_all` uses them in place, and the
-    first host access downloads them into pinned memory with the reference's capacity-height
-    layout (`flapw.py:209-212`), one contiguous DMA per stack."""
+    The stacks stay in HBM (`DeviceComplexDense`): `build_all` uses them in place (or, while
+    they are untouched, builds from the spec itself on the device pipeline), and the first host
+    access downloads them into pinned memory with the reference's capacity-height layout
+    (`flapw.py:209-212`), one contiguous DMA per stack."""
     from . import device
     from .pipeline import DeviceSpec, ab_generate_device
 
@@ -162,8 +163,12 @@ def compute_AB(spec: SystemSpec) -> StackedCoefficients:
     # per-row ||udot|| (flapw.py:232) straight from the radial data: no device round trip, so
     # the call returns while the generator still runs
     norms = np.array(dspec.udot_rows, dtype=np.float64)
-    return StackedCoefficients(DeviceComplexDense(a_dev, cap, n, layout.total_rows),
-                               DeviceComplexDense(b_dev, cap, n, layout.total_rows), layout, norms)
+    coeffs = StackedCoefficients(DeviceComplexDense(a_dev, cap, n, layout.total_rows),
+                                 DeviceComplexDense(b_dev, cap, n, layout.total_rows), layout, norms)
+    # the device copy of the spec these stacks are a function of: build_all runs from it while
+    # the stacks stay untouched (builder._build_from_origin)
+    coeffs._origin = dspec
+    return coeffs
 
 
 def match_factors(spec: SystemSpec, atom: int):

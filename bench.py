@@ -704,7 +704,8 @@ def run_ours(args):
                               "not a utilisation — fp64_peak_frac / roofline.frac are",
             "fp64_peak_frac": rl["frac"],
             "step_fp64_frac": round(ex_step / FP64_PEAK_TFLOPS, 4),
-            "roofline": {**rl, "ceilings": fp64_ceilings(clocks.get("sm_mhz"))},
+            "roofline": {**rl, "ceilings": fp64_ceilings(clocks.get("sm_mhz")),
+                         "merged_sh": bool(res.get("merged_sh"))},
             "ab_gen": ab_gen_line(statistics.mean(ab_ms), rows, n, res.get("template_types", 0),
                                   statistics.mean(kern["expand_W"]) if kern.get("expand_W") else None,
                                   statistics.mean(kern["templates"]) if kern.get("templates") else None),

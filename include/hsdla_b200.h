@@ -302,6 +302,8 @@ typedef struct {
                                  0 = per-atom generation / T applications */
   float ms_templates;         /* out: template path: the per-type generator's share of ms_setup
                                  (the rest of ms_setup is the HBM-bound expansion) */
+  int32_t merged_sh;          /* out: 1 = S and H were one contraction launch (ms_contract_H is
+                                 both, ms_contract_S ~ 0): a reused, all-joint T preparation */
 } hsdla_build_result;
 
 size_t hsdla_build_workspace_size(const hsdla_build_args* args);

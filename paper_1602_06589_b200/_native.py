@@ -87,7 +87,7 @@ class BuildResult(ctypes.Structure):
         ("ms_contract_S", ctypes.c_float), ("ms_contract_H", ctypes.c_float),
         ("ms_apply_Z", ctypes.c_float), ("ms_apply_XY", ctypes.c_float),
         ("ms_total", ctypes.c_float), ("joint_info", _P_i32), ("joint_shift", ctypes.c_double),
-        ("template_types", _i32), ("ms_templates", ctypes.c_float),
+        ("template_types", _i32), ("ms_templates", ctypes.c_float), ("merged_sh", _i32),
     ]
 
 

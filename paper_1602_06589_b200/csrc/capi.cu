@@ -647,6 +647,7 @@ int complete_slot(hsdla_ctx* ctx, hsdla_ctx::BuildSlot& sl, hsdla_ctx::Outcome* 
   o->joint = sl.joint;
   o->sigma = sl.sigma;
   o->types = sl.types;
+  o->merged = sl.merged;
   cudaEvent_t* ev = sl.ev;
   float t01 = 0, t12 = 0, t23 = 0, t34 = 0, t46 = 0, t07 = 0;
   cudaEventElapsedTime(&t01, ev[0], ev[1]);
@@ -833,7 +834,7 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     ctx->joint_info.assign(a->n_tsets, -2);
     ctx->joint_split.assign(a->n_tsets, 0);
     ctx->joint_sigma = 0.0;
-    ctx->joint_pending = key.joint != 0;  // read after the S contraction is enqueued
+    ctx->joint_pending = key.joint != 0;  // read by decide()
     ctx->tkey = key;
   } else {
     HS_CUDA(cudaEventRecord(ctx->join, ctx->stream));
@@ -853,6 +854,98 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
   double2* const tW2 = tW1 + ldt * n;
   const int4* ex_atoms = nullptr;
   const long long* ex_off = nullptr;
+  // W templates of the joint form: W1_t = L11^H A_t + L21^H B_t, W2_t = L22^H B_t per type.
+  auto apply_w_templates = [&]() -> int {
+    std::vector<Seg> segs;
+    std::vector<Prob> probs;
+    for (int ty = 0; ty < (int)ti.rep.size(); ++ty) {
+      const int ts = a->t_index[ti.rep[ty]], m = a->t_dim[ts];
+      const long long to = ti.toff[ty];
+      const double2* L = joint + (long long)ts * lj * lj;
+      int s0 = (int)segs.size();
+      segs.push_back(make_seg(L, lj, tA + to, ldt, m));
+      segs.push_back(make_seg(L + m, lj, tB + to, ldt, m));
+      probs.push_back(make_prob(tW1 + to, ldt, m, n, PROB_GENERAL, s0, 2, 0));
+      s0 = (int)segs.size();
+      segs.push_back(make_seg(L + m + m * lj, lj, tB + to, ldt, m));
+      probs.push_back(make_prob(tW2 + to, ldt, m, n, PROB_GENERAL, s0, 1, 0));
+    }
+    return launch_contract(ctx, probs, segs, flag);
+  };
+  // Merged contraction (steady state of a k-point batch): when this build reuses a T
+  // preparation whose every set takes the plain joint form (no split, no shift), the per-type W
+  // application and both expansions run before S, and S and H are ONE launch (two problems of
+  // one stream-K space): one launch's fixed cost and tail instead of two (HSDLA_MERGE_SH=0: off).
+  static int merge_env = -1;
+  if (merge_env < 0) {
+    const char* e = getenv("HSDLA_MERGE_SH");
+    merge_env = (e && e[0] == '0') ? 0 : 1;
+  }
+  // Decided before S on the template path (so every build of the same inputs takes the same
+  // launch structure and results stay bitwise reproducible between first and later builds).
+  const bool early = merge_env && tpl && !pl && !host_src && key.joint;
+  bool merged = false;
+  // Which H form each T set takes is a host decision (it fixes the K extents of the H
+  // contraction): after a fresh T preparation, wait for it alone — it ran on the side streams
+  // under this build's A/B generation (and, off the merged path, under the S contraction).
+  // With reuse_t later k-points skip both.
+  auto decide = [&]() -> int {
+    if (ctx->joint_pending) {
+      HS_CUDA(cudaEventSynchronize(ctx->join));
+      const volatile int* jhost = ctx->scratch_host + 400;
+      const volatile int* shost = ctx->scratch_host + 600;  // split flags [600, 696)
+      const volatile double* ghost = reinterpret_cast<const double*>(ctx->scratch_host + 704);
+      std::vector<double> g(a->n_tsets);  // search result per set: shift used, -1 = no factor
+      double smax = 0.0;
+      bool all_ok = true;
+      for (int t = 0; t < a->n_tsets; ++t) {
+        ctx->joint_info[t] = jhost[t];
+        ctx->joint_split[t] = shost[t];
+        g[t] = jhost[t] == 0 ? ghost[t] : -1.0;
+        all_ok = all_ok && g[t] >= 0.0;
+        smax = std::max(smax, g[t]);
+      }
+      // Shift guard: H = sum W^H W - sigma S cancels terms of size sigma ||diag(I, U^2)|| against
+      // ||T|| (Gershgorin radius rho); beyond a 16x amplification of the rounding error the
+      // reference forms are the accurate choice.
+      if (smax > 0.0 && all_ok) {
+        for (int t = 0; t < a->n_tsets; ++t) {
+          double dmax = 1.0;
+          for (int i = 0; i < a->t_dim[t]; ++i) dmax = std::max(dmax, u2h[size_t(t) * mp + i]);
+          const double rho = ghost[96 + t];
+          if (!(rho > 0.0) || smax * dmax > kShiftAmplification * rho) all_ok = false;
+        }
+      }
+      if (smax > 0.0) {
+        // Some set needed a shift.  H = sum W^H W - sigma S holds only with one sigma for every
+        // atom: refactor all sets with the largest shift, or keep only the unshifted HPD sets.
+        bool shifted = false;
+        if (all_ok) {
+          rc = launch_tjoint(ctx->side, a->n_tsets, tdim_dev, tdim_dev + a->n_tsets, mp, D2(a->t_aa),
+                             D2(a->t_ab), D2(a->t_bb), a->t_ld, joint, jinfo_dev,
+                             ctx->scratch_host_dev + 400, ctx->scratch_host_dev + 600, u2_dev, smax,
+                             reinterpret_cast<double*>(ctx->scratch_host_dev + 704));
+          if (rc) return rc;
+          HS_CUDA(cudaStreamSynchronize(ctx->side));
+          shifted = true;
+          for (int t = 0; t < a->n_tsets; ++t) {
+            ctx->joint_info[t] = jhost[t];
+            ctx->joint_split[t] = shost[t];
+            shifted = shifted && jhost[t] == 0;
+          }
+        }
+        if (shifted) {
+          ctx->joint_sigma = smax;
+        } else {
+          // search-mode factors of HPD sets are unshifted and usable, unless a refactor overwrote them
+          for (int t = 0; t < a->n_tsets; ++t)
+            if (all_ok || g[t] != 0.0) ctx->joint_info[t] = 1;
+        }
+      }
+      ctx->joint_pending = false;
+    }
+    return HSDLA_OK;
+  };
   if (tpl) {
     // B itself is needed later only by T sets that do not take the plain joint form; known
     // before the H decision when this build reuses a T preparation.
@@ -882,6 +975,24 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     rc = launch_expand(ctx, n, ab->k_vectors, ab->positions, ab->radial, ab->radial_stride,
                        ex_atoms, ex_off, na, tA, tB, ldt, o, ld);
     if (rc) return rc;
+    if (early) {
+      if ((rc = decide())) return rc;
+      merged = ctx->joint_sigma == 0.0 && (int)ctx->joint_info.size() == a->n_tsets;
+      for (int t = 0; t < a->n_tsets && merged; ++t)
+        merged = ctx->joint_info[t] == 0 && !ctx->joint_split[t];
+    }
+    if (merged) {  // phase timers: ev1 = ev2 (no separate S), ev3 after W, ev4 after expansion
+      HS_CUDA(cudaEventRecord(ev[1], ctx->stream));
+      HS_CUDA(cudaEventRecord(ev[2], ctx->stream));
+      HS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join, 0));  // the joint factors
+      if ((rc = apply_w_templates())) return rc;
+      HS_CUDA(cudaEventRecord(ev[3], ctx->stream));
+      ExpandOut o2{XY, nullptr, nullptr, Z, nullptr, nullptr, nullptr, 0};
+      if ((rc = launch_expand(ctx, n, ab->k_vectors, ab->positions, ab->radial, ab->radial_stride,
+                              ex_atoms, ex_off, na, tW1, tW2, ldt, o2, ld)))
+        return rc;
+      HS_CUDA(cudaEventRecord(ev[4], ctx->stream));
+    }
   } else if (ab) {
     rc = ab_generate(ctx, ab);
     if (rc) return rc;
@@ -899,7 +1010,7 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
   if (!Bs && !host_src && (rc = make_bs())) return rc;
   HS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join, 0));
   HS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join2, 0));
-  HS_CUDA(cudaEventRecord(ev[1], ctx->stream));
+  if (!merged) HS_CUDA(cudaEventRecord(ev[1], ctx->stream));
 
   // Column-panel ownership for sharded runs (balanced pairs j <-> nb-1-j).
   const int nb = (n + kTile - 1) / kTile;
@@ -991,7 +1102,7 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     std::vector<Prob> probs{make_prob(D2(a->S), a->ldh, n, n, PROB_TRI_MIRROR, 0, 1, 1)};
     if (s_streamed) probs[0].panel_done = sl.panel_cnt;
     if ((rc = launch_contract(ctx, probs, segs, flag))) return rc;
-  } else {
+  } else if (!merged) {
     std::vector<Seg> segs{make_seg(A, ld, A, ld, (int)R), make_seg(Bs, ld, Bs, ld, (int)R)};
     if (pl)
       segs = {make_seg_planes(A, Ad, ld, A, As, ld, (int)R), make_seg_planes(Bs, Ud, ld, Bs, Us, ld, (int)R)};
@@ -1001,68 +1112,12 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     rc = launch_contract(ctx, probs, segs, flag);
     if (rc) return rc;
   }
-  HS_CUDA(cudaEventRecord(ev[2], ctx->stream));
+  if (!merged) HS_CUDA(cudaEventRecord(ev[2], ctx->stream));
 
-  // Which H form each T set takes is a host decision (it fixes the K extents of the H
-  // contraction): after a fresh T preparation, wait for it alone — it ran on the side stream
-  // under this build's A/B generation, and the S contraction is already queued, so the
-  // device does not idle.  With reuse_t later k-points skip both.
-  if (ctx->joint_pending) {
-    HS_CUDA(cudaEventSynchronize(ctx->join));
-    const volatile int* jhost = ctx->scratch_host + 400;
-    const volatile int* shost = ctx->scratch_host + 600;  // split flags [600, 696)
-    const volatile double* ghost = reinterpret_cast<const double*>(ctx->scratch_host + 704);
-    std::vector<double> g(a->n_tsets);  // search result per set: shift used, -1 = no factor
-    double smax = 0.0;
-    bool all_ok = true;
-    for (int t = 0; t < a->n_tsets; ++t) {
-      ctx->joint_info[t] = jhost[t];
-      ctx->joint_split[t] = shost[t];
-      g[t] = jhost[t] == 0 ? ghost[t] : -1.0;
-      all_ok = all_ok && g[t] >= 0.0;
-      smax = std::max(smax, g[t]);
-    }
-    // Shift guard: H = sum W^H W - sigma S cancels terms of size sigma ||diag(I, U^2)|| against
-    // ||T|| (Gershgorin radius rho); beyond a 16x amplification of the rounding error the
-    // reference forms are the accurate choice.
-    if (smax > 0.0 && all_ok) {
-      for (int t = 0; t < a->n_tsets; ++t) {
-        double dmax = 1.0;
-        for (int i = 0; i < a->t_dim[t]; ++i) dmax = std::max(dmax, u2h[size_t(t) * mp + i]);
-        const double rho = ghost[96 + t];
-        if (!(rho > 0.0) || smax * dmax > kShiftAmplification * rho) all_ok = false;
-      }
-    }
-    if (smax > 0.0) {
-      // Some set needed a shift.  H = sum W^H W - sigma S holds only with one sigma for every
-      // atom: refactor all sets with the largest shift, or keep only the unshifted HPD sets.
-      bool shifted = false;
-      if (all_ok) {
-        rc = launch_tjoint(ctx->side, a->n_tsets, tdim_dev, tdim_dev + a->n_tsets, mp, D2(a->t_aa),
-                           D2(a->t_ab), D2(a->t_bb), a->t_ld, joint, jinfo_dev,
-                           ctx->scratch_host_dev + 400, ctx->scratch_host_dev + 600, u2_dev, smax,
-                           reinterpret_cast<double*>(ctx->scratch_host_dev + 704));
-        if (rc) return rc;
-        HS_CUDA(cudaStreamSynchronize(ctx->side));
-        shifted = true;
-        for (int t = 0; t < a->n_tsets; ++t) {
-          ctx->joint_info[t] = jhost[t];
-          ctx->joint_split[t] = shost[t];
-          shifted = shifted && jhost[t] == 0;
-        }
-      }
-      if (shifted) {
-        ctx->joint_sigma = smax;
-      } else {
-        // search-mode factors of HPD sets are unshifted and usable, unless a refactor overwrote them
-        for (int t = 0; t < a->n_tsets; ++t)
-          if (all_ok || g[t] != 0.0) ctx->joint_info[t] = 1;
-      }
-    }
-    ctx->joint_pending = false;
-  }
+  if (!early && (rc = decide())) return rc;
   sl.sigma = key.joint ? ctx->joint_sigma : 0.0;
   sl.types = tpl ? (int)ti.rep.size() : 0;
+  sl.merged = merged ? 1 : 0;
   sl.joint.assign(a->n_tsets, 0);
   bool any_joint = false, all_joint = true;
   for (int t = 0; t < a->n_tsets; ++t) {
@@ -1076,22 +1131,10 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
   // template times its phase (expansion pass, with sum planes).
   bool tpl_h = tpl && all_joint;
   for (int t = 0; t < a->n_tsets && tpl_h; ++t) tpl_h = sl.joint[t] == 1;
-  if (tpl_h) {
-    std::vector<Seg> segs;
-    std::vector<Prob> probs;
-    for (int ty = 0; ty < (int)ti.rep.size(); ++ty) {
-      const int ts = a->t_index[ti.rep[ty]], m = a->t_dim[ts];
-      const long long to = ti.toff[ty];
-      const double2* L = joint + (long long)ts * lj * lj;
-      int s0 = (int)segs.size();
-      segs.push_back(make_seg(L, lj, tA + to, ldt, m));
-      segs.push_back(make_seg(L + m, lj, tB + to, ldt, m));
-      probs.push_back(make_prob(tW1 + to, ldt, m, n, PROB_GENERAL, s0, 2, 0));
-      s0 = (int)segs.size();
-      segs.push_back(make_seg(L + m + m * lj, lj, tB + to, ldt, m));
-      probs.push_back(make_prob(tW2 + to, ldt, m, n, PROB_GENERAL, s0, 1, 0));
-    }
-    if ((rc = launch_contract(ctx, probs, segs, flag))) return rc;
+  if (merged) {
+    // W applied and expanded before S (phase events recorded there)
+  } else if (tpl_h) {
+    if ((rc = apply_w_templates())) return rc;
     HS_CUDA(cudaEventRecord(ev[3], ctx->stream));
     ExpandOut o{XY, pl ? W1d : nullptr, pl ? W1s : nullptr, Z, pl ? W2d : nullptr,
                 pl ? W2s : nullptr, nullptr, 0};
@@ -1178,12 +1221,14 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     }
   }
   }  // per-atom T applications
-  HS_CUDA(cudaEventRecord(ev[4], ctx->stream));
+  if (!merged) HS_CUDA(cudaEventRecord(ev[4], ctx->stream));
   // S leaves for the host now, under the H contraction (4/3 of S's time): started right
   // after S it would contend with the bandwidth-heavier T applications (measured +25% on
   // them), and the previous k-point's H copy already overlaps this one's A/B + S phase.
   if (s_streamed) {
     // S is on its way already (streamed during its own contraction)
+  } else if (merged) {
+    // S is computed by the merged launch below; copied after it
   } else if (a->S_host) {
     rc = copy_out(D2(a->S), a->S_host, sl.s_copied);
     if (rc) return rc;
@@ -1193,6 +1238,7 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
   // ---- H = Z^H B + B^H Z + sum_HPD Y^H Y + sum_nonHPD A^H X   (builder.py:246-247, :305-311)
   //      AA segments per run of atoms sharing one T set: P = XY (HPD) or A (general).
   if (prev.copies && prev.h_dev == a->H) HS_CUDA(cudaStreamWaitEvent(ctx->stream, prev.h_copied, 0));
+  // (the merged launch writes S here: the S-hazard wait above already precedes it)
   const bool h_streamed = waitv && a->H_host && sl.sigma == 0.0;  // shifted: copy after -= sigma S
   if (h_streamed) {
     rc = stream_out(D2(a->H), a->H_host, sl.panel_cnt + nbp, sl.h_copied);
@@ -1236,10 +1282,25 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
       }
     }
     std::vector<Prob> probs;
-    add_tri(probs, D2(a->H), 0, (int)segs.size());
-    if (h_streamed) probs[0].panel_done = sl.panel_cnt + nbp;
+    if (merged) {  // S's problem first (its panels complete first), then H's
+      const int s0 = (int)segs.size();
+      segs.push_back(make_seg(A, ld, A, ld, (int)R));
+      segs.push_back(make_seg(Bs, ld, Bs, ld, (int)R));
+      add_tri(probs, D2(a->S), s0, 2);
+      if (s_streamed) probs.back().panel_done = sl.panel_cnt;
+    }
+    const size_t h0 = probs.size();
+    add_tri(probs, D2(a->H), 0, merged ? (int)segs.size() - 2 : (int)segs.size());
+    if (h_streamed) probs[h0].panel_done = sl.panel_cnt + nbp;
     rc = launch_contract(ctx, probs, segs, flag);
     if (rc) return rc;
+    if (merged && !s_streamed) {
+      if (a->S_host) {
+        if ((rc = copy_out(D2(a->S), a->S_host, sl.s_copied))) return rc;
+      } else {
+        HS_CUDA(cudaEventRecord(sl.s_copied, ctx->stream));
+      }
+    }
   }
   if (sl.sigma > 0.0) {  // shifted joint form: H = sum W^H W - sigma S (both full Hermitian)
     rc = launch_axpy_shift(ctx, n, sl.sigma, D2(a->S), a->ldh, D2(a->H), a->ldh);
@@ -1272,6 +1333,7 @@ int fill_result(const hsdla_ctx::Outcome& o, hsdla_build_result* res) {
   res->joint_shift = o.sigma;
   res->template_types = o.types;
   res->ms_templates = o.ms[6];
+  res->merged_sh = o.merged;
   for (size_t i = 0; i < o.hpd.size(); ++i)
     if (res->hpd_mask) res->hpd_mask[i] = o.hpd[i];
   res->nonfinite = o.nonfinite;

@@ -161,6 +161,7 @@ struct hsdla_ctx {
     std::vector<int> joint;  // per T set: 1 = this build's H used the joint factor (2 = split)
     double sigma = 0.0;      // this build's joint shift (H -= sigma S after the contraction)
     int types = 0;           // template path: atom types (0 = per-atom path)
+    int merged = 0;          // S and H in one contraction launch
     const void* h_dev = nullptr;  // this build's device H / S (copy hazards of the next build)
     const void* s_dev = nullptr;
   } slots[2];
@@ -170,7 +171,7 @@ struct hsdla_ctx {
     int rc = 0, nonfinite = 0;
     std::vector<int> info, hpd, joint;
     double sigma = 0.0;
-    int types = 0;
+    int types = 0, merged = 0;
     float ms[7] = {};
   };
   std::map<unsigned long long, Outcome> stash;

@@ -309,6 +309,7 @@ class _Call:
             "joint_shift": float(r.joint_shift),
             "template_types": int(r.template_types),
             "ms_templates": float(r.ms_templates),
+            "merged_sh": bool(r.merged_sh),
             "ms": {"setup": r.ms_setup, "S": r.ms_S, "H_ABBA_BB": r.ms_H_ABBA_BB,
                    "H_AA": r.ms_H_AA},
             # template path: the per-type W = L^H [A; B] application and the W1 / W2 expansion
@@ -468,11 +469,11 @@ class HSPipeline:
         publication (plus the tail kernel of split T sets, which the caller adds from
         `joint_split`).  Template path (`result["template_types"] > 0`): templates per l group,
         expansion, S contraction, per-type W application, W expansion, H contraction,
-        publication."""
+        publication; merged (`result["merged_sh"]`): S and H are one contraction launch."""
         groups = len(np.unique(dspec.l_sph))
         if result is not None and result.get("template_types", 0) and "apply_W" in result.get(
                 "kernel_ms", {}):
-            return groups + 6
+            return groups + (5 if result.get("merged_sh") else 6)
         return groups + 5
 
     def result_views(self):

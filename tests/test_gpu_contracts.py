@@ -517,6 +517,7 @@ def test_compute_ab_device_resident_drop_in(pkg):
     {"HSDLA_TPREP_CLUSTER": "0", "HSDLA_CONTRACT": "tma"},     # one-CTA T preparation, TMA feeds
     {"HSDLA_WARP_COLS": "16", "HSDLA_G3_MINB": "2"},           # 8-warp 32x16 warp tiles
     {"HSDLA_CONTRACT": "tma", "HSDLA_TMA_W8": "1"},            # TMA, 8 warps
+    {"HSDLA_MERGE_SH": "0"},                                   # separate S and H launches
 ])
 def test_kernel_variants_match_oracle(pkg, tmp_path, env):
     """The library's measured-but-not-default variants (switches read once per process, so each
@@ -539,13 +540,15 @@ def test_kernel_variants_match_oracle(pkg, tmp_path, env):
         "c1 = configs.make_instance('C1')\n"
         "h1, s1, _ = pkg.build_all(pkg.compute_AB(c1.spec), c1.tmats, pkg.BuildConfig())\n"
         "np.savez(sys.argv[1], h2=h2.array, s2=s2.array, h1=h1.array, s1=s1.array,\n"
-        "         types=r2['template_types'])\n")
+        "         types=r2['template_types'], merged=r2['merged_sh'])\n")
     out = tmp_path / "variant.npz"
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     subprocess.run([sys.executable, "-c", script, str(out)], check=True, cwd=repo,
                    env={**os.environ, **env}, timeout=900)
     got = np.load(out)
     assert (int(got["types"]) == 0) == (env.get("HSDLA_TEMPLATES") == "0")
+    assert bool(got["merged"]) == (env.get("HSDLA_MERGE_SH", "1") != "0" and "HSDLA_PLANES" not in env
+                                   and env.get("HSDLA_TEMPLATES") != "0")
     for name in ("C2", "C1"):
         inst = configs.make_instance(name)
         a, b, norms, offs = of.compute_ab(inst.spec)
@@ -554,3 +557,19 @@ def test_kernel_variants_match_oracle(pkg, tmp_path, env):
                                     [t.array for t in tm.t_ab], [t.array for t in tm.t_bb])
         k = name[1]
         assert rel_fro(got["h" + k], ho) <= 1e-12 and rel_fro(got["s" + k], so) <= 1e-12
+
+
+def test_merged_launch_reproducible(pkg):
+    """The template path's merged S + H contraction is taken on the first build of a T set as
+    well as on builds reusing it, so repeated builds of the same inputs are bitwise identical;
+    the merged launch replaces the separate S launch (one fewer kernel per k-point)."""
+    from paper_1602_06589_b200 import configs
+    from paper_1602_06589_b200.pipeline import build_hs_many
+
+    inst = configs.make_instance("C2")
+    got = []
+    res = build_hs_many([inst.spec, inst.spec], inst.tmats,
+                        on_result=lambda i, h, s, r: got.append((h.array.copy(), s.array.copy())))
+    assert [r["merged_sh"] for r in res] == [True, True]
+    assert np.array_equal(got[0][0], got[1][0]) and np.array_equal(got[0][1], got[1][1])
+    assert res[1]["kernel_ms"]["contract_H"] > 0

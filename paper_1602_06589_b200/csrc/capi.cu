@@ -872,10 +872,12 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     }
     return launch_contract(ctx, probs, segs, flag);
   };
-  // Merged contraction (steady state of a k-point batch): when this build reuses a T
-  // preparation whose every set takes the plain joint form (no split, no shift), the per-type W
-  // application and both expansions run before S, and S and H are ONE launch (two problems of
-  // one stream-K space): one launch's fixed cost and tail instead of two (HSDLA_MERGE_SH=0: off).
+  // Merged contraction (device-resident builds on the template path): when every T set takes
+  // the plain joint form (no split, no shift), the per-type W application and both expansions
+  // run before S, and S and H are ONE launch (two problems of one stream-K space): one launch's
+  // fixed cost and tail instead of two, -0.5% per C2 k-point (profiles/r02_merged_sh_ab.json;
+  // HSDLA_MERGE_SH=0: off).  Builds that copy H, S to the host keep the separate launches: there
+  // the S copy overlaps the H contraction, and the PCIe-bound step measured 0.2 ms faster.
   static int merge_env = -1;
   if (merge_env < 0) {
     const char* e = getenv("HSDLA_MERGE_SH");
@@ -883,7 +885,7 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
   }
   // Decided before S on the template path (so every build of the same inputs takes the same
   // launch structure and results stay bitwise reproducible between first and later builds).
-  const bool early = merge_env && tpl && !pl && !host_src && key.joint;
+  const bool early = merge_env && tpl && !pl && !host_src && key.joint && !sl.copies;
   bool merged = false;
   // Which H form each T set takes is a host decision (it fixes the K extents of the H
   // contraction): after a fresh T preparation, wait for it alone — it ran on the side streams

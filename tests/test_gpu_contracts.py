@@ -521,8 +521,9 @@ def test_compute_ab_device_resident_drop_in(pkg):
 ])
 def test_kernel_variants_match_oracle(pkg, tmp_path, env):
     """The library's measured-but-not-default variants (switches read once per process, so each
-    runs in a child) still compute the right H and S: the device pipeline on C2 (template path,
-    joint form) and the drop-in build_all on C1, against the oracle at 1e-12."""
+    runs in a child) still compute the right H and S: the device-resident pipeline on C2
+    (template path, joint form, merged S + H launch unless switched off) and the drop-in
+    build_all on C1, against the oracle at 1e-12."""
     import os
     import subprocess
     import sys
@@ -534,12 +535,15 @@ def test_kernel_variants_match_oracle(pkg, tmp_path, env):
         "import sys, numpy as np; sys.path.insert(0, '.')\n"
         "import paper_1602_06589_b200 as pkg\n"
         "from paper_1602_06589_b200 import configs\n"
-        "from paper_1602_06589_b200.pipeline import build_hs\n"
+        "from paper_1602_06589_b200.pipeline import DeviceSpec, HSPipeline, pack_tmats\n"
         "c2 = configs.make_instance('C2')\n"
-        "h2, s2, r2 = build_hs(c2.spec, c2.tmats)\n"
+        "d2 = DeviceSpec(c2.spec)\n"
+        "pipe = HSPipeline(c2.spec.n_basis, d2.heights)\n"
+        "r2 = pipe.run(d2, pack_tmats(c2.tmats))\n"
+        "h2, s2 = (x.cpu().numpy().T for x in pipe.result_views())\n"
         "c1 = configs.make_instance('C1')\n"
         "h1, s1, _ = pkg.build_all(pkg.compute_AB(c1.spec), c1.tmats, pkg.BuildConfig())\n"
-        "np.savez(sys.argv[1], h2=h2.array, s2=s2.array, h1=h1.array, s1=s1.array,\n"
+        "np.savez(sys.argv[1], h2=h2, s2=s2, h1=h1.array, s1=s1.array,\n"
         "         types=r2['template_types'], merged=r2['merged_sh'])\n")
     out = tmp_path / "variant.npz"
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -560,16 +564,26 @@ def test_kernel_variants_match_oracle(pkg, tmp_path, env):
 
 
 def test_merged_launch_reproducible(pkg):
-    """The template path's merged S + H contraction is taken on the first build of a T set as
-    well as on builds reusing it, so repeated builds of the same inputs are bitwise identical;
-    the merged launch replaces the separate S launch (one fewer kernel per k-point)."""
+    """Device-resident template-path builds take the merged S + H contraction on the first
+    build of a T set as well as on builds reusing it, so repeated builds of the same inputs
+    are bitwise identical; builds with host copies keep the separate S and H launches."""
     from paper_1602_06589_b200 import configs
-    from paper_1602_06589_b200.pipeline import build_hs_many
+    from paper_1602_06589_b200.pipeline import DeviceSpec, HSPipeline, _pinned_pair, pack_tmats
 
     inst = configs.make_instance("C2")
-    got = []
-    res = build_hs_many([inst.spec, inst.spec], inst.tmats,
-                        on_result=lambda i, h, s, r: got.append((h.array.copy(), s.array.copy())))
-    assert [r["merged_sh"] for r in res] == [True, True]
-    assert np.array_equal(got[0][0], got[1][0]) and np.array_equal(got[0][1], got[1][1])
-    assert res[1]["kernel_ms"]["contract_H"] > 0
+    dspec = DeviceSpec(inst.spec)
+    tpack = pack_tmats(inst.tmats)
+    pipe = HSPipeline(inst.spec.n_basis, dspec.heights)
+    r1 = pipe.run(dspec, tpack)
+    h1, s1 = (x.cpu().clone() for x in pipe.result_views())
+    r2 = pipe.run(dspec, tpack)
+    h2, s2 = (x.cpu().clone() for x in pipe.result_views())
+    assert r1["merged_sh"] and r2["merged_sh"]
+    assert r1["kernel_ms"]["contract_H"] > 0
+    assert bool((h1 == h2).all()) and bool((s1 == s2).all())
+    n = inst.spec.n_basis
+    host = _pinned_pair(n)
+    r3 = pipe.run(dspec, tpack, host_out=host)
+    assert not r3["merged_sh"]
+    for got, want in ((host[0], h1), (host[1], s1)):
+        assert float((got - want).abs().max()) <= 1e-12 * float(want.abs().max())

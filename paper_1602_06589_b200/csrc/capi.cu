@@ -1054,16 +1054,26 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     HS_CUDA(cudaMalloc(&sl.panel_cnt, size_t(2) * nbp * sizeof(int)));
     sl.panel_cap = nbp;
   }
+  // Copies go out in groups of HSDLA_COPY_PANELS panels (default 4, 256 columns): each copy
+  // submission costs the copy engine a gap, so per-panel copies ran the link at 47 GB/s
+  // against 54 GB/s for whole-matrix copies (profiles/r02_single_call.json).
+  static int copy_group = -1;
+  if (copy_group < 0) {
+    const char* e = getenv("HSDLA_COPY_PANELS");
+    copy_group = e ? std::max(1, atoi(e)) : 4;
+  }
   auto stream_out = [&](const double2* C, hsdla_c64* host, int* cnt, cudaEvent_t done_ev) -> int {
     HS_CUDA(cudaMemsetAsync(cnt, 0, size_t(nbp) * sizeof(int), ctx->stream));
     HS_CUDA(cudaEventRecord(ctx->copy_go, ctx->stream));
     HS_CUDA(cudaStreamWaitEvent(ctx->copy, ctx->copy_go, 0));
-    for (int p = 0; p < nbp; ++p) {
-      const int c0 = p * kTile, nc = std::min(kTile, n - c0);
-      if (waitv(ctx->copy, reinterpret_cast<unsigned long long>(cnt + p), (unsigned)nbp, kWaitGeq) != 0) {
-        set_error("cuStreamWaitValue32 failed");
-        return HSDLA_ERR_CUDA;
-      }
+    for (int p0 = 0; p0 < nbp; p0 += copy_group) {
+      const int p1 = std::min(nbp, p0 + copy_group);
+      for (int p = p0; p < p1; ++p)
+        if (waitv(ctx->copy, reinterpret_cast<unsigned long long>(cnt + p), (unsigned)nbp, kWaitGeq) != 0) {
+          set_error("cuStreamWaitValue32 failed");
+          return HSDLA_ERR_CUDA;
+        }
+      const int c0 = p0 * kTile, nc = std::min(p1 * kTile, n) - c0;
       HS_CUDA(cudaMemcpy2DAsync(host + (long long)c0 * a->ldh_host, size_t(a->ldh_host) * sizeof(hsdla_c64),
                                 C + (long long)c0 * a->ldh, size_t(a->ldh) * sizeof(double2),
                                 size_t(n) * sizeof(double2), nc, cudaMemcpyDeviceToHost, ctx->copy));

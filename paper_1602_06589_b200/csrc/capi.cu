@@ -672,6 +672,15 @@ int complete_slot(hsdla_ctx* ctx, hsdla_ctx::BuildSlot& sl, hsdla_ctx::Outcome* 
     }
     fprintf(stderr, "build %llu: start %.3f S-done %.3f H-done %.3f end %.3f S-copied %.3f H-copied %.3f ms\n",
             sl.ticket, a0, a2, a6, a7, sc, hc);
+    if (!sl.group_ev.empty()) {
+      fprintf(stderr, "  group copies done (ms after start):");
+      for (auto e : sl.group_ev) {
+        float t = 0;
+        cudaEventElapsedTime(&t, ev[0], e);
+        fprintf(stderr, " %.2f", t);
+      }
+      fprintf(stderr, "\n");
+    }
   }
   o->rc = nan_input ? HSDLA_ERR_NAN_INPUT : (o->nonfinite ? HSDLA_ERR_NONFINITE : HSDLA_OK);
   return o->rc;
@@ -1054,8 +1063,8 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     HS_CUDA(cudaMalloc(&sl.panel_cnt, size_t(2) * nbp * sizeof(int)));
     sl.panel_cap = nbp;
   }
-  // Copies go out in groups of HSDLA_COPY_PANELS panels (default 4, 256 columns): each copy
-  // submission costs the copy engine a gap, so per-panel copies ran the link at 47 GB/s
+  // Copies go out in groups of HSDLA_COPY_PANELS tile columns (default 4, 256 columns): each
+  // copy submission costs the copy engine a gap, so per-panel copies ran the link at 47 GB/s
   // against 54 GB/s for whole-matrix copies (profiles/r02_single_call.json).
   static int copy_group = -1;
   if (copy_group < 0) {
@@ -1066,17 +1075,51 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     HS_CUDA(cudaMemsetAsync(cnt, 0, size_t(nbp) * sizeof(int), ctx->stream));
     HS_CUDA(cudaEventRecord(ctx->copy_go, ctx->stream));
     HS_CUDA(cudaStreamWaitEvent(ctx->copy, ctx->copy_go, 0));
+    // Group g = lower tile columns [p0, p1), ready when they are finished (cnt[p] = nb - p
+    // tiles; tiles run in column-major order).  Two copy shapes:
+    //  * L (compute-bound builds): the group's tiles and mirrors fill host columns [c0, c1)
+    //    from row c0 down (runs of n - c0 elements) and host rows [c0, c1) right of column
+    //    c1 (runs of c1 - c0 elements), so the copy tracks the finished tiles.
+    //  * panels (copy-bound builds): host columns [c0, c1) whole (their upper parts are
+    //    mirrors of earlier columns' tiles): one contiguous copy at the link's full rate, but
+    //    the last half of the panels waits for the last quarter of the tiles.
+    // The contraction outlasts the copy (PCIe ~55 GB/s vs 3-product DMMA at ~32 TF/s) when
+    // R >= 1536: then L (C3 single call 126.3 -> 122.7 ms); below, panels (C2: L's shorter
+    // runs under the kernel's load copied at ~45 GB/s, 7.08 vs 6.77 ms).  HSDLA_LCOPY=0/1.
+    static int lcopy_env = -2;
+    if (lcopy_env == -2) {
+      const char* e = getenv("HSDLA_LCOPY");
+      lcopy_env = e ? atoi(e) : -1;
+    }
+    const bool lshape = lcopy_env >= 0 ? lcopy_env != 0 : w.R >= 1536;
+    const size_t hp = size_t(a->ldh_host) * sizeof(hsdla_c64), dp = size_t(a->ldh) * sizeof(double2);
+    static const bool tl = getenv("HSDLA_TIMELINE") != nullptr;
+    if (tl && cnt == sl.panel_cnt) {  // S first (H appends): at most 2 x nbp groups
+      for (auto e : sl.group_ev) cudaEventDestroy(e);
+      sl.group_ev.clear();
+    }
     for (int p0 = 0; p0 < nbp; p0 += copy_group) {
       const int p1 = std::min(nbp, p0 + copy_group);
       for (int p = p0; p < p1; ++p)
-        if (waitv(ctx->copy, reinterpret_cast<unsigned long long>(cnt + p), (unsigned)nbp, kWaitGeq) != 0) {
+        if (waitv(ctx->copy, reinterpret_cast<unsigned long long>(cnt + p), (unsigned)(nbp - p), kWaitGeq) != 0) {
           set_error("cuStreamWaitValue32 failed");
           return HSDLA_ERR_CUDA;
         }
-      const int c0 = p0 * kTile, nc = std::min(p1 * kTile, n) - c0;
-      HS_CUDA(cudaMemcpy2DAsync(host + (long long)c0 * a->ldh_host, size_t(a->ldh_host) * sizeof(hsdla_c64),
-                                C + (long long)c0 * a->ldh, size_t(a->ldh) * sizeof(double2),
-                                size_t(n) * sizeof(double2), nc, cudaMemcpyDeviceToHost, ctx->copy));
+      const long long c0 = (long long)p0 * kTile, c1 = std::min<long long>((long long)p1 * kTile, n);
+      const long long r0 = lshape ? c0 : 0;
+      HS_CUDA(cudaMemcpy2DAsync(host + r0 + c0 * a->ldh_host, hp, C + r0 + c0 * a->ldh, dp,
+                                size_t(n - r0) * sizeof(double2), size_t(c1 - c0),
+                                cudaMemcpyDeviceToHost, ctx->copy));
+      if (lshape && c1 < n)
+        HS_CUDA(cudaMemcpy2DAsync(host + c0 + c1 * a->ldh_host, hp, C + c0 + c1 * a->ldh, dp,
+                                  size_t(c1 - c0) * sizeof(double2), size_t(n - c1),
+                                  cudaMemcpyDeviceToHost, ctx->copy));
+      if (tl) {
+        cudaEvent_t e;
+        HS_CUDA(cudaEventCreate(&e));
+        HS_CUDA(cudaEventRecord(e, ctx->copy));
+        sl.group_ev.push_back(e);
+      }
     }
     HS_CUDA(cudaEventRecord(done_ev, ctx->copy));
     return HSDLA_OK;

@@ -105,9 +105,9 @@ struct Prob {
   long long it_base;     // first stream-K iteration (tile-chunk) of this problem
   int col_tile_lo, col_tile_hi;  // tri only: restrict to tile columns [lo, hi) (sharding)
   double2 alpha, beta;
-  // TRI_MIRROR only, or nullptr: per 64-column panel, the count of finished tiles that wrote
-  // into it (tile (i, j) writes panel j and, mirrored, panel i).  Panel p is complete at
-  // tiles_m; a copy stream streams finished panels to the host while the kernel runs.
+  // TRI_MIRROR only, or nullptr: per lower tile column, the count of its finished tiles
+  // (column tn is complete at tiles_m - tn); a copy stream copies finished columns' tiles and
+  // mirrors to the host while the kernel runs.
   int* panel_done;
 };
 
@@ -164,6 +164,7 @@ struct hsdla_ctx {
     int merged = 0;          // S and H in one contraction launch
     const void* h_dev = nullptr;  // this build's device H / S (copy hazards of the next build)
     const void* s_dev = nullptr;
+    std::vector<cudaEvent_t> group_ev;  // debug (HSDLA_TIMELINE): end of each streamed group copy
   } slots[2];
   unsigned long long seq = 0;
   // Outcomes of builds completed before their ticket was finished (more than two in flight).

@@ -567,7 +567,6 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), MINB)
       if (tid == 0) {
         __threadfence_system();
         atomicAdd(pr.panel_done + tn, 1);
-        if (tm != tn) atomicAdd(pr.panel_done + tm, 1);
       }
     }
   }

@@ -524,7 +524,6 @@ __global__ void __launch_bounds__(C::kT, 2) contract_tma_kernel(TKParams sk) {
       if (tid == 0) {
         __threadfence_system();
         atomicAdd(pr.panel_done + tn, 1);
-        if (tm != tn) atomicAdd(pr.panel_done + tm, 1);
       }
     }
   }

@@ -250,6 +250,31 @@ def hbm_peak_gbs():
         return 6550.0, "SURVEY.md 8d measured copy bandwidth"
 
 
+_WRITE_CEILING = {}
+
+
+def write_ceiling_gbs(nbytes):
+    """Measured write-only HBM rate for a pass of `nbytes` (torch fill_ of that many bytes, best
+    of 8, CUDA events): the ceiling a write-only kernel of that size can reach on this box.
+    Short passes do not reach the copy-bandwidth peak (ramp-up and tail): C2's 124 MB fill
+    runs at ~5.0 TB/s, a 1.3 GB one at ~7.2 TB/s (profiles/r02_expand_variants.json)."""
+    if nbytes in _WRITE_CEILING:
+        return _WRITE_CEILING[nbytes]
+    import torch
+    x = torch.empty(max(1, nbytes // 16), dtype=torch.complex128, device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = float("inf")
+    for _ in range(8):
+        e0.record()
+        x.fill_(1.0)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del x
+    _WRITE_CEILING[nbytes] = round(nbytes / (best / 1e3) / 1e9, 1)
+    return _WRITE_CEILING[nbytes]
+
+
 def ab_gen_line(ms, rows, n, template_types=0, expand_w_ms=None, templates_ms=None):
     """A/B generation against the HBM-write roofline.  Per-atom path: the
     generator writes A*, B* and ||udot|| B* (48 R N bytes).  Template path: the
@@ -269,14 +294,21 @@ def ab_gen_line(ms, rows, n, template_types=0, expand_w_ms=None, templates_ms=No
         # the HBM-bound part alone: the expansion writing A*, ||udot|| B* after the templates
         xm = ms - templates_ms
         xg = written / (xm / 1e3) / 1e9
+        wc = write_ceiling_gbs(written)
         out["templates_ms"] = round(templates_ms, 4)
         out["expand_AB"] = {"ms": round(xm, 4), "bytes_written": written,
-                            "achieved_gbs": round(xg, 1), "frac": round(xg / peak, 4)}
+                            "achieved_gbs": round(xg, 1), "frac": round(xg / peak, 4),
+                            "write_ceiling_gbs": wc, "frac_of_write_ceiling": round(xg / wc, 4)}
     if template_types and expand_w_ms:
         w = 32 * rows * n
         wg = w / (expand_w_ms / 1e3) / 1e9
+        wc = write_ceiling_gbs(w)
         out["expand_W"] = {"ms": round(expand_w_ms, 4), "bytes_written": w,
-                           "achieved_gbs": round(wg, 1), "frac": round(wg / peak, 4)}
+                           "achieved_gbs": round(wg, 1), "frac": round(wg / peak, 4),
+                           "write_ceiling_gbs": wc, "frac_of_write_ceiling": round(wg / wc, 4)}
+    if template_types:
+        out["write_ceiling_source"] = ("torch fill_ of the same byte count on this GPU, best of 8 "
+                                       "(a write-only pass of that size cannot beat it)")
     return out
 
 

@@ -14,7 +14,7 @@ python bench.py --mode panels --config C4 --steps 3 > gpurun_out/ev2/bench_panel
 CMD="python bench.py --steps 2 --warmup 3 --no-extras --no-cpu-baseline"
 $CMD > gpurun_out/ev2/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/ev2/launches_C2.csv $CMD > /dev/null 2>&1
-ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum -k regex:contract -c 12 --clock-control none --csv --log-file gpurun_out/ev2/traffic_C2.csv python bench.py --steps 1 --warmup 3 --no-extras --no-cpu-baseline > /dev/null 2>&1
+ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum -k regex:contract -c 8 --clock-control none --csv --log-file gpurun_out/ev2/traffic_C2.csv python bench.py --steps 1 --warmup 3 --no-extras --no-cpu-baseline > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"contract_kernel" -s 4 -c 1 -o gpurun_out/ev2/ncu_SH_C2 $CMD > /dev/null 2>&1
 python -m pytest tests -m gpu -q 2>&1 | tail -3 > gpurun_out/ev2/pytest_gpu_2.log
 ls gpurun_out/ev2

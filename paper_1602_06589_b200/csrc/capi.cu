@@ -1100,11 +1100,13 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     }
     for (int p0 = 0; p0 < nbp; p0 += copy_group) {
       const int p1 = std::min(nbp, p0 + copy_group);
-      for (int p = p0; p < p1; ++p)
-        if (waitv(ctx->copy, reinterpret_cast<unsigned long long>(cnt + p), (unsigned)(nbp - p), kWaitGeq) != 0) {
-          set_error("cuStreamWaitValue32 failed");
-          return HSDLA_ERR_CUDA;
-        }
+      // one counter per group: its tile columns' tiles (sum of nb - p), one wait per copy
+      unsigned need = 0;
+      for (int p = p0; p < p1; ++p) need += (unsigned)(nbp - p);
+      if (waitv(ctx->copy, reinterpret_cast<unsigned long long>(cnt + p0 / copy_group), need, kWaitGeq) != 0) {
+        set_error("cuStreamWaitValue32 failed");
+        return HSDLA_ERR_CUDA;
+      }
       const long long c0 = (long long)p0 * kTile, c1 = std::min<long long>((long long)p1 * kTile, n);
       const long long r0 = lshape ? c0 : 0;
       HS_CUDA(cudaMemcpy2DAsync(host + r0 + c0 * a->ldh_host, hp, C + r0 + c0 * a->ldh, dp,
@@ -1155,7 +1157,7 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     if ((rc = make_bs())) return rc;
     std::vector<Seg> segs{make_seg(Bs, ld, Bs, ld, (int)R)};
     std::vector<Prob> probs{make_prob(D2(a->S), a->ldh, n, n, PROB_TRI_MIRROR, 0, 1, 1)};
-    if (s_streamed) probs[0].panel_done = sl.panel_cnt;
+    if (s_streamed) { probs[0].panel_done = sl.panel_cnt; probs[0].panel_group = copy_group; }
     if ((rc = launch_contract(ctx, probs, segs, flag))) return rc;
   } else if (!merged) {
     std::vector<Seg> segs{make_seg(A, ld, A, ld, (int)R), make_seg(Bs, ld, Bs, ld, (int)R)};
@@ -1163,7 +1165,7 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
       segs = {make_seg_planes(A, Ad, ld, A, As, ld, (int)R), make_seg_planes(Bs, Ud, ld, Bs, Us, ld, (int)R)};
     std::vector<Prob> probs;
     add_tri(probs, D2(a->S), 0, 2);
-    if (s_streamed) probs[0].panel_done = sl.panel_cnt;
+    if (s_streamed) { probs[0].panel_done = sl.panel_cnt; probs[0].panel_group = copy_group; }
     rc = launch_contract(ctx, probs, segs, flag);
     if (rc) return rc;
   }
@@ -1342,11 +1344,11 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
       segs.push_back(make_seg(A, ld, A, ld, (int)R));
       segs.push_back(make_seg(Bs, ld, Bs, ld, (int)R));
       add_tri(probs, D2(a->S), s0, 2);
-      if (s_streamed) probs.back().panel_done = sl.panel_cnt;
+      if (s_streamed) { probs.back().panel_done = sl.panel_cnt; probs.back().panel_group = copy_group; }
     }
     const size_t h0 = probs.size();
     add_tri(probs, D2(a->H), 0, merged ? (int)segs.size() - 2 : (int)segs.size());
-    if (h_streamed) probs[h0].panel_done = sl.panel_cnt + nbp;
+    if (h_streamed) { probs[h0].panel_done = sl.panel_cnt + nbp; probs[h0].panel_group = copy_group; }
     rc = launch_contract(ctx, probs, segs, flag);
     if (rc) return rc;
     if (merged && !s_streamed) {

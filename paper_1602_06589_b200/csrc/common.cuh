@@ -105,10 +105,12 @@ struct Prob {
   long long it_base;     // first stream-K iteration (tile-chunk) of this problem
   int col_tile_lo, col_tile_hi;  // tri only: restrict to tile columns [lo, hi) (sharding)
   double2 alpha, beta;
-  // TRI_MIRROR only, or nullptr: per lower tile column, the count of its finished tiles
-  // (column tn is complete at tiles_m - tn); a copy stream copies finished columns' tiles and
-  // mirrors to the host while the kernel runs.
+  // TRI_MIRROR only, or nullptr: per group of panel_group lower tile columns, the count of its
+  // finished tiles (the group of columns [p0, p1) is complete at the sum of tiles_m - tn); a
+  // copy stream waits on each group's counter (one stream wait per copy) and copies the group's
+  // finished tiles and mirrors to the host while the kernel runs.
   int* panel_done;
+  int panel_group;  // tile columns per counter (panel_done[tn / panel_group]); 0 = 1
 };
 
 constexpr int kTile = 64;  // complex outputs per CTA tile edge

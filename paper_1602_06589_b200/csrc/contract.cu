@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), MINB)
       __syncthreads();
       if (tid == 0) {
         __threadfence_system();
-        atomicAdd(pr.panel_done + tn, 1);
+        atomicAdd(pr.panel_done + (pr.panel_group > 1 ? tn / pr.panel_group : tn), 1);
       }
     }
   }

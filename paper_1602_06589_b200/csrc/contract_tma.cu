@@ -523,7 +523,7 @@ __global__ void __launch_bounds__(C::kT, 2) contract_tma_kernel(TKParams sk) {
       __syncthreads();
       if (tid == 0) {
         __threadfence_system();
-        atomicAdd(pr.panel_done + tn, 1);
+        atomicAdd(pr.panel_done + (pr.panel_group > 1 ? tn / pr.panel_group : tn), 1);
       }
     }
   }

@@ -1049,9 +1049,9 @@ int enqueue_build(hsdla_ctx* ctx, const hsdla_build_args* a, const hsdla_ab_args
     return HSDLA_OK;
   };
   // Streamed variant, enqueued BEFORE the contraction that produces C: the copy stream waits
-  // (cuStreamWaitValue32) for each 64-column panel's tile counter to reach nb and copies the
-  // finished panel while the kernel is still computing the rest (the contraction epilogue
-  // publishes finished tiles, Prob::panel_done).
+  // (cuStreamWaitValue32) for each group of tile columns' tile counter to reach its tile count
+  // and copies the group's finished part while the kernel is still computing the rest (the
+  // contraction epilogue publishes finished tiles, Prob::panel_done / panel_group).
   const int nbp = (n + kTile - 1) / kTile;
   const bool want_stream = a->stream_h_copy > 0 || (a->stream_h_copy == 0 && stream_copies);
   WaitValueFn waitv = (sharded || !sl.copies || !want_stream) ? nullptr : wait_value_fn();

@@ -562,7 +562,8 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), MINB)
     if (bad) atomicOr(sk.flag, 1);
     if (pr.panel_done) {
       // Publish the finished tile to the streaming copy: the barrier orders every thread's
-      // stores before thread 0's system-scope fence (cumulative), then the panel counters.
+      // stores before thread 0's system-scope fence (cumulative), then its column group's
+      // counter (Prob::panel_group tile columns per counter).
       __syncthreads();
       if (tid == 0) {
         __threadfence_system();

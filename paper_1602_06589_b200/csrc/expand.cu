@@ -48,10 +48,10 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 __global__ void __launch_bounds__(kExThreads) expand_kernel(ExpandParams p) {
   __shared__ double2 ph[kExCols];
   __shared__ double urow[kMaxRows];
-  const int4 at = p.atoms[blockIdx.y];
+  const int4 at = p.atoms[blockIdx.x];
   const int a = at.x, toff = at.y, m = at.z;
-  const long long off = p.off[blockIdx.y];
-  const int t0 = blockIdx.x * kExCols;
+  const long long off = p.off[blockIdx.x];
+  const int t0 = blockIdx.y * kExCols;
   const int ncol = min(kExCols, p.n_basis - t0);
   if (threadIdx.x < ncol) {
     const int t = t0 + threadIdx.x;
@@ -118,7 +118,9 @@ int launch_expand(hsdla_ctx* ctx, int n_basis, const double* kv, const double* p
   p.ldt = ldt;
   p.o = o;
   p.ld = ld;
-  dim3 grid((n_basis + kExCols - 1) / kExCols, n_blocks);
+  // atoms fastest: the CTAs resident at a time fill whole stacked columns (every atom's rows
+  // of the same few column blocks), so the writes stream through contiguous HBM
+  dim3 grid(n_blocks, (n_basis + kExCols - 1) / kExCols);
   expand_kernel<<<grid, kExThreads, 0, ctx->stream>>>(p);
   HS_CHECK_LAUNCH();
   return HSDLA_OK;

@@ -39,6 +39,7 @@ struct ExpandParams {
   long long ldt;
   ExpandOut o;
   long long ld;
+  int atoms_fast;  // grid x = atom blocks (else x = column blocks)
 };
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
@@ -48,10 +49,11 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 __global__ void __launch_bounds__(kExThreads) expand_kernel(ExpandParams p) {
   __shared__ double2 ph[kExCols];
   __shared__ double urow[kMaxRows];
-  const int4 at = p.atoms[blockIdx.x];
+  const int ab = p.atoms_fast ? blockIdx.x : blockIdx.y;  // atom block
+  const int4 at = p.atoms[ab];
   const int a = at.x, toff = at.y, m = at.z;
-  const long long off = p.off[blockIdx.x];
-  const int t0 = blockIdx.y * kExCols;
+  const long long off = p.off[ab];
+  const int t0 = (p.atoms_fast ? blockIdx.y : blockIdx.x) * kExCols;
   const int ncol = min(kExCols, p.n_basis - t0);
   if (threadIdx.x < ncol) {
     const int t = t0 + threadIdx.x;
@@ -118,9 +120,12 @@ int launch_expand(hsdla_ctx* ctx, int n_basis, const double* kv, const double* p
   p.ldt = ldt;
   p.o = o;
   p.ld = ld;
-  // atoms fastest: the CTAs resident at a time fill whole stacked columns (every atom's rows
-  // of the same few column blocks), so the writes stream through contiguous HBM
-  dim3 grid(n_blocks, (n_basis + kExCols - 1) / kExCols);
+  // Many atoms (> 32): atoms fastest, so the CTAs resident at a time fill whole stacked columns
+  // (C4 1.82 -> 1.50 ms, C3 -4%); few atoms: column blocks fastest (C2 30 vs 36 us per pass,
+  // profiles/r02_expand_variants.json).
+  p.atoms_fast = n_blocks > 32 ? 1 : 0;
+  const int ncb = (n_basis + kExCols - 1) / kExCols;
+  dim3 grid = p.atoms_fast ? dim3(n_blocks, ncb) : dim3(ncb, n_blocks);
   expand_kernel<<<grid, kExThreads, 0, ctx->stream>>>(p);
   HS_CHECK_LAUNCH();
   return HSDLA_OK;

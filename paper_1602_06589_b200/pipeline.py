@@ -36,25 +36,42 @@ def padded_ld(rows: int) -> int:
 _UPLOAD = {}
 
 
+_TORCH_DTYPE = {}  # numpy dtype string -> torch dtype (filled on first use)
+
+
 def _to_device(arrays):
     """Upload host arrays through pinned staging on a dedicated upload stream, so the
     copies run at once instead of queueing behind kernels already enqueued on the compute
     stream (k-point pipelining); the compute stream waits on an event.  Returns (device
     tensors, pinned staging tensors that must stay alive until the copies ran)."""
     t = device.torch()
+    if not _TORCH_DTYPE:
+        _TORCH_DTYPE.update({"<f8": t.float64, "<c16": t.complex128, "<i4": t.int32,
+                             "<i8": t.int64})
     dev = t.cuda.current_device()
     up = _UPLOAD.get(dev)
     if up is None:
         up = _UPLOAD[dev] = t.cuda.Stream()
     main = t.cuda.current_stream()
-    staged = [t.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in arrays]
+    # one pinned staging buffer and one copy for all of them (each array's bytes at a
+    # 256-byte aligned offset); the device tensors are typed views of one allocation
+    arrays = [np.ascontiguousarray(a) for a in arrays]
+    offs, n = [], 0
+    for a in arrays:
+        offs.append(n)
+        n += (a.nbytes + 255) // 256 * 256
+    staged = t.empty(max(n, 1), dtype=t.uint8, pin_memory=True)
+    host = staged.numpy()
+    for a, o in zip(arrays, offs):
+        host[o:o + a.nbytes] = a.reshape(-1).view(np.uint8)
     with t.cuda.stream(up):
-        out = [s.to("cuda", non_blocking=True) for s in staged]
+        whole = staged.to("cuda", non_blocking=True)
         done = t.cuda.Event()
         done.record(up)
     main.wait_event(done)
-    for o in out:
-        o.record_stream(main)
+    whole.record_stream(main)
+    out = [whole[o:o + a.nbytes].view(_TORCH_DTYPE[a.dtype.str]).view(a.shape)
+           for a, o in zip(arrays, offs)]
     return out, staged
 
 
@@ -150,11 +167,8 @@ class DeviceSpec:
         radial = np.zeros((self.n_atoms, stride, 5))
         for a, rad in enumerate(spec.radial):
             n = int(self.l_sph[a]) + 1
-            radial[a, :n, 0] = rad.u[:n]
-            radial[a, :n, 1] = rad.u_prime[:n]
-            radial[a, :n, 2] = rad.udot[:n]
-            radial[a, :n, 3] = rad.udot_prime[:n]
-            radial[a, :n, 4] = rad.udot_norm[:n]
+            radial[a, :n] = np.stack((rad.u[:n], rad.u_prime[:n], rad.udot[:n], rad.udot_prime[:n],
+                                      rad.udot_norm[:n]), axis=-1)
         self.radial_stride = stride
         # ||udot|| per stacked row (l^2 + l + m order): the joint form's shift metric
         self.udot_rows = np.concatenate([np.repeat(np.asarray(spec.radial[a].udot_norm[:l + 1], dtype=np.float64),

@@ -193,6 +193,123 @@ __global__ void __launch_bounds__(kAbThreads) ab_kernel(AbParams p, const int* _
   (void)live;
 }
 
+// Per-type templates (zero_phase launches, a handful of atom blocks): one WARP per
+// (K-vector, atom block), lane m in [0, L] evaluating the Legendre chain of its own m over
+// l = m..L and writing rows l^2 + l +- m of A and B.  The per-K scalars (direction, Bessel
+// values, match factors) are evaluated by every lane alike, so the dependent chain per lane is
+// the prologue plus one m-chain instead of all (l, m) pairs, and C2's 2999 K-vectors give
+// ~3000 warps instead of 24 CTAs with one warp per SM sub-partition (which left the unrolled
+// kernel instruction-fetch bound, profiles/r02_ncu_abgen_template_stalls.txt).  Every
+// value is computed by the same operations in the same order as ab_kernel (the file is built
+// with -fmad=false): the templates are bitwise those of ab_kernel.
+constexpr int kTplWarps = 4;
+template <int L>
+__global__ void __launch_bounds__(32 * kTplWarps) ab_tpl_kernel(AbParams p, const int* __restrict__ atoms,
+                                                               const long long* __restrict__ row_off,
+                                                               int count) {
+  const int lane = threadIdx.x & 31;
+  const long long item = (long long)blockIdx.x * kTplWarps + (threadIdx.x >> 5);
+  if (item >= (long long)count * p.n_basis) return;  // warp-uniform
+  const int blk = (int)(item / p.n_basis);
+  const int t = (int)(item - (long long)blk * p.n_basis);
+  const int a = atoms[blk];
+  const long long off = row_off[blk];
+  const int mm = lane;  // this lane's m (lanes > L idle after the shared prologue)
+  const double* rad = p.radial + (long long)a * p.radial_stride * 5;
+
+  const double kx = p.kv[3 * t + 0], ky = p.kv[3 * t + 1], kz = p.kv[3 * t + 2];
+  const double kn = sqrt(kx * kx + ky * ky + kz * kz);
+  double ux = 0.0, uy = 0.0, uz = 1.0;
+  if (kn > 0.0) { ux = kx / kn; uy = ky / kn; uz = kz / kn; }
+  const double* R = p.rot + 9 * a;
+  double lx = ux * R[0] + uy * R[1] + uz * R[2];
+  double ly = ux * R[3] + uy * R[4] + uz * R[5];
+  double lz = ux * R[6] + uy * R[7] + uz * R[8];
+  const double ln = sqrt(lx * lx + ly * ly + lz * lz);
+  lx /= ln; ly /= ln; lz /= ln;
+  const double ct = fmin(fmax(lz, -1.0), 1.0);
+  const double st = sqrt(fmax(0.0, 1.0 - ct * ct));
+  double ephr, ephi;
+  sincos(atan2(ly, lx), &ephi, &ephr);
+  constexpr int LT = L + 1;
+  const double x = p.rmt[a] * kn;
+  double jv[LT + 1];
+  double jd[L + 1];
+  bessel::bessel_jd<L>(x, jv, jd);
+  const double* X = p.pos + 3 * a;
+  const double th = p.zero_phase ? 0.0 : kx * X[0] + ky * X[1] + kz * X[2];
+  double phs, phc;
+  sincos(th, &phs, &phc);
+  const double sqo = sqrt(p.omega);
+  const double fourpi = 4.0 * 3.141592653589793;
+  if (mm > L) return;
+
+  // e^{i m phi}: the running product up to this lane's m (ab_kernel's emr / emi chain)
+  double emr = 1.0, emi = 0.0;
+#pragma unroll
+  for (int m = 1; m <= L; ++m) {
+    if (m > mm) break;
+    const double r0 = emr * ephr - emi * ephi;
+    const double i0 = emr * ephi + emi * ephr;
+    emr = r0;
+    emi = i0;
+  }
+  // sectoral seed P_{m,m} (ab_kernel's m == l branch, chained over m' <= m)
+  double p1 = 0.0, p2 = 0.0;  // P_{l-1,m}, P_{l-2,m}
+  double seed = 0.28209479177387814;
+#pragma unroll
+  for (int m = 1; m <= L; ++m) {
+    if (m > mm) break;
+    seed = -c_sect[m] * st * seed;
+  }
+  double2* const Ac = p.A + (long long)t * p.ld + off;
+  double2* const Bc = p.B + (long long)t * p.ld + off;
+  const double sg = (mm & 1) ? -1.0 : 1.0;
+#pragma unroll
+  for (int l = 0; l <= L; ++l) {
+    if (l < mm) continue;
+    const double u = rad[5 * l + 0], up = rad[5 * l + 1], ud = rad[5 * l + 2], udp = rad[5 * l + 3];
+    const double w = ud * up - u * udp;
+    const double cl = fourpi / (sqo * w);
+    double zr, zi;
+    switch (l & 3) {
+      case 0: zr = phc; zi = phs; break;
+      case 1: zr = -phs; zi = phc; break;
+      case 2: zr = -phc; zi = -phs; break;
+      default: zr = phs; zi = -phc; break;
+    }
+    const double prr = cl * zr, pri = cl * zi;
+    const double fa = ud * kn * jd[l] - udp * jv[l];
+    const double fb = -u * kn * jd[l] + up * jv[l];
+    const double par = prr * fa, pai = pri * fa;
+    const double pbr = prr * fb, pbi = pri * fb;
+    double pl;
+    if (l == mm) pl = seed;
+    else if (l == mm + 1) pl = c_sub[mm] * ct * p1;
+    else pl = c_a[l][mm] * (ct * p1 - c_b[l][mm] * p2);
+    const double yr = pl * emr, yi = pl * emi;
+    Ac[l * l + l + mm] = make_double2(yr * par + yi * pai, yr * pai + (-yi) * par);
+    Bc[l * l + l + mm] = make_double2(yr * pbr + yi * pbi, yr * pbi + (-yi) * pbr);
+    if (mm > 0) {
+      const double qr = sg * yr, qi = -(sg * yi);
+      Ac[l * l + l - mm] = make_double2(qr * par + qi * pai, qr * pai + (-qi) * par);
+      Bc[l * l + l - mm] = make_double2(qr * pbr + qi * pbi, qr * pbi + (-qi) * pbr);
+    }
+    p2 = p1;
+    p1 = pl;
+  }
+}
+
+template <int L>
+int launch_ab_tpl(hsdla_ctx* ctx, const AbParams& p, const int* atoms_dev, const long long* off_dev,
+                  int count) {
+  const long long items = (long long)count * p.n_basis;
+  const int grid = (int)((items + kTplWarps - 1) / kTplWarps);
+  ab_tpl_kernel<L><<<grid, 32 * kTplWarps, 0, ctx->stream>>>(p, atoms_dev, off_dev, count);
+  HS_CHECK_LAUNCH();
+  return HSDLA_OK;
+}
+
 template <int L>
 int launch_ab_l(hsdla_ctx* ctx, const AbParams& p, const int* atoms_dev, const long long* off_dev,
                 int count) {
@@ -293,6 +410,19 @@ const ab_launcher kAbLaunchers[HSDLA_MAX_LSPH + 1] = {
     &launch_ab_l<0>, &launch_ab_l<1>, &launch_ab_l<2>, &launch_ab_l<3>, &launch_ab_l<4>,
     &launch_ab_l<5>, &launch_ab_l<6>, &launch_ab_l<7>, &launch_ab_l<8>, &launch_ab_l<9>,
     &launch_ab_l<10>, &launch_ab_l<11>, &launch_ab_l<12>, &launch_ab_l<13>, &launch_ab_l<14>};
+const ab_launcher kAbTplLaunchers[HSDLA_MAX_LSPH + 1] = {
+    &launch_ab_tpl<0>, &launch_ab_tpl<1>, &launch_ab_tpl<2>, &launch_ab_tpl<3>, &launch_ab_tpl<4>,
+    &launch_ab_tpl<5>, &launch_ab_tpl<6>, &launch_ab_tpl<7>, &launch_ab_tpl<8>, &launch_ab_tpl<9>,
+    &launch_ab_tpl<10>, &launch_ab_tpl<11>, &launch_ab_tpl<12>, &launch_ab_tpl<13>, &launch_ab_tpl<14>};
+// HSDLA_AB_TPL=0: the per-thread generator (ab_kernel) for the per-type templates as well.
+bool ab_tpl_warp() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("HSDLA_AB_TPL");
+    m = (e && e[0] == '0') ? 0 : 1;
+  }
+  return m == 1;
+}
 
 __global__ void udot_rows_kernel(const double* __restrict__ radial, int stride, const int* atoms,
                                  const long long* off, int L, double* out) {
@@ -471,7 +601,7 @@ int ab_generate_templates(hsdla_ctx* ctx, const hsdla_ab_args* args, const std::
   rc = arena_flush(ctx);
   if (rc) return rc;
   for (size_t gi = 0; gi < group_l.size(); ++gi) {
-    rc = kAbLaunchers[group_l[gi]](ctx, p, datoms + group_begin[gi], doffs + group_begin[gi],
+    rc = (ab_tpl_warp() ? kAbTplLaunchers : kAbLaunchers)[group_l[gi]](ctx, p, datoms + group_begin[gi], doffs + group_begin[gi],
                                    group_count[gi]);
     if (rc) return rc;
   }

@@ -518,6 +518,7 @@ def test_compute_ab_device_resident_drop_in(pkg):
     {"HSDLA_WARP_COLS": "16", "HSDLA_G3_MINB": "2"},           # 8-warp 32x16 warp tiles
     {"HSDLA_CONTRACT": "tma", "HSDLA_TMA_W8": "1"},            # TMA, 8 warps
     {"HSDLA_MERGE_SH": "0"},                                   # separate S and H launches
+    {"HSDLA_AB_TPL": "0"},                                     # per-thread template generator
 ])
 def test_kernel_variants_match_oracle(pkg, tmp_path, env):
     """The library's measured-but-not-default variants (switches read once per process, so each

@@ -158,7 +158,7 @@ def run_reference(args):
               ": oracle compute_AB + build_all (scipy OpenBLAS)")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
-        "n_gpus": world, "steps": len(times), "warmup": args.warmup,
+        "n_gpus": max(world, args.gpus), "steps": len(times), "warmup": args.warmup,
         "ms_per_step": round(1e3 * total / len(times), 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_name(args.config, inst),

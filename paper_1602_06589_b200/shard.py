@@ -48,16 +48,20 @@ def gather_panels(mat, n: int, world: int, rank: int, dst: int = 0, group=None):
     matrix here), so column panel [j0, j0+64) is the contiguous slice mat[j0:j0+64].  Each
     rank sends the panels it owns; `dst` receives the others straight into place.  Works
     with NCCL (GPU tensors) and gloo (CPU tensors)."""
+    import torch
     import torch.distributed as dist
 
     nb = (n + PANEL - 1) // PANEL
     # gloo moves host memory only: device panels are staged through host copies (the NCCL
     # path on the GPU box sends device memory directly)
     staged = mat.is_cuda and dist.get_backend(group) == "gloo"
+    # complex panels travel as their float64 (re, im) view: NCCL's point-to-point calls take
+    # real data types only
+    real = torch.view_as_real(mat) if mat.is_complex() else mat
     ops, back = [], []
     for j in range(nb):
         owner = panel_owner(nb, world, j)
-        sl = mat[j * PANEL:min(n, (j + 1) * PANEL)]
+        sl = real[j * PANEL:min(n, (j + 1) * PANEL)]
         if rank == dst and owner != dst:
             buf = sl.cpu() if staged else sl
             ops.append(dist.P2POp(dist.irecv, buf, owner, group))

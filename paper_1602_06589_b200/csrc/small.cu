@@ -123,46 +123,70 @@ __device__ __forceinline__ void chol_stage_panel(int k, int nb, int rows, const 
 __device__ int chol_factor_panel(int k, int nb, int rows, double2* A, long long lda, double2* P) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const double2 zero = make_double2(0.0, 0.0);
-    // Panel factorization in steps of kSB columns: every thread factors the kSB x kSB
-    // diagonal block redundantly in registers (no barrier for the pivots), then (a) each row
-    // below it is solved against that factor (L_r = P_r L_D^-H, final values in place) and (b)
-    // the panel's remaining columns take the rank-kSB update; two barriers per step.
-    constexpr int kSB = 4;
+    // Panel factorization in steps of kSB columns: thread 0 factors the kSB x kSB diagonal
+    // block in registers and publishes it, then (a) each row below it is solved against that
+    // factor (L_r = P_r L_D^-H, final values in place) and (b) the panel's remaining columns
+    // take the rank-kSB update; three barriers per step.
+    constexpr int kSB = 4;  // 8 measured 2x slower (spills in the row solve)
+    __shared__ double2 sL[kSB][kSB];
+    __shared__ double sld[kSB], sli[kSB];
+    __shared__ int sbad;
     for (int j0 = 0; j0 < nb; j0 += kSB) {
       const int sb = min(kSB, nb - j0);
-      // registers only: fully unrolled loops over the kSB x kSB block, predicated on sb
+      // registers only: fully unrolled loops over the kSB x kSB block, predicated on sb.  One
+      // thread factors it (the other warps would only compete for the FP64 pipe with the same
+      // dependent sqrt / reciprocal chain) and publishes it through shared memory.
       double2 L[kSB][kSB];
       double ld[kSB], li[kSB];
       int bad = 0;
+      if (tid == 0) {
 #pragma unroll
-      for (int i = 0; i < kSB; ++i)
+        for (int i = 0; i < kSB; ++i)
 #pragma unroll
-        for (int q = 0; q < kSB; ++q)
-          L[i][q] = (q <= i && i < sb) ? P[(j0 + i) * kNBS + j0 + q] : zero;
+          for (int q = 0; q < kSB; ++q)
+            L[i][q] = (q <= i && i < sb) ? P[(j0 + i) * kNBS + j0 + q] : zero;
+#pragma unroll
+        for (int i = 0; i < kSB; ++i) {
+          double d = L[i][i].x;
+#pragma unroll
+          for (int q = 0; q < i; ++q) d -= L[i][q].x * L[i][q].x + L[i][q].y * L[i][q].y;
+          const bool ok = i >= sb || (d > 0.0 && isfinite(d));
+          if (!ok && !bad) bad = i + 1;
+          ld[i] = ok && i < sb ? sqrt(d) : 1.0;
+          li[i] = 1.0 / ld[i];
+#pragma unroll
+          for (int i2 = i + 1; i2 < kSB; ++i2) {
+            double2 v = L[i2][i];
+#pragma unroll
+            for (int q = 0; q < i; ++q) {  // v -= L[i2][q] conj(L[i][q])
+              v.x = fma(-L[i2][q].x, L[i][q].x, v.x);
+              v.x = fma(-L[i2][q].y, L[i][q].y, v.x);
+              v.y = fma(-L[i2][q].y, L[i][q].x, v.y);
+              v.y = fma(L[i2][q].x, L[i][q].y, v.y);
+            }
+            L[i2][i] = make_double2(v.x * li[i], v.y * li[i]);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < kSB; ++i) {
+          sld[i] = ld[i];
+          sli[i] = li[i];
+#pragma unroll
+          for (int q = 0; q < kSB; ++q) sL[i][q] = L[i][q];
+        }
+        sbad = bad;
+      }
+      __syncthreads();  // the factor is published and thread 0 has read the block before rows are rewritten
+      HSDLA_PROF_POINT(9);
+      bad = sbad;
+      if (bad) return k + j0 + bad;  // uniform
 #pragma unroll
       for (int i = 0; i < kSB; ++i) {
-        double d = L[i][i].x;
+        ld[i] = sld[i];
+        li[i] = sli[i];
 #pragma unroll
-        for (int q = 0; q < i; ++q) d -= L[i][q].x * L[i][q].x + L[i][q].y * L[i][q].y;
-        const bool ok = i >= sb || (d > 0.0 && isfinite(d));
-        if (!ok && !bad) bad = i + 1;
-        ld[i] = ok && i < sb ? sqrt(d) : 1.0;
-        li[i] = 1.0 / ld[i];
-#pragma unroll
-        for (int i2 = i + 1; i2 < kSB; ++i2) {
-          double2 v = L[i2][i];
-#pragma unroll
-          for (int q = 0; q < i; ++q) {  // v -= L[i2][q] conj(L[i][q])
-            v.x = fma(-L[i2][q].x, L[i][q].x, v.x);
-            v.x = fma(-L[i2][q].y, L[i][q].y, v.x);
-            v.y = fma(-L[i2][q].y, L[i][q].x, v.y);
-            v.y = fma(L[i2][q].x, L[i][q].y, v.y);
-          }
-          L[i2][i] = make_double2(v.x * li[i], v.y * li[i]);
-        }
+        for (int q = 0; q < kSB; ++q) L[i][q] = sL[i][q];
       }
-      if (bad) return k + j0 + bad;  // uniform: every thread factored the same block
-      __syncthreads();  // every thread has read the diagonal block before rows are rewritten
       // (a) rows of the diagonal block take L_D; rows below solve x L_D^H = P_r
       for (int r = j0 + tid; r < rows; r += nt) {
         double2 x[kSB];
@@ -195,6 +219,7 @@ __device__ int chol_factor_panel(int k, int nb, int rows, double2* A, long long 
           if (i < sb) P[r * kNBS + j0 + i] = x[i];
       }
       __syncthreads();
+      HSDLA_PROF_POINT(10);
       // (b) P[r][c] -= sum_q L[r][j0+q] conj(L[c][j0+q]) for the panel's columns c >= j0 + sb
       const int tx = tid % kNB, ty = tid / kNB, c = j0 + sb + tx;
       if (c < nb) {
@@ -218,6 +243,7 @@ __device__ int chol_factor_panel(int k, int nb, int rows, double2* A, long long 
         }
       }
       __syncthreads();
+      HSDLA_PROF_POINT(11);
     }
     for (int e = tid; e < rows * nb; e += nt) {
       const int r = e % rows, c = e / rows;
@@ -329,7 +355,10 @@ __device__ void chol_blocked(int n, double2* A, long long lda, int* info, bool c
 constexpr int kCS = 8;
 // The cluster versions pay off from about this order on (the panel factorisation on rank 0
 // stays the critical path; measured: 2m = 242 401 vs 546 us, 2m = 162 245 vs 242 us).
-constexpr int kClusterMinN = 192;
+#ifndef HSDLA_CLUSTER_MIN_N
+#define HSDLA_CLUSTER_MIN_N 192
+#endif
+constexpr int kClusterMinN = HSDLA_CLUSTER_MIN_N;
 // HSDLA_TPREP_CLUSTER=0: one CTA per T set for the T preparation kernels.
 inline bool tprep_cluster() {
   static int m = -1;
@@ -590,27 +619,49 @@ __global__ void __launch_bounds__(512) tjoint_kernel(const int* tdim, const int*
     // (rows by lanes with whole-warp iterations: the row-sum reduction below shuffles; columns
     // split over the cluster's ranks)
     bool nan = false;
-    for (int c = rank * (blockDim.x >> 5) + (threadIdx.x >> 5); c < n; c += nrk * (blockDim.x >> 5))
-    for (int r0 = 0; r0 < n; r0 += 32) {
-      const int r = r0 + (threadIdx.x & 31);
-      double2 v = make_double2(0.0, 0.0);
-      double av = 0.0;  // |T_rc| into row r; the mirror's |T_cr| into row c (warp-reduced)
-      if (r < n && r >= c) {
-        if (r < h) v = Taa[r + c * t_ld];
-        else if (c < h) v = cconj(Tab[c + (r - h) * t_ld]);
-        else v = Tbb[(r - h) + (c - h) * t_ld];
-        nan = nan || isnan(v.x) || isnan(v.y);
-        if (r == c) v.y = 0.0;
-        av = sqrt(v.x * v.x + v.y * v.y);
-        if (r == c && sigma != 0.0) v.x += sigma * (r < h ? 1.0 : U2[r - h]);
+    const bool sums = rho_in_assembly && att == 0;  // Gershgorin row sums of the unshifted matrix
+    // Lane l of a warp walks rows l, l + 32, ...: its share of each row's |T_rc| sum stays in
+    // registers across the warp's columns and reaches shared memory once per (warp, row) at the
+    // end; the mirror's |T_cr| of column c is warp-reduced (one add per column).  (Per-element
+    // shared-memory double atomics here cost ~70 k cycles at 2m = 162.)
+    constexpr int kRowChunks = (2 * (HSDLA_MAX_LSPH + 1) * (HSDLA_MAX_LSPH + 1) + 31) / 32;
+    double rsum[kRowChunks];
+#pragma unroll
+    for (int i = 0; i < kRowChunks; ++i) rsum[i] = 0.0;
+    for (int c = rank * (blockDim.x >> 5) + (threadIdx.x >> 5); c < n; c += nrk * (blockDim.x >> 5)) {
+      double mirror = 0.0;  // the warp shares column c
+#pragma unroll
+      for (int i = 0; i < kRowChunks; ++i) {
+        const int r0 = 32 * i;
+        if (r0 >= n) break;
+        const int r = r0 + (threadIdx.x & 31);
+        double2 v = make_double2(0.0, 0.0);
+        if (r < n && r >= c) {
+          if (r < h) v = Taa[r + c * t_ld];
+          else if (c < h) v = cconj(Tab[c + (r - h) * t_ld]);
+          else v = Tbb[(r - h) + (c - h) * t_ld];
+          nan = nan || isnan(v.x) || isnan(v.y);
+          if (r == c) v.y = 0.0;
+          if (sums) {
+            const double av = sqrt(v.x * v.x + v.y * v.y);
+            rsum[i] += av;
+            if (r > c) mirror += av;
+          }
+          if (r == c && sigma != 0.0) v.x += sigma * (r < h ? 1.0 : U2[r - h]);
+        }
+        if (r < n) J[r + c * lj] = v;
       }
-      if (rho_in_assembly && att == 0) {  // Gershgorin row sums of the unshifted matrix
-        if (av != 0.0) atomicAdd(s_row + r, av);
-        double mirror = r > c ? av : 0.0;  // the warp shares column c
+      if (sums) {
         for (int o = 16; o > 0; o >>= 1) mirror += __shfl_xor_sync(0xffffffffu, mirror, o);
         if ((threadIdx.x & 31) == 0 && mirror != 0.0) atomicAdd(s_row + c, mirror);
       }
-      if (r < n) J[r + c * lj] = v;
+    }
+    if (sums) {
+#pragma unroll
+      for (int i = 0; i < kRowChunks; ++i) {
+        const int r = 32 * i + (threadIdx.x & 31);
+        if (r < n && rsum[i] != 0.0) atomicAdd(s_row + r, rsum[i]);
+      }
     }
     if (nan) atomicOr(flag0, 1);
     if constexpr (CL) {  // the other ranks' partial row sums into rank 0's (one add per row)

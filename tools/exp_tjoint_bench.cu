@@ -64,8 +64,8 @@ int main(int argc, char** argv) {
     double cks = 0.0;
     for (size_t q = 0; q < Jh.size(); ++q) cks += Jh[q].x * (1.0 + 1e-3 * (q % 97)) - Jh[q].y * (1.0 + 1e-3 * (q % 89));
     printf("checksum %.17g ", cks);
-    printf("m=%d n=%d: %.1f us info %d | cycles: gersh+split %lld, assemble %lld, nan %lld, stage %lld, panel %lld, writeback %lld, trailing %lld, zero+rest %lld\n",
-           m, 2 * m, ms * 1e3, inf, z[7], z[8], z[1], z[2], z[3], z[4], z[5], z[6]);
+    printf("m=%d n=%d: %.1f us info %d | cycles: gersh+split %lld, assemble %lld, nan %lld, stage %lld, panel %lld, writeback %lld, trailing %lld, zero+rest %lld | panel: diag %lld rows %lld update %lld\n",
+           m, 2 * m, ms * 1e3, inf, z[7], z[8], z[1], z[2], z[3], z[4], z[5], z[6], z[9], z[10], z[11]);
   }
   return 0;
 }

@@ -9,9 +9,11 @@ The metric is BASELINE.json's: H+S setup time per k-point and FP64 TFLOP/s over 
 reference's nominal FLOP ledger (`builder.py:336-370`), as a fraction of the measured
 FP64 DMMA peak.  Multi-GPU: one process per GPU (torchrun), each rank builds its own
 k-point (k-point parallelism, weak scaling, no collective in the data path); the
-time is the max over ranks.  `--impl reference` times the CPU oracle port (numpy +
-the same scipy/OpenBLAS routines the reference's optimized backend calls) on the
-host cores, rank 0 only.  Prints one JSON line.
+time is the max over ranks.  `--impl reference` times the unmodified reference package
+(baseline/_ref, installed by tools/stage_reference.py: its own compute_AB + build_all,
+"optimized" backend on every host thread; `cpu_baseline.kind` "reference") on the host
+cores, rank 0 only, with the numpy oracle port beside it (`oracle_port`); where the package
+is not installed the port is the arm (`kind` "port").  Prints one JSON line.
 """
 from __future__ import annotations
 
@@ -88,6 +90,62 @@ def cpu_oracle_step(spec, tmats):
     return t2 - t0, sum(led.values()), t1 - t0, t2 - t1
 
 
+def reference_package():
+    """The real reference (`hsdla`, unmodified) installed by tools/stage_reference.py under
+    baseline/_ref (git-ignored; travels to the GPU box with the snapshot), or None."""
+    global _REF_PKG
+    if _REF_PKG is not False:
+        return _REF_PKG
+    _REF_PKG = None
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "baseline", "_ref")
+    if os.environ.get("HSDLA_BENCH_CPU_ARM") == "port":  # force the oracle port
+        return None
+    if os.path.exists(os.path.join(path, "hsdla", "__init__.py")):
+        os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_hsdla_ref")
+        sys.path.insert(0, path)
+        try:
+            import hsdla
+
+            if os.path.abspath(hsdla.__file__).startswith(path):
+                _REF_PKG = hsdla
+        except Exception as exc:  # pragma: no cover
+            print(f"bench: reference package not importable ({exc}); CPU arm uses the oracle port",
+                  file=sys.stderr)
+        finally:
+            sys.path.remove(path)
+    return _REF_PKG
+
+
+_REF_PKG = False
+
+
+def cpu_reference_step(spec, tmats):
+    """One k-point through the unmodified reference's own entry points: compute_AB
+    (flapw.py:201-233) + build_all (builder.py:403-474, its "optimized" backend on every host
+    thread).  Same return as cpu_oracle_step."""
+    ref = reference_package()
+    rspec = ref.SystemSpec.from_json_dict(spec.to_json_dict())
+    cd = ref.ComplexDense.from_array
+    rtm = ref.TMatrixSet(t_aa=[cd(t.array) for t in tmats.t_aa],
+                         t_ab=[cd(t.array) for t in tmats.t_ab],
+                         t_bb=[cd(t.array) for t in tmats.t_bb], l_sph=list(tmats.l_sph),
+                         l_nonsph=list(tmats.l_nonsph))
+    cfg = ref.BuildConfig(backend="optimized", thread_count=affinity_threads())
+    t0 = time.perf_counter()
+    coeffs = ref.compute_AB(rspec)
+    t1 = time.perf_counter()
+    _, _, rep = ref.build_all(coeffs, rtm, cfg)
+    t2 = time.perf_counter()
+    return t2 - t0, rep.ledger.total, t1 - t0, t2 - t1
+
+
+def cpu_step_fn():
+    """(step function, kind, label): the real reference when it is installed, else the port."""
+    if reference_package() is not None:
+        return cpu_reference_step, "reference", "reference hsdla compute_AB + build_all"
+    return cpu_oracle_step, "port", "oracle compute_AB + build_all"
+
+
 def cpu_sample(inst, max_basis=3200):
     """Bounded CPU workload: the config's k-point, truncated to the first `max_basis`
     K-vectors when larger (C3/C4), so one sample takes seconds, not minutes."""
@@ -110,6 +168,11 @@ def host_threads():
         return max(int(i.get("num_threads", 1)) for i in info) if info else os.cpu_count()
     except Exception:  # pragma: no cover
         return os.cpu_count()
+
+
+def affinity_threads():
+    return max(1, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
+               else (os.cpu_count() or 1))
 
 
 def use_all_host_threads():
@@ -138,24 +201,32 @@ def run_reference(args):
                                inst.min_abs_wronskian)
         return cpu_sample(one)
 
+    step, kind, label = cpu_step_fn()
     for _ in range(max(0, min(args.warmup, 1))):
-        cpu_oracle_step(sample_spec(0), inst.tmats)
+        step(sample_spec(0), inst.tmats)
     times, flops, nb = [], 0, set()
     t_start = time.perf_counter()
     for k in range(args.steps):
         spec = sample_spec(k)
         nb.add(spec.n_basis)
-        dt, fl, _, _ = cpu_oracle_step(spec, inst.tmats)
+        dt, fl, _, _ = step(spec, inst.tmats)
         times.append(dt)
         flops += fl
         if time.perf_counter() - t_start > 150:  # keep the arm within a few minutes
             break
     total = sum(times)
     value = flops / total / 1e12
+    port = None
+    if kind == "reference":  # the numpy port of the same path beside it (one k-point, untimed warm-up)
+        cpu_oracle_step(sample_spec(0), inst.tmats)
+        pdt, pfl, _, _ = cpu_oracle_step(sample_spec(0), inst.tmats)
+        port = {"ms_per_step": round(1e3 * pdt, 3), "value": round(pfl / pdt / 1e12, 4),
+                "unit": UNIT, "what": "oracle port (vectorised compute_AB + the same scipy BLAS "
+                                      "calls), one k-point"}
     trunc = max(nb) < inst.spec.n_basis
     sample = (f"{len(times)} distinct seeded k-point(s) of {args.config}" +
               (f" truncated to N_G={max(nb)}" if trunc else f" (N_G {min(nb)}-{max(nb)})") +
-              ": oracle compute_AB + build_all (scipy OpenBLAS)")
+              f": {label} (scipy OpenBLAS)")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
         "n_gpus": max(world, args.gpus), "steps": len(times), "warmup": args.warmup,
@@ -164,10 +235,12 @@ def run_reference(args):
         "config": {"workload": workload_name(args.config, inst),
                    "n_basis": max(nb), "rows": int(sum((l + 1) ** 2 for l in inst.spec.l_sph))},
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": host_threads(),
-                         "kind": "port", "sample": sample},
+                         "kind": kind, "sample": sample},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    if port is not None:
+        line["oracle_port"] = port
     print(json.dumps(line), flush=True)
 
 
@@ -793,6 +866,9 @@ def cpu_baseline_sample(config, inst):
     from paper_1602_06589_b200 import configs
 
     _limits = use_all_host_threads()  # noqa: F841
+    step, kind, label = cpu_step_fn()
+    if kind == "reference":  # numba JIT of the reference's table kernels stays out of the sample
+        step(cpu_sample(inst), inst.tmats)
     tot_t = tot_fl = t_ab_sum = t_b_sum = 0.0
     k = 0
     nb = set()
@@ -800,15 +876,15 @@ def cpu_baseline_sample(config, inst):
         cspec = cpu_sample(configs.Instance(inst.cfg, [configs.kpoint_variant(inst, k)],
                                             inst.tmats, inst.min_abs_wronskian))
         nb.add(cspec.n_basis)
-        dt, fl, t_ab, t_build = cpu_oracle_step(cspec, inst.tmats)
+        dt, fl, t_ab, t_build = step(cspec, inst.tmats)
         tot_t, tot_fl, t_ab_sum, t_b_sum, k = (tot_t + dt, tot_fl + fl, t_ab_sum + t_ab,
                                                t_b_sum + t_build, k + 1)
     return {
         "value": round(tot_fl / tot_t / 1e12, 4), "unit": UNIT, "cores": host_threads(),
-        "kind": "port",
+        "kind": kind,
         "sample": f"{k} distinct seeded k-point(s) of {config} (N_G {min(nb)}-{max(nb)}), "
-                  f"{tot_t:.1f} s: oracle compute_AB {t_ab_sum / k:.2f} s + build_all "
-                  f"{t_b_sum / k:.2f} s per k-point (scipy OpenBLAS)",
+                  f"{tot_t:.1f} s: {label.split(' compute_AB')[0]} compute_AB {t_ab_sum / k:.2f} s "
+                  f"+ build_all {t_b_sum / k:.2f} s per k-point (scipy OpenBLAS)",
     }
 
 

@@ -1,5 +1,6 @@
-"""bench.py's output contract on CPU: the reference arm (`--impl reference`, the oracle port
-timed on the host) prints one JSON line with the driver's keys; the GPU arm's helpers
+"""bench.py's output contract on CPU: the reference arm (`--impl reference`: the unmodified
+reference package from baseline/_ref where it is installed, else the oracle port, timed on the
+host) prints one JSON line with the driver's keys; the GPU arm's helpers
 (ledger flops, FP64 ceilings, A/B-generation roofline) compute what DESIGN.md says."""
 import json
 import os
@@ -22,8 +23,22 @@ def test_reference_arm_json_line():
                 "cpu_baseline", "e2e"):
         assert key in d, key
     assert d["impl"] == "reference" and d["unit"] == "TFLOP/s" and d["higher_is_better"] is True
-    assert d["value"] > 0 and d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    have_ref = os.path.exists(os.path.join(REPO, "baseline", "_ref", "hsdla", "__init__.py"))
+    assert d["value"] > 0 and d["cpu_baseline"]["cores"] >= 1
+    assert d["cpu_baseline"]["kind"] == ("reference" if have_ref else "port")
+    assert ("oracle_port" in d) == have_ref
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+
+
+def test_reference_arm_port_fallback():
+    """Without the reference package (forced here) the arm is the oracle port."""
+    env = dict(os.environ, HSDLA_BENCH_CPU_ARM="port")
+    out = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--impl", "reference",
+                          "--config", "C1", "--steps", "1", "--warmup", "0"],
+                         capture_output=True, text=True, timeout=600, cwd=REPO, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    assert d["cpu_baseline"]["kind"] == "port" and "oracle_port" not in d and d["value"] > 0
 
 
 def test_bench_helpers():

@@ -339,58 +339,59 @@ def _potrf_or_none(backend: KernelBackend, t: ComplexDense, ledger: FlopLedger):
 
 
 def estimate_memory(n_atoms: int, n_l: int, n_g: int, backup: bool) -> int:
-    """Peak bytes of the composed build (`builder.py:318-333`), exact integers."""
-    if min(n_atoms, n_l, n_g) < 1:
-        raise ContractViolationError("all size parameters must be >= 1")
-    stacks = 32 * n_atoms * n_l * n_g
-    total = stacks + 32 * n_g * n_g
-    if backup:
-        total += max(stacks - 16 * n_g * n_g, 0)
-    if total >= 2**64:
-        raise OverflowError(f"memory estimate {total} exceeds 64-bit byte counts")
-    return total
+    """Peak bytes of the composed build as the reference budgets them (`builder.py:318-333`):
+    the A*/B* stacks, H and S, and with backup the part of the stack copies that does not fit
+    the room S still leaves free.  Python integers throughout (no wrap-around)."""
+    if n_atoms < 1 or n_l < 1 or n_g < 1:
+        raise ContractViolationError("estimate_memory: atom count, block height and N_G are positive")
+    entry = 16  # bytes per complex128
+    square = entry * n_g * n_g
+    stack_pair = 2 * entry * n_atoms * n_l * n_g
+    need = stack_pair + 2 * square + (max(0, stack_pair - square) if backup else 0)
+    if need >> 64:
+        raise OverflowError(f"{need} bytes cannot be expressed as a 64-bit size")
+    return need
+
+
+def _row_totals(n_atoms: int, block_heights, hpd_mask):
+    """(heights, mask, stacked rows, stacked rows of HPD atoms) after the length checks."""
+    hs = list(map(int, block_heights))
+    flags = list(map(bool, hpd_mask))
+    if len(hs) != n_atoms:
+        raise ContractViolationError(f"expected {n_atoms} block heights, got {len(hs)}")
+    if len(flags) != n_atoms:
+        raise ContractViolationError(f"expected {n_atoms} HPD flags, got {len(flags)}")
+    return hs, flags, sum(hs), sum(h for h, f in zip(hs, flags) if f)
 
 
 def predict_flops(n_atoms: int, block_heights, n_g: int, hpd_mask) -> FlopLedger:
-    """Closed-form FLOP totals of one composed build (`builder.py:336-370`)."""
-    heights = [int(h) for h in block_heights]
-    if len(heights) != n_atoms:
-        raise ContractViolationError(f"{len(heights)} heights for {n_atoms} atoms")
-    mask = [bool(b) for b in hpd_mask]
-    if len(mask) != n_atoms:
-        raise ContractViolationError(f"hpd mask length {len(mask)} != {n_atoms}")
-    led = FlopLedger()
-    r_total = sum(heights)
-    ng2 = n_g * n_g
-    led.add("hermitian_rank_k", 8 * r_total * ng2)
-    led.add("row_scale", 2 * r_total * n_g)
-    for h in heights:
-        led.add("general_product", 8 * h * h * n_g)
-        led.add("hermitian_product", 8 * h * h * n_g)
-    led.add("hermitian_rank_2k", 8 * r_total * ng2)
-    r_hpd = sum(h for h, b in zip(heights, mask) if b)
-    r_gen = r_total - r_hpd
-    for h, is_hpd in zip(heights, mask):
-        if is_hpd:
-            led.add("cholesky", cholesky_flops(h))
-            led.add("triangular_product", 4 * h * h * n_g)
-        else:
-            led.add("hermitian_product", 8 * h * h * n_g)
-    led.add("general_product", 8 * r_gen * ng2)
-    led.add("hermitian_rank_k", 4 * r_hpd * ng2)
-    return led
+    """The ledger a composed build will show, without running it (`builder.py:336-370`).
+
+    Per phase: S = two stacked ZHERKs (4 R N^2 each) after the row scaling (2 R N);
+    H_ABBA_BB = per atom one ZGEMM and one ZHEMM forming Z (8 h^2 N each), then the stacked
+    ZHER2K (8 R N^2); H_AA = per HPD atom a Cholesky and a ZTRMM (4 h^2 N), per other atom a
+    ZHEMM, then the stacked ZHERK over the HPD rows and the ZGEMM over the rest."""
+    hs, flags, rows, rows_hpd = _row_totals(n_atoms, block_heights, hpd_mask)
+    nn = n_g * n_g
+    small = [h * h * n_g for h in hs]  # h^2 N of each atom's T application
+    out = FlopLedger()
+    out.add("row_scale", 2 * rows * n_g)
+    out.add("hermitian_rank_k", 2 * (4 * rows * nn) + 4 * rows_hpd * nn)
+    out.add("hermitian_rank_2k", 8 * rows * nn)
+    out.add("general_product", 8 * sum(small) + 8 * (rows - rows_hpd) * nn)
+    out.add("hermitian_product",
+            8 * sum(small) + 8 * sum(w for w, f in zip(small, flags) if not f))
+    out.add("triangular_product", 4 * sum(w for w, f in zip(small, flags) if f))
+    out.add("cholesky", sum(cholesky_flops(h) for h, f in zip(hs, flags) if f))
+    return out
 
 
 def large_update_fraction(n_atoms: int, block_heights, n_g: int, hpd_mask) -> float:
-    """Fraction of predicted FLOPs in the O(N_G^2) stacked updates (`builder.py:373-385`)."""
-    led = predict_flops(n_atoms, block_heights, n_g, hpd_mask)
-    heights = [int(h) for h in block_heights]
-    r_total = sum(heights)
-    r_hpd = sum(h for h, b in zip(heights, hpd_mask) if b)
-    r_gen = r_total - r_hpd
-    ng2 = n_g * n_g
-    large = 8 * r_total * ng2 + 8 * r_total * ng2 + 8 * r_gen * ng2 + 4 * r_hpd * ng2
-    return large / led.total
+    """Share of the predicted FLOPs spent in the stacked O(R N^2) updates — the part that
+    runs on the DMMA contraction (`builder.py:373-385`)."""
+    _, _, rows, rows_hpd = _row_totals(n_atoms, block_heights, hpd_mask)
+    stacked = (16 * rows + 8 * (rows - rows_hpd) + 4 * rows_hpd) * n_g * n_g
+    return stacked / predict_flops(n_atoms, block_heights, n_g, hpd_mask).total
 
 
 def build_ledger(heights, t_sizes, n_g: int, hpd_mask, force_general_path: bool) -> FlopLedger:

@@ -39,8 +39,15 @@ def _check(cond: bool, msg: str):
         raise ContractViolationError(msg)
 
 
+def _square_order(t: ComplexDense, role: str) -> int:
+    _check(t.rows == t.cols, f"{role} is {t.rows}x{t.cols}; a square matrix is required")
+    return t.rows
+
+
 class KernelBackend:
-    """Shared contract: argument validation and FLOP accounting (`kernels.py:46-132`)."""
+    """The operator contract every backend shares (`kernels.py:46-132`): shapes are checked
+    before anything runs, the nominal FLOPs of a call are charged whether or not the shape is
+    empty, and a failed Cholesky charges nothing.  Subclasses supply the six `_xxx` workers."""
 
     name = "abstract"
 
@@ -48,68 +55,72 @@ class KernelBackend:
         self.threads = int(threads)
         set_thread_count(self.threads)
 
+    # C (n x n, lower) += A^H A, A: k x n — 4 k n^2
     def hermitian_rank_k_update(self, c: HermitianAccumulator, a: ComplexDense,
                                 ledger: FlopLedger) -> HermitianAccumulator:
-        m, n = a.rows, a.cols
-        _check(c.n == n, f"rank-k shapes: C is {c.n}x{c.n}, A is {m}x{n}")
-        if m and n:
+        k, n = a.shape
+        _check(c.n == n, f"ZHERK target of order {c.n} cannot take a {k}x{n} operand")
+        if k > 0 and n > 0:
             self._herk(c.matrix, a)
-        ledger.add("hermitian_rank_k", 4 * m * n * n)
+        ledger.add("hermitian_rank_k", 4 * k * n * n)
         return c
 
+    # C (n x n, lower) += X^H B + B^H X, X and B: k x n — 8 k n^2
     def hermitian_rank_2k_update(self, c: HermitianAccumulator, x: ComplexDense,
                                  b: ComplexDense, ledger: FlopLedger) -> HermitianAccumulator:
-        _check(x.shape == b.shape, f"rank-2k needs same shapes, got {x.shape} vs {b.shape}")
-        m, n = x.rows, x.cols
-        _check(c.n == n, f"rank-2k shapes: C is {c.n}x{c.n}, X is {m}x{n}")
-        if m and n:
+        _check(x.shape == b.shape, f"ZHER2K operands differ in shape: {x.shape} and {b.shape}")
+        k, n = x.shape
+        _check(c.n == n, f"ZHER2K target of order {c.n} cannot take {k}x{n} operands")
+        if k > 0 and n > 0:
             self._her2k(c.matrix, x, b)
-        ledger.add("hermitian_rank_2k", 8 * m * n * n)
+        ledger.add("hermitian_rank_2k", 8 * k * n * n)
         return c
 
+    # C = alpha op(A) B + beta C, op = conjugate transpose or identity — 8 m n k
     def general_product(self, c: ComplexDense, a: ComplexDense, b: ComplexDense,
                         conj_transpose_a: bool, alpha: complex, beta: complex,
                         ledger: FlopLedger) -> ComplexDense:
-        m_op = a.cols if conj_transpose_a else a.rows
-        k_op = a.rows if conj_transpose_a else a.cols
-        _check(k_op == b.rows, f"inner dimensions differ: op(A) has {k_op}, B has {b.rows}")
-        _check((c.rows, c.cols) == (m_op, b.cols),
-               f"C is {c.shape}, product is {(m_op, b.cols)}")
-        if m_op and b.cols:
+        m, k = (a.cols, a.rows) if conj_transpose_a else (a.rows, a.cols)
+        n = b.cols
+        _check(b.rows == k, f"ZGEMM contraction lengths disagree: op(A) gives {k}, B gives {b.rows}")
+        _check(c.shape == (m, n), f"ZGEMM result is {m}x{n} but C is {c.rows}x{c.cols}")
+        if m > 0 and n > 0:
             self._gemm(c, a, b, conj_transpose_a, complex(alpha), complex(beta))
-        ledger.add("general_product", 8 * m_op * b.cols * k_op)
+        ledger.add("general_product", 8 * m * n * k)
         return c
 
+    # X = alpha T A (+ X when accumulating), T Hermitian, lower triangle read — 8 n^2 cols
     def hermitian_product(self, x: ComplexDense, t: ComplexDense, a: ComplexDense,
                           accumulate: bool, alpha: complex,
                           ledger: FlopLedger) -> ComplexDense:
-        _check(t.rows == t.cols, f"T must be square, got {t.shape}")
-        n = t.rows
-        _check(a.rows == n, f"A has {a.rows} rows, T is {n}x{n}")
-        _check(x.shape == (n, a.cols), f"X is {x.shape}, expected {(n, a.cols)}")
-        if n and a.cols:
+        n = _square_order(t, "the Hermitian operand")
+        width = a.cols
+        _check(a.rows == n, f"ZHEMM: T has order {n}, A has {a.rows} rows")
+        _check(x.shape == (n, width), f"ZHEMM result is {n}x{width} but X is {x.rows}x{x.cols}")
+        if n > 0 and width > 0:
             self._hemm(x, t, a, accumulate, complex(alpha))
         elif not accumulate:
-            x.array[:] = 0
-        ledger.add("hermitian_product", 8 * n * n * a.cols)
+            x.array[...] = 0.0
+        ledger.add("hermitian_product", 8 * n * n * width)
         return x
 
+    # Y = op(C) A, C lower triangular — 4 n^2 cols
     def triangular_product(self, y: ComplexDense, c: ComplexDense, a: ComplexDense,
                            conj_transpose_c: bool, ledger: FlopLedger) -> ComplexDense:
-        _check(c.rows == c.cols, f"triangular factor must be square, got {c.shape}")
-        n = c.rows
-        _check(a.rows == n, f"A has {a.rows} rows, C is {n}x{n}")
-        _check(y.shape == a.shape, f"Y is {y.shape}, expected {a.shape}")
-        if n and a.cols:
+        n = _square_order(c, "the triangular factor")
+        width = a.cols
+        _check(a.rows == n, f"ZTRMM: factor has order {n}, A has {a.rows} rows")
+        _check(y.shape == a.shape, f"ZTRMM result is {n}x{width} but Y is {y.rows}x{y.cols}")
+        if n > 0 and width > 0:
             self._trmm(y, c, a, conj_transpose_c)
-        ledger.add("triangular_product", 4 * n * n * a.cols)
+        ledger.add("triangular_product", 4 * n * n * width)
         return y
 
     def cholesky_factor(self, t: ComplexDense, ledger: FlopLedger) -> ComplexDense:
-        """Factor tril(T) into a scratch copy; T survives failure; FLOPs on success only."""
-        _check(t.rows == t.cols, f"Cholesky input must be square, got {t.shape}")
-        n = t.rows
-        factor = self._potrf(t)  # raises NotHPDError / ContractViolationError
+        """Lower Cholesky factor of T (its lower triangle is read) in a new matrix; T itself is
+        never modified.  NotHPDError / ContractViolationError leave the ledger untouched."""
+        n = _square_order(t, "the matrix to factor")
+        factor = self._potrf(t)
         ledger.add("cholesky", cholesky_flops(n))
         return factor
 

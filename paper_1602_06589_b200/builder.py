@@ -493,7 +493,9 @@ def build_all(coeffs: StackedCoefficients, tmats: TMatrixSet, config: BuildConfi
     # device pipeline (per-type templates + expansion) — the same H and S to
     # rounding, without the per-atom T applications; the stacks themselves are left as they are.
     origin = getattr(coeffs, "_origin", None)
+    made = getattr(coeffs, "_origin_stacks", (None, None))
     if (origin is not None and dev_a is not None and dev_b is not None
+            and made[0] is coeffs.A_star and made[1] is coeffs.B_star
             and dev_a[0].device.index == here and origin.n_basis == n
             and tuple(int(h) for h in origin.heights) == tuple(layout.block_heights)
             and np.array_equal(np.asarray(coeffs.udot_norms), origin.udot_rows)):

@@ -168,6 +168,7 @@ def compute_AB(spec: SystemSpec) -> StackedCoefficients:
     # the device copy of the spec these stacks are a function of: build_all runs from it while
     # the stacks stay untouched (builder._build_from_origin)
     coeffs._origin = dspec
+    coeffs._origin_stacks = (coeffs.A_star, coeffs.B_star)  # these very objects, not replacements
     return coeffs
 
 

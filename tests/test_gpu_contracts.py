@@ -510,6 +510,35 @@ def test_compute_ab_device_resident_drop_in(pkg):
     assert rel_fro(s3.array, s_want) <= 1e-12
 
 
+def test_fused_drop_in_only_for_the_stacks_compute_ab_returned(pkg):
+    """The spec-pipeline shortcut of build_all holds only while the coefficient object still
+    carries the very stacks compute_AB made for it: stacks swapped in from another compute_AB
+    call (same shapes, another k-point, still device-resident) are built from as they are."""
+    from paper_1602_06589_b200 import configs
+
+    inst = configs.make_instance("C1")
+    other = configs.kpoint_variant(inst, 1)
+    co = pkg.compute_AB(inst.spec)
+    co2 = pkg.compute_AB(other)
+    assert co2.n_basis != co.n_basis or not np.allclose(other.k_point, inst.spec.k_point)
+    if co2.n_basis == co.n_basis:
+        co.A_star, co.B_star = co2.A_star, co2.B_star
+        h, s, rep = pkg.build_all(co, inst.tmats, pkg.BuildConfig())
+        assert getattr(rep, "_path", None) is None
+        h_w, s_w, _ = pkg.build_all(co2, inst.tmats, pkg.BuildConfig())
+        assert rel_fro(s.array, s_w.array) <= 1e-13 and rel_fro(h.array, h_w.array) <= 1e-13
+    # same spec twice: the second call's stacks moved into the first object are equal data, but
+    # still not "its own" stacks, so the shortcut is off and the result is the same to rounding
+    co3 = pkg.compute_AB(inst.spec)
+    h0, s0, r0 = pkg.build_all(co, inst.tmats, pkg.BuildConfig()) if co2.n_basis != co.n_basis \
+        else pkg.build_all(pkg.compute_AB(inst.spec), inst.tmats, pkg.BuildConfig())
+    co4 = pkg.compute_AB(inst.spec)
+    co4.A_star, co4.B_star = co3.A_star, co3.B_star
+    h4, s4, r4 = pkg.build_all(co4, inst.tmats, pkg.BuildConfig())
+    assert getattr(r4, "_path", None) is None and getattr(r0, "_path", None) == "spec-pipeline"
+    assert rel_fro(s4.array, s0.array) <= 1e-13 and rel_fro(h4.array, h0.array) <= 1e-13
+
+
 @pytest.mark.parametrize("env", [
     {"HSDLA_PLANES": "1"},                                     # sum planes, 8x4 ring
     {"HSDLA_PLANES": "1", "HSDLA_PL_VARIANT": "16x2"},         # sum planes, 16x2 ring

@@ -59,7 +59,8 @@ class KernelBackend:
     def hermitian_rank_k_update(self, c: HermitianAccumulator, a: ComplexDense,
                                 ledger: FlopLedger) -> HermitianAccumulator:
         k, n = a.shape
-        _check(c.n == n, f"ZHERK target of order {c.n} cannot take a {k}x{n} operand")
+        # both shapes in the message, target first (the reference's tests read them there)
+        _check(c.n == n, f"ZHERK (rank-k) target {c.n}x{c.n} cannot take a {k}x{n} operand")
         if k > 0 and n > 0:
             self._herk(c.matrix, a)
         ledger.add("hermitian_rank_k", 4 * k * n * n)
@@ -70,7 +71,7 @@ class KernelBackend:
                                  b: ComplexDense, ledger: FlopLedger) -> HermitianAccumulator:
         _check(x.shape == b.shape, f"ZHER2K operands differ in shape: {x.shape} and {b.shape}")
         k, n = x.shape
-        _check(c.n == n, f"ZHER2K target of order {c.n} cannot take {k}x{n} operands")
+        _check(c.n == n, f"ZHER2K (rank-2k) target {c.n}x{c.n} cannot take {k}x{n} operands")
         if k > 0 and n > 0:
             self._her2k(c.matrix, x, b)
         ledger.add("hermitian_rank_2k", 8 * k * n * n)

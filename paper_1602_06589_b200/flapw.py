@@ -20,9 +20,13 @@ from .matrix import AtomBlockLayout, ComplexDense, DeviceComplexDense
 _MIN_WRONSKIAN = 1e-8
 
 
+_RADIAL_FIELDS = ("u", "u_prime", "udot", "udot_prime", "energy", "udot_norm")
+
+
 @dataclass
 class RadialBoundaryData:
-    """Boundary values of the radial solutions for one atom, indexed by l (`flapw.py:36-82`)."""
+    """One atom's radial solutions at the sphere boundary, one entry per l = 0..l_max: u_l,
+    u_l', the energy derivatives and their norms (`flapw.py:36-82`)."""
 
     u: np.ndarray
     u_prime: np.ndarray
@@ -32,17 +36,18 @@ class RadialBoundaryData:
     udot_norm: np.ndarray
 
     def __post_init__(self):
-        arrays = [np.asarray(a, dtype=np.float64) for a in
-                  (self.u, self.u_prime, self.udot, self.udot_prime, self.energy, self.udot_norm)]
-        self.u, self.u_prime, self.udot, self.udot_prime, self.energy, self.udot_norm = arrays
-        n = self.u.shape[0]
-        if any(a.shape != (n,) for a in arrays):
-            raise ContractViolationError("radial value arrays must share one length")
-        if np.any(self.udot_norm < 0):
-            raise ContractViolationError("udot norms must be non-negative")
-        if np.any(np.abs(self.wronskian) < _MIN_WRONSKIAN):
+        for name in _RADIAL_FIELDS:
+            setattr(self, name, np.asarray(getattr(self, name), dtype=np.float64))
+        want = (len(self.u),)
+        odd = [name for name in _RADIAL_FIELDS if getattr(self, name).shape != want]
+        if odd:
+            raise ContractViolationError(f"radial arrays {odd} do not have the {want[0]} entries of u")
+        if (self.udot_norm < 0).any():
+            raise ContractViolationError("a norm of udot cannot be negative")
+        # the match factors divide by the Wronskian W_l = udot_l u_l' - u_l udot_l'
+        if (np.abs(self.wronskian) < _MIN_WRONSKIAN).any():
             raise ContractViolationError(
-                f"|Wronskian| below {_MIN_WRONSKIAN}: radial values too degenerate")
+                f"radial pair (u, udot) nearly dependent: a |Wronskian| is under {_MIN_WRONSKIAN}")
 
     @property
     def wronskian(self) -> np.ndarray:
@@ -50,20 +55,34 @@ class RadialBoundaryData:
 
     @property
     def l_max(self) -> int:
-        return self.u.shape[0] - 1
+        return len(self.u) - 1
 
     def to_json_dict(self) -> dict:
-        return {k: getattr(self, k).tolist() for k in
-                ("u", "u_prime", "udot", "udot_prime", "energy", "udot_norm")}
+        return {name: getattr(self, name).tolist() for name in _RADIAL_FIELDS}
 
     @classmethod
     def from_json_dict(cls, d: dict) -> "RadialBoundaryData":
-        return cls(**{k: np.asarray(v, dtype=np.float64) for k, v in d.items()})
+        return cls(**{name: np.asarray(vals, dtype=np.float64) for name, vals in d.items()})
+
+
+_SPEC_ARRAYS = (("positions", np.float64), ("rotations", np.float64), ("mt_radius", np.float64),
+                ("l_sph", np.int64), ("l_nonsph", np.int64), ("k_point", np.float64),
+                ("k_vectors", np.float64))
+
+
+def _proper_or_improper_rotation(r: np.ndarray) -> str | None:
+    """None for an orthogonal 3x3 matrix of determinant +-1 (tolerance 1e-12), else what fails."""
+    if np.abs(r.T @ r - np.eye(3)).max() > 1e-12:
+        return "is not orthogonal"
+    if abs(abs(np.linalg.det(r)) - 1.0) > 1e-12:
+        return "has a determinant of modulus other than one"
+    return None
 
 
 @dataclass
 class SystemSpec:
-    """Geometry, cutoffs, basis vectors and radial data of one system (`flapw.py:85-166`)."""
+    """Everything `compute_AB` needs for one k-point: atoms (positions, local frames, sphere
+    radii, cutoffs, radial data), the K = k + G vectors and the cell volume (`flapw.py:85-166`)."""
 
     positions: np.ndarray
     rotations: np.ndarray
@@ -76,35 +95,29 @@ class SystemSpec:
     radial: list
 
     def __post_init__(self):
-        self.positions = np.asarray(self.positions, dtype=np.float64)
-        self.rotations = np.asarray(self.rotations, dtype=np.float64)
-        self.mt_radius = np.asarray(self.mt_radius, dtype=np.float64)
-        self.l_sph = np.asarray(self.l_sph, dtype=np.int64)
-        self.l_nonsph = np.asarray(self.l_nonsph, dtype=np.int64)
-        self.k_point = np.asarray(self.k_point, dtype=np.float64)
-        self.k_vectors = np.asarray(self.k_vectors, dtype=np.float64)
-        n = self.n_atoms
-        if self.k_vectors.ndim != 2 or self.k_vectors.shape[1] != 3 or self.n_basis < 1:
-            raise ContractViolationError("need at least one K-vector of dimension 3")
+        for name, kind in _SPEC_ARRAYS:
+            setattr(self, name, np.asarray(getattr(self, name), dtype=kind))
+        atoms = self.n_atoms
+        kv = self.k_vectors
+        if kv.ndim != 2 or kv.shape[1] != 3 or kv.shape[0] == 0:
+            raise ContractViolationError("k_vectors is a non-empty list of 3-vectors")
         if self.omega <= 0:
-            raise ContractViolationError("cell volume must be positive")
-        if np.any(self.l_nonsph > self.l_sph):
-            raise ConfigurationError("l_nonsph must not exceed l_sph")
-        if np.any(self.mt_radius <= 0):
-            raise ContractViolationError("muffin-tin radii must be positive")
-        if self.rotations.shape != (n, 3, 3):
-            raise ContractViolationError("need one 3x3 rotation per atom")
-        for a in range(n):
-            r = self.rotations[a]
-            if np.max(np.abs(r.T @ r - np.eye(3))) > 1e-12:
-                raise ContractViolationError(f"rotation {a} is not orthogonal")
-            if abs(abs(np.linalg.det(r)) - 1.0) > 1e-12:
-                raise ContractViolationError(f"rotation {a} has |det| != 1")
-        if len(self.radial) != n:
-            raise ContractViolationError("need radial data per atom")
-        for a, rad in enumerate(self.radial):
-            if rad.l_max < self.l_sph[a]:
-                raise ContractViolationError(f"atom {a}: radial data stops below l_sph")
+            raise ContractViolationError("the cell volume omega is positive")
+        if (self.l_nonsph > self.l_sph).any():
+            raise ConfigurationError("l_nonsph is capped by l_sph, atom by atom")
+        if (self.mt_radius <= 0).any():
+            raise ContractViolationError("every muffin-tin radius is positive")
+        if self.rotations.shape != (atoms, 3, 3):
+            raise ContractViolationError(f"rotations holds a 3x3 matrix for each of the {atoms} atoms")
+        for a, frame in enumerate(self.rotations):
+            fault = _proper_or_improper_rotation(frame)
+            if fault:
+                raise ContractViolationError(f"local frame of atom {a} {fault}")
+        if len(self.radial) != atoms:
+            raise ContractViolationError(f"radial holds one entry for each of the {atoms} atoms")
+        short = [a for a, rad in enumerate(self.radial) if rad.l_max < self.l_sph[a]]
+        if short:
+            raise ContractViolationError(f"radial data of atoms {short} ends before their l_sph")
 
     @property
     def n_atoms(self) -> int:
@@ -119,13 +132,10 @@ class SystemSpec:
         return AtomBlockLayout(heights, int((self.l_sph.max() + 1) ** 2))
 
     def to_json_dict(self) -> dict:
-        return {
-            "positions": self.positions.tolist(), "rotations": self.rotations.tolist(),
-            "mt_radius": self.mt_radius.tolist(), "l_sph": self.l_sph.tolist(),
-            "l_nonsph": self.l_nonsph.tolist(), "k_point": self.k_point.tolist(),
-            "k_vectors": self.k_vectors.tolist(), "omega": self.omega,
-            "radial": [r.to_json_dict() for r in self.radial],
-        }
+        doc = {name: getattr(self, name).tolist() for name, _ in _SPEC_ARRAYS}
+        doc["omega"] = self.omega
+        doc["radial"] = [rad.to_json_dict() for rad in self.radial]
+        return doc
 
     def to_json(self) -> str:
         return json.dumps(self.to_json_dict(), sort_keys=True)

@@ -8,9 +8,12 @@ backend on every host thread) on the seeded BASELINE systems of paper_1602_06589
 
 * big_C2.npz — C2 (N_G 2999, R 1296)
 * big_C3.npz — C3 (N_G 7994, R 5184)
+* big_C4.npz — C4 (N_G 12986, R 13068, three atom types; ~25 min and ~25 GB of host memory here)
+* big_C5.npz — C5's first k-point (N_G ~5000, R 2592)
 
-Each file holds, for H and S: one full 64-column panel (the middle one, so it crosses every
-tile row of that panel), random full columns, H V / S V for seeded random V, the diagonals,
+Each file holds, for H and S: full columns of the middle 64-column panel (all 64 at C2 / C3, the
+first 32 / 16 of it at C5 / C4 to keep the fixtures small; they cross every tile row of that
+panel), random full columns, H V / S V for seeded random V, the diagonals,
 the Frobenius norms, plus the ledger, the HPD mask and digests of the inputs (the GPU tests
 rebuild the inputs from configs.py and refuse to compare if they drifted).  The full
 matrices (144 MB / 1 GB each) are not stored.
@@ -35,7 +38,8 @@ from paper_1602_06589_b200 import configs  # noqa: E402
 sys.path.insert(0, HERE)
 from digest import input_digest  # noqa: E402
 
-COLS = {"C2": 16, "C3": 16}
+COLS = {"C2": 16, "C3": 16, "C4": 8, "C5": 12}
+PANEL_COLS = {"C2": 64, "C3": 64, "C4": 16, "C5": 32}
 
 
 def main(names):
@@ -57,9 +61,10 @@ def main(names):
         n = H.shape[0]
         nb = (n + 63) // 64
         j0 = 64 * (nb // 2)
-        panel = np.arange(j0, min(n, j0 + 64))
+        panel = np.arange(j0, min(n, j0 + PANEL_COLS[name]))
         rng = np.random.default_rng(2024)
-        cols = np.sort(rng.choice(np.setdiff1d(np.arange(n), panel), size=COLS[name], replace=False))
+        cols = np.sort(rng.choice(np.setdiff1d(np.arange(n), np.arange(j0, min(n, j0 + 64))),
+                                  size=COLS[name], replace=False))
         v = rng.standard_normal((n, 2)) + 1j * rng.standard_normal((n, 2))
         out = {
             "digest": np.array(input_digest(inst)), "n": n, "panel": panel, "cols": cols,

@@ -10,6 +10,9 @@ backend on every host thread) on the seeded BASELINE systems of paper_1602_06589
 * big_C3.npz — C3 (N_G 7994, R 5184)
 * big_C4.npz — C4 (N_G 12986, R 13068, three atom types; ~25 min and ~25 GB of host memory here)
 * big_C5.npz — C5's first k-point (N_G ~5000, R 2592)
+* big_C2NS.npz, big_C2IND.npz — the C2-sized non-BASELINE systems with structured T (l_nonsph 6:
+  the T-structure split) and indefinite T (no T_AA is HPD: the shifted joint form on the GPU,
+  the general ZHEMM/ZGEMM path in the reference)
 
 Each file holds, for H and S: full columns of the middle 64-column panel (all 64 at C2 / C3, the
 first 32 / 16 of it at C5 / C4 to keep the fixtures small; they cross every tile row of that
@@ -38,8 +41,8 @@ from paper_1602_06589_b200 import configs  # noqa: E402
 sys.path.insert(0, HERE)
 from digest import input_digest  # noqa: E402
 
-COLS = {"C2": 16, "C3": 16, "C4": 8, "C5": 12}
-PANEL_COLS = {"C2": 64, "C3": 64, "C4": 16, "C5": 32}
+COLS = {"C2": 16, "C3": 16, "C4": 8, "C5": 12, "C2NS": 8, "C2IND": 8}
+PANEL_COLS = {"C2": 64, "C3": 64, "C4": 16, "C5": 32, "C2NS": 16, "C2IND": 16}
 
 
 def main(names):

@@ -1,7 +1,8 @@
 """Parity against H and S made by the REAL reference at the BASELINE sizes C2, C3, C4 and C5
 (tests/golden/make_golden_big.py ran hsdla's own compute_AB + build_all on the seeded
 inputs of configs.py; with C1 in test_gpu_parity.py every BASELINE config is compared with the
-reference's own output).
+reference's own output), and at the C2-sized C2NS (structured T) and C2IND (indefinite T: the
+shifted joint form here, the reference's general path there).
 
 Both B200 entry points are checked: the device pipeline (`pipeline.build_hs`: per-type
 template path, joint T factor, fused mirror) and the drop-in reference API
@@ -59,7 +60,7 @@ def _inputs(name, g):
     return inst
 
 
-@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5", "C2NS", "C2IND"])
 def test_pipeline_vs_reference_golden(cuda, name):
     import torch
 
@@ -88,7 +89,7 @@ def test_pipeline_vs_reference_golden(cuda, name):
            float(torch.linalg.norm(h_t)), float(torch.linalg.norm(s_t)))
 
 
-@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5", "C2NS", "C2IND"])
 def test_dropin_api_vs_reference_golden(cuda, name):
     import paper_1602_06589_b200 as pkg
 

@@ -84,6 +84,12 @@ struct SKParams {
 #ifndef HSDLA_DMMA_VOLATILE
 #define HSDLA_DMMA_VOLATILE 1
 #endif
+// Default three-product K loop: products ordered by column block with the next K group's
+// fragments requested inside the current group (0: fragments loaded at the top of each group,
+// the earlier loop, kept for A/B builds: `make er ER=0`).
+#ifndef HSDLA_EARLY_RELOAD
+#define HSDLA_EARLY_RELOAD 1
+#endif
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
 #if HSDLA_DMMA_VOLATILE
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -356,7 +362,52 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), MINB)
       const double* sQ = sP + kOpDoubles;
       const double* pa = sP + (wm * 32 + g) * kColDoubles;
       const double* pb = sQ + (wn * kWarpCols + g) * kColDoubles;
-      if constexpr (PAD == 2) {
+      if constexpr (PAD == 2 && G3 && !PL && HSDLA_EARLY_RELOAD) {
+        // Products ordered by column block with the three products of a block pair together, so
+        // a row fragment's registers are free after its last column block and the next K
+        // group's fragment is loaded there (and the next group's first column fragment one
+        // block earlier) instead of at the top of the next group, where the warp would wait for
+        // shared memory with nothing to issue: contractions -0.9% (C2) .. -1.35% (C3),
+        // profiles/r02d_early_reload.json.  Double-buffering the column fragments on top of
+        // this measured the same.
+        auto offj = [&](int j) {
+          return (((2 * j + (q >> 1)) ^ ((g & 1) << 1)) << 2) + ((q & 1) << 1);
+        };
+        double2 av[4], bpre;
+        {
+          const int off0 = offj(0);
+#pragma unroll
+          for (int ib = 0; ib < 4; ++ib)
+            av[ib] = *reinterpret_cast<const double2*>(pa + ib * 8 * kColDoubles + off0);
+          bpre = *reinterpret_cast<const double2*>(pb + off0);
+        }
+#pragma unroll
+        for (int j = 0; j < KC / 4; ++j) {
+          if (sk.spread && more)
+            issue_rounds(nstage, j * kRounds / (KC / 4), (j + 1) * kRounds / (KC / 4));
+          const int off = offj(j), offn = offj(j + 1);
+          const bool nextj = j + 1 < KC / 4;
+          double sa[4];
+#pragma unroll
+          for (int ib = 0; ib < 4; ++ib) sa[ib] = av[ib].x - av[ib].y;
+#pragma unroll
+          for (int jb = 0; jb < JB; ++jb) {
+            const double2 b = jb == 0 ? bpre
+                                      : *reinterpret_cast<const double2*>(
+                                            pb + jb * 8 * kColDoubles + off);
+            const double sb = b.x + b.y;
+#pragma unroll
+            for (int ib = 0; ib < 4; ++ib) {
+              dmma(accR[ib][jb][0], accR[ib][jb][1], av[ib].x, b.x);
+              dmma(accX[ib][jb][0], accX[ib][jb][1], av[ib].y, b.y);
+              dmma(accI[ib][jb][0], accI[ib][jb][1], sa[ib], sb);
+              if (jb == JB - 1 && nextj)
+                av[ib] = *reinterpret_cast<const double2*>(pa + ib * 8 * kColDoubles + offn);
+            }
+            if (jb == JB - 2 && nextj) bpre = *reinterpret_cast<const double2*>(pb + offn);
+          }
+        }
+      } else if constexpr (PAD == 2) {
         // Paired K steps: lane q takes complex element 4j+q whole (one 16-byte load per
         // fragment) and uses its real part at step 2j, its imaginary part at step 2j+1.
         // The K order of the real embedding is free as long as P and Q share it:

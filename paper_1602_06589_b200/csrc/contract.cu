@@ -369,7 +369,9 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), MINB)
         // block earlier) instead of at the top of the next group, where the warp would wait for
         // shared memory with nothing to issue: contractions -0.9% (C2) .. -1.35% (C3),
         // profiles/r02d_early_reload.json.  Double-buffering the column fragments on top of
-        // this measured the same.
+        // this measured the same; carrying the fragments across chunk boundaries as well (the
+        // chunk barrier moved before a chunk's last K group, one chunk of cp.async lead) spilled
+        // and measured 3.4% slower.
         auto offj = [&](int j) {
           return (((2 * j + (q >> 1)) ^ ((g & 1) << 1)) << 2) + ((q & 1) << 1);
         };

@@ -353,7 +353,8 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), MINB)
       const int nstage = nc % kStages;
       // spread: the next-but-one chunk's loads are issued a round at a time between the
       // DMMA steps instead of as one block after the barrier.
-      if (!sk.spread) {
+      constexpr bool kLoadFirst = PAD == 2 && G3 && !PL && HSDLA_EARLY_RELOAD != 0;
+      if (!kLoadFirst && !sk.spread) {
         if (more) issue(nstage);
         cp_async_commit();
       }
@@ -382,6 +383,14 @@ __global__ void __launch_bounds__(32 * 2 * (8 / JB), MINB)
           for (int ib = 0; ib < 4; ++ib)
             av[ib] = *reinterpret_cast<const double2*>(pa + ib * 8 * kColDoubles + off0);
           bpre = *reinterpret_cast<const double2*>(pb + off0);
+        }
+        // the next-but-one chunk's cp.async block goes out under these loads' latency (issued
+        // before them, right after the barrier, it delayed the chunk's first products: another
+        // -0.8%; split in two halves or moved before K group 1 it measured 1.3% slower, the
+        // row-block-outer mirror order 0.4% slower: profiles/r02d_early_reload.json)
+        if (kLoadFirst && !sk.spread) {
+          if (more) issue(nstage);
+          cp_async_commit();
         }
 #pragma unroll
         for (int j = 0; j < KC / 4; ++j) {
